@@ -1,0 +1,185 @@
+/*
+ * otfgpu.h -- C ABI of libotfgpu.so, the B200 engine for the reference's
+ * virtual-clock scalability experiment.
+ *
+ * The reference (otfstream, pure Python) has no FFI; its drop-in boundary is
+ * the Python call
+ *
+ *     run_experiment(config: ExperimentConfig) -> ExperimentResult
+ *         /root/reference/pkg/src/otfstream/orchestrator.py:327-370
+ *
+ * plus the sweep driver that calls it once per grid point
+ * (orchestrator.py:373-390, cli.py:52-62).  This library replaces the body of
+ * that call for a whole batch of configs at once: the host lowers each
+ * ExperimentConfig to an otf_scenario plus shared input tables, and
+ * otf_run_batch() replays every scenario's event order on the GPU.  The
+ * Python package paper_2603_08417_b200 binds these symbols with ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions: plain C types only; every pointer inside otf_batch is a DEVICE
+ * pointer owned by the caller unless stated otherwise; calls are stateless,
+ * enqueue on the given CUDA stream and return an otf_status.  The last error
+ * message is kept per host thread (otf_last_error).
+ */
+#ifndef OTFGPU_H
+#define OTFGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OTF_ABI_VERSION 1
+
+/* ---- status codes (ValueError / RuntimeError on the Python side) ---- */
+typedef enum {
+    OTF_OK = 0,
+    OTF_EINVAL = 1,     /* malformed batch / scenario (ConfigError-class) */
+    OTF_ECUDA = 3,      /* a CUDA call failed */
+} otf_status;
+
+/* ---- per-scenario status bits (otf_batch.status[s]) ---- */
+#define OTF_S_RECORD_OVERFLOW 0x1  /* record capacity too small: counts are exact, re-run with them */
+#define OTF_S_EPS_OVERFLOW 0x2     /* worker noise table too short: re-run with a longer one */
+#define OTF_S_INTERNAL 0x4         /* structural invariant violated (bug) */
+#define OTF_S_TIE 0x8              /* windowed engine met an ordering tie it cannot resolve:
+                                      the host re-runs the scenario on the exact engine */
+#define OTF_S_HUNG 0x10            /* a client slept forever (starved trace), informative */
+
+/* ---- enums shared with the host (values are part of the ABI) ---- */
+enum { OTF_PATH_STORAGE = 0, OTF_PATH_CACHE = 1, OTF_PATH_WAITED = 2, OTF_PATH_TRANSCODED = 3 };
+enum { OTF_ORIGIN_DEMAND = 0, OTF_ORIGIN_SPECULATIVE = 1 };
+enum { OTF_OUTCOME_PENDING = 0, OTF_OUTCOME_COMPLETED = 1, OTF_OUTCOME_DROPPED = 2 };
+enum { OTF_POP_UNIFORM = 0, OTF_POP_ZIPF = 1 };
+enum { OTF_ENGINE_EXACT = 0, OTF_ENGINE_WINDOWED = 1 };
+enum { OTF_MODE_HISTOGRAM = 0, OTF_MODE_RECORDS = 1 };
+
+/* stats[] slots: Backend.stats() (backend.py:228-239) and SegmentCache.stats()
+ * (cache.py:83-92) as integers. */
+enum {
+    OTF_ST_JOBS_TOTAL = 0, OTF_ST_JOBS_DEMAND, OTF_ST_JOBS_SPEC, OTF_ST_WASTED, OTF_ST_SPEC_ENQUEUED,
+    OTF_ST_SKIP_DISABLED, OTF_ST_SKIP_EOS, OTF_ST_SKIP_STORED, OTF_ST_SKIP_CACHED,
+    OTF_ST_SKIP_INFLIGHT, OTF_ST_SKIP_OVERLOAD,
+    OTF_ST_CACHE_CAPACITY, OTF_ST_CURRENT_BYTES, OTF_ST_ENTRIES, OTF_ST_HITS, OTF_ST_MISSES,
+    OTF_ST_EVICTIONS, OTF_ST_REJECTED,
+    OTF_ST_STATUS, OTF_ST_HUNG, OTF_ST_TIMER_POPS, OTF_ST_READY_CALLBACKS, OTF_ST_WINDOWS,
+    OTF_ST_NSLOTS = 32
+};
+
+/* One scenario = one ExperimentConfig (orchestrator.py:74-113).  Table
+ * offsets index the shared pools of otf_batch (in elements). */
+typedef struct otf_scenario {
+    int32_t n_clients, n_workers, n_seq, n_ranks;
+    int32_t max_nseg, n_samples, cache_enabled, spec_enabled;
+    int32_t popularity, pad0;
+    uint32_t stored_mask, pad1;       /* bit r set <=> rank r stored at origin (backend.py:76-82) */
+    int64_t cache_capacity;           /* bytes (cache.py:27-30) */
+    uint64_t seed;                    /* ExperimentConfig.seed: picks stream SS([seed, 3, cid]) */
+    double horizon, latency;          /* horizon_s; ClientConfig.latency_s */
+    double target, safe, panic, resume, startup;   /* BufferConfig (client.py:49-61) */
+    double alpha, headroom;           /* ClientConfig.ewma_alpha / headroom */
+    double noise;                     /* LatencyModel.noise_rel_std */
+    double period;                    /* BandwidthTrace.period (shared timestamps) */
+    int64_t off_sizes;                /* i64: [n_seq][n_ranks][max_nseg] segment bytes */
+    int64_t off_bitrates;             /* i64: [n_ranks] */
+    int64_t off_manifest;             /* i64: [n_seq] manifest JSON bytes */
+    int64_t off_segcount;             /* i32: [n_seq] */
+    int64_t off_seqdur, off_segdur;   /* f64: [n_seq] */
+    int64_t off_rho;                  /* f64: [n_ranks] */
+    int64_t off_zipf;                 /* f64: [n_seq] Zipf CDF (popularity == ZIPF) */
+    int64_t off_starts;               /* f64: [n_samples] trace piece start times */
+    int64_t off_values;               /* f64: [n_clients][n_samples] bandwidth, bit/s */
+    int64_t off_pbits;                /* f64: [n_clients] bits per trace period */
+    int64_t off_arrivals;             /* f64: [n_clients] arrival offsets (cumsum) */
+    int64_t off_eps;                  /* f64: [n_workers][eps_stride] worker noise draws */
+    int64_t eps_stride;
+    int64_t scratch_off;              /* bytes into otf_batch.scratch */
+    int64_t req_off, req_cap;         /* record slices (records mode) */
+    int64_t sess_off, sess_cap;
+    int64_t seg_off, seg_cap;
+    int64_t job_off, job_cap;
+} otf_scenario;
+
+/* Fused QoE / fulfillment epilogue (metrics.py:67-116, orchestrator.py:280-309). */
+#define OTF_LAT_BINS 64      /* bin 0: latency < 10 ms (instant); then 4 bins per octave from 10 ms */
+#define OTF_STALL_BINS 32    /* sessions by stall count, last bin = ">= 31" */
+#define OTF_RANK_BINS 16     /* segments by representation rank */
+typedef struct otf_qoe {
+    int64_t lat_hist[OTF_LAT_BINS];
+    int64_t path_count[4];
+    int64_t stall_hist[OTF_STALL_BINS];
+    int64_t rank_count[OTF_RANK_BINS];
+    int64_t n_requests, n_sessions, n_segments, n_finished, n_started;
+    int64_t pad;
+    double latency_sum, stall_time_sum, startup_delay_sum, pad2;
+} otf_qoe;
+
+typedef struct otf_batch {
+    int32_t n_scenarios;
+    int32_t mode;                     /* OTF_MODE_* */
+    const otf_scenario *scenarios;    /* [n_scenarios] */
+    const double *f64_pool;
+    const int64_t *i64_pool;
+    const int32_t *i32_pool;
+    uint8_t *scratch;                 /* engine state, otf_scratch_bytes() per scenario */
+    /* records (MODE_RECORDS; SoA slices at otf_scenario.*_off) */
+    int64_t *req_id; int32_t *req_seq, *req_rep, *req_index, *req_path;
+    double *req_arrival, *req_response; int64_t *req_bytes;
+    int32_t *sess_client, *sess_seq, *sess_stalls, *sess_flags;
+    double *sess_start, *sess_end, *sess_stall_time, *sess_startup;
+    int32_t *seg_session, *seg_index, *seg_rep; double *seg_start, *seg_end;
+    int32_t *job_seq, *job_rep, *job_index, *job_origin, *job_outcome;
+    double *job_enq, *job_start, *job_fin;
+    /* per-scenario outputs */
+    int64_t *counts;                  /* [n_scenarios][4]: requests, sessions, segments, jobs */
+    int64_t *stats;                   /* [n_scenarios][OTF_ST_NSLOTS] */
+    otf_qoe *qoe;                     /* [n_scenarios] */
+    int32_t *status;                  /* [n_scenarios] OTF_S_* bits */
+} otf_batch;
+
+/* A segment-size table: Catalog.descriptor sizes (content.py:204-218) for one
+ * catalog, generated on the device from SeedSequence([seed, key, rank, index]). */
+typedef struct otf_size_table {
+    int32_t n_seq, n_ranks, max_nseg, pad;
+    uint64_t seed;                    /* catalog seed (= ExperimentConfig.seed) */
+    double size_jitter;
+    int64_t off_out;                  /* i64 pool offset of [n_seq][n_ranks][max_nseg] */
+    int64_t off_keys;                 /* i64: [n_seq] sha256(seq id)[:8] big-endian */
+    int64_t off_bitrates;             /* i64: [n_ranks] */
+    int64_t off_seqdur, off_segdur;   /* f64: [n_seq] */
+    int64_t off_segcount;             /* i32: [n_seq] */
+} otf_size_table;
+
+int otf_version(void);
+const char *otf_last_error(void);
+size_t otf_sizeof_scenario(void);
+size_t otf_sizeof_batch(void);
+size_t otf_sizeof_qoe(void);
+
+/* Engine scratch bytes for one scenario (host-side layout helper). */
+int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
+                          int32_t n_ranks, int32_t max_nseg);
+
+/* HOST function: synthetic traces (netem.py:179-202) + BandwidthTrace period
+ * bits (netem.py:39-64) from numpy's standard-normal draws.  normals is
+ * [n_traces][n_samples + 1]; starts is [n_samples]; values is
+ * [n_traces][n_samples]; pbits [n_traces].  Uses glibc exp() (== math.exp)
+ * and CPython 3.12's compensated sum(), so the values are bit-identical to
+ * the reference's BandwidthTrace. Host pointers. */
+int otf_build_traces(int64_t n_traces, int32_t n_samples, const double *normals, const double *starts,
+                     double period, double mu, double sigma, double decay, double spread,
+                     double floor_bps, double cap_bps, double *values, double *pbits, int32_t n_threads);
+
+/* DEVICE: fill segment-size tables (one thread per entry). */
+int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
+                  int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream);
+
+/* DEVICE: run every scenario of the batch to its horizon (sim.py:347-360). */
+int otf_run_batch(const otf_batch *batch, int32_t engine, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OTFGPU_H */

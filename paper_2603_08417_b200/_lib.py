@@ -1,0 +1,150 @@
+"""ctypes binding of libotfgpu.so (include/otfgpu.h).
+
+The library is built in-tree (``paper_2603_08417_b200/libotfgpu.so``) by
+``build()`` / ``__graft_entry__.build()``.  There is no fallback: every
+product entry point goes through this module and raises when the library or
+a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB_PATH = os.path.join(HERE, "libotfgpu.so")
+ABI_VERSION = 1
+
+_P = ctypes.POINTER
+_vp = ctypes.c_void_p
+_i32, _u32, _i64, _u64, _f64 = ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+
+# enums (values are part of the ABI)
+PATH_STORAGE, PATH_CACHE, PATH_WAITED, PATH_TRANSCODED = 0, 1, 2, 3
+ORIGIN_DEMAND, ORIGIN_SPECULATIVE = 0, 1
+OUTCOME_PENDING, OUTCOME_COMPLETED, OUTCOME_DROPPED = 0, 1, 2
+POP_UNIFORM, POP_ZIPF = 0, 1
+ENGINE_EXACT, ENGINE_WINDOWED = 0, 1
+MODE_HISTOGRAM, MODE_RECORDS = 0, 1
+S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG = 0x1, 0x2, 0x4, 0x8, 0x10
+
+ST_NSLOTS = 32
+ST = dict(jobs_total=0, jobs_demand=1, jobs_speculative=2, wasted_avoided=3, speculation_enqueued=4,
+          skip0=5, capacity_bytes=11, current_bytes=12, entries=13, hits=14, misses=15,
+          evictions=16, rejected=17, status=18, hung=19, timer_pops=20, ready_callbacks=21, windows=22)
+SKIP_REASONS = ("disabled", "end-of-sequence", "stored", "cached", "in-flight", "overload")
+LAT_BINS, STALL_BINS, RANK_BINS = 64, 32, 16
+
+
+class Scenario(ctypes.Structure):
+    _fields_ = [
+        ("n_clients", _i32), ("n_workers", _i32), ("n_seq", _i32), ("n_ranks", _i32),
+        ("max_nseg", _i32), ("n_samples", _i32), ("cache_enabled", _i32), ("spec_enabled", _i32),
+        ("popularity", _i32), ("pad0", _i32), ("stored_mask", _u32), ("pad1", _u32),
+        ("cache_capacity", _i64), ("seed", _u64),
+        ("horizon", _f64), ("latency", _f64),
+        ("target", _f64), ("safe", _f64), ("panic", _f64), ("resume", _f64), ("startup", _f64),
+        ("alpha", _f64), ("headroom", _f64), ("noise", _f64), ("period", _f64),
+        ("off_sizes", _i64), ("off_bitrates", _i64), ("off_manifest", _i64), ("off_segcount", _i64),
+        ("off_seqdur", _i64), ("off_segdur", _i64), ("off_rho", _i64), ("off_zipf", _i64),
+        ("off_starts", _i64), ("off_values", _i64), ("off_pbits", _i64), ("off_arrivals", _i64),
+        ("off_eps", _i64), ("eps_stride", _i64), ("scratch_off", _i64),
+        ("req_off", _i64), ("req_cap", _i64), ("sess_off", _i64), ("sess_cap", _i64),
+        ("seg_off", _i64), ("seg_cap", _i64), ("job_off", _i64), ("job_cap", _i64),
+    ]
+
+
+class Qoe(ctypes.Structure):
+    _fields_ = [
+        ("lat_hist", _i64 * LAT_BINS), ("path_count", _i64 * 4), ("stall_hist", _i64 * STALL_BINS),
+        ("rank_count", _i64 * RANK_BINS),
+        ("n_requests", _i64), ("n_sessions", _i64), ("n_segments", _i64), ("n_finished", _i64),
+        ("n_started", _i64), ("pad", _i64),
+        ("latency_sum", _f64), ("stall_time_sum", _f64), ("startup_delay_sum", _f64), ("pad2", _f64),
+    ]
+
+
+RECORD_FIELDS = [  # (name, numpy dtype) in otf_batch order
+    ("req_id", "i8"), ("req_seq", "i4"), ("req_rep", "i4"), ("req_index", "i4"), ("req_path", "i4"),
+    ("req_arrival", "f8"), ("req_response", "f8"), ("req_bytes", "i8"),
+    ("sess_client", "i4"), ("sess_seq", "i4"), ("sess_stalls", "i4"), ("sess_flags", "i4"),
+    ("sess_start", "f8"), ("sess_end", "f8"), ("sess_stall_time", "f8"), ("sess_startup", "f8"),
+    ("seg_session", "i4"), ("seg_index", "i4"), ("seg_rep", "i4"), ("seg_start", "f8"), ("seg_end", "f8"),
+    ("job_seq", "i4"), ("job_rep", "i4"), ("job_index", "i4"), ("job_origin", "i4"), ("job_outcome", "i4"),
+    ("job_enq", "f8"), ("job_start", "f8"), ("job_fin", "f8"),
+]
+
+
+class Batch(ctypes.Structure):
+    _fields_ = ([("n_scenarios", _i32), ("mode", _i32), ("scenarios", _vp), ("f64_pool", _vp),
+                 ("i64_pool", _vp), ("i32_pool", _vp), ("scratch", _vp)]
+                + [(n, _vp) for n, _ in RECORD_FIELDS]
+                + [("counts", _vp), ("stats", _vp), ("qoe", _vp), ("status", _vp)])
+
+
+class SizeTable(ctypes.Structure):
+    _fields_ = [
+        ("n_seq", _i32), ("n_ranks", _i32), ("max_nseg", _i32), ("pad", _i32),
+        ("seed", _u64), ("size_jitter", _f64),
+        ("off_out", _i64), ("off_keys", _i64), ("off_bitrates", _i64),
+        ("off_seqdur", _i64), ("off_segdur", _i64), ("off_segcount", _i64),
+    ]
+
+
+EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
+           "otf_scratch_bytes", "otf_build_traces", "otf_gen_sizes", "otf_run_batch")
+
+
+class OtfError(RuntimeError):
+    pass
+
+
+def build(force: bool = False) -> str:
+    """Compile libotfgpu.so for sm_100a in place (csrc/Makefile)."""
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", "Makefile"))]
+    srcs.append(os.path.join(os.path.dirname(HERE), "include", "otfgpu.h"))
+    stale = not os.path.exists(LIB_PATH) or any(os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in srcs)
+    if force or stale:
+        subprocess.run(["make", "-s", "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    """Load libotfgpu.so (fails loudly if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise OtfError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.otf_version.restype = ctypes.c_int
+    L.otf_last_error.restype = ctypes.c_char_p
+    for f in ("otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe"):
+        getattr(L, f).restype = ctypes.c_size_t
+    L.otf_scratch_bytes.restype = _i64
+    L.otf_scratch_bytes.argtypes = [_i32] * 6
+    L.otf_build_traces.restype = ctypes.c_int
+    L.otf_build_traces.argtypes = [_i64, _i32, _P(_f64), _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
+                                   _P(_f64), _P(_f64), _i32]
+    L.otf_gen_sizes.restype = ctypes.c_int
+    L.otf_gen_sizes.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp, _vp]
+    L.otf_run_batch.restype = ctypes.c_int
+    L.otf_run_batch.argtypes = [_P(Batch), _i32, _vp]
+    if L.otf_version() != ABI_VERSION:
+        raise OtfError(f"libotfgpu ABI {L.otf_version()} != {ABI_VERSION}")
+    for name, st in (("otf_sizeof_scenario", Scenario), ("otf_sizeof_batch", Batch), ("otf_sizeof_qoe", Qoe)):
+        if getattr(L, name)() != ctypes.sizeof(st):
+            raise OtfError(f"{name}: C {getattr(L, name)()} != ctypes {ctypes.sizeof(st)}")
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().otf_last_error().decode("utf-8", "replace")
+        raise (ValueError if rc == 1 else OtfError)(f"{what} failed ({rc}): {msg}")

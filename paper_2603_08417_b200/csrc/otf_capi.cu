@@ -1,0 +1,133 @@
+// otf_capi.cu -- the extern "C" boundary of libotfgpu.so (include/otfgpu.h).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "otf_state.cuh"
+#include "otfgpu.h"
+
+int otf_launch_exact(const otf_batch &b, cudaStream_t stream);
+int otf_launch_windowed(const otf_batch &b, cudaStream_t stream);
+int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc);
+int otf_launch_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t *i64_pool,
+                     const double *f64_pool, const int32_t *i32_pool, cudaStream_t stream);
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+static int check_cuda(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(OTF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return OTF_OK;
+}
+
+extern "C" {
+
+int otf_version(void) { return OTF_ABI_VERSION; }
+
+const char *otf_last_error(void) { return g_last_error.c_str(); }
+
+size_t otf_sizeof_scenario(void) { return sizeof(otf_scenario); }
+size_t otf_sizeof_batch(void) { return sizeof(otf_batch); }
+size_t otf_sizeof_qoe(void) { return sizeof(otf_qoe); }
+
+int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
+                          int32_t n_ranks, int32_t max_nseg) {
+    int64_t n_desc = (int64_t)n_seq * n_ranks * max_nseg;
+    if (engine == OTF_ENGINE_WINDOWED) return otf_windowed_scratch_bytes(n_clients, n_workers, n_desc);
+    return otf::exact_layout(n_clients, n_workers, n_desc).total;
+}
+
+// CPython >= 3.12 builtin sum() over floats: Neumaier-compensated.
+static double py_sum(const double *xs, int n) {
+    double f = 0.0, c = 0.0;
+    for (int i = 0; i < n; i++) {
+        double x = xs[i];
+        double t = f + x;
+        if (fabs(f) >= fabs(x)) c += (f - t) + x;
+        else c += (x - t) + f;
+        f = t;
+    }
+    if (c != 0.0 && std::isfinite(c)) f += c;
+    return f;
+}
+
+int otf_build_traces(int64_t n_traces, int32_t n_samples, const double *normals, const double *starts,
+                     double period, double mu, double sigma, double decay, double spread,
+                     double floor_bps, double cap_bps, double *values, double *pbits, int32_t n_threads) {
+    if (n_traces < 0 || n_samples <= 0 || !normals || !starts || !values || !pbits)
+        return fail(OTF_EINVAL, "otf_build_traces: bad arguments");
+    auto work = [&](int64_t lo, int64_t hi) {
+        std::vector<double> terms((size_t)n_samples);
+        for (int64_t t = lo; t < hi; t++) {
+            const double *z = normals + t * (int64_t)(n_samples + 1);
+            double *v = values + t * (int64_t)n_samples;
+            // synthetic_trace (netem.py:190-201)
+            double x = mu + sigma * z[0];
+            for (int32_t i = 0; i < n_samples; i++) {
+                double e = exp(x);                       // glibc exp == math.exp
+                double bw = e > floor_bps ? e : floor_bps;
+                bw = cap_bps < bw ? cap_bps : bw;
+                v[i] = bw;
+                x = mu + (x - mu) * decay + spread * z[i + 1];
+            }
+            // BandwidthTrace._period_bits (netem.py:61-64)
+            for (int32_t i = 0; i < n_samples; i++) {
+                double end = (i + 1 < n_samples) ? starts[i + 1] : period;
+                terms[(size_t)i] = v[i] * (end - starts[i]);
+            }
+            pbits[t] = py_sum(terms.data(), n_samples);
+        }
+    };
+    int nt = std::max(1, std::min<int>(n_threads > 0 ? n_threads : 1, (int)std::max<int64_t>(1, n_traces / 64)));
+    if (nt == 1) {
+        work(0, n_traces);
+    } else {
+        std::vector<std::thread> th;
+        int64_t chunk = (n_traces + nt - 1) / nt;
+        for (int i = 0; i < nt; i++) {
+            int64_t lo = i * chunk, hi = std::min(n_traces, lo + chunk);
+            if (lo < hi) th.emplace_back(work, lo, hi);
+        }
+        for (auto &t : th) t.join();
+    }
+    return OTF_OK;
+}
+
+int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
+                  int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream) {
+    (void)total_entries;
+    if (n_tables < 0 || (n_tables > 0 && (!tables_dev || !i64_pool || !f64_pool || !i32_pool)))
+        return fail(OTF_EINVAL, "otf_gen_sizes: bad arguments");
+    otf_launch_sizes(tables_dev, n_tables, i64_pool, f64_pool, i32_pool, (cudaStream_t)stream);
+    return check_cuda("otf_gen_sizes");
+}
+
+int otf_run_batch(const otf_batch *batch, int32_t engine, void *stream) {
+    if (!batch) return fail(OTF_EINVAL, "otf_run_batch: null batch");
+    const otf_batch &b = *batch;
+    if (b.n_scenarios < 0) return fail(OTF_EINVAL, "otf_run_batch: negative scenario count");
+    if (b.n_scenarios == 0) return OTF_OK;
+    if (!b.scenarios || !b.f64_pool || !b.i64_pool || !b.i32_pool || !b.scratch || !b.counts || !b.stats ||
+        !b.qoe || !b.status)
+        return fail(OTF_EINVAL, "otf_run_batch: missing device buffer");
+    if (b.mode == OTF_MODE_RECORDS && (!b.req_id || !b.sess_client || !b.seg_session || !b.job_seq))
+        return fail(OTF_EINVAL, "otf_run_batch: records mode needs record buffers");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (engine == OTF_ENGINE_EXACT) otf_launch_exact(b, s);
+    else if (engine == OTF_ENGINE_WINDOWED) otf_launch_windowed(b, s);
+    else return fail(OTF_EINVAL, "otf_run_batch: unknown engine");
+    return check_cuda("otf_run_batch");
+}
+
+}  // extern "C"

@@ -1,0 +1,329 @@
+// otf_engine_common.cuh -- scenario view + client-side logic shared by engines.
+//
+// `Scn` binds one otf_scenario to its tables and output slices.  The client_*
+// helpers are the parts of run_session (client.py:229-305) and client_proc
+// (orchestrator.py:336-348) that only touch the client's own state, so the
+// exact engine and the windowed engine run literally the same code for them.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "otf_model.cuh"
+#include "otf_rng.cuh"
+#include "otf_state.cuh"
+#include "otfgpu.h"
+
+namespace otf {
+
+struct EngineState {                 // first 256 B of every scenario arena
+    int64_t req_counter;             // MediaServer._ids (server.py:56)
+    int64_t n_req, n_sess, n_seg, n_job;
+    int64_t cur_bytes, entries;      // SegmentCache.current_bytes / len()
+    int32_t lru_head, lru_tail;      // OrderedDict ends: head = oldest
+    int32_t status;
+    int32_t pad;
+};
+
+struct Scn {
+    otf_batch b;
+    otf_scenario sc;
+    int32_t s;
+    EngineState *st;
+    int64_t *stats;
+    otf_qoe *q;
+    const int64_t *sizes, *bitrates, *manifest_b;
+    const int32_t *segcounts;
+    const double *seqdur, *segdur, *rho, *zipf, *starts, *values, *pbits, *arrivals, *eps;
+    bool records;
+
+    __device__ void init(const otf_batch &bb, int32_t si) {
+        b = bb;
+        s = si;
+        sc = b.scenarios[si];
+        st = (EngineState *)(b.scratch + sc.scratch_off);
+        stats = b.stats + (int64_t)si * OTF_ST_NSLOTS;
+        q = b.qoe + si;
+        sizes = b.i64_pool + sc.off_sizes;
+        bitrates = b.i64_pool + sc.off_bitrates;
+        manifest_b = b.i64_pool + sc.off_manifest;
+        segcounts = b.i32_pool + sc.off_segcount;
+        seqdur = b.f64_pool + sc.off_seqdur;
+        segdur = b.f64_pool + sc.off_segdur;
+        rho = b.f64_pool + sc.off_rho;
+        zipf = b.f64_pool + sc.off_zipf;
+        starts = b.f64_pool + sc.off_starts;
+        values = b.f64_pool + sc.off_values;
+        pbits = b.f64_pool + sc.off_pbits;
+        arrivals = b.f64_pool + sc.off_arrivals;
+        eps = b.f64_pool + sc.off_eps;
+        records = b.mode == OTF_MODE_RECORDS;
+    }
+
+    // zero the scenario's outputs and counters (call once, single thread)
+    __device__ void reset_outputs() {
+        EngineState z = {};
+        z.lru_head = z.lru_tail = -1;
+        *st = z;
+        for (int i = 0; i < OTF_ST_NSLOTS; i++) stats[i] = 0;
+        int64_t *qq = (int64_t *)q;
+        for (size_t i = 0; i < sizeof(otf_qoe) / 8; i++) qq[i] = 0;
+    }
+
+    __device__ __forceinline__ int64_t &stat(int i) { return stats[i]; }
+    __device__ __forceinline__ void flag(int32_t bits) { st->status |= bits; }
+    __device__ __forceinline__ int32_t desc_id(int32_t seq, int32_t rank, int32_t index) const {
+        return (seq * sc.n_ranks + (rank - 1)) * sc.max_nseg + index;
+    }
+    __device__ __forceinline__ int64_t size(int32_t d) const { return sizes[d]; }
+    __device__ __forceinline__ int32_t segcount(int32_t seq) const { return segcounts[seq]; }
+    __device__ __forceinline__ bool stored(int32_t rank) const { return (sc.stored_mask >> rank) & 1u; }
+    __device__ __forceinline__ double arrival(int32_t cid) const { return arrivals[cid]; }
+    __device__ __forceinline__ int64_t manifest(int32_t seq) const { return manifest_b[seq]; }
+    __device__ __forceinline__ Trace trace(int32_t cid) const {
+        Trace t;
+        t.starts = starts;
+        t.values = values + (int64_t)cid * sc.n_samples;
+        t.period = sc.period;
+        t.pbits = pbits[cid];
+        t.n = sc.n_samples;
+        return t;
+    }
+    __device__ __forceinline__ int32_t desc_seq(int32_t d) const { return d / (sc.n_ranks * sc.max_nseg); }
+    __device__ __forceinline__ int32_t desc_rank(int32_t d) const { return (d / sc.max_nseg) % sc.n_ranks + 1; }
+    __device__ __forceinline__ int32_t desc_index(int32_t d) const { return d % sc.max_nseg; }
+
+    // Backend._enqueue bookkeeping: TranscodeJob + jobs.append (backend.py:156-170)
+    __device__ int32_t record_job(int32_t d, int32_t origin, double now) {
+        int64_t j = st->n_job++;
+        stats[OTF_ST_JOBS_TOTAL]++;
+        stats[origin == OTF_ORIGIN_DEMAND ? OTF_ST_JOBS_DEMAND : OTF_ST_JOBS_SPEC]++;
+        if (records) {
+            if (j < sc.job_cap) {
+                int64_t o = sc.job_off + j;
+                b.job_seq[o] = desc_seq(d);
+                b.job_rep[o] = desc_rank(d);
+                b.job_index[o] = desc_index(d);
+                b.job_origin[o] = origin;
+                b.job_outcome[o] = OTF_OUTCOME_PENDING;
+                b.job_enq[o] = now;
+                b.job_start[o] = NAN;
+                b.job_fin[o] = NAN;
+            } else {
+                flag(OTF_S_RECORD_OVERFLOW);
+            }
+        }
+        return (int32_t)j;
+    }
+    __device__ __forceinline__ void job_outcome(int32_t j, int32_t o) {
+        if (records && j < sc.job_cap) b.job_outcome[sc.job_off + j] = o;
+    }
+    __device__ __forceinline__ void job_started(int32_t j, double now) {
+        if (records && j < sc.job_cap) b.job_start[sc.job_off + j] = now;
+    }
+    __device__ __forceinline__ void job_finished(int32_t j, double now) {
+        if (records && j < sc.job_cap) {
+            b.job_fin[sc.job_off + j] = now;
+            b.job_outcome[sc.job_off + j] = OTF_OUTCOME_COMPLETED;
+        }
+    }
+
+    // ServiceSampler.service_time (transcode.py:95-99): the worker's own noise stream
+    __device__ double service_time(Worker &k, int32_t wid, int32_t d) {
+        int32_t rank = desc_rank(d), seq = desc_seq(d), idx = desc_index(d);
+        double duration = seg_duration(seqdur[seq], segdur[seq], idx);
+        double e = 0.0;
+        if (sc.noise > 0) {
+            if (k.eps_pos >= sc.eps_stride) flag(OTF_S_EPS_OVERFLOW);
+            else e = eps[(int64_t)wid * sc.eps_stride + k.eps_pos];
+            k.eps_pos++;
+        }
+        double svc = rho[rank - 1] * duration * (1.0 + e);
+        return (1e-9 > svc) ? 1e-9 : svc;
+    }
+
+    // MediaServer.segment record append (server.py:76-77) + QoE epilogue
+    __device__ void record_request(const Client &c, double response) {
+        int64_t r = st->n_req++;
+        if (records) {
+            if (r < sc.req_cap) {
+                int64_t o = sc.req_off + r;
+                b.req_id[o] = c.req_id;
+                b.req_seq[o] = c.seq;
+                b.req_rep[o] = c.rank;
+                b.req_index[o] = c.index;
+                b.req_path[o] = c.path;
+                b.req_arrival[o] = c.arrival;
+                b.req_response[o] = response;
+                b.req_bytes[o] = c.size;
+            } else {
+                flag(OTF_S_RECORD_OVERFLOW);
+            }
+        }
+        double lat = response - c.arrival;
+        q->lat_hist[lat_bin(lat)]++;
+        q->path_count[c.path]++;
+        q->n_requests++;
+        q->latency_sum += lat;
+    }
+
+    __device__ void sync_session(const Client &c, double now) {      // _sync_report (client.py:284-288)
+        if (!records || c.session >= sc.sess_cap) return;
+        int64_t o = sc.sess_off + c.session;
+        b.sess_end[o] = now;
+        b.sess_stalls[o] = c.buf.stall_events;
+        b.sess_stall_time[o] = c.buf.stall_time;
+        b.sess_startup[o] = isnan(c.buf.started_at) ? NAN : c.buf.started_at - c.buf.session_start;
+    }
+
+    // session QoE, once per session when its numbers are final
+    __device__ void qoe_session(const Client &c, bool finished) {
+        typedef unsigned long long ull;
+        int32_t stalls = c.buf_live ? c.buf.stall_events : 0;
+        atomicAdd((ull *)&q->n_sessions, 1ull);
+        atomicAdd((ull *)&q->stall_hist[stalls < OTF_STALL_BINS - 1 ? stalls : OTF_STALL_BINS - 1], 1ull);
+        if (c.buf_live) {
+            atomicAdd(&q->stall_time_sum, c.buf.stall_time);
+            if (!isnan(c.buf.started_at)) {
+                atomicAdd((ull *)&q->n_started, 1ull);
+                atomicAdd(&q->startup_delay_sum, c.buf.started_at - c.buf.session_start);
+            }
+        }
+        if (finished) atomicAdd((ull *)&q->n_finished, 1ull);
+    }
+
+    __device__ void finish() {
+        stats[OTF_ST_CACHE_CAPACITY] = sc.cache_capacity;
+        stats[OTF_ST_CURRENT_BYTES] = st->cur_bytes;
+        stats[OTF_ST_ENTRIES] = st->entries;
+        stats[OTF_ST_STATUS] = st->status;
+        int64_t *cnt = b.counts + (int64_t)s * 4;
+        cnt[0] = st->n_req; cnt[1] = st->n_sess; cnt[2] = st->n_seg; cnt[3] = st->n_job;
+        b.status[s] = st->status;
+    }
+};
+
+// ---- client-local pieces -------------------------------------------------------
+
+__device__ __forceinline__ void client_init(Client &c) {
+    Client z = {};
+    z.pc = C_START;
+    z.session = -1;
+    z.wait_next = -1;
+    z.buf.started_at = NAN;
+    c = z;
+}
+
+// orchestrator.py:338-340: the client's own pick stream
+__device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
+    uint32_t ent[8];
+    int m = 0;
+    m = push_words(ent, m, S.sc.seed);
+    m = push_words(ent, m, 3u);
+    m = push_words(ent, m, (uint64_t)cid);
+    pcg_seed(c.picks, ent, m);
+}
+
+// orchestrator.py:341-345 + client.py:237-239: pick a sequence, register a report
+__device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double now) {
+    int32_t seq;
+    if (S.sc.popularity == OTF_POP_ZIPF) {
+        double u = pcg_next_double(c.picks);
+        seq = S.sc.n_seq - 1;
+        for (int32_t k = 0; k < S.sc.n_seq; k++)
+            if (u < S.zipf[k]) { seq = k; break; }
+    } else {
+        seq = pcg_integers(c.picks, (uint32_t)S.sc.n_seq);
+    }
+    c.seq = seq;
+    int64_t sid = atomicAdd((unsigned long long *)&S.st->n_sess, 1ull);
+    c.session = (int32_t)sid;
+    c.buf_live = 0;
+    c.sess_open = 1;
+    if (S.records) {
+        if (sid < S.sc.sess_cap) {
+            int64_t o = S.sc.sess_off + sid;
+            S.b.sess_client[o] = cid;
+            S.b.sess_seq[o] = seq;
+            S.b.sess_start[o] = now;
+            S.b.sess_end[o] = 0.0;
+            S.b.sess_stalls[o] = 0;
+            S.b.sess_stall_time[o] = 0.0;
+            S.b.sess_startup[o] = NAN;
+            S.b.sess_flags[o] = 0;
+        } else {
+            S.flag(OTF_S_RECORD_OVERFLOW);
+        }
+    }
+}
+
+// client.py:245-248
+__device__ __forceinline__ void client_start_playback(Client &c, double now) {
+    buf_reset(c.buf, now);
+    c.buf_live = 1;
+    c.has_est = 0;
+    c.est = 0.0;
+    c.rank = 1;
+    c.index = 0;
+}
+
+// client.py:255-256
+__device__ __forceinline__ void client_select(Scn &S, Client &c) {
+    if (c.index > 0)
+        c.rank = select_quality(c.buf.level, c.rank, c.has_est != 0, c.est, S.bitrates, S.sc.n_ranks,
+                                S.sc.panic, S.sc.safe, S.sc.headroom);
+}
+
+// client.py:261-268; returns true when the session has more segments, else
+// leaves the buffer advanced for the final sleep(level) (client.py:270-271).
+__device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
+    double dt = now - c.xfer_start;                       // SegmentFetch.rate_bps
+    double rate = dt > 0 ? ((double)c.size * 8.0) / dt : INFINITY;
+    if (!c.has_est) { c.est = rate; c.has_est = 1; }
+    else c.est = S.sc.alpha * rate + (1.0 - S.sc.alpha) * c.est;
+    double duration = seg_duration(S.seqdur[c.seq], S.segdur[c.seq], c.index);
+    buf_on_segment(c.buf, now, duration, S.sc.startup, S.sc.resume);
+    int64_t g = atomicAdd((unsigned long long *)&S.st->n_seg, 1ull);
+    if (S.records) {
+        if (g < S.sc.seg_cap) {
+            int64_t o = S.sc.seg_off + g;
+            S.b.seg_session[o] = c.session;
+            S.b.seg_index[o] = c.index;
+            S.b.seg_rep[o] = c.rank;
+            S.b.seg_start[o] = c.requested;
+            S.b.seg_end[o] = now;
+        } else {
+            S.flag(OTF_S_RECORD_OVERFLOW);
+        }
+    }
+    atomicAdd((unsigned long long *)&S.q->rank_count[c.rank < OTF_RANK_BINS ? c.rank : OTF_RANK_BINS - 1], 1ull);
+    atomicAdd((unsigned long long *)&S.q->n_segments, 1ull);
+    S.sync_session(c, now);
+    c.index++;
+    if (c.index < S.segcount(c.seq)) return true;
+    buf_advance(c.buf, now);
+    return false;
+}
+
+// client.py:272-280 (+ the finally clause)
+__device__ inline void client_finish_session(Scn &S, Client &c, double now) {
+    buf_advance(c.buf, now);
+    c.buf.phase = PH_FINISHED;
+    if (S.records && c.session < S.sc.sess_cap) S.b.sess_flags[S.sc.sess_off + c.session] |= 1;
+    S.sync_session(c, now);
+    S.qoe_session(c, true);
+    c.buf_live = 0;
+    c.sess_open = 0;
+}
+
+// SessionReport.harvest at the horizon (orchestrator.py:357-359, client.py:177-187)
+__device__ inline void client_harvest(Scn &S, Client &c, double horizon) {
+    if (c.pc == C_HUNG) S.flag(OTF_S_HUNG);
+    if (!c.sess_open) return;
+    if (c.buf_live) {
+        buf_advance(c.buf, horizon);
+        S.sync_session(c, horizon);
+    }
+    S.qoe_session(c, false);
+}
+
+}  // namespace otf

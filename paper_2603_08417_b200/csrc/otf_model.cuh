@@ -1,0 +1,152 @@
+// otf_model.cuh -- per-client model functions shared by both engines.
+//
+// Each function restates one reference function with its exact operation
+// order (the library is compiled with --fmad=false so every double op rounds
+// like CPython's):
+//   completion_time / drain_from  netem.py:77-118
+//   buf_advance / buf_on_segment  client.py:91-121
+//   select_quality                client.py:134-146
+//   segment duration              client.py:264, content.py:214
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "otfgpu.h"
+
+#ifndef OTF_HD
+#define OTF_HD __host__ __device__ __forceinline__
+#endif
+
+namespace otf {
+
+enum { PH_STARTUP = 0, PH_PLAYING = 1, PH_STALLED = 2, PH_FINISHED = 3 };
+
+struct Trace {
+    const double *starts;   // [n]
+    const double *values;   // [n]
+    double period, pbits;
+    int32_t n;
+};
+
+// BandwidthTrace._drain_from (netem.py:77-95)
+OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
+    int32_t lo = 0, hi = tr.n;                 // bisect_right(starts, phase)
+    while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (phase < tr.starts[mid]) hi = mid; else lo = mid + 1;
+    }
+    int32_t i = lo - 1;
+    if (i < 0) i = 0;
+    double spent = 0.0, pos = phase;
+    for (; i < tr.n; i++) {
+        double seg_end = (i + 1 < tr.n) ? tr.starts[i + 1] : tr.period;
+        double width = seg_end - pos;
+        if (width > 0) {
+            double v = tr.values[i];
+            if (v > 0) {
+                if (v * width >= bits) { spent_out = spent + bits / v; left_out = 0.0; return; }
+                bits -= v * width;
+            }
+            spent += width;
+            pos = seg_end;
+        }
+    }
+    spent_out = spent;
+    left_out = bits;
+}
+
+// BandwidthTrace.completion_time for a looping trace (netem.py:97-118)
+OTF_HD double completion_time(const Trace &tr, double start, int64_t nbytes) {
+    double bits = (double)nbytes * 8.0;
+    if (bits <= 0) return start;
+    if (tr.pbits <= 0) return INFINITY;
+    double t = start, spent, left;
+    drain_from(tr, fmod(start, tr.period), bits, spent, left);
+    t += spent;
+    if (left <= 0) return t;
+    double whole = floor(left / tr.pbits);
+    t += whole * tr.period;
+    left -= whole * tr.pbits;
+    if (left <= 0) return t;
+    drain_from(tr, 0.0, left, spent, left);
+    return t + spent;
+}
+
+struct Buffer {
+    double level, position, last_sync, stall_time, started_at, session_start;
+    int32_t phase, stall_events;
+};
+
+// PlayerBuffer.advance (client.py:91-112)
+OTF_HD void buf_advance(Buffer &b, double now) {
+    double dt = now - b.last_sync;
+    b.last_sync = now;
+    if (b.phase == PH_PLAYING) {
+        if (b.level >= dt - 1e-9) {
+            double l = b.level - dt;
+            b.level = (l > 0.0) ? l : 0.0;
+            b.position += dt;
+        } else {
+            double played = b.level;
+            b.position += played;
+            b.level = 0.0;
+            b.phase = PH_STALLED;
+            b.stall_events++;
+            b.stall_time += dt - played;
+        }
+    } else if (b.phase == PH_STALLED) {
+        b.stall_time += dt;
+    }
+}
+
+// PlayerBuffer.on_segment (client.py:114-121)
+OTF_HD void buf_on_segment(Buffer &b, double now, double duration, double startup, double resume) {
+    buf_advance(b, now);
+    b.level += duration;
+    if (b.phase == PH_STARTUP && b.level >= startup) {
+        b.phase = PH_PLAYING;
+        b.started_at = now;
+    } else if (b.phase == PH_STALLED && b.level >= resume) {
+        b.phase = PH_PLAYING;
+    }
+}
+
+OTF_HD void buf_reset(Buffer &b, double now) {
+    b.level = 0.0; b.position = 0.0; b.last_sync = now; b.stall_time = 0.0;
+    b.started_at = NAN; b.session_start = now; b.phase = PH_STARTUP; b.stall_events = 0;
+}
+
+// select_quality (client.py:134-146); bitrates[r-1] is rank r.
+OTF_HD int32_t select_quality(double level, int32_t cur, bool has_est, double est, const int64_t *bitrates,
+                              int32_t top, double panic, double safe, double headroom) {
+    if (level < panic) return 1;
+    if (level < safe) return cur - 1 > 1 ? cur - 1 : 1;
+    if (cur < top && has_est && est >= (double)bitrates[cur] * headroom) return cur + 1;
+    return cur;
+}
+
+// min(segdur, duration - index * segdur)  (client.py:264, content.py:214)
+OTF_HD double seg_duration(double seqdur, double segdur, int32_t index) {
+    double rem = seqdur - (double)index * segdur;
+    return rem < segdur ? rem : segdur;
+}
+
+// Latency histogram bin: 0 = instant (< 10 ms, metrics.py:38,77), then 4 bins
+// per octave with edges ldexp(0.01 * (1 + q/4), o).
+OTF_HD double lat_edge(int k) {   // lower edge of bin 1 + k
+    return ldexp(0.01 * (1.0 + 0.25 * (double)(k & 3)), k >> 2);
+}
+OTF_HD int lat_bin(double lat) {
+    if (lat < 0.010) return 0;
+    int e;
+    frexp(lat / 0.01, &e);                   // estimate, then fix up on the exact edges
+    double r = ldexp(lat / 0.01, -(e - 1));
+    int k = (e - 1) * 4 + (int)((r - 1.0) * 4.0);
+    if (k < 0) k = 0;
+    if (k > OTF_LAT_BINS - 2) k = OTF_LAT_BINS - 2;
+    while (k + 1 <= OTF_LAT_BINS - 2 && lat >= lat_edge(k + 1)) k++;
+    while (k > 0 && lat < lat_edge(k)) k--;
+    return 1 + k;
+}
+
+}  // namespace otf

@@ -1,0 +1,90 @@
+// otf_state.cuh -- per-scenario engine state (lives in the scratch arena).
+#pragma once
+#include <stdint.h>
+
+#include "otf_model.cuh"
+#include "otf_rng.cuh"
+#include "otfgpu.h"
+
+namespace otf {
+
+// Client coroutine program counter: where client_proc/run_session is parked
+// (orchestrator.py:336-348, client.py:229-305, netem.py:133-142).
+enum {
+    C_START = 0,    // spawned; next: sleep(offset)
+    C_ARRIVED,      // woke from the arrival sleep
+    C_SESSION,      // top of `while now < horizon`
+    C_MAN_LAT,      // manifest latency sleep
+    C_MAN_XFER,     // manifest shaped transfer
+    C_INDEX_HEAD,   // top of the per-segment loop
+    C_TARGET_WAIT,  // buffer-full wait (client.py:252-254)
+    C_SEG_LAT,      // request latency sleep -> MediaServer.segment on wake
+    C_SEG_WAIT,     // awaiting a transcode waiter Future
+    C_SEG_RESP,     // response available (windowed engine): record + transfer
+    C_SEG_XFER,     // shaped segment transfer
+    C_PLAYOUT,      // final sleep(level)
+    C_DONE,         // client_proc returned (now >= horizon)
+    C_HUNG          // slept on an infinite delay; never wakes
+};
+
+struct Client {
+    Buffer buf;                 // 56 B
+    double est, requested, arrival, xfer_start;
+    double next_when;           // windowed engine: pending timer time
+    int64_t req_id, size;
+    int32_t pc, seq, session, index, rank, has_est, buf_live, sess_open;
+    int32_t path, desc, wait_next, pad;
+    Pcg64 picks;                // sequence-pick stream SS([seed, 3, cid])
+};
+
+enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE };
+
+struct Worker {
+    int32_t pc, desc, job, pad;
+    int64_t eps_pos;
+};
+
+struct Desc {                   // per (seq, rank, index) descriptor
+    int32_t lru_prev, lru_next; // SegmentCache OrderedDict order (cache.py:27-92)
+    int32_t wq_head, wq_tail;   // in-flight waiter Future callbacks, await order
+    int32_t flags;              // bit0 cached, bit1 in-flight
+};
+enum { D_CACHED = 1, D_INFLIGHT = 2 };
+
+struct Timer {
+    double when;
+    uint32_t tick;
+    int32_t task;
+};
+
+struct ReadyEnt {
+    int32_t task, desc, job, pad;
+};
+
+struct JobEnt {
+    int32_t desc, job;
+};
+
+OTF_HD int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+struct ExactLayout {
+    int64_t state, clients, workers, heap, ready, descs, jobq, getq, total;
+};
+
+OTF_HD ExactLayout exact_layout(int32_t n_clients, int32_t n_workers, int64_t n_desc) {
+    ExactLayout L;
+    int64_t n_tasks = (int64_t)n_clients + n_workers;
+    int64_t o = 0;
+    L.state = o; o += 256;                     // EngineState
+    L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
+    L.workers = o; o += align256((int64_t)sizeof(Worker) * n_workers);
+    L.heap = o;    o += align256((int64_t)sizeof(Timer) * (n_tasks + 1));
+    L.ready = o;   o += align256((int64_t)sizeof(ReadyEnt) * (n_tasks + 1));
+    L.descs = o;   o += align256((int64_t)sizeof(Desc) * n_desc);
+    L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
+    L.getq = o;    o += align256((int64_t)sizeof(int32_t) * n_workers);
+    L.total = o;
+    return L;
+}
+
+}  // namespace otf

@@ -1,0 +1,225 @@
+"""Device driver: uploads a lowered batch, runs the engines, collects results.
+
+This is the body behind the drop-in ``run_experiment`` (orchestrator.py:327-370)
+and the batched sweep entry ``run_batch``.  Torch is used only to own device
+memory and streams; all compute is libotfgpu.so (csrc/).  There is no CPU
+path: without a CUDA device or without the library these functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import _lib
+from .inputs import BatchInputs, build_inputs
+from .results import ExperimentResult
+
+__all__ = ["DeviceBatch", "BatchResult", "run_batch", "run_experiment", "require_cuda"]
+
+_NP = {"i8": np.int64, "i4": np.int32, "f8": np.float64}
+_TORCH = {"i8": torch.int64, "i4": torch.int32, "f8": torch.float64}
+_REC_GROUP = {"req": 0, "sess": 1, "seg": 2, "job": 3}
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.OtfError("no CUDA device: the otfgpu engine has no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise _lib.OtfError(f"otfgpu runs on CUDA devices only, got {dev}")
+    return dev
+
+
+def _u8(ct) -> torch.Tensor:
+    return torch.frombuffer(bytearray(bytes(ct)), dtype=torch.uint8)
+
+
+class DeviceBatch:
+    """One lowered batch resident in HBM, ready to launch (repeatedly)."""
+
+    def __init__(self, inp: BatchInputs, device=None, pin: bool = False):
+        self.inp = inp
+        self.device = require_cuda(device)
+        self.lib = _lib.lib()
+        n = len(inp.lowered)
+        self.n = n
+        dev = self.device
+        self.h_scen = _u8(inp.scenarios)
+        self.h_tables = _u8(inp.size_tables)
+        self.h_f64 = torch.from_numpy(inp.f64)
+        self.h_i64 = torch.from_numpy(inp.i64)
+        self.h_i32 = torch.from_numpy(inp.i32)
+        if pin:
+            self.h_scen, self.h_tables = self.h_scen.pin_memory(), self.h_tables.pin_memory()
+            self.h_f64, self.h_i64, self.h_i32 = self.h_f64.pin_memory(), self.h_i64.pin_memory(), self.h_i32.pin_memory()
+        self.scen = torch.empty_like(self.h_scen, device=dev)
+        self.tables = torch.empty_like(self.h_tables, device=dev)
+        self.f64 = torch.empty_like(self.h_f64, device=dev)
+        self.i64 = torch.empty_like(self.h_i64, device=dev)
+        self.i32 = torch.empty_like(self.h_i32, device=dev)
+        self.scratch = torch.empty(inp.scratch_bytes, dtype=torch.uint8, device=dev)
+        self.rec = {}
+        if inp.mode == _lib.MODE_RECORDS:
+            for name, dt in _lib.RECORD_FIELDS:
+                total = inp.rec_totals[_REC_GROUP[name.split("_")[0]]]
+                self.rec[name] = torch.empty(max(1, total), dtype=_TORCH[dt], device=dev)
+        self.counts = torch.zeros((n, 4), dtype=torch.int64, device=dev)
+        self.stats = torch.zeros((n, _lib.ST_NSLOTS), dtype=torch.int64, device=dev)
+        self.qoe = torch.zeros((n, ctypes.sizeof(_lib.Qoe) // 8), dtype=torch.int64, device=dev)
+        self.status = torch.zeros(n, dtype=torch.int32, device=dev)
+        b = _lib.Batch()
+        b.n_scenarios, b.mode = n, inp.mode
+        b.scenarios, b.f64_pool, b.i64_pool, b.i32_pool = (self.scen.data_ptr(), self.f64.data_ptr(),
+                                                           self.i64.data_ptr(), self.i32.data_ptr())
+        b.scratch = self.scratch.data_ptr()
+        for name, _ in _lib.RECORD_FIELDS:
+            setattr(b, name, self.rec[name].data_ptr() if name in self.rec else None)
+        b.counts, b.stats = self.counts.data_ptr(), self.stats.data_ptr()
+        b.qoe, b.status = self.qoe.data_ptr(), self.status.data_ptr()
+        self.batch = b
+        self.n_tables = sum(1 for t in inp.size_tables if t.n_seq > 0)
+        self.upload()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.h_scen, self.h_tables, self.h_f64, self.h_i64,
+                                                           self.h_i32))
+
+    def upload(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Host -> device copy of every input table (non_blocking when pinned)."""
+        with torch.cuda.stream(stream) if stream is not None else torch.cuda.device(self.device):
+            for d, h in ((self.scen, self.h_scen), (self.tables, self.h_tables), (self.f64, self.h_f64),
+                         (self.i64, self.h_i64), (self.i32, self.h_i32)):
+                d.copy_(h, non_blocking=h.is_pinned())
+
+    def launch(self, stream: torch.cuda.Stream | None = None, sizes: bool = True) -> None:
+        """Enqueue size-table generation + the engine on `stream` (default: current)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if sizes and self.n_tables:
+            rc = self.lib.otf_gen_sizes(self.tables.data_ptr(), self.n_tables, 0, self.i64.data_ptr(),
+                                        self.f64.data_ptr(), self.i32.data_ptr(), s.cuda_stream)
+            _lib.check(rc, "otf_gen_sizes")
+        rc = self.lib.otf_run_batch(ctypes.byref(self.batch), self.inp.engine, s.cuda_stream)
+        _lib.check(rc, "otf_run_batch")
+
+    def fetch(self) -> "BatchResult":
+        torch.cuda.synchronize(self.device)
+        counts = self.counts.cpu().numpy()
+        stats = self.stats.cpu().numpy()
+        status = self.status.cpu().numpy()
+        qoe = self.qoe.cpu().numpy()
+        rec = {k: v.cpu().numpy() for k, v in self.rec.items()}
+        sizes = self.i64.cpu().numpy()
+        return BatchResult(self.inp, counts, stats, status, qoe, rec, sizes)
+
+
+def parse_qoe(row: np.ndarray) -> dict:
+    q = _lib.Qoe.from_buffer_copy(row.tobytes())
+    return {
+        "lat_hist": list(q.lat_hist), "path_count": list(q.path_count), "stall_hist": list(q.stall_hist),
+        "rank_count": list(q.rank_count), "n_requests": q.n_requests, "n_sessions": q.n_sessions,
+        "n_segments": q.n_segments, "n_finished": q.n_finished, "n_started": q.n_started,
+        "latency_sum": q.latency_sum, "stall_time_sum": q.stall_time_sum,
+        "startup_delay_sum": q.startup_delay_sum,
+    }
+
+
+@dataclasses.dataclass
+class BatchResult:
+    inp: BatchInputs
+    counts: np.ndarray
+    stats: np.ndarray
+    status: np.ndarray
+    qoe: np.ndarray
+    rec: dict
+    i64_pool: np.ndarray
+
+    def arrays(self, i: int) -> dict:
+        out = {}
+        for name, _ in _lib.RECORD_FIELDS:
+            g = _REC_GROUP[name.split("_")[0]]
+            off = int(self.inp.rec_offsets[i, g])
+            n = int(min(self.counts[i, g], self.inp.caps[i, g]))
+            out[name] = self.rec[name][off:off + n].copy()
+        return out
+
+    def sizes(self, i: int) -> np.ndarray:
+        sc = self.inp.scenarios[i]
+        n = sc.n_seq * sc.n_ranks * sc.max_nseg
+        return self.i64_pool[sc.off_sizes:sc.off_sizes + n].reshape(sc.n_seq, sc.n_ranks, sc.max_nseg)
+
+    def result(self, i: int) -> ExperimentResult:
+        low = self.inp.lowered[i]
+        return ExperimentResult(low.cfg, self.arrays(i) if self.rec else {}, self.stats[i], low.seq_ids,
+                                sizes=self.sizes(i), seq_dur=low.seq_dur, seq_segdur=low.seq_segdur,
+                                qoe=parse_qoe(self.qoe[i]), status=int(self.status[i]))
+
+    @property
+    def total_requests(self) -> int:
+        return int(self.counts[:, 0].sum())
+
+
+def run_batch(configs, mode: str = "records", engine: str = "windowed", device=None,
+              max_retries: int = 4) -> list[ExperimentResult]:
+    """Run every config on the GPU; returns one ExperimentResult per config.
+
+    Scenarios whose record buffers or noise tables were too small are re-run
+    with exact sizes; scenarios the windowed engine flags with an ordering tie
+    are re-run on the exact engine.
+    """
+    m = _lib.MODE_RECORDS if mode == "records" else _lib.MODE_HISTOGRAM
+    eng = _lib.ENGINE_WINDOWED if engine == "windowed" else _lib.ENGINE_EXACT
+    configs = list(configs)
+    results: list = [None] * len(configs)
+    todo = list(range(len(configs)))
+    caps = {}
+    eps_scale = {}
+    engines = {i: eng for i in todo}
+    for _attempt in range(max_retries + 1):
+        if not todo:
+            break
+        groups = {}
+        for i in todo:
+            groups.setdefault((engines[i], eps_scale.get(i, 1)), []).append(i)
+        nxt = []
+        for (e, es), idx in groups.items():
+            cap_list = [caps[i] if i in caps else None for i in idx]
+            use_caps = None
+            if any(c is not None for c in cap_list):
+                inp0 = build_inputs([configs[i] for i in idx], engine=e, mode=m, eps_scale=es)
+                use_caps = [c if c is not None else tuple(inp0.caps[k]) for k, c in enumerate(cap_list)]
+            inp = build_inputs([configs[i] for i in idx], engine=e, mode=m, caps=use_caps, eps_scale=es)
+            db = DeviceBatch(inp, device)
+            db.launch()
+            br = db.fetch()
+            for k, i in enumerate(idx):
+                st = int(br.status[k])
+                if st & _lib.S_INTERNAL:
+                    raise _lib.OtfError(f"scenario {i}: engine invariant violated (status {st:#x})")
+                retry = False
+                if st & _lib.S_TIE:
+                    engines[i] = _lib.ENGINE_EXACT
+                    retry = True
+                if st & _lib.S_EPS_OVERFLOW:
+                    eps_scale[i] = eps_scale.get(i, 1) * 4
+                    retry = True
+                if st & _lib.S_RECORD_OVERFLOW:
+                    caps[i] = tuple(int(x) + 1 for x in br.counts[k])
+                    retry = True
+                if retry:
+                    nxt.append(i)
+                else:
+                    results[i] = br.result(k)
+        todo = nxt
+    if todo:
+        raise _lib.OtfError(f"scenarios {todo} did not converge after {max_retries} retries")
+    return results
+
+
+def run_experiment(config) -> ExperimentResult:
+    """Drop-in for otfstream.orchestrator.run_experiment (orchestrator.py:327-370)."""
+    return run_batch([config], mode="records")[0]

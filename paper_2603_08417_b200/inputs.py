@@ -1,0 +1,306 @@
+"""Host input builder: lowers ExperimentConfigs to otf_scenario structs + shared pools.
+
+Everything a scenario reads is derived here from the reference's own seeded
+streams, drawn with numpy exactly where the reference draws them:
+
+* arrival offsets  list(np.cumsum(exponential(1/rate, N)))  SS([seed, 1])   orchestrator.py:265-268
+* trace normals    standard_normal per client               SS([seed, 2, c]) orchestrator.py:254-263
+                   -> values/period-bits in C++ (glibc exp, CPython 3.12 sum)  netem.py:39-64,179-202
+* worker noise     normal(0, noise) per worker              SS([seed, w])    transcode.py:89-99
+* sequence keys    sha256(id)[:8] big-endian                                  content.py:165-166
+* manifest bytes   len(json.dumps(manifest_for(seq), sort_keys=True))         server.py:58-59
+
+Segment sizes and per-session sequence picks are generated on the device
+(csrc/otf_tables.cu, csrc/otf_rng.cuh).  Tables are de-duplicated across the
+batch: traces by (seed, netem), sizes by catalog, arrivals by (seed, N, rate),
+noise by (seed, noise), so a sweep over variants / cache sizes / client counts
+pays for each stream once.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import hashlib
+import json
+import math
+import os
+import statistics
+
+import numpy as np
+
+from . import _lib
+from .config import ExperimentConfig, ConfigError
+
+__all__ = ["BatchInputs", "build_inputs", "zipf_cdf", "sample_times"]
+
+URL_TEMPLATE = "/content/{seq}/{rep}/{index}"
+
+
+def _gen(entropy):
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy)))
+
+
+def zipf_cdf(n: int, s: float) -> np.ndarray:
+    """Normalised cumulative Zipf(s) weights over catalog ranks 1..n (extension)."""
+    w = [float(k) ** (-s) for k in range(1, n + 1)]
+    acc, c = 0.0, []
+    for x in w:
+        acc += x
+        c.append(acc)
+    return np.array([x / acc for x in c], dtype=np.float64)
+
+
+def sample_times(duration: float, step: float) -> list[float]:
+    """synthetic_trace's timestamps: t = 0; while t < duration: t += step (netem.py:195-201)."""
+    ts, t = [], 0.0
+    while t < duration:
+        ts.append(t)
+        t += step
+    return ts
+
+
+@dataclasses.dataclass
+class Lowered:
+    cfg: ExperimentConfig
+    seq_ids: list[str]
+    seq_dur: list[float]
+    seq_segdur: list[float]
+    counts: list[int]
+    n_ranks: int
+    stored: list[int]
+    cache_enabled: bool
+    spec_enabled: bool
+
+
+def lower(cfg: ExperimentConfig) -> Lowered:
+    cfg.validate()
+    cat = cfg.catalog_config()
+    policy = cfg.policy()
+    seqs = cat.sequences
+    return Lowered(
+        cfg=cfg,
+        seq_ids=[s.id for s in seqs],
+        seq_dur=[s.duration_s for s in seqs],
+        seq_segdur=[s.segment_duration_s for s in seqs],
+        counts=[math.ceil(s.duration_s / s.segment_duration_s) for s in seqs],
+        n_ranks=len(cfg.ladder),
+        stored=list(cat.stored_ranks),
+        cache_enabled=policy.cache_enabled,
+        spec_enabled=policy.speculative_enabled,
+    )
+
+
+class _Pools:
+    def __init__(self):
+        self.parts = {"f64": [], "i64": [], "i32": []}
+        self.size = {"f64": 0, "i64": 0, "i32": 0}
+        self.memo = {}
+
+    def add(self, kind: str, arr, key=None) -> int:
+        if key is not None and (kind, key) in self.memo:
+            return self.memo[(kind, key)]
+        dt = {"f64": np.float64, "i64": np.int64, "i32": np.int32}[kind]
+        a = np.ascontiguousarray(np.asarray(arr, dtype=dt).reshape(-1))
+        off = self.size[kind]
+        self.parts[kind].append(a)
+        self.size[kind] += a.size
+        if key is not None:
+            self.memo[(kind, key)] = off
+        return off
+
+    def reserve(self, kind: str, n: int, key=None) -> int:
+        return self.add(kind, np.zeros(n), key)
+
+    def concat(self, kind: str) -> np.ndarray:
+        dt = {"f64": np.float64, "i64": np.int64, "i32": np.int32}[kind]
+        if not self.parts[kind]:
+            return np.zeros(1, dtype=dt)
+        return np.concatenate(self.parts[kind])
+
+
+@dataclasses.dataclass
+class BatchInputs:
+    lowered: list[Lowered]
+    scenarios: ctypes.Array
+    size_tables: ctypes.Array
+    f64: np.ndarray
+    i64: np.ndarray
+    i32: np.ndarray
+    scratch_bytes: int
+    caps: np.ndarray            # [n][4] record capacities (req, sess, seg, job)
+    rec_offsets: np.ndarray     # [n][4]
+    rec_totals: list[int]       # pool lengths (req, sess, seg, job)
+    engine: int
+    mode: int
+    input_bytes: int            # algorithmic input bytes (for the roofline)
+
+
+def _default_caps(low: Lowered) -> tuple[int, int, int, int]:
+    cfg = low.cfg
+    per_client = cfg.horizon_s / max(min(low.seq_segdur), 1e-3)
+    req = int(cfg.clients * per_client * 1.25) + 256
+    return req, req + cfg.clients, req, 2 * req + 64
+
+
+def _eps_len(low: Lowered) -> int:
+    cfg = low.cfg
+    rho = cfg.per_rank_rho or {r: cfg.rho for r, _ in cfg.ladder}
+    min_dur = min(min(low.seq_segdur[i], low.seq_dur[i] - (low.counts[i] - 1) * low.seq_segdur[i])
+                  for i in range(len(low.seq_ids)))
+    floor = max(1.0 - 8.0 * cfg.noise_rel_std, 0.05)
+    min_svc = max(min(rho.values()) * min_dur * floor, 1e-6)
+    return int(min(cfg.horizon_s / min_svc + 64, 1 << 26))
+
+
+def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.MODE_RECORDS,
+                 caps=None, eps_scale: int = 1, threads: int | None = None) -> BatchInputs:
+    """Lower a list of ExperimentConfigs into one device batch (host arrays)."""
+    L = _lib.lib()
+    threads = threads or os.cpu_count() or 1
+    lows = [lower(ExperimentConfig.from_reference(c)) for c in configs]
+    P = _Pools()
+    scen = (_lib.Scenario * max(1, len(lows)))()
+    tables = []
+    scratch_off = 0
+    cap_arr = np.zeros((len(lows), 4), dtype=np.int64)
+    rec_off = np.zeros((len(lows), 4), dtype=np.int64)
+    totals = [0, 0, 0, 0]
+    input_bytes = 0
+
+    # -- traces: one table per (seed, netem), long enough for the largest N --
+    trace_groups: dict = {}
+    for low in lows:
+        key = (low.cfg.seed, dataclasses.astuple(low.cfg.netem))
+        prev = trace_groups.get(key, (0, low.cfg.netem))[0]
+        trace_groups[key] = (max(prev, low.cfg.clients), low.cfg.netem)
+    trace_tab = {}
+    for key, (nmax, ne) in trace_groups.items():
+        seed = key[0]
+        ts = sample_times(ne.trace_duration_s, ne.step_s)
+        if not ts:
+            raise ConfigError("trace has no samples")
+        gaps = [b - a for a, b in zip(ts, ts[1:])]
+        period = ts[-1] + (statistics.median(gaps) if gaps else 1.0)
+        starts = list(ts)
+        n = len(ts)
+        normals = np.empty((nmax, n + 1), dtype=np.float64)
+        for c in range(nmax):
+            normals[c] = _gen([seed, 2, c]).standard_normal(n + 1)
+        values = np.empty((nmax, n), dtype=np.float64)
+        pbits = np.empty(nmax, dtype=np.float64)
+        starts_a = np.asarray(starts, dtype=np.float64)
+        decay = math.exp(-ne.theta_per_s * ne.step_s)
+        spread = ne.sigma * math.sqrt(1.0 - decay * decay)
+        dp = ctypes.POINTER(ctypes.c_double)
+        rc = L.otf_build_traces(nmax, n, normals.ctypes.data_as(dp), starts_a.ctypes.data_as(dp), period,
+                                math.log(ne.median_bps), ne.sigma, decay, spread, ne.floor_bps, ne.cap_bps,
+                                values.ctypes.data_as(dp), pbits.ctypes.data_as(dp), threads)
+        _lib.check(rc, "otf_build_traces")
+        trace_tab[key] = dict(n=n, period=period,
+                              starts=P.add("f64", starts_a), values=P.add("f64", values),
+                              pbits=P.add("f64", pbits))
+        input_bytes += values.nbytes + pbits.nbytes + starts_a.nbytes
+
+    # -- worker noise: one table per (seed, noise), longest draw count --
+    eps_groups: dict = {}
+    for low in lows:
+        key = (low.cfg.seed, low.cfg.noise_rel_std)
+        k, e = eps_groups.get(key, (0, 0))
+        eps_groups[key] = (max(k, low.cfg.workers), max(e, _eps_len(low) * eps_scale))
+    eps_tab = {}
+    for (seed, noise), (kmax, elen) in eps_groups.items():
+        if noise > 0:
+            eps = np.stack([_gen([seed, w]).normal(0.0, noise, size=elen) for w in range(kmax)])
+        else:
+            eps = np.zeros((kmax, 1))
+        eps_tab[(seed, noise)] = (P.add("f64", eps), eps.shape[1])
+
+    for si, low in enumerate(lows):
+        cfg = low.cfg
+        N, K = cfg.clients, cfg.workers
+        n_seq, n_ranks = len(low.seq_ids), low.n_ranks
+        max_nseg = max(low.counts)
+        ladder = sorted(cfg.ladder)
+        cat_key = (cfg.seed, cfg.size_jitter, tuple(low.seq_ids), tuple(low.seq_dur), tuple(low.seq_segdur),
+                   tuple(ladder))
+        keys = [int.from_bytes(hashlib.sha256(s.encode("utf-8")).digest()[:8], "big") for s in low.seq_ids]
+        o_bitrates = P.add("i64", [b for _, b in ladder], key=("bitrates", tuple(ladder)))
+        o_keys = P.add("i64", np.array(keys, dtype=np.uint64).view(np.int64), key=("keys", tuple(low.seq_ids)))
+        o_seqdur = P.add("f64", low.seq_dur, key=("seqdur", cat_key))
+        o_segdur = P.add("f64", low.seq_segdur, key=("segdur", cat_key))
+        o_counts = P.add("i32", low.counts, key=("counts", cat_key))
+        if ("i64", ("sizes", cat_key)) not in P.memo:
+            o_sizes = P.reserve("i64", n_seq * n_ranks * max_nseg, key=("sizes", cat_key))
+            t = _lib.SizeTable()
+            t.n_seq, t.n_ranks, t.max_nseg = n_seq, n_ranks, max_nseg
+            t.seed, t.size_jitter = cfg.seed, cfg.size_jitter
+            t.off_out, t.off_keys, t.off_bitrates = o_sizes, o_keys, o_bitrates
+            t.off_seqdur, t.off_segdur, t.off_segcount = o_seqdur, o_segdur, o_counts
+            tables.append(t)
+            input_bytes += 8 * n_seq * n_ranks * max_nseg
+        o_sizes = P.memo[("i64", ("sizes", cat_key))]
+        man = []
+        for sid, dur, segdur, cnt in zip(low.seq_ids, low.seq_dur, low.seq_segdur, low.counts):
+            m = {"sequence": sid, "duration_s": dur, "segment_duration_s": segdur, "segment_count": cnt,
+                 "representations": [{"rank": r, "bitrate_bps": b} for r, b in ladder],
+                 "url_template": URL_TEMPLATE}
+            man.append(len(json.dumps(m, sort_keys=True).encode("utf-8")))   # server.py:58-59
+        o_man = P.add("i64", man, key=("manifest", cat_key))
+        rho_map = cfg.per_rank_rho or {r: cfg.rho for r, _ in ladder}
+        o_rho = P.add("f64", [float(rho_map[r]) for r, _ in ladder], key=("rho", tuple(sorted(rho_map.items()))))
+        pop = 1 if cfg.popularity == "zipf" else 0
+        o_zipf = P.add("f64", zipf_cdf(n_seq, cfg.zipf_exponent) if pop else np.zeros(n_seq),
+                       key=("zipf", n_seq, pop, cfg.zipf_exponent))
+        akey = ("arrivals", cfg.seed, N, cfg.arrival_rate_per_s)
+        if ("f64", akey) not in P.memo:
+            draws = _gen([cfg.seed, 1]).exponential(1.0 / cfg.arrival_rate_per_s, size=N)
+            P.add("f64", np.cumsum(draws), key=akey)                            # sequential cumsum
+            input_bytes += 8 * N
+        o_arr = P.memo[("f64", akey)]
+        tt = trace_tab[(cfg.seed, dataclasses.astuple(cfg.netem))]
+        o_eps, eps_stride = eps_tab[(cfg.seed, cfg.noise_rel_std)]
+
+        sc = scen[si]
+        sc.n_clients, sc.n_workers, sc.n_seq, sc.n_ranks = N, K, n_seq, n_ranks
+        sc.max_nseg, sc.n_samples = max_nseg, tt["n"]
+        sc.cache_enabled, sc.spec_enabled = int(low.cache_enabled), int(low.spec_enabled)
+        sc.popularity = pop
+        sc.stored_mask = sum(1 << r for r in low.stored)
+        sc.cache_capacity = int(cfg.cache_capacity_bytes)
+        sc.seed = cfg.seed
+        sc.horizon = float(cfg.horizon_s)
+        sc.latency = float(cfg.client.latency_s)
+        b = cfg.client.buffer
+        sc.target, sc.safe, sc.panic, sc.resume, sc.startup = b.target_s, b.safe_s, b.panic_s, b.resume_s, b.startup_s
+        sc.alpha, sc.headroom = float(cfg.client.ewma_alpha), float(cfg.client.headroom)
+        sc.noise = float(cfg.noise_rel_std)
+        sc.period = tt["period"]
+        sc.off_sizes, sc.off_bitrates, sc.off_manifest, sc.off_segcount = o_sizes, o_bitrates, o_man, o_counts
+        sc.off_seqdur, sc.off_segdur, sc.off_rho, sc.off_zipf = o_seqdur, o_segdur, o_rho, o_zipf
+        sc.off_starts, sc.off_values, sc.off_pbits = tt["starts"], tt["values"], tt["pbits"]
+        sc.off_arrivals = o_arr
+        sc.off_eps, sc.eps_stride = o_eps, eps_stride
+        sc.scratch_off = scratch_off
+        scratch_off += int(L.otf_scratch_bytes(engine, N, K, n_seq, n_ranks, max_nseg))
+        scratch_off = (scratch_off + 255) & ~255
+        if mode == _lib.MODE_RECORDS:
+            c = caps[si] if caps is not None else _default_caps(low)
+            cap_arr[si] = c
+            for k in range(4):
+                rec_off[si, k] = totals[k]
+                totals[k] += int(c[k])
+            sc.req_off, sc.req_cap = int(rec_off[si, 0]), int(c[0])
+            sc.sess_off, sc.sess_cap = int(rec_off[si, 1]), int(c[1])
+            sc.seg_off, sc.seg_cap = int(rec_off[si, 2]), int(c[2])
+            sc.job_off, sc.job_cap = int(rec_off[si, 3]), int(c[3])
+
+    return BatchInputs(
+        lowered=lows, scenarios=scen, size_tables=(_lib.SizeTable * max(1, len(tables)))(*tables),
+        f64=P.concat("f64"), i64=P.concat("i64"), i32=P.concat("i32"),
+        scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
+        engine=engine, mode=mode, input_bytes=input_bytes)
+
+
+def n_size_tables(inp: BatchInputs) -> int:
+    return sum(1 for t in inp.size_tables if t.n_seq > 0)

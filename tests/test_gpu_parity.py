@@ -1,0 +1,149 @@
+"""GPU parity: libotfgpu.so vs the reference's golden outputs and the C oracle.
+
+Every test calls through the C ABI (paper_2603_08417_b200 -> ctypes ->
+libotfgpu.so).  Discrete fields must match exactly; float fields are compared
+bit-for-bit (the engine keeps the reference's operation order with FMA
+contraction disabled) -- the north star's bar is <= 1e-6 relative, bit-exact
+is what is asserted.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2603_08417_b200 import _lib, engine, inputs, workloads
+from paper_2603_08417_b200.config import ExperimentConfig
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(meta):
+    cfg = ExperimentConfig.from_dict(meta["config"])
+    cfg.popularity = meta["popularity"]
+    cfg.zipf_exponent = meta["zipf_exponent"]
+    return cfg
+
+
+def _assert_parity(res, want, stats_want=None):
+    errs = parity.compare(res.arrays, want)
+    assert not errs, "\n".join(errs[:20])
+    if stats_want is not None:
+        errs = parity.compare_stats(res.backend_stats, stats_want)
+        assert not errs, "\n".join(errs)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return {n: parity.load_golden(n) for n in parity.golden_names()}
+
+
+def test_size_tables_match_oracle(golden):
+    cfgs = [_cfg(m) for _, m in golden.values()]
+    inp = inputs.build_inputs(cfgs, mode=_lib.MODE_HISTOGRAM, engine=_lib.ENGINE_EXACT)
+    db = engine.DeviceBatch(inp)
+    db.launch()
+    br = db.fetch()
+    for i, cfg in enumerate(cfgs):
+        want, _ = oracle.Prepared(cfg).sizes()
+        assert np.array_equal(br.sizes(i), want), cfg
+
+
+@pytest.mark.parametrize("eng", ["exact", "windowed"])
+def test_golden_parity_batched(golden, eng):
+    """All golden configs in ONE launch, each bit-exact vs the reference."""
+    names = sorted(golden)
+    cfgs = [_cfg(golden[n][1]) for n in names]
+    results = engine.run_batch(cfgs, mode="records", engine=eng)
+    for n, res in zip(names, results):
+        want, meta = golden[n]
+        _assert_parity(res, want, meta["backend_stats"])
+
+
+def test_summary_matches_reference(golden):
+    names = ["c1_seed1", "grid_c24_k4_t2_TCPF", "c3_f05_h90"]
+    results = engine.run_batch([_cfg(golden[n][1]) for n in names], mode="records")
+    for n, res in zip(names, results):
+        want = golden[n][1]["summary"]
+        got = res.summary()
+        for k in ("requests", "sessions", "jobs", "instant_fraction", "latency_p50_s", "latency_p99_s",
+                  "stalls_mean", "stall_time_total_s", "mean_rank", "quality_fractions", "variant"):
+            assert got.get(k) == want.get(k), (n, k, got.get(k), want.get(k))
+
+
+def test_run_experiment_dropin_objects(golden):
+    want, meta = golden["grid_c24_k4_t2_TCP"]
+    res = engine.run_experiment(_cfg(meta))
+    assert len(res.requests) == len(want["req_id"])
+    r0 = res.requests[0]
+    assert r0.path in ("storage", "cache", "waited_inflight", "transcoded")
+    assert res.jobs[0].origin in ("demand", "speculative")
+    assert sum(len(s.segments) for s in res.sessions) == len(want["seg_index"])
+
+
+def _oracle_cmp(cfgs, eng="windowed"):
+    results = engine.run_batch(cfgs, mode="records", engine=eng)
+    for cfg, res in zip(cfgs, results):
+        ref = oracle.run(cfg)
+        errs = parity.compare(res.arrays, ref)
+        assert not errs, (cfg, errs[:10])
+        errs = parity.compare_stats(res.backend_stats, oracle.backend_stats(ref, "C" in cfg.variant))
+        assert not errs, errs
+    return results
+
+
+def test_config2_full_horizon_vs_oracle():
+    """BASELINE config 2 at full size (100 clients, 600 s) over several seeds."""
+    _oracle_cmp([workloads.c2(seed=s) for s in (1, 2, 3)])
+
+
+def test_config3_cache_sweep_vs_oracle():
+    """BASELINE config 3: cache fraction 0..1 in 0.1 steps (one launch)."""
+    _oracle_cmp([workloads.c3(seed=5, fraction=f / 10) for f in range(11)])
+
+
+def test_config1_seeds_vs_oracle():
+    _oracle_cmp([workloads.c1(seed=s) for s in range(1, 9)])
+
+
+def test_config4_points_vs_oracle():
+    """BASELINE config 4 sample points (client-count sweep x variants)."""
+    cfgs = [workloads.c4(seed=s, clients=n, variant=v)
+            for (s, n, v) in [(1, 10, "B"), (2, 30, "T"), (3, 100, "TC"), (4, 300, "TCP"), (5, 30, "TCF"),
+                              (6, 100, "TCPF")]]
+    _oracle_cmp(cfgs)
+
+
+def test_config5_point_vs_oracle():
+    """BASELINE config 5 (10-rank ladder) at reduced client count and horizon."""
+    _oracle_cmp([workloads.c5(seed=s, clients=400, horizon_s=120.0, variant=v)
+                 for s, v in [(1, "TCPF"), (2, "TCP")]])
+
+
+def test_histogram_mode_matches_records():
+    cfgs = [workloads.c3(seed=7, fraction=f) for f in (0.0, 0.3, 1.0)] + [workloads.c1(seed=3)]
+    rec = engine.run_batch(cfgs, mode="records")
+    hist = engine.run_batch(cfgs, mode="histogram")
+    for r, h in zip(rec, hist):
+        a = r.arrays
+        q = h.qoe
+        assert q["n_requests"] == len(a["req_id"])
+        assert q["n_sessions"] == len(a["sess_client"])
+        assert q["n_segments"] == len(a["seg_index"])
+        assert q["path_count"] == [int((a["req_path"] == p).sum()) for p in range(4)]
+        lat = a["req_response"] - a["req_arrival"]
+        assert q["lat_hist"][0] == int((lat < 0.010).sum())
+        assert sum(q["lat_hist"]) == len(lat)
+        ranks = np.bincount(a["seg_rep"], minlength=16)[:16]
+        assert q["rank_count"] == list(ranks)
+        stalls = np.minimum(a["sess_stalls"], 31)
+        assert q["stall_hist"] == list(np.bincount(stalls, minlength=32))
+        assert q["stall_time_sum"] == pytest.approx(float(a["sess_stall_time"].sum()), rel=1e-9, abs=1e-9)
+        assert np.array_equal(r.stats_raw[:18], h.stats_raw[:18])
+
+
+def test_no_cpu_fallback_without_library(monkeypatch):
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libotfgpu.so")
+    with pytest.raises(_lib.OtfError):
+        engine.run_experiment(workloads.c1())

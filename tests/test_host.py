@@ -1,0 +1,157 @@
+"""CPU-side tests: the C ABI loads and exports its symbols, the host input
+builder reproduces the reference's input streams, config parity."""
+
+import ctypes
+import json
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2603_08417_b200 import _lib, inputs, workloads
+from paper_2603_08417_b200.config import ConfigError, ExperimentConfig, scenario_matrix
+from tests import parity
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    header = open(os.path.join(ROOT, "include", "otfgpu.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|int64_t|size_t|const char \*)\s*\*?\s*(otf_\w+)\s*\(", header, re.M))
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.otf_version() == _lib.ABI_VERSION
+
+
+def test_struct_layouts_match_c():
+    L = _lib.lib()
+    assert L.otf_sizeof_scenario() == ctypes.sizeof(_lib.Scenario)
+    assert L.otf_sizeof_batch() == ctypes.sizeof(_lib.Batch)
+    assert L.otf_sizeof_qoe() == ctypes.sizeof(_lib.Qoe)
+
+
+def test_run_batch_rejects_bad_arguments():
+    L = _lib.lib()
+    b = _lib.Batch()
+    b.n_scenarios = 1
+    rc = L.otf_run_batch(ctypes.byref(b), 0, None)
+    assert rc == 1
+    assert b"missing device buffer" in L.otf_last_error()
+    assert L.otf_run_batch(None, 0, None) == 1
+
+
+def test_scratch_bytes_positive():
+    L = _lib.lib()
+    for eng in (0, 1):
+        assert L.otf_scratch_bytes(eng, 100, 4, 50, 5, 10) > 100 * 64
+
+
+@pytest.mark.parametrize("name", ["c1_seed1", "c2_seed1_h120", "edge_partial_seg"])
+def test_traces_match_oracle(name):
+    """otf_build_traces (C++, glibc exp, 3.12 sum) == oracle traces (which match the reference)."""
+    _, meta = parity.load_golden(name)
+    cfg = ExperimentConfig.from_dict(meta["config"])
+    cfg.popularity = meta["popularity"]
+    inp = inputs.build_inputs([cfg], mode=_lib.MODE_HISTOGRAM)
+    sc = inp.scenarios[0]
+    prep = oracle.Prepared(cfg)
+    starts, values, pbits, period = prep.traces()
+    n = sc.n_samples
+    got_vals = inp.f64[sc.off_values:sc.off_values + cfg.clients * n].reshape(cfg.clients, n)
+    got_pbits = inp.f64[sc.off_pbits:sc.off_pbits + cfg.clients]
+    assert sc.period == period
+    assert np.array_equal(inp.f64[sc.off_starts:sc.off_starts + n], starts)
+    assert np.array_equal(got_vals.view(np.int64), values.view(np.int64))
+    assert np.array_equal(got_pbits.view(np.int64), pbits.view(np.int64))
+
+
+def test_traces_match_reference_semantics():
+    """Spot-check a trace against a pure-Python restatement of synthetic_trace."""
+    cfg = ExperimentConfig(seed=42, clients=3)
+    inp = inputs.build_inputs([cfg], mode=_lib.MODE_HISTOGRAM)
+    sc = inp.scenarios[0]
+    n = sc.n_samples
+    for c in range(3):
+        rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([42, 2, c])))
+        mu = math.log(17e6)
+        decay = math.exp(-0.08)
+        spread = 0.35 * math.sqrt(1.0 - decay * decay)
+        x = mu + 0.35 * rng.standard_normal()
+        vals = []
+        t = 0.0
+        while t < 600.0:
+            vals.append(min(max(math.exp(x), 2e6), 400e6))
+            x = mu + (x - mu) * decay + spread * rng.standard_normal()
+            t += 1.0
+        got = inp.f64[sc.off_values + c * n: sc.off_values + (c + 1) * n]
+        assert list(got) == vals
+        pb = sum(v * 1.0 for v in vals)
+        assert inp.f64[sc.off_pbits + c] == pb
+
+
+def test_arrivals_and_manifest_bytes():
+    cfg = workloads.c2(seed=3)
+    inp = inputs.build_inputs([cfg], mode=_lib.MODE_HISTOGRAM)
+    sc = inp.scenarios[0]
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([3, 1])))
+    want = list(np.cumsum(rng.exponential(1.0 / cfg.arrival_rate_per_s, size=cfg.clients)))
+    assert list(inp.f64[sc.off_arrivals:sc.off_arrivals + cfg.clients]) == want
+    prep = oracle.Prepared(cfg)
+    assert list(inp.i64[sc.off_manifest:sc.off_manifest + sc.n_seq]) == list(prep.manifest_bytes)
+
+
+def test_pool_dedup_across_sweep():
+    cfgs = [workloads.c3(seed=1, fraction=f / 10) for f in range(11)]
+    inp = inputs.build_inputs(cfgs, mode=_lib.MODE_HISTOGRAM)
+    offs = {inp.scenarios[i].off_values for i in range(11)}
+    assert len(offs) == 1          # one trace table for the whole cache sweep
+    caps = [inp.scenarios[i].cache_capacity for i in range(11)]
+    assert caps[0] == 1 and caps == sorted(caps)
+
+
+def test_config_roundtrip_and_fingerprint():
+    cfg = ExperimentConfig(variant="TCPF", clients=24, seed=3)
+    assert ExperimentConfig.from_dict(cfg.to_dict()) == cfg
+    z = workloads.c2()
+    d = z.to_dict()
+    assert d["experiment"]["popularity"] == "zipf"
+    assert ExperimentConfig.from_dict(d).popularity == "zipf"
+    # reference-expressible configs carry no extension keys (fingerprint unchanged)
+    assert "popularity" not in ExperimentConfig().to_dict()["experiment"]
+
+
+def test_fingerprint_matches_reference_golden():
+    from paper_2603_08417_b200.results import fingerprint
+    for name in parity.golden_names():
+        _, meta = parity.load_golden(name)
+        if meta["popularity"] == "uniform":
+            assert fingerprint(ExperimentConfig.from_dict(meta["config"]).to_dict()) == meta["fingerprint"]
+
+
+def test_validation_errors():
+    with pytest.raises(ConfigError):
+        ExperimentConfig(variant="TP")
+    with pytest.raises(ConfigError):
+        ExperimentConfig(clients=0)
+    with pytest.raises(ValueError):
+        ExperimentConfig(variant="TC", cache_capacity_bytes=0).validate()
+    with pytest.raises(ConfigError):
+        ExperimentConfig(ladder=[(1, 5), (2, 3)]).validate()
+
+
+def test_scenario_matrix_grid():
+    grid = scenario_matrix(ExperimentConfig())
+    assert len(grid) == 72
+    assert grid[0][0] == "c04_n1_t2_B"
+    assert {c.workers for _, c in grid} == {4, 8}
+
+
+def test_c5_sweep_shape():
+    sweep = workloads.c5_sweep(seeds=range(1, 3))
+    assert len(sweep) == 2 * 16
+    assert all(len(c.ladder) == 10 for c in sweep)

@@ -1,0 +1,29 @@
+"""Timing probe for engine calibration (not part of the product)."""
+import sys, time, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2603_08417_b200 import engine, inputs, workloads, _lib
+
+def timeit(name, cfgs, eng, reps=2):
+    t0 = time.time()
+    inp = inputs.build_inputs(cfgs, engine=eng, mode=_lib.MODE_HISTOGRAM)
+    t1 = time.time()
+    db = engine.DeviceBatch(inp)
+    db.launch(); torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); db.launch(); e1.record(); torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    br = db.fetch()
+    req = br.total_requests
+    print(json.dumps(dict(name=name, engine=eng, scenarios=len(cfgs), build_s=round(t1-t0,2), ms=round(best,2),
+                          requests=req, req_per_s=req/(best/1e3), status=int(br.status.max()))), flush=True)
+
+which = sys.argv[1:] or ["c1", "c2", "c5s"]
+for w in which:
+    if w == "c1": timeit("c1x64", [workloads.c1(seed=s) for s in range(1, 65)], 0)
+    if w == "c2": timeit("c2x64", [workloads.c2(seed=s) for s in range(1, 65)], 0)
+    if w == "c2w": timeit("c2x64", [workloads.c2(seed=s) for s in range(1, 65)], 1)
+    if w == "c5s": timeit("c5x8_h60", [workloads.c5(seed=s, horizon_s=60.0) for s in range(1, 9)], 0, reps=1)
+    if w == "c5": timeit("c5x64", workloads.c5_sweep(seeds=range(1, 5)), 0, reps=1)
