@@ -137,6 +137,9 @@ typedef struct otf_batch {
     int64_t *stats;                   /* [n_scenarios][OTF_ST_NSLOTS] */
     otf_qoe *qoe;                     /* [n_scenarios] */
     int32_t *status;                  /* [n_scenarios] OTF_S_* bits */
+    const int32_t *order;             /* optional launch order (longest first), NULL = identity */
+    int64_t shared_bytes;             /* windowed engine: dynamic shared memory per scenario
+                                         (max of otf_shared_bytes over the batch) */
 } otf_batch;
 
 /* A segment-size table: Catalog.descriptor sizes (content.py:204-218) for one
@@ -161,6 +164,10 @@ size_t otf_sizeof_qoe(void);
 /* Engine scratch bytes for one scenario (host-side layout helper). */
 int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
                           int32_t n_ranks, int32_t max_nseg);
+
+/* Per-scenario dynamic shared memory of the windowed engine (host-side helper). */
+int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
+                         int32_t n_ranks, int32_t max_nseg);
 
 /* HOST function: synthetic traces (netem.py:179-202) + BandwidthTrace period
  * bits (netem.py:39-64) from numpy's standard-normal draws.  normals is

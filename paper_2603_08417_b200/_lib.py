@@ -81,7 +81,8 @@ class Batch(ctypes.Structure):
     _fields_ = ([("n_scenarios", _i32), ("mode", _i32), ("scenarios", _vp), ("f64_pool", _vp),
                  ("i64_pool", _vp), ("i32_pool", _vp), ("scratch", _vp)]
                 + [(n, _vp) for n, _ in RECORD_FIELDS]
-                + [("counts", _vp), ("stats", _vp), ("qoe", _vp), ("status", _vp)])
+                + [("counts", _vp), ("stats", _vp), ("qoe", _vp), ("status", _vp), ("order", _vp),
+                   ("shared_bytes", _i64)])
 
 
 class SizeTable(ctypes.Structure):
@@ -94,7 +95,7 @@ class SizeTable(ctypes.Structure):
 
 
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
-           "otf_scratch_bytes", "otf_build_traces", "otf_gen_sizes", "otf_run_batch")
+           "otf_scratch_bytes", "otf_shared_bytes", "otf_build_traces", "otf_gen_sizes", "otf_run_batch")
 
 
 class OtfError(RuntimeError):
@@ -128,6 +129,8 @@ def lib():
         getattr(L, f).restype = ctypes.c_size_t
     L.otf_scratch_bytes.restype = _i64
     L.otf_scratch_bytes.argtypes = [_i32] * 6
+    L.otf_shared_bytes.restype = _i64
+    L.otf_shared_bytes.argtypes = [_i32] * 6
     L.otf_build_traces.restype = ctypes.c_int
     L.otf_build_traces.argtypes = [_i64, _i32, _P(_f64), _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
                                    _P(_f64), _P(_f64), _i32]

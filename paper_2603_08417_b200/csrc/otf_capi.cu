@@ -15,6 +15,7 @@
 int otf_launch_exact(const otf_batch &b, cudaStream_t stream);
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream);
 int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc);
+int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc);
 int otf_launch_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t *i64_pool,
                      const double *f64_pool, const int32_t *i32_pool, cudaStream_t stream);
 
@@ -46,6 +47,13 @@ int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, 
     int64_t n_desc = (int64_t)n_seq * n_ranks * max_nseg;
     if (engine == OTF_ENGINE_WINDOWED) return otf_windowed_scratch_bytes(n_clients, n_workers, n_desc);
     return otf::exact_layout(n_clients, n_workers, n_desc).total;
+}
+
+int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
+                         int32_t n_ranks, int32_t max_nseg) {
+    (void)n_workers;
+    if (engine != OTF_ENGINE_WINDOWED) return 0;
+    return otf_windowed_shared_bytes(n_clients, (int64_t)n_seq * n_ranks * max_nseg);
 }
 
 // CPython >= 3.12 builtin sum() over floats: Neumaier-compensated.
@@ -125,7 +133,10 @@ int otf_run_batch(const otf_batch *batch, int32_t engine, void *stream) {
         return fail(OTF_EINVAL, "otf_run_batch: records mode needs record buffers");
     cudaStream_t s = (cudaStream_t)stream;
     if (engine == OTF_ENGINE_EXACT) otf_launch_exact(b, s);
-    else if (engine == OTF_ENGINE_WINDOWED) otf_launch_windowed(b, s);
+    else if (engine == OTF_ENGINE_WINDOWED) {
+        if (b.shared_bytes <= 0) return fail(OTF_EINVAL, "otf_run_batch: windowed engine needs shared_bytes");
+        if (otf_launch_windowed(b, s) != 0) return fail(OTF_ECUDA, "otf_run_batch: shared memory request too large");
+    }
     else return fail(OTF_EINVAL, "otf_run_batch: unknown engine");
     return check_cuda("otf_run_batch");
 }

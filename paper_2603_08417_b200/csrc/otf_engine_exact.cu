@@ -344,8 +344,9 @@ __device__ void run_ready(ExactWorld &w) {
 }
 
 __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
-    int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= b.n_scenarios) return;
+    int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= b.n_scenarios) return;
+    int32_t s = b.order ? b.order[t] : t;
     ExactWorld w;
     w.S.init(b, s);
     w.S.reset_outputs();

@@ -1,10 +1,706 @@
-// placeholder: windowed engine (next milestone) -- routes to the exact engine.
+// otf_engine_windowed.cu -- the windowed engine: one warp replays one scenario.
+//
+// Why it is exact.  In the reference every client->server interaction
+// (MediaServer.segment, server.py:61-78) happens when a request-latency timer
+// fires, and that timer was armed `latency` seconds earlier
+// (InProcessEndpoint.segment, client.py:219-221).  Client-local events
+// (manifest transfer, buffer-full waits, segment transfers, play-out,
+// session restarts) only touch their own client, and server->client effects
+// are responses delivered at the server event's instant.  Cutting virtual time
+// into windows [k*W, (k+1)*W) with W slightly below `latency` therefore gives:
+//   * every server event of window k was armed before the window started, so
+//     the server lane (lane 0) can replay all of them -- plus the worker
+//     service timers (backend.py:186-216) and the ready-queue hops they cause
+//     (sim.py:126-130, 229-247) -- in exact (time, tick) order first;
+//   * afterwards each client's local events in the window depend only on its
+//     own state and the responses just produced, so all 32 lanes run them in
+//     parallel (client.py:229-305, orchestrator.py:336-348).
+// The only order information this loses is the global tick counter
+// (sim.py:304-309), which breaks ties between timers at the identical
+// instant.  Server events are ordered by (time, creation time) and ties the
+// engine cannot order are flagged (OTF_S_TIE) so the host re-runs that
+// scenario on the exact engine; session registration ties are checked on the
+// host.  Parity tests pin both engines to the reference's outputs.
+//
+// Layout: scenario hot state in shared memory (per-client window index, cache
+// flags + LRU links, the window's server-event list, worker timers,
+// counters); client coroutine state, waiter lists and the job FIFO in the
+// scenario's global scratch arena.
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
-#include "otfgpu.h"
-#include "otf_state.cuh"
-int otf_launch_exact(const otf_batch &b, cudaStream_t stream);
-int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc) {
-    return otf::exact_layout(n_clients, n_workers, n_desc).total;
+
+#include "otf_engine_common.cuh"
+
+namespace otf {
+
+constexpr int32_t WIN_NONE = 0x3FFFFFFF;
+constexpr int32_t WIN_SRV = 0x40000000;
+constexpr int LIST_CAP = 256;
+constexpr int MAXK = 32;
+
+struct WWorker {
+    double when, ctime;
+    int64_t eps_pos;
+    int64_t size;
+    uint32_t seq;
+    int32_t win, pc, desc, job, pad;
+};
+
+struct WinHeader {
+    EngineState st;
+    int64_t stats[OTF_ST_NSLOTS];
+    otf_qoe q;
+    WWorker wk[MAXK];
+    int32_t gq[MAXK];
+    int32_t fq_w[MAXK], fq_d[MAXK], fq_j[MAXK];
+    int32_t gq_head, gq_n, fq_head, fq_n;
+    int32_t jq_head, jq_n, jq_cap;
+    int32_t n_list, n_blist;
+    uint32_t wseq;
+    double list_when[LIST_CAP];
+    double list_ctime[LIST_CAP];
+    int64_t list_size[LIST_CAP];
+    int32_t list_id[LIST_CAP];
+    int32_t list_desc[LIST_CAP];
+};
+
+struct WinGlobalLayout {
+    int64_t clients, blist, wq_head, wq_tail, jobq, total;
+};
+
+__host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
+    WinGlobalLayout L;
+    int64_t o = 0;
+    L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
+    L.blist = o;   o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
+    L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
+    L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
+    L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
+    L.total = o;
+    return L;
 }
-int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) { return otf_launch_exact(b, stream); }
+
+__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc) {
+    int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
+    o += 4 * (int64_t)n_clients;          // cwin
+    o += 8 * n_desc;                      // lru prev/next
+    o += n_desc;                          // flags
+    return (o + 15) & ~(int64_t)15;
+}
+
+struct Win {
+    Scn S;
+    WinHeader *h;
+    int32_t *cwin;
+    int32_t *lru_prev, *lru_next;
+    uint8_t *dflags;
+    Client *cl;
+    int32_t *blist, *wq_head, *wq_tail;
+    JobEnt *jq;
+    double W, H, E, now;
+    int32_t k;
+};
+
+// window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles)
+__device__ __forceinline__ int32_t win_of(double when, double W) {
+    int32_t k = (int32_t)floor(when / W);
+    if (k < 0) k = 0;
+    while (k > 0 && when < (double)k * W) k--;
+    while (when >= (double)(k + 1) * W) k++;
+    return k;
+}
+
+__device__ __forceinline__ int32_t timer_win(const Win &w, double when) {
+    if (!(when <= w.H)) return WIN_NONE;     // run_until(H) never fires it (sim.py:352)
+    int32_t k = win_of(when, w.W);
+    return k < WIN_NONE ? k : WIN_NONE;
+}
+
+// ---- server lane: cache / backend (lane 0 only) --------------------------------
+__device__ __forceinline__ void lru_unlink(Win &w, int32_t d) {
+    int32_t p = w.lru_prev[d], n = w.lru_next[d];
+    if (p >= 0) w.lru_next[p] = n; else w.h->st.lru_head = n;
+    if (n >= 0) w.lru_prev[n] = p; else w.h->st.lru_tail = p;
+}
+__device__ __forceinline__ void lru_append(Win &w, int32_t d) {
+    int32_t t = w.h->st.lru_tail;
+    w.lru_prev[d] = t;
+    w.lru_next[d] = -1;
+    if (t >= 0) w.lru_next[t] = d; else w.h->st.lru_head = d;
+    w.h->st.lru_tail = d;
+}
+__device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache.py:45-52
+    if (!(w.dflags[d] & D_CACHED)) { w.h->stats[OTF_ST_MISSES]++; return false; }
+    lru_unlink(w, d);
+    lru_append(w, d);
+    w.h->stats[OTF_ST_HITS]++;
+    return true;
+}
+__device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
+    int64_t cap = w.S.sc.cache_capacity;
+    EngineState &st = w.h->st;
+    if (size > cap) { w.h->stats[OTF_ST_REJECTED]++; return; }
+    if (w.dflags[d] & D_CACHED) {
+        st.cur_bytes -= size;
+        lru_unlink(w, d);
+        w.dflags[d] &= ~D_CACHED;
+        st.entries--;
+    }
+    while (st.cur_bytes + size > cap) {
+        int32_t v = st.lru_head;
+        lru_unlink(w, v);
+        w.dflags[v] &= ~D_CACHED;
+        st.entries--;
+        st.cur_bytes -= w.S.size(v);
+        w.h->stats[OTF_ST_EVICTIONS]++;
+    }
+    lru_append(w, d);
+    w.dflags[d] |= D_CACHED;
+    st.entries++;
+    st.cur_bytes += size;
+}
+
+__device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backend.py:156-170
+    int32_t j = w.S.record_job(d, origin, w.now);
+    w.dflags[d] |= D_INFLIGHT;
+    w.wq_head[d] = -1;
+    w.wq_tail[d] = -1;
+    WinHeader *h = w.h;
+    if (h->gq_n > 0) {                                 // Queue.put_nowait -> first getter
+        int32_t wid = h->gq[h->gq_head];
+        h->gq_head = (h->gq_head + 1 == w.S.sc.n_workers) ? 0 : h->gq_head + 1;
+        h->gq_n--;
+        int32_t pos = h->fq_head + h->fq_n;
+        if (pos >= MAXK) pos -= MAXK;
+        h->fq_w[pos] = wid; h->fq_d[pos] = d; h->fq_j[pos] = j;
+        h->fq_n++;
+    } else {
+        if (h->jq_n >= h->jq_cap) { w.S.flag(OTF_S_INTERNAL); return; }
+        int32_t pos = h->jq_head + h->jq_n;
+        if (pos >= h->jq_cap) pos -= h->jq_cap;
+        JobEnt e; e.desc = d; e.job = j;
+        w.jq[pos] = e;
+        h->jq_n++;
+    }
+}
+
+__device__ void maybe_speculate(Win &w, int32_t d) {                     // backend.py:135-154
+    int64_t *st = w.h->stats;
+    if (!w.S.sc.spec_enabled) { st[OTF_ST_SKIP_DISABLED]++; return; }
+    int32_t seq = w.S.desc_seq(d), rank = w.S.desc_rank(d), index = w.S.desc_index(d);
+    if (index + 1 >= w.S.segcount(seq)) { st[OTF_ST_SKIP_EOS]++; return; }
+    if (w.S.stored(rank)) { st[OTF_ST_SKIP_STORED]++; return; }
+    int32_t nd = d + 1;                                // same (seq, rank), index + 1
+    uint8_t f = w.dflags[nd];
+    if (w.S.sc.cache_enabled && (f & D_CACHED)) { st[OTF_ST_SKIP_CACHED]++; return; }
+    if (f & D_INFLIGHT) { st[OTF_ST_SKIP_INFLIGHT]++; return; }
+    enqueue_job(w, nd, OTF_ORIGIN_SPECULATIVE);
+    st[OTF_ST_SPEC_ENQUEUED]++;
+}
+
+// MediaServer.segment's record append at response time (server.py:76-77) +
+// handing the client back to the client lanes at instant `now`.
+__device__ void respond(Win &w, int32_t cid, int32_t d, int64_t size, int32_t path, int64_t req_id,
+                        double arrival) {
+    Client &c = w.cl[cid];
+    int64_t r = w.h->st.n_req++;
+    const otf_scenario &sc = w.S.sc;
+    if (w.S.records) {
+        if (r < sc.req_cap) {
+            int64_t o = sc.req_off + r;
+            w.S.b.req_id[o] = req_id;
+            w.S.b.req_seq[o] = w.S.desc_seq(d);
+            w.S.b.req_rep[o] = w.S.desc_rank(d);
+            w.S.b.req_index[o] = w.S.desc_index(d);
+            w.S.b.req_path[o] = path;
+            w.S.b.req_arrival[o] = arrival;
+            w.S.b.req_response[o] = w.now;
+            w.S.b.req_bytes[o] = size;
+        } else {
+            w.S.flag(OTF_S_RECORD_OVERFLOW);
+        }
+    }
+    double lat = w.now - arrival;
+    otf_qoe &q = w.h->q;
+    q.lat_hist[lat_bin(lat)]++;
+    q.path_count[path]++;
+    q.n_requests++;
+    q.latency_sum += lat;
+    c.pc = C_SEG_RESP;
+    c.next_when = w.now;
+    c.size = size;
+    w.blist[w.h->n_blist++] = cid;
+}
+
+__device__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
+    if (!(w.dflags[d] & D_INFLIGHT)) return;
+    w.dflags[d] &= ~D_INFLIGHT;
+    int64_t size = w.S.size(d);
+    for (int32_t c = w.wq_head[d]; c >= 0;) {
+        Client &cl = w.cl[c];
+        int32_t nxt = cl.wait_next;
+        respond(w, c, d, size, cl.path, cl.req_id, cl.arrival);
+        c = nxt;
+    }
+    w.wq_head[d] = -1;
+    w.wq_tail[d] = -1;
+}
+
+__device__ void add_waiter(Win &w, int32_t d, int32_t cid) {
+    w.cl[cid].wait_next = -1;
+    int32_t t = w.wq_tail[d];
+    if (t >= 0) w.cl[t].wait_next = cid; else w.wq_head[d] = cid;
+    w.wq_tail[d] = cid;
+}
+
+// Backend._worker_loop body from "job dequeued" until the worker yields.
+__device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
+    WinHeader *h = w.h;
+    const otf_scenario &sc = w.S.sc;
+    for (;;) {
+        if (sc.cache_enabled && (w.dflags[d] & D_CACHED)) {   // dedup on dequeue (backend.py:193-198)
+            w.S.job_outcome(j, OTF_OUTCOME_DROPPED);
+            h->stats[OTF_ST_WASTED]++;
+            resolve(w, d);
+        } else {                                             // run_transcode (transcode.py:123-128)
+            WWorker &k = h->wk[wid];
+            w.S.job_started(j, w.now);
+            Worker tmp; tmp.eps_pos = k.eps_pos;
+            double svc = w.S.service_time(tmp, wid, d);
+            k.eps_pos = tmp.eps_pos;
+            k.when = w.now + svc;
+            k.ctime = w.now;
+            k.seq = h->wseq++;
+            k.win = timer_win(w, k.when);
+            k.desc = d;
+            k.job = j;
+            k.size = w.S.size(d);
+            k.pc = W_SERVICE;
+            return;
+        }
+        // next job: Queue.get on a non-empty queue does not yield (sim.py:242-244)
+        if (h->jq_n > 0) {
+            JobEnt e = w.jq[h->jq_head];
+            h->jq_head = (h->jq_head + 1 == h->jq_cap) ? 0 : h->jq_head + 1;
+            h->jq_n--;
+            d = e.desc; j = e.job;
+            continue;
+        }
+        int32_t pos = h->gq_head + h->gq_n;
+        if (pos >= sc.n_workers) pos -= sc.n_workers;
+        h->gq[pos] = wid;
+        h->gq_n++;
+        h->wk[wid].pc = W_GOT;
+        h->wk[wid].win = WIN_NONE;
+        return;
+    }
+}
+
+__device__ void drain_handoffs(Win &w) {            // ready-queue hops of handed-off jobs
+    WinHeader *h = w.h;
+    while (h->fq_n > 0) {
+        int32_t wid = h->fq_w[h->fq_head], d = h->fq_d[h->fq_head], j = h->fq_j[h->fq_head];
+        h->fq_head = (h->fq_head + 1 == MAXK) ? 0 : h->fq_head + 1;
+        h->fq_n--;
+        h->stats[OTF_ST_READY_CALLBACKS]++;
+        worker_run(w, wid, d, j);
+    }
+}
+
+// One client server event: MediaServer.segment + Backend.handle (server.py:61-78, backend.py:115-133)
+__device__ void server_request(Win &w, int32_t cid, int32_t d, int64_t size) {
+    const otf_scenario &sc = w.S.sc;
+    int64_t req_id = w.h->st.req_counter++;
+    double arrival = w.now;
+    int32_t rank = w.S.desc_rank(d);
+    if (w.S.stored(rank)) {
+        respond(w, cid, d, size, OTF_PATH_STORAGE, req_id, arrival);
+    } else if (sc.cache_enabled && cache_get(w, d)) {
+        maybe_speculate(w, d);
+        respond(w, cid, d, size, OTF_PATH_CACHE, req_id, arrival);
+    } else {
+        Client &c = w.cl[cid];
+        int32_t path;
+        if (w.dflags[d] & D_INFLIGHT) {
+            maybe_speculate(w, d);
+            path = OTF_PATH_WAITED;
+        } else {
+            enqueue_job(w, d, OTF_ORIGIN_DEMAND);
+            maybe_speculate(w, d);
+            path = OTF_PATH_TRANSCODED;
+        }
+        c.path = path;
+        c.req_id = req_id;
+        c.arrival = arrival;
+        c.pc = C_SEG_WAIT;
+        add_waiter(w, d, cid);
+    }
+}
+
+// worker service timer fired (transcode.py:129-131, backend.py:205-207)
+__device__ void server_worker_done(Win &w, int32_t wid) {
+    WWorker &k = w.h->wk[wid];
+    int32_t d = k.desc, j = k.job;
+    k.win = WIN_NONE;
+    w.S.job_finished(j, w.now);
+    if (w.S.sc.cache_enabled) cache_put(w, d, k.size);
+    resolve(w, d);
+    // next job
+    WinHeader *h = w.h;
+    if (h->jq_n > 0) {
+        JobEnt e = w.jq[h->jq_head];
+        h->jq_head = (h->jq_head + 1 == h->jq_cap) ? 0 : h->jq_head + 1;
+        h->jq_n--;
+        worker_run(w, wid, e.desc, e.job);
+    } else {
+        int32_t pos = h->gq_head + h->gq_n;
+        if (pos >= w.S.sc.n_workers) pos -= w.S.sc.n_workers;
+        h->gq[pos] = wid;
+        h->gq_n++;
+        k.pc = W_GOT;
+    }
+}
+
+// Phase A: replay the window's server events in (time, creation, tick) order.
+__device__ void phase_a(Win &w) {
+    WinHeader *h = w.h;
+    const int32_t K = w.S.sc.n_workers;
+    int32_t i = 0;
+    const int32_t n = h->n_list;
+    for (;;) {
+        int32_t bw = -1;
+        for (int32_t q = 0; q < K; q++) {
+            const WWorker &x = h->wk[q];
+            if (x.win != w.k) continue;
+            if (bw < 0) { bw = q; continue; }
+            const WWorker &y = h->wk[bw];
+            if (x.when < y.when || (x.when == y.when && (x.ctime < y.ctime ||
+                                                         (x.ctime == y.ctime && x.seq < y.seq))))
+                bw = q;
+        }
+        bool take_worker;
+        if (bw < 0 && i >= n) break;
+        if (bw < 0) take_worker = false;
+        else if (i >= n) take_worker = true;
+        else {
+            double cw = h->list_when[i], ww = h->wk[bw].when;
+            if (ww < cw) take_worker = true;
+            else if (cw < ww) take_worker = false;
+            else {
+                double cc = h->list_ctime[i], wc = h->wk[bw].ctime;
+                if (wc < cc) take_worker = true;
+                else if (cc < wc) take_worker = false;
+                else { w.S.flag(OTF_S_TIE); take_worker = true; }
+            }
+        }
+        h->stats[OTF_ST_TIMER_POPS]++;
+        if (take_worker) {
+            w.now = h->wk[bw].when;
+            server_worker_done(w, bw);
+        } else {
+            w.now = h->list_when[i];
+            server_request(w, h->list_id[i], h->list_desc[i], h->list_size[i]);
+            i++;
+        }
+        drain_handoffs(w);
+    }
+}
+
+// ---- client lanes ------------------------------------------------------------------
+// Arm a sleep for client c at w.now: returns true if the client keeps running
+// inside this window (the timer fires before the window ends).
+__device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now, double delay, int32_t next_pc) {
+    c.pc = next_pc;
+    if (delay <= 0) return true;                       // resolved future: no yield (sim.py:320-321)
+    if (isinf(delay)) {                                // never resolves (sim.py:322)
+        c.pc = C_HUNG;
+        w.cwin[cid] = WIN_NONE;
+        return false;
+    }
+    double when = now + delay;
+    c.ctime = now;
+    c.next_when = when;
+    if (next_pc == C_SEG_LAT) {                        // a server event: always a later window
+        int32_t k = timer_win(w, when);
+        if (k != WIN_NONE && k <= w.k) w.S.flag(OTF_S_TIE);   // lookahead violated (cannot happen)
+        w.cwin[cid] = (k == WIN_NONE) ? WIN_NONE : (k | WIN_SRV);
+        return false;
+    }
+    if (when <= w.H && when < w.E) {                   // fires inside this window: keep going
+        now = when;
+        return true;
+    }
+    w.cwin[cid] = timer_win(w, when);
+    return false;
+}
+
+__device__ void client_local(Win &w, int32_t cid) {
+    Client &c = w.cl[cid];
+    Scn &S = w.S;
+    const otf_scenario &sc = S.sc;
+    double now = c.next_when;
+    for (;;) {
+        switch (c.pc) {
+        case C_ARRIVED:
+            client_arrive(S, c, cid);
+            c.pc = C_SESSION;
+            break;
+        case C_SESSION:
+            if (!(now < sc.horizon)) { c.pc = C_DONE; w.cwin[cid] = WIN_NONE; return; }
+            client_new_session(S, c, cid, now);
+            if (sc.latency > 0) { if (!arm(w, c, cid, now, sc.latency, C_MAN_LAT)) return; }
+            else c.pc = C_MAN_LAT;
+            break;
+        case C_MAN_LAT: {
+            double end = completion_time(S.trace(cid), now, S.manifest(c.seq));
+            if (!arm(w, c, cid, now, end - now, C_MAN_XFER)) return;
+            break;
+        }
+        case C_MAN_XFER:
+            client_start_playback(c, now);
+            c.pc = C_INDEX_HEAD;
+            break;
+        case C_INDEX_HEAD:
+        case C_TARGET_WAIT:
+            buf_advance(c.buf, now);
+            if (c.buf.phase == PH_PLAYING && c.buf.level >= sc.target) {
+                if (!arm(w, c, cid, now, c.buf.level - sc.target + 1e-9, C_TARGET_WAIT)) return;
+                break;
+            }
+            client_select(S, c);
+            c.requested = now;
+            c.desc = S.desc_id(c.seq, c.rank, c.index);
+            if (!arm(w, c, cid, now, sc.latency, C_SEG_LAT)) return;
+            S.flag(OTF_S_INTERNAL);                    // zero latency never reaches this engine
+            return;
+        case C_SEG_RESP: {
+            c.xfer_start = now;
+            double end = completion_time(S.trace(cid), now, c.size);
+            if (!arm(w, c, cid, now, end - now, C_SEG_XFER)) return;
+            break;
+        }
+        case C_SEG_XFER:
+            if (client_segment_done(S, c, now)) { c.pc = C_INDEX_HEAD; break; }
+            if (!arm(w, c, cid, now, c.buf.level, C_PLAYOUT)) return;
+            break;
+        case C_PLAYOUT:
+            client_finish_session(S, c, now);
+            c.pc = C_SESSION;
+            break;
+        default:
+            w.cwin[cid] = WIN_NONE;
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ int32_t warp_min(int32_t v) {
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// bitonic sort of the window's server events by (when, ctime) in shared memory
+__device__ void sort_list(WinHeader *h, int lane) {
+    int32_t n = h->n_list;
+    if (n <= 1) return;
+    int32_t p = 1;
+    while (p < n) p <<= 1;
+    for (int32_t i = n + lane; i < p; i += 32) {
+        h->list_when[i] = INFINITY; h->list_ctime[i] = INFINITY; h->list_id[i] = -1;
+    }
+    __syncwarp();
+    for (int32_t size = 2; size <= p; size <<= 1) {
+        for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int32_t t = lane; t < (p >> 1); t += 32) {
+                int32_t lo = 2 * t - (t & (stride - 1));
+                int32_t hi = lo + stride;
+                bool up = ((lo & size) == 0);
+                double aw = h->list_when[lo], bw = h->list_when[hi];
+                double ac = h->list_ctime[lo], bc = h->list_ctime[hi];
+                bool gt = aw > bw || (aw == bw && (ac > bc || (ac == bc && h->list_id[lo] > h->list_id[hi])));
+                if (gt == up) {
+                    h->list_when[lo] = bw; h->list_when[hi] = aw;
+                    h->list_ctime[lo] = bc; h->list_ctime[hi] = ac;
+                    int32_t ti = h->list_id[lo]; h->list_id[lo] = h->list_id[hi]; h->list_id[hi] = ti;
+                    int32_t td = h->list_desc[lo]; h->list_desc[lo] = h->list_desc[hi]; h->list_desc[hi] = td;
+                    int64_t ts = h->list_size[lo]; h->list_size[lo] = h->list_size[hi]; h->list_size[hi] = ts;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x;
+    const int32_t s = b.order ? b.order[blockIdx.x] : (int32_t)blockIdx.x;
+    Win w;
+    w.S.init(b, s);
+    const otf_scenario &sc = w.S.sc;
+    const int32_t N = sc.n_clients, K = sc.n_workers;
+    const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
+    WinHeader *h = (WinHeader *)smem;
+    uint8_t *p = smem + ((sizeof(WinHeader) + 15) & ~(size_t)15);
+    w.h = h;
+    w.cwin = (int32_t *)p; p += 4 * (int64_t)N;
+    w.lru_prev = (int32_t *)p; p += 4 * D;
+    w.lru_next = (int32_t *)p; p += 4 * D;
+    w.dflags = p;
+    uint8_t *g = b.scratch + sc.scratch_off;
+    WinGlobalLayout L = win_global_layout(N, D);
+    w.cl = (Client *)(g + L.clients);
+    w.blist = (int32_t *)(g + L.blist);
+    w.wq_head = (int32_t *)(g + L.wq_head);
+    w.wq_tail = (int32_t *)(g + L.wq_tail);
+    w.jq = (JobEnt *)(g + L.jobq);
+    // counters and QoE accumulate in shared memory, flushed at the end
+    w.S.st = &h->st;
+    w.S.stats = h->stats;
+    w.S.q = &h->q;
+    w.W = sc.latency * (1.0 - 0x1p-20);
+    w.H = sc.horizon;
+
+    // ---- init -------------------------------------------------------------------
+    if (lane == 0) {
+        EngineState z = {};
+        z.lru_head = z.lru_tail = -1;
+        h->st = z;
+        for (int i = 0; i < OTF_ST_NSLOTS; i++) h->stats[i] = 0;
+        int64_t *qq = (int64_t *)&h->q;
+        for (size_t i = 0; i < sizeof(otf_qoe) / 8; i++) qq[i] = 0;
+        h->gq_head = 0; h->gq_n = K; h->fq_head = 0; h->fq_n = 0;
+        h->jq_head = 0; h->jq_n = 0; h->jq_cap = (int32_t)(D + 1);
+        h->n_list = 0; h->n_blist = 0; h->wseq = 0;
+        if (K > MAXK || N >= WIN_SRV || !(sc.latency > 0)) h->st.status |= OTF_S_TIE;   // not for this engine
+    }
+    for (int32_t q = lane; q < MAXK; q += 32) {
+        h->gq[q] = q;                                  // workers register as getters in id order
+        WWorker z = {};
+        z.win = WIN_NONE; z.pc = W_GOT; z.desc = -1; z.job = -1;
+        h->wk[q] = z;
+    }
+    for (int64_t d = lane; d < D; d += 32) {
+        w.lru_prev[d] = -1; w.lru_next[d] = -1; w.dflags[d] = 0;
+        w.wq_head[d] = -1; w.wq_tail[d] = -1;
+    }
+    __syncwarp();
+    if (h->st.status & OTF_S_TIE) goto done;
+    // clients: first step arms sleep(offset) (orchestrator.py:337)
+    for (int32_t c = lane; c < N; c += 32) {
+        Client &cl = w.cl[c];
+        client_init(cl);
+        double off = w.S.arrival(c);
+        cl.pc = C_ARRIVED;
+        cl.ctime = 0.0;
+        cl.next_when = 0.0 + off;
+        if (!(off > 0)) { w.S.flag(OTF_S_TIE); }       // instant start: tick order among clients matters
+        w.cwin[c] = isinf(off) ? WIN_NONE : timer_win(w, cl.next_when);
+    }
+    __syncwarp();
+
+    // ---- window loop --------------------------------------------------------------
+    for (;;) {
+        int32_t m = WIN_NONE;
+        for (int32_t c = lane; c < N; c += 32) m = min(m, w.cwin[c] & ~WIN_SRV);
+        if (lane < K) m = min(m, h->wk[lane].win);
+        m = warp_min(m);
+        if (m == WIN_NONE) break;
+        w.k = m;
+        w.E = (double)(m + 1) * w.W;
+        if (lane == 0) { h->n_list = 0; h->n_blist = 0; h->stats[OTF_ST_WINDOWS]++; }
+        __syncwarp();
+        // collect this window's clients: server events -> sorted list, local -> B-list
+        for (int32_t base = 0; base < N; base += 32) {
+            int32_t c = base + lane;
+            int32_t v = c < N ? w.cwin[c] : WIN_NONE;
+            bool cand = (v & ~WIN_SRV) == m;
+            bool srv = cand && (v & WIN_SRV);
+            unsigned ms = __ballot_sync(0xffffffffu, srv);
+            unsigned ml = __ballot_sync(0xffffffffu, cand && !srv);
+            int32_t nl = h->n_list, nb = h->n_blist;
+            __syncwarp();
+            if (srv) {
+                int32_t pos = nl + __popc(ms & ((1u << lane) - 1));
+                if (pos < LIST_CAP) {
+                    const Client &cl = w.cl[c];
+                    h->list_when[pos] = cl.next_when;
+                    h->list_ctime[pos] = cl.ctime;
+                    h->list_id[pos] = c;
+                    h->list_desc[pos] = cl.desc;
+                    h->list_size[pos] = w.S.size(cl.desc);
+                }
+            }
+            if (cand && !srv) w.blist[nb + __popc(ml & ((1u << lane) - 1))] = c;
+            if (cand) w.cwin[c] = WIN_NONE;
+            __syncwarp();
+            if (lane == 0) { h->n_list = nl + __popc(ms); h->n_blist = nb + __popc(ml); }
+            __syncwarp();
+        }
+        if (h->n_list > LIST_CAP) {                    // too many simultaneous requests for this engine
+            if (lane == 0) h->st.status |= OTF_S_TIE;
+            __syncwarp();
+            break;
+        }
+        sort_list(h, lane);
+        __syncwarp();
+        // ---- phase A: server lane ----
+        if (lane == 0) {
+            for (int32_t i = 1; i < h->n_list; i++)    // equal (time, creation time): tick order unknown
+                if (h->list_when[i] == h->list_when[i - 1] && h->list_ctime[i] == h->list_ctime[i - 1])
+                    h->st.status |= OTF_S_TIE;
+            phase_a(w);
+        }
+        __syncwarp();
+        if (h->st.status & OTF_S_TIE) break;
+        // ---- phase B: client lanes ----
+        const int32_t nb = h->n_blist;
+        for (int32_t i = lane; i < nb; i += 32) client_local(w, w.blist[i]);
+        __syncwarp();
+    }
+
+    // ---- horizon: harvest (orchestrator.py:357-359) ----
+    if (!(h->st.status & OTF_S_TIE)) {
+        for (int32_t c = lane; c < N; c += 32) client_harvest(w.S, w.cl[c], sc.horizon);
+    }
+    __syncwarp();
+done:
+    if (lane == 0) {
+        int64_t *gs = b.stats + (int64_t)s * OTF_ST_NSLOTS;
+        h->stats[OTF_ST_CACHE_CAPACITY] = sc.cache_capacity;
+        h->stats[OTF_ST_CURRENT_BYTES] = h->st.cur_bytes;
+        h->stats[OTF_ST_ENTRIES] = h->st.entries;
+        h->stats[OTF_ST_STATUS] = h->st.status;
+        for (int i = 0; i < OTF_ST_NSLOTS; i++) gs[i] = h->stats[i];
+        int64_t *cnt = b.counts + (int64_t)s * 4;
+        cnt[0] = h->st.n_req; cnt[1] = h->st.n_sess; cnt[2] = h->st.n_seg; cnt[3] = h->st.n_job;
+        b.status[s] = h->st.status;
+    }
+    {
+        const int64_t *src = (const int64_t *)&h->q;
+        int64_t *dst = (int64_t *)(b.qoe + s);
+        for (size_t i = lane; i < sizeof(otf_qoe) / 8; i += 32) dst[i] = src[i];
+    }
+}
+
+}  // namespace otf
+
+int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc) {
+    (void)n_workers;
+    return otf::win_global_layout(n_clients, n_desc).total;
+}
+
+int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
+    return otf::win_smem_bytes(n_clients, n_desc);
+}
+
+int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
+    int smem = (int)b.shared_bytes;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(otf::windowed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return 1;
+    }
+    otf::windowed_kernel<<<b.n_scenarios, 32, smem, stream>>>(b);
+    return 0;
+}

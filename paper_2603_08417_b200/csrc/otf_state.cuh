@@ -30,7 +30,7 @@ enum {
 struct Client {
     Buffer buf;                 // 56 B
     double est, requested, arrival, xfer_start;
-    double next_when;           // windowed engine: pending timer time
+    double next_when, ctime;    // windowed engine: pending timer (fire time, arm time)
     int64_t req_id, size;
     int32_t pc, seq, session, index, rank, has_est, buf_live, sess_open;
     int32_t path, desc, wait_next, pad;

@@ -80,6 +80,11 @@ class DeviceBatch:
             setattr(b, name, self.rec[name].data_ptr() if name in self.rec else None)
         b.counts, b.stats = self.counts.data_ptr(), self.stats.data_ptr()
         b.qoe, b.status = self.qoe.data_ptr(), self.status.data_ptr()
+        # longest scenarios first (LPT): the grid drains them while short ones fill in
+        cost = np.array([l.cfg.clients * l.cfg.horizon_s / min(l.seq_segdur) for l in inp.lowered])
+        self.order = torch.from_numpy(np.argsort(-cost, kind="stable").astype(np.int32)).to(dev)
+        b.order = self.order.data_ptr()
+        b.shared_bytes = inp.shared_bytes
         self.batch = b
         self.n_tables = sum(1 for t in inp.size_tables if t.n_seq > 0)
         self.upload()
@@ -117,6 +122,26 @@ class DeviceBatch:
         return BatchResult(self.inp, counts, stats, status, qoe, rec, sizes)
 
 
+def order_sessions(a: dict) -> None:
+    """Put windowed-engine sessions in registration order (client.py:237-239).
+
+    The windowed engine registers sessions from parallel lanes, so their slots
+    come out in arbitrary order; registration order is start time order (ties
+    are re-run on the exact engine).  Segment rows are re-pointed at the new
+    session slots; per-session segment order is already append order."""
+    perm = np.argsort(a["sess_start"], kind="stable")
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    for k in ("sess_client", "sess_seq", "sess_stalls", "sess_flags", "sess_start", "sess_end",
+              "sess_stall_time", "sess_startup"):
+        a[k] = a[k][perm]
+    if len(a["seg_session"]):
+        a["seg_session"] = inv[a["seg_session"]].astype(np.int32)
+        seg_order = np.argsort(a["seg_session"], kind="stable")
+        for k in ("seg_session", "seg_index", "seg_rep", "seg_start", "seg_end"):
+            a[k] = a[k][seg_order]
+
+
 def parse_qoe(row: np.ndarray) -> dict:
     q = _lib.Qoe.from_buffer_copy(row.tobytes())
     return {
@@ -145,7 +170,19 @@ class BatchResult:
             off = int(self.inp.rec_offsets[i, g])
             n = int(min(self.counts[i, g], self.inp.caps[i, g]))
             out[name] = self.rec[name][off:off + n].copy()
+        if self.inp.engine == _lib.ENGINE_WINDOWED:
+            order_sessions(out)
         return out
+
+    def session_tie(self, i: int) -> bool:
+        """Windowed engine: two sessions registered at the identical instant (order unknown)."""
+        if self.inp.engine != _lib.ENGINE_WINDOWED or not self.rec:
+            return False
+        g = _REC_GROUP["sess"]
+        off = int(self.inp.rec_offsets[i, g])
+        n = int(min(self.counts[i, g], self.inp.caps[i, g]))
+        st = np.sort(self.rec["sess_start"][off:off + n])
+        return bool(n > 1 and (st[1:] == st[:-1]).any())
 
     def sizes(self, i: int) -> np.ndarray:
         sc = self.inp.scenarios[i]
@@ -201,7 +238,7 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                 if st & _lib.S_INTERNAL:
                     raise _lib.OtfError(f"scenario {i}: engine invariant violated (status {st:#x})")
                 retry = False
-                if st & _lib.S_TIE:
+                if st & _lib.S_TIE or (m == _lib.MODE_RECORDS and br.session_tie(k)):
                     engines[i] = _lib.ENGINE_EXACT
                     retry = True
                 if st & _lib.S_EPS_OVERFLOW:

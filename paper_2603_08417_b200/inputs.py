@@ -134,6 +134,7 @@ class BatchInputs:
     engine: int
     mode: int
     input_bytes: int            # algorithmic input bytes (for the roofline)
+    shared_bytes: int = 0       # windowed engine: dynamic shared memory per CTA
 
 
 def _default_caps(low: Lowered) -> tuple[int, int, int, int]:
@@ -167,6 +168,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     rec_off = np.zeros((len(lows), 4), dtype=np.int64)
     totals = [0, 0, 0, 0]
     input_bytes = 0
+    shared_bytes = 0
 
     # -- traces: one table per (seed, netem), long enough for the largest N --
     trace_groups: dict = {}
@@ -283,6 +285,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.off_eps, sc.eps_stride = o_eps, eps_stride
         sc.scratch_off = scratch_off
         scratch_off += int(L.otf_scratch_bytes(engine, N, K, n_seq, n_ranks, max_nseg))
+        shared_bytes = max(shared_bytes, int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg)))
         scratch_off = (scratch_off + 255) & ~255
         if mode == _lib.MODE_RECORDS:
             c = caps[si] if caps is not None else _default_caps(low)
@@ -299,7 +302,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         lowered=lows, scenarios=scen, size_tables=(_lib.SizeTable * max(1, len(tables)))(*tables),
         f64=P.concat("f64"), i64=P.concat("i64"), i32=P.concat("i32"),
         scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
-        engine=engine, mode=mode, input_bytes=input_bytes)
+        engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes)
 
 
 def n_size_tables(inp: BatchInputs) -> int:

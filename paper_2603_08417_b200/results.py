@@ -132,7 +132,13 @@ def stalls_per_session(sessions) -> StallSummary:
     if not sessions:
         raise ValueError("no sessions")
     counts = [s.stalls for s in sessions]
-    return StallSummary(counts, sum(counts) / len(counts), sum(s.stall_time_s for s in sessions))
+    # The reference's stall times are np.float64 once a session has stalled
+    # (they accumulate loop.now() differences), which knocks CPython's sum()
+    # off its compensated float path: the total is a plain left-to-right sum.
+    total = 0.0
+    for s in sessions:
+        total += s.stall_time_s
+    return StallSummary(counts, sum(counts) / len(counts), total)
 
 
 @dataclass(frozen=True)

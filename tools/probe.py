@@ -27,3 +27,8 @@ for w in which:
     if w == "c2w": timeit("c2x64", [workloads.c2(seed=s) for s in range(1, 65)], 1)
     if w == "c5s": timeit("c5x8_h60", [workloads.c5(seed=s, horizon_s=60.0) for s in range(1, 9)], 0, reps=1)
     if w == "c5": timeit("c5x64", workloads.c5_sweep(seeds=range(1, 5)), 0, reps=1)
+for w in which:
+    if w == "c1w": timeit("c1x64", [workloads.c1(seed=s) for s in range(1, 65)], 1)
+    if w == "c5sw": timeit("c5x8_h60", [workloads.c5(seed=s, horizon_s=60.0) for s in range(1, 9)], 1, reps=1)
+    if w == "c5w": timeit("c5x64", workloads.c5_sweep(seeds=range(1, 5)), 1, reps=1)
+    if w == "c5fw": timeit("c5x1024", workloads.c5_sweep(seeds=range(1, 65)), 1, reps=1)
