@@ -65,6 +65,8 @@ enum {
     OTF_ST_CACHE_CAPACITY, OTF_ST_CURRENT_BYTES, OTF_ST_ENTRIES, OTF_ST_HITS, OTF_ST_MISSES,
     OTF_ST_EVICTIONS, OTF_ST_REJECTED,
     OTF_ST_STATUS, OTF_ST_HUNG, OTF_ST_TIMER_POPS, OTF_ST_READY_CALLBACKS, OTF_ST_WINDOWS,
+    /* windowed engine profile: SM cycles spent per phase (lane 0's clock) */
+    OTF_ST_CYC_SCAN, OTF_ST_CYC_SORT, OTF_ST_CYC_SERVER, OTF_ST_CYC_CLIENTS, OTF_ST_CYC_TOTAL,
     OTF_ST_NSLOTS = 32
 };
 
@@ -82,6 +84,7 @@ typedef struct otf_scenario {
     double alpha, headroom;           /* ClientConfig.ewma_alpha / headroom */
     double noise;                     /* LatencyModel.noise_rel_std */
     double period;                    /* BandwidthTrace.period (shared timestamps) */
+    double grid_step;                 /* > 0 when starts[i] == i * grid_step exactly (bisect-free lookup) */
     int64_t off_sizes;                /* i64: [n_seq][n_ranks][max_nseg] segment bytes */
     int64_t off_bitrates;             /* i64: [n_ranks] */
     int64_t off_manifest;             /* i64: [n_seq] manifest JSON bytes */

@@ -33,7 +33,8 @@ S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG = 0x1, 0x2, 0x4, 0x
 ST_NSLOTS = 32
 ST = dict(jobs_total=0, jobs_demand=1, jobs_speculative=2, wasted_avoided=3, speculation_enqueued=4,
           skip0=5, capacity_bytes=11, current_bytes=12, entries=13, hits=14, misses=15,
-          evictions=16, rejected=17, status=18, hung=19, timer_pops=20, ready_callbacks=21, windows=22)
+          evictions=16, rejected=17, status=18, hung=19, timer_pops=20, ready_callbacks=21, windows=22,
+          cyc_scan=23, cyc_sort=24, cyc_server=25, cyc_clients=26, cyc_total=27)
 SKIP_REASONS = ("disabled", "end-of-sequence", "stored", "cached", "in-flight", "overload")
 LAT_BINS, STALL_BINS, RANK_BINS = 64, 32, 16
 
@@ -46,7 +47,7 @@ class Scenario(ctypes.Structure):
         ("cache_capacity", _i64), ("seed", _u64),
         ("horizon", _f64), ("latency", _f64),
         ("target", _f64), ("safe", _f64), ("panic", _f64), ("resume", _f64), ("startup", _f64),
-        ("alpha", _f64), ("headroom", _f64), ("noise", _f64), ("period", _f64),
+        ("alpha", _f64), ("headroom", _f64), ("noise", _f64), ("period", _f64), ("grid_step", _f64),
         ("off_sizes", _i64), ("off_bitrates", _i64), ("off_manifest", _i64), ("off_segcount", _i64),
         ("off_seqdur", _i64), ("off_segdur", _i64), ("off_rho", _i64), ("off_zipf", _i64),
         ("off_starts", _i64), ("off_values", _i64), ("off_pbits", _i64), ("off_arrivals", _i64),

@@ -25,8 +25,8 @@ struct EngineState {                 // first 256 B of every scenario arena
 };
 
 struct Scn {
-    otf_batch b;
-    otf_scenario sc;
+    const otf_batch *b;              // shared memory (windowed) or a local copy (exact)
+    const otf_scenario *sc;          // shared memory (windowed) or global (exact)
     int32_t s;
     EngineState *st;
     int64_t *stats;
@@ -36,27 +36,27 @@ struct Scn {
     const double *seqdur, *segdur, *rho, *zipf, *starts, *values, *pbits, *arrivals, *eps;
     bool records;
 
-    __device__ void init(const otf_batch &bb, int32_t si) {
+    __device__ void init(const otf_batch *bb, const otf_scenario *scp, int32_t si) {
         b = bb;
         s = si;
-        sc = b.scenarios[si];
-        st = (EngineState *)(b.scratch + sc.scratch_off);
-        stats = b.stats + (int64_t)si * OTF_ST_NSLOTS;
-        q = b.qoe + si;
-        sizes = b.i64_pool + sc.off_sizes;
-        bitrates = b.i64_pool + sc.off_bitrates;
-        manifest_b = b.i64_pool + sc.off_manifest;
-        segcounts = b.i32_pool + sc.off_segcount;
-        seqdur = b.f64_pool + sc.off_seqdur;
-        segdur = b.f64_pool + sc.off_segdur;
-        rho = b.f64_pool + sc.off_rho;
-        zipf = b.f64_pool + sc.off_zipf;
-        starts = b.f64_pool + sc.off_starts;
-        values = b.f64_pool + sc.off_values;
-        pbits = b.f64_pool + sc.off_pbits;
-        arrivals = b.f64_pool + sc.off_arrivals;
-        eps = b.f64_pool + sc.off_eps;
-        records = b.mode == OTF_MODE_RECORDS;
+        sc = scp;
+        st = (EngineState *)(b->scratch + sc->scratch_off);
+        stats = b->stats + (int64_t)si * OTF_ST_NSLOTS;
+        q = b->qoe + si;
+        sizes = b->i64_pool + sc->off_sizes;
+        bitrates = b->i64_pool + sc->off_bitrates;
+        manifest_b = b->i64_pool + sc->off_manifest;
+        segcounts = b->i32_pool + sc->off_segcount;
+        seqdur = b->f64_pool + sc->off_seqdur;
+        segdur = b->f64_pool + sc->off_segdur;
+        rho = b->f64_pool + sc->off_rho;
+        zipf = b->f64_pool + sc->off_zipf;
+        starts = b->f64_pool + sc->off_starts;
+        values = b->f64_pool + sc->off_values;
+        pbits = b->f64_pool + sc->off_pbits;
+        arrivals = b->f64_pool + sc->off_arrivals;
+        eps = b->f64_pool + sc->off_eps;
+        records = b->mode == OTF_MODE_RECORDS;
     }
 
     // zero the scenario's outputs and counters (call once, single thread)
@@ -72,25 +72,26 @@ struct Scn {
     __device__ __forceinline__ int64_t &stat(int i) { return stats[i]; }
     __device__ __forceinline__ void flag(int32_t bits) { st->status |= bits; }
     __device__ __forceinline__ int32_t desc_id(int32_t seq, int32_t rank, int32_t index) const {
-        return (seq * sc.n_ranks + (rank - 1)) * sc.max_nseg + index;
+        return (seq * sc->n_ranks + (rank - 1)) * sc->max_nseg + index;
     }
     __device__ __forceinline__ int64_t size(int32_t d) const { return sizes[d]; }
     __device__ __forceinline__ int32_t segcount(int32_t seq) const { return segcounts[seq]; }
-    __device__ __forceinline__ bool stored(int32_t rank) const { return (sc.stored_mask >> rank) & 1u; }
+    __device__ __forceinline__ bool stored(int32_t rank) const { return (sc->stored_mask >> rank) & 1u; }
     __device__ __forceinline__ double arrival(int32_t cid) const { return arrivals[cid]; }
     __device__ __forceinline__ int64_t manifest(int32_t seq) const { return manifest_b[seq]; }
     __device__ __forceinline__ Trace trace(int32_t cid) const {
         Trace t;
         t.starts = starts;
-        t.values = values + (int64_t)cid * sc.n_samples;
-        t.period = sc.period;
+        t.values = values + (int64_t)cid * sc->n_samples;
+        t.period = sc->period;
+        t.grid = sc->grid_step;
         t.pbits = pbits[cid];
-        t.n = sc.n_samples;
+        t.n = sc->n_samples;
         return t;
     }
-    __device__ __forceinline__ int32_t desc_seq(int32_t d) const { return d / (sc.n_ranks * sc.max_nseg); }
-    __device__ __forceinline__ int32_t desc_rank(int32_t d) const { return (d / sc.max_nseg) % sc.n_ranks + 1; }
-    __device__ __forceinline__ int32_t desc_index(int32_t d) const { return d % sc.max_nseg; }
+    __device__ __forceinline__ int32_t desc_seq(int32_t d) const { return d / (sc->n_ranks * sc->max_nseg); }
+    __device__ __forceinline__ int32_t desc_rank(int32_t d) const { return (d / sc->max_nseg) % sc->n_ranks + 1; }
+    __device__ __forceinline__ int32_t desc_index(int32_t d) const { return d % sc->max_nseg; }
 
     // Backend._enqueue bookkeeping: TranscodeJob + jobs.append (backend.py:156-170)
     __device__ int32_t record_job(int32_t d, int32_t origin, double now) {
@@ -98,16 +99,16 @@ struct Scn {
         stats[OTF_ST_JOBS_TOTAL]++;
         stats[origin == OTF_ORIGIN_DEMAND ? OTF_ST_JOBS_DEMAND : OTF_ST_JOBS_SPEC]++;
         if (records) {
-            if (j < sc.job_cap) {
-                int64_t o = sc.job_off + j;
-                b.job_seq[o] = desc_seq(d);
-                b.job_rep[o] = desc_rank(d);
-                b.job_index[o] = desc_index(d);
-                b.job_origin[o] = origin;
-                b.job_outcome[o] = OTF_OUTCOME_PENDING;
-                b.job_enq[o] = now;
-                b.job_start[o] = NAN;
-                b.job_fin[o] = NAN;
+            if (j < sc->job_cap) {
+                int64_t o = sc->job_off + j;
+                b->job_seq[o] = desc_seq(d);
+                b->job_rep[o] = desc_rank(d);
+                b->job_index[o] = desc_index(d);
+                b->job_origin[o] = origin;
+                b->job_outcome[o] = OTF_OUTCOME_PENDING;
+                b->job_enq[o] = now;
+                b->job_start[o] = NAN;
+                b->job_fin[o] = NAN;
             } else {
                 flag(OTF_S_RECORD_OVERFLOW);
             }
@@ -115,15 +116,15 @@ struct Scn {
         return (int32_t)j;
     }
     __device__ __forceinline__ void job_outcome(int32_t j, int32_t o) {
-        if (records && j < sc.job_cap) b.job_outcome[sc.job_off + j] = o;
+        if (records && j < sc->job_cap) b->job_outcome[sc->job_off + j] = o;
     }
     __device__ __forceinline__ void job_started(int32_t j, double now) {
-        if (records && j < sc.job_cap) b.job_start[sc.job_off + j] = now;
+        if (records && j < sc->job_cap) b->job_start[sc->job_off + j] = now;
     }
     __device__ __forceinline__ void job_finished(int32_t j, double now) {
-        if (records && j < sc.job_cap) {
-            b.job_fin[sc.job_off + j] = now;
-            b.job_outcome[sc.job_off + j] = OTF_OUTCOME_COMPLETED;
+        if (records && j < sc->job_cap) {
+            b->job_fin[sc->job_off + j] = now;
+            b->job_outcome[sc->job_off + j] = OTF_OUTCOME_COMPLETED;
         }
     }
 
@@ -132,9 +133,9 @@ struct Scn {
         int32_t rank = desc_rank(d), seq = desc_seq(d), idx = desc_index(d);
         double duration = seg_duration(seqdur[seq], segdur[seq], idx);
         double e = 0.0;
-        if (sc.noise > 0) {
-            if (k.eps_pos >= sc.eps_stride) flag(OTF_S_EPS_OVERFLOW);
-            else e = eps[(int64_t)wid * sc.eps_stride + k.eps_pos];
+        if (sc->noise > 0) {
+            if (k.eps_pos >= sc->eps_stride) flag(OTF_S_EPS_OVERFLOW);
+            else e = eps[(int64_t)wid * sc->eps_stride + k.eps_pos];
             k.eps_pos++;
         }
         double svc = rho[rank - 1] * duration * (1.0 + e);
@@ -145,16 +146,16 @@ struct Scn {
     __device__ void record_request(const Client &c, double response) {
         int64_t r = st->n_req++;
         if (records) {
-            if (r < sc.req_cap) {
-                int64_t o = sc.req_off + r;
-                b.req_id[o] = c.req_id;
-                b.req_seq[o] = c.seq;
-                b.req_rep[o] = c.rank;
-                b.req_index[o] = c.index;
-                b.req_path[o] = c.path;
-                b.req_arrival[o] = c.arrival;
-                b.req_response[o] = response;
-                b.req_bytes[o] = c.size;
+            if (r < sc->req_cap) {
+                int64_t o = sc->req_off + r;
+                b->req_id[o] = c.req_id;
+                b->req_seq[o] = c.seq;
+                b->req_rep[o] = c.rank;
+                b->req_index[o] = c.index;
+                b->req_path[o] = c.path;
+                b->req_arrival[o] = c.arrival;
+                b->req_response[o] = response;
+                b->req_bytes[o] = c.size;
             } else {
                 flag(OTF_S_RECORD_OVERFLOW);
             }
@@ -167,12 +168,12 @@ struct Scn {
     }
 
     __device__ void sync_session(const Client &c, double now) {      // _sync_report (client.py:284-288)
-        if (!records || c.session >= sc.sess_cap) return;
-        int64_t o = sc.sess_off + c.session;
-        b.sess_end[o] = now;
-        b.sess_stalls[o] = c.buf.stall_events;
-        b.sess_stall_time[o] = c.buf.stall_time;
-        b.sess_startup[o] = isnan(c.buf.started_at) ? NAN : c.buf.started_at - c.buf.session_start;
+        if (!records || c.session >= sc->sess_cap) return;
+        int64_t o = sc->sess_off + c.session;
+        b->sess_end[o] = now;
+        b->sess_stalls[o] = c.buf.stall_events;
+        b->sess_stall_time[o] = c.buf.stall_time;
+        b->sess_startup[o] = isnan(c.buf.started_at) ? NAN : c.buf.started_at - c.buf.session_start;
     }
 
     // session QoE, once per session when its numbers are final
@@ -192,13 +193,13 @@ struct Scn {
     }
 
     __device__ void finish() {
-        stats[OTF_ST_CACHE_CAPACITY] = sc.cache_capacity;
+        stats[OTF_ST_CACHE_CAPACITY] = sc->cache_capacity;
         stats[OTF_ST_CURRENT_BYTES] = st->cur_bytes;
         stats[OTF_ST_ENTRIES] = st->entries;
         stats[OTF_ST_STATUS] = st->status;
-        int64_t *cnt = b.counts + (int64_t)s * 4;
+        int64_t *cnt = b->counts + (int64_t)s * 4;
         cnt[0] = st->n_req; cnt[1] = st->n_sess; cnt[2] = st->n_seg; cnt[3] = st->n_job;
-        b.status[s] = st->status;
+        b->status[s] = st->status;
     }
 };
 
@@ -217,7 +218,7 @@ __device__ __forceinline__ void client_init(Client &c) {
 __device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
     uint32_t ent[8];
     int m = 0;
-    m = push_words(ent, m, S.sc.seed);
+    m = push_words(ent, m, S.sc->seed);
     m = push_words(ent, m, 3u);
     m = push_words(ent, m, (uint64_t)cid);
     pcg_seed(c.picks, ent, m);
@@ -226,13 +227,13 @@ __device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
 // orchestrator.py:341-345 + client.py:237-239: pick a sequence, register a report
 __device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double now) {
     int32_t seq;
-    if (S.sc.popularity == OTF_POP_ZIPF) {
+    if (S.sc->popularity == OTF_POP_ZIPF) {
         double u = pcg_next_double(c.picks);
-        seq = S.sc.n_seq - 1;
-        for (int32_t k = 0; k < S.sc.n_seq; k++)
+        seq = S.sc->n_seq - 1;
+        for (int32_t k = 0; k < S.sc->n_seq; k++)
             if (u < S.zipf[k]) { seq = k; break; }
     } else {
-        seq = pcg_integers(c.picks, (uint32_t)S.sc.n_seq);
+        seq = pcg_integers(c.picks, (uint32_t)S.sc->n_seq);
     }
     c.seq = seq;
     int64_t sid = atomicAdd((unsigned long long *)&S.st->n_sess, 1ull);
@@ -240,16 +241,16 @@ __device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double
     c.buf_live = 0;
     c.sess_open = 1;
     if (S.records) {
-        if (sid < S.sc.sess_cap) {
-            int64_t o = S.sc.sess_off + sid;
-            S.b.sess_client[o] = cid;
-            S.b.sess_seq[o] = seq;
-            S.b.sess_start[o] = now;
-            S.b.sess_end[o] = 0.0;
-            S.b.sess_stalls[o] = 0;
-            S.b.sess_stall_time[o] = 0.0;
-            S.b.sess_startup[o] = NAN;
-            S.b.sess_flags[o] = 0;
+        if (sid < S.sc->sess_cap) {
+            int64_t o = S.sc->sess_off + sid;
+            S.b->sess_client[o] = cid;
+            S.b->sess_seq[o] = seq;
+            S.b->sess_start[o] = now;
+            S.b->sess_end[o] = 0.0;
+            S.b->sess_stalls[o] = 0;
+            S.b->sess_stall_time[o] = 0.0;
+            S.b->sess_startup[o] = NAN;
+            S.b->sess_flags[o] = 0;
         } else {
             S.flag(OTF_S_RECORD_OVERFLOW);
         }
@@ -269,8 +270,8 @@ __device__ __forceinline__ void client_start_playback(Client &c, double now) {
 // client.py:255-256
 __device__ __forceinline__ void client_select(Scn &S, Client &c) {
     if (c.index > 0)
-        c.rank = select_quality(c.buf.level, c.rank, c.has_est != 0, c.est, S.bitrates, S.sc.n_ranks,
-                                S.sc.panic, S.sc.safe, S.sc.headroom);
+        c.rank = select_quality(c.buf.level, c.rank, c.has_est != 0, c.est, S.bitrates, S.sc->n_ranks,
+                                S.sc->panic, S.sc->safe, S.sc->headroom);
 }
 
 // client.py:261-268; returns true when the session has more segments, else
@@ -279,18 +280,18 @@ __device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
     double dt = now - c.xfer_start;                       // SegmentFetch.rate_bps
     double rate = dt > 0 ? ((double)c.size * 8.0) / dt : INFINITY;
     if (!c.has_est) { c.est = rate; c.has_est = 1; }
-    else c.est = S.sc.alpha * rate + (1.0 - S.sc.alpha) * c.est;
+    else c.est = S.sc->alpha * rate + (1.0 - S.sc->alpha) * c.est;
     double duration = seg_duration(S.seqdur[c.seq], S.segdur[c.seq], c.index);
-    buf_on_segment(c.buf, now, duration, S.sc.startup, S.sc.resume);
+    buf_on_segment(c.buf, now, duration, S.sc->startup, S.sc->resume);
     int64_t g = atomicAdd((unsigned long long *)&S.st->n_seg, 1ull);
     if (S.records) {
-        if (g < S.sc.seg_cap) {
-            int64_t o = S.sc.seg_off + g;
-            S.b.seg_session[o] = c.session;
-            S.b.seg_index[o] = c.index;
-            S.b.seg_rep[o] = c.rank;
-            S.b.seg_start[o] = c.requested;
-            S.b.seg_end[o] = now;
+        if (g < S.sc->seg_cap) {
+            int64_t o = S.sc->seg_off + g;
+            S.b->seg_session[o] = c.session;
+            S.b->seg_index[o] = c.index;
+            S.b->seg_rep[o] = c.rank;
+            S.b->seg_start[o] = c.requested;
+            S.b->seg_end[o] = now;
         } else {
             S.flag(OTF_S_RECORD_OVERFLOW);
         }
@@ -308,7 +309,7 @@ __device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
 __device__ inline void client_finish_session(Scn &S, Client &c, double now) {
     buf_advance(c.buf, now);
     c.buf.phase = PH_FINISHED;
-    if (S.records && c.session < S.sc.sess_cap) S.b.sess_flags[S.sc.sess_off + c.session] |= 1;
+    if (S.records && c.session < S.sc->sess_cap) S.b->sess_flags[S.sc->sess_off + c.session] |= 1;
     S.sync_session(c, now);
     S.qoe_session(c, true);
     c.buf_live = 0;

@@ -106,7 +106,7 @@ __device__ bool cache_get(ExactWorld &w, int32_t d) {
 }
 __device__ void cache_put(ExactWorld &w, int32_t d) {
     int64_t size = w.S.size(d);
-    int64_t cap = w.S.sc.cache_capacity;
+    int64_t cap = w.S.sc->cache_capacity;
     EngineState *st = w.S.st;
     if (size > cap) { w.S.stat(OTF_ST_REJECTED)++; return; }
     if (w.descs[d].flags & D_CACHED) {
@@ -138,7 +138,7 @@ __device__ void enqueue_job(ExactWorld &w, int32_t d, int32_t origin) {
     D.wq_head = D.wq_tail = -1;
     if (w.gq_n > 0) {                         // hand to the first waiting getter
         int32_t wid = w.gq[w.gq_head];
-        w.gq_head = (w.gq_head + 1 == w.S.sc.n_workers) ? 0 : w.gq_head + 1;
+        w.gq_head = (w.gq_head + 1 == w.S.sc->n_workers) ? 0 : w.gq_head + 1;
         w.gq_n--;
         ready_push(w, wid, d, j);
     } else {
@@ -153,13 +153,13 @@ __device__ void enqueue_job(ExactWorld &w, int32_t d, int32_t origin) {
 
 // Backend.maybe_speculate (backend.py:135-154)
 __device__ void maybe_speculate(ExactWorld &w, int32_t seq, int32_t rank, int32_t index) {
-    if (!w.S.sc.spec_enabled) { w.S.stat(OTF_ST_SKIP_DISABLED)++; return; }
+    if (!w.S.sc->spec_enabled) { w.S.stat(OTF_ST_SKIP_DISABLED)++; return; }
     int32_t ni = index + 1;
     if (ni >= w.S.segcount(seq)) { w.S.stat(OTF_ST_SKIP_EOS)++; return; }
     if (w.S.stored(rank)) { w.S.stat(OTF_ST_SKIP_STORED)++; return; }
     int32_t d = w.S.desc_id(seq, rank, ni);
     int32_t f = w.descs[d].flags;
-    if (w.S.sc.cache_enabled && (f & D_CACHED)) { w.S.stat(OTF_ST_SKIP_CACHED)++; return; }
+    if (w.S.sc->cache_enabled && (f & D_CACHED)) { w.S.stat(OTF_ST_SKIP_CACHED)++; return; }
     if (f & D_INFLIGHT) { w.S.stat(OTF_ST_SKIP_INFLIGHT)++; return; }
     enqueue_job(w, d, OTF_ORIGIN_SPECULATIVE);
     w.S.stat(OTF_ST_SPEC_ENQUEUED)++;
@@ -171,7 +171,7 @@ __device__ void resolve(ExactWorld &w, int32_t d) {
     if (!(D.flags & D_INFLIGHT)) return;
     D.flags &= ~D_INFLIGHT;
     for (int32_t c = D.wq_head; c >= 0; c = w.cl[c].wait_next)
-        ready_push(w, w.S.sc.n_workers + c, 0, 0);
+        ready_push(w, w.S.sc->n_workers + c, 0, 0);
     D.wq_head = D.wq_tail = -1;
 }
 
@@ -184,7 +184,7 @@ __device__ void add_waiter(ExactWorld &w, int32_t d, int32_t cid) {
 
 // ---- client coroutine ---------------------------------------------------------
 __device__ void client_step(ExactWorld &w, int32_t cid) {
-    const otf_scenario &sc = w.S.sc;
+    const otf_scenario &sc = *w.S.sc;
     Client &c = w.cl[cid];
     const int32_t task = sc.n_workers + cid;
     for (;;) {
@@ -282,7 +282,7 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
 
 // ---- worker coroutine (backend.py:186-207) -------------------------------------
 __device__ void worker_step(ExactWorld &w, int32_t wid, int32_t desc, int32_t job) {
-    const otf_scenario &sc = w.S.sc;
+    const otf_scenario &sc = *w.S.sc;
     Worker &k = w.wk[wid];
     for (;;) {
         switch (k.pc) {
@@ -338,8 +338,8 @@ __device__ void run_ready(ExactWorld &w) {
         w.rq_head = (w.rq_head + 1 == w.rq_cap) ? 0 : w.rq_head + 1;
         w.rq_n--;
         w.S.stat(OTF_ST_READY_CALLBACKS)++;
-        if (e.task < w.S.sc.n_workers) worker_step(w, e.task, e.desc, e.job);
-        else client_step(w, e.task - w.S.sc.n_workers);
+        if (e.task < w.S.sc->n_workers) worker_step(w, e.task, e.desc, e.job);
+        else client_step(w, e.task - w.S.sc->n_workers);
     }
 }
 
@@ -348,9 +348,10 @@ __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
     if (t >= b.n_scenarios) return;
     int32_t s = b.order ? b.order[t] : t;
     ExactWorld w;
-    w.S.init(b, s);
+    otf_batch bl = b;
+    w.S.init(&bl, &b.scenarios[s], s);
     w.S.reset_outputs();
-    const otf_scenario &sc = w.S.sc;
+    const otf_scenario &sc = *w.S.sc;
     int64_t n_desc = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
     ExactLayout L = exact_layout(sc.n_clients, sc.n_workers, n_desc);
     uint8_t *base = b.scratch + sc.scratch_off;

@@ -35,9 +35,11 @@
 namespace otf {
 
 constexpr int32_t WIN_NONE = 0x3FFFFFFF;
-constexpr int32_t WIN_SRV = 0x40000000;
-constexpr int LIST_CAP = 256;
-constexpr int MAXK = 32;
+constexpr int LIST_CAP = 256;      // server events per window (more -> exact engine)
+constexpr int MAXK = 32;           // transcode workers
+constexpr int RING = 2048;         // timer-wheel buckets (windows); farther timers wait on a far list
+constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory
+constexpr uint8_t K_SRV = 1;       // client's pending timer is a server event (request latency)
 
 struct WWorker {
     double when, ctime;
@@ -47,7 +49,11 @@ struct WWorker {
     int32_t win, pc, desc, job, pad;
 };
 
+// Shared-memory header of one scenario (followed by the per-client and
+// per-descriptor arrays, see win_smem_bytes).
 struct WinHeader {
+    otf_batch b;                     // copies: every lane reads these at L1 latency
+    otf_scenario sc;
     EngineState st;
     int64_t stats[OTF_ST_NSLOTS];
     otf_qoe q;
@@ -58,6 +64,15 @@ struct WinHeader {
     int32_t jq_head, jq_n, jq_cap;
     int32_t n_list, n_blist;
     uint32_t wseq;
+    int32_t far_head, far_n, far_min, k_done;
+    // small read-only tables
+    int32_t t_segcount[MAXTAB];
+    double t_seqdur[MAXTAB], t_segdur[MAXTAB], t_zipf[MAXTAB], t_rho[MAXTAB];
+    int64_t t_bitrates[MAXTAB], t_manifest[MAXTAB];
+    // timer wheel
+    uint32_t bits[RING / 32];
+    int32_t bhead[RING];
+    // the window's server events
     double list_when[LIST_CAP];
     double list_ctime[LIST_CAP];
     int64_t list_size[LIST_CAP];
@@ -83,17 +98,20 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
 
 __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc) {
     int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
-    o += 4 * (int64_t)n_clients;          // cwin
-    o += 8 * n_desc;                      // lru prev/next
-    o += n_desc;                          // flags
+    o += 4 * (int64_t)n_clients;          // bucket next links
+    o += (int64_t)n_clients;              // pending-timer kind
+    o = (o + 15) & ~(int64_t)15;
+    o += 4 * n_desc;                      // lru prev/next (int16)
+    o += n_desc;                          // descriptor flags
     return (o + 15) & ~(int64_t)15;
 }
 
 struct Win {
     Scn S;
     WinHeader *h;
-    int32_t *cwin;
-    int32_t *lru_prev, *lru_next;
+    int32_t *bnext;
+    uint8_t *ckind;
+    int16_t *lru_prev, *lru_next;
     uint8_t *dflags;
     Client *cl;
     int32_t *blist, *wq_head, *wq_tail;
@@ -104,7 +122,8 @@ struct Win {
 
 // window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles)
 __device__ __forceinline__ int32_t win_of(double when, double W) {
-    int32_t k = (int32_t)floor(when / W);
+    double q = floor(when / W);
+    int32_t k = q < 1.0e9 ? (int32_t)q : 1000000000;
     if (k < 0) k = 0;
     while (k > 0 && when < (double)k * W) k--;
     while (when >= (double)(k + 1) * W) k++;
@@ -115,6 +134,23 @@ __device__ __forceinline__ int32_t timer_win(const Win &w, double when) {
     if (!(when <= w.H)) return WIN_NONE;     // run_until(H) never fires it (sim.py:352)
     int32_t k = win_of(when, w.W);
     return k < WIN_NONE ? k : WIN_NONE;
+}
+
+// Put client c on the bucket of window `wk` (any lane; lock-free push).
+__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, uint8_t kind) {
+    WinHeader *h = w.h;
+    w.ckind[c] = kind;
+    if (wk - w.k < RING) {
+        int32_t slot = wk & (RING - 1);
+        int32_t old = atomicExch(&h->bhead[slot], c);
+        w.bnext[c] = old;
+        atomicOr(&h->bits[slot >> 5], 1u << (slot & 31));
+    } else {
+        int32_t old = atomicExch(&h->far_head, c);
+        w.bnext[c] = old;
+        atomicAdd(&h->far_n, 1);
+        atomicMin(&h->far_min, wk);
+    }
 }
 
 // ---- server lane: cache / backend (lane 0 only) --------------------------------
@@ -138,7 +174,7 @@ __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache
     return true;
 }
 __device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
-    int64_t cap = w.S.sc.cache_capacity;
+    int64_t cap = w.S.sc->cache_capacity;
     EngineState &st = w.h->st;
     if (size > cap) { w.h->stats[OTF_ST_REJECTED]++; return; }
     if (w.dflags[d] & D_CACHED) {
@@ -169,7 +205,7 @@ __device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backe
     WinHeader *h = w.h;
     if (h->gq_n > 0) {                                 // Queue.put_nowait -> first getter
         int32_t wid = h->gq[h->gq_head];
-        h->gq_head = (h->gq_head + 1 == w.S.sc.n_workers) ? 0 : h->gq_head + 1;
+        h->gq_head = (h->gq_head + 1 == w.S.sc->n_workers) ? 0 : h->gq_head + 1;
         h->gq_n--;
         int32_t pos = h->fq_head + h->fq_n;
         if (pos >= MAXK) pos -= MAXK;
@@ -187,13 +223,13 @@ __device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backe
 
 __device__ void maybe_speculate(Win &w, int32_t d) {                     // backend.py:135-154
     int64_t *st = w.h->stats;
-    if (!w.S.sc.spec_enabled) { st[OTF_ST_SKIP_DISABLED]++; return; }
+    if (!w.S.sc->spec_enabled) { st[OTF_ST_SKIP_DISABLED]++; return; }
     int32_t seq = w.S.desc_seq(d), rank = w.S.desc_rank(d), index = w.S.desc_index(d);
     if (index + 1 >= w.S.segcount(seq)) { st[OTF_ST_SKIP_EOS]++; return; }
     if (w.S.stored(rank)) { st[OTF_ST_SKIP_STORED]++; return; }
     int32_t nd = d + 1;                                // same (seq, rank), index + 1
     uint8_t f = w.dflags[nd];
-    if (w.S.sc.cache_enabled && (f & D_CACHED)) { st[OTF_ST_SKIP_CACHED]++; return; }
+    if (w.S.sc->cache_enabled && (f & D_CACHED)) { st[OTF_ST_SKIP_CACHED]++; return; }
     if (f & D_INFLIGHT) { st[OTF_ST_SKIP_INFLIGHT]++; return; }
     enqueue_job(w, nd, OTF_ORIGIN_SPECULATIVE);
     st[OTF_ST_SPEC_ENQUEUED]++;
@@ -205,18 +241,18 @@ __device__ void respond(Win &w, int32_t cid, int32_t d, int64_t size, int32_t pa
                         double arrival) {
     Client &c = w.cl[cid];
     int64_t r = w.h->st.n_req++;
-    const otf_scenario &sc = w.S.sc;
+    const otf_scenario &sc = *w.S.sc;
     if (w.S.records) {
         if (r < sc.req_cap) {
             int64_t o = sc.req_off + r;
-            w.S.b.req_id[o] = req_id;
-            w.S.b.req_seq[o] = w.S.desc_seq(d);
-            w.S.b.req_rep[o] = w.S.desc_rank(d);
-            w.S.b.req_index[o] = w.S.desc_index(d);
-            w.S.b.req_path[o] = path;
-            w.S.b.req_arrival[o] = arrival;
-            w.S.b.req_response[o] = w.now;
-            w.S.b.req_bytes[o] = size;
+            w.S.b->req_id[o] = req_id;
+            w.S.b->req_seq[o] = w.S.desc_seq(d);
+            w.S.b->req_rep[o] = w.S.desc_rank(d);
+            w.S.b->req_index[o] = w.S.desc_index(d);
+            w.S.b->req_path[o] = path;
+            w.S.b->req_arrival[o] = arrival;
+            w.S.b->req_response[o] = w.now;
+            w.S.b->req_bytes[o] = size;
         } else {
             w.S.flag(OTF_S_RECORD_OVERFLOW);
         }
@@ -257,7 +293,7 @@ __device__ void add_waiter(Win &w, int32_t d, int32_t cid) {
 // Backend._worker_loop body from "job dequeued" until the worker yields.
 __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
     WinHeader *h = w.h;
-    const otf_scenario &sc = w.S.sc;
+    const otf_scenario &sc = *w.S.sc;
     for (;;) {
         if (sc.cache_enabled && (w.dflags[d] & D_CACHED)) {   // dedup on dequeue (backend.py:193-198)
             w.S.job_outcome(j, OTF_OUTCOME_DROPPED);
@@ -310,7 +346,7 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
 
 // One client server event: MediaServer.segment + Backend.handle (server.py:61-78, backend.py:115-133)
 __device__ void server_request(Win &w, int32_t cid, int32_t d, int64_t size) {
-    const otf_scenario &sc = w.S.sc;
+    const otf_scenario &sc = *w.S.sc;
     int64_t req_id = w.h->st.req_counter++;
     double arrival = w.now;
     int32_t rank = w.S.desc_rank(d);
@@ -344,7 +380,7 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
     int32_t d = k.desc, j = k.job;
     k.win = WIN_NONE;
     w.S.job_finished(j, w.now);
-    if (w.S.sc.cache_enabled) cache_put(w, d, k.size);
+    if (w.S.sc->cache_enabled) cache_put(w, d, k.size);
     resolve(w, d);
     // next job
     WinHeader *h = w.h;
@@ -355,7 +391,7 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
         worker_run(w, wid, e.desc, e.job);
     } else {
         int32_t pos = h->gq_head + h->gq_n;
-        if (pos >= w.S.sc.n_workers) pos -= w.S.sc.n_workers;
+        if (pos >= w.S.sc->n_workers) pos -= w.S.sc->n_workers;
         h->gq[pos] = wid;
         h->gq_n++;
         k.pc = W_GOT;
@@ -365,7 +401,7 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
 // Phase A: replay the window's server events in (time, creation, tick) order.
 __device__ void phase_a(Win &w) {
     WinHeader *h = w.h;
-    const int32_t K = w.S.sc.n_workers;
+    const int32_t K = w.S.sc->n_workers;
     int32_t i = 0;
     const int32_t n = h->n_list;
     for (;;) {
@@ -408,37 +444,36 @@ __device__ void phase_a(Win &w) {
 }
 
 // ---- client lanes ------------------------------------------------------------------
-// Arm a sleep for client c at w.now: returns true if the client keeps running
-// inside this window (the timer fires before the window ends).
+// Arm a sleep for client c at `now` (loop.sleep, sim.py:317-324): returns true
+// if the client keeps running inside this window (the timer fires before the
+// window ends), else files the timer on the wheel and returns false.
 __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now, double delay, int32_t next_pc) {
     c.pc = next_pc;
     if (delay <= 0) return true;                       // resolved future: no yield (sim.py:320-321)
-    if (isinf(delay)) {                                // never resolves (sim.py:322)
-        c.pc = C_HUNG;
-        w.cwin[cid] = WIN_NONE;
-        return false;
-    }
+    if (isinf(delay)) { c.pc = C_HUNG; return false; } // never resolves (sim.py:322)
     double when = now + delay;
     c.ctime = now;
     c.next_when = when;
     if (next_pc == C_SEG_LAT) {                        // a server event: always a later window
         int32_t k = timer_win(w, when);
-        if (k != WIN_NONE && k <= w.k) w.S.flag(OTF_S_TIE);   // lookahead violated (cannot happen)
-        w.cwin[cid] = (k == WIN_NONE) ? WIN_NONE : (k | WIN_SRV);
+        if (k == WIN_NONE) return false;
+        if (k <= w.k) w.S.flag(OTF_S_TIE);             // lookahead violated (cannot happen)
+        bucket_push(w, cid, k, K_SRV);
         return false;
     }
     if (when <= w.H && when < w.E) {                   // fires inside this window: keep going
         now = when;
         return true;
     }
-    w.cwin[cid] = timer_win(w, when);
+    int32_t k = timer_win(w, when);
+    if (k != WIN_NONE) bucket_push(w, cid, k, 0);
     return false;
 }
 
 __device__ void client_local(Win &w, int32_t cid) {
     Client &c = w.cl[cid];
     Scn &S = w.S;
-    const otf_scenario &sc = S.sc;
+    const otf_scenario &sc = *S.sc;
     double now = c.next_when;
     for (;;) {
         switch (c.pc) {
@@ -447,7 +482,7 @@ __device__ void client_local(Win &w, int32_t cid) {
             c.pc = C_SESSION;
             break;
         case C_SESSION:
-            if (!(now < sc.horizon)) { c.pc = C_DONE; w.cwin[cid] = WIN_NONE; return; }
+            if (!(now < sc.horizon)) { c.pc = C_DONE; return; }
             client_new_session(S, c, cid, now);
             if (sc.latency > 0) { if (!arm(w, c, cid, now, sc.latency, C_MAN_LAT)) return; }
             else c.pc = C_MAN_LAT;
@@ -489,7 +524,6 @@ __device__ void client_local(Win &w, int32_t cid) {
             c.pc = C_SESSION;
             break;
         default:
-            w.cwin[cid] = WIN_NONE;
             return;
         }
     }
@@ -500,53 +534,78 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) {
     return v;
 }
 
-// bitonic sort of the window's server events by (when, ctime) in shared memory
+// Order the window's server events by (time, arm time, client): each lane
+// ranks its entries against all others (ties are flagged afterwards).
 __device__ void sort_list(WinHeader *h, int lane) {
-    int32_t n = h->n_list;
+    const int32_t n = h->n_list;
     if (n <= 1) return;
-    int32_t p = 1;
-    while (p < n) p <<= 1;
-    for (int32_t i = n + lane; i < p; i += 32) {
-        h->list_when[i] = INFINITY; h->list_ctime[i] = INFINITY; h->list_id[i] = -1;
+    double my_w[LIST_CAP / 32], my_c[LIST_CAP / 32];
+    int64_t my_s[LIST_CAP / 32];
+    int32_t my_id[LIST_CAP / 32], my_d[LIST_CAP / 32], my_r[LIST_CAP / 32];
+    int32_t m = 0;
+    for (int32_t i = lane; i < n; i += 32, m++) {
+        double wi = h->list_when[i], ci = h->list_ctime[i];
+        int32_t idi = h->list_id[i];
+        int32_t r = 0;
+        for (int32_t j = 0; j < n; j++) {
+            double wj = h->list_when[j], cj = h->list_ctime[j];
+            r += (wj < wi) || (wj == wi && (cj < ci || (cj == ci && h->list_id[j] < idi)));
+        }
+        my_w[m] = wi; my_c[m] = ci; my_id[m] = idi; my_r[m] = r;
+        my_d[m] = h->list_desc[i]; my_s[m] = h->list_size[i];
     }
     __syncwarp();
-    for (int32_t size = 2; size <= p; size <<= 1) {
-        for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int32_t t = lane; t < (p >> 1); t += 32) {
-                int32_t lo = 2 * t - (t & (stride - 1));
-                int32_t hi = lo + stride;
-                bool up = ((lo & size) == 0);
-                double aw = h->list_when[lo], bw = h->list_when[hi];
-                double ac = h->list_ctime[lo], bc = h->list_ctime[hi];
-                bool gt = aw > bw || (aw == bw && (ac > bc || (ac == bc && h->list_id[lo] > h->list_id[hi])));
-                if (gt == up) {
-                    h->list_when[lo] = bw; h->list_when[hi] = aw;
-                    h->list_ctime[lo] = bc; h->list_ctime[hi] = ac;
-                    int32_t ti = h->list_id[lo]; h->list_id[lo] = h->list_id[hi]; h->list_id[hi] = ti;
-                    int32_t td = h->list_desc[lo]; h->list_desc[lo] = h->list_desc[hi]; h->list_desc[hi] = td;
-                    int64_t ts = h->list_size[lo]; h->list_size[lo] = h->list_size[hi]; h->list_size[hi] = ts;
-                }
-            }
-            __syncwarp();
+    for (int32_t t = 0; t < m; t++) {
+        int32_t r = my_r[t];
+        h->list_when[r] = my_w[t]; h->list_ctime[r] = my_c[t]; h->list_id[r] = my_id[t];
+        h->list_desc[r] = my_d[t]; h->list_size[r] = my_s[t];
+    }
+    __syncwarp();
+}
+
+// Next non-empty window after k_done on the wheel (warp-wide bitmap scan).
+__device__ int32_t wheel_next(WinHeader *h, int32_t k_done, int lane) {
+    const int32_t start = k_done + 1;
+    const int32_t p0 = start & (RING - 1);
+    const int32_t w0 = p0 >> 5;
+    constexpr int32_t NW = RING / 32;
+    int32_t best = WIN_NONE;
+    // virtual words 0..NW: word 0 = first word from bit p0, word NW = its low bits (wrap)
+    for (int32_t v = lane; v <= NW; v += 32) {
+        uint32_t bits;
+        if (v == 0) bits = h->bits[w0] & (0xffffffffu << (p0 & 31));
+        else if (v == NW) bits = (p0 & 31) ? (h->bits[w0] & ((1u << (p0 & 31)) - 1)) : 0u;
+        else bits = h->bits[(w0 + v) & (NW - 1)];
+        if (bits) {
+            int32_t slot = (((v == NW ? w0 : (w0 + v) & (NW - 1))) << 5) + (__ffs(bits) - 1);
+            int32_t dist = (slot - p0) & (RING - 1);
+            if (v == NW && dist == 0) dist = RING;
+            best = min(best, start + dist);
         }
     }
+    return warp_min(best);
 }
 
 __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x;
+    long long t_start = 0, t0 = 0, t1 = 0;
     const int32_t s = b.order ? b.order[blockIdx.x] : (int32_t)blockIdx.x;
+    WinHeader *h = (WinHeader *)smem;
+    if (lane == 0) { h->b = b; h->sc = b.scenarios[s]; }
+    __syncwarp();
     Win w;
-    w.S.init(b, s);
-    const otf_scenario &sc = w.S.sc;
+    w.S.init(&h->b, &h->sc, s);
+    const otf_scenario &sc = h->sc;
     const int32_t N = sc.n_clients, K = sc.n_workers;
     const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
-    WinHeader *h = (WinHeader *)smem;
     uint8_t *p = smem + ((sizeof(WinHeader) + 15) & ~(size_t)15);
     w.h = h;
-    w.cwin = (int32_t *)p; p += 4 * (int64_t)N;
-    w.lru_prev = (int32_t *)p; p += 4 * D;
-    w.lru_next = (int32_t *)p; p += 4 * D;
+    w.bnext = (int32_t *)p; p += 4 * (int64_t)N;
+    w.ckind = p; p += N;
+    p = (uint8_t *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    w.lru_prev = (int16_t *)p; p += 2 * D;
+    w.lru_next = (int16_t *)p; p += 2 * D;
     w.dflags = p;
     uint8_t *g = b.scratch + sc.scratch_off;
     WinGlobalLayout L = win_global_layout(N, D);
@@ -555,14 +614,17 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     w.wq_head = (int32_t *)(g + L.wq_head);
     w.wq_tail = (int32_t *)(g + L.wq_tail);
     w.jq = (JobEnt *)(g + L.jobq);
-    // counters and QoE accumulate in shared memory, flushed at the end
+    // counters, QoE and small tables live in shared memory
     w.S.st = &h->st;
     w.S.stats = h->stats;
     w.S.q = &h->q;
     w.W = sc.latency * (1.0 - 0x1p-20);
     w.H = sc.horizon;
+    w.k = -1;
 
     // ---- init -------------------------------------------------------------------
+    const bool fits = K <= MAXK && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB && D < 32767 &&
+                      sc.latency > 0 && sc.horizon / (sc.latency * (1.0 - 0x1p-20)) < 5.0e8;
     if (lane == 0) {
         EngineState z = {};
         z.lru_head = z.lru_tail = -1;
@@ -573,21 +635,43 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         h->gq_head = 0; h->gq_n = K; h->fq_head = 0; h->fq_n = 0;
         h->jq_head = 0; h->jq_n = 0; h->jq_cap = (int32_t)(D + 1);
         h->n_list = 0; h->n_blist = 0; h->wseq = 0;
-        if (K > MAXK || N >= WIN_SRV || !(sc.latency > 0)) h->st.status |= OTF_S_TIE;   // not for this engine
+        h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
+        if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
     }
+    __syncwarp();
+    if (!fits) goto done;
     for (int32_t q = lane; q < MAXK; q += 32) {
         h->gq[q] = q;                                  // workers register as getters in id order
         WWorker z = {};
         z.win = WIN_NONE; z.pc = W_GOT; z.desc = -1; z.job = -1;
         h->wk[q] = z;
     }
+    for (int32_t i = lane; i < RING; i += 32) h->bhead[i] = -1;
+    for (int32_t i = lane; i < RING / 32; i += 32) h->bits[i] = 0;
+    for (int32_t i = lane; i < sc.n_seq; i += 32) {
+        h->t_segcount[i] = w.S.segcounts[i];
+        h->t_seqdur[i] = w.S.seqdur[i];
+        h->t_segdur[i] = w.S.segdur[i];
+        h->t_zipf[i] = w.S.zipf[i];
+        h->t_manifest[i] = w.S.manifest_b[i];
+    }
+    for (int32_t i = lane; i < sc.n_ranks; i += 32) {
+        h->t_rho[i] = w.S.rho[i];
+        h->t_bitrates[i] = w.S.bitrates[i];
+    }
     for (int64_t d = lane; d < D; d += 32) {
         w.lru_prev[d] = -1; w.lru_next[d] = -1; w.dflags[d] = 0;
         w.wq_head[d] = -1; w.wq_tail[d] = -1;
     }
     __syncwarp();
-    if (h->st.status & OTF_S_TIE) goto done;
-    // clients: first step arms sleep(offset) (orchestrator.py:337)
+    w.S.segcounts = h->t_segcount;
+    w.S.seqdur = h->t_seqdur;
+    w.S.segdur = h->t_segdur;
+    w.S.zipf = h->t_zipf;
+    w.S.manifest_b = h->t_manifest;
+    w.S.rho = h->t_rho;
+    w.S.bitrates = h->t_bitrates;
+    // clients: the first step arms sleep(offset) (orchestrator.py:337)
     for (int32_t c = lane; c < N; c += 32) {
         Client &cl = w.cl[c];
         client_init(cl);
@@ -595,70 +679,109 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         cl.pc = C_ARRIVED;
         cl.ctime = 0.0;
         cl.next_when = 0.0 + off;
-        if (!(off > 0)) { w.S.flag(OTF_S_TIE); }       // instant start: tick order among clients matters
-        w.cwin[c] = isinf(off) ? WIN_NONE : timer_win(w, cl.next_when);
+        if (!(off > 0)) w.S.flag(OTF_S_TIE);           // instant start: tick order among clients matters
+        int32_t wk = isinf(off) ? WIN_NONE : timer_win(w, cl.next_when);
+        if (wk != WIN_NONE) bucket_push(w, c, wk, 0);
     }
     __syncwarp();
 
     // ---- window loop --------------------------------------------------------------
+    t_start = clock64();
     for (;;) {
-        int32_t m = WIN_NONE;
-        for (int32_t c = lane; c < N; c += 32) m = min(m, w.cwin[c] & ~WIN_SRV);
-        if (lane < K) m = min(m, h->wk[lane].win);
-        m = warp_min(m);
+        t0 = clock64();
+        // next window: wheel, far list, worker timers
+        int32_t m = wheel_next(h, h->k_done, lane);
+        int32_t mw = lane < K ? h->wk[lane].win : WIN_NONE;
+        m = min(m, warp_min(mw));
+        m = min(m, h->far_min);
         if (m == WIN_NONE) break;
-        w.k = m;
-        w.E = (double)(m + 1) * w.W;
-        if (lane == 0) { h->n_list = 0; h->n_blist = 0; h->stats[OTF_ST_WINDOWS]++; }
-        __syncwarp();
-        // collect this window's clients: server events -> sorted list, local -> B-list
-        for (int32_t base = 0; base < N; base += 32) {
-            int32_t c = base + lane;
-            int32_t v = c < N ? w.cwin[c] : WIN_NONE;
-            bool cand = (v & ~WIN_SRV) == m;
-            bool srv = cand && (v & WIN_SRV);
-            unsigned ms = __ballot_sync(0xffffffffu, srv);
-            unsigned ml = __ballot_sync(0xffffffffu, cand && !srv);
-            int32_t nl = h->n_list, nb = h->n_blist;
-            __syncwarp();
-            if (srv) {
-                int32_t pos = nl + __popc(ms & ((1u << lane) - 1));
-                if (pos < LIST_CAP) {
-                    const Client &cl = w.cl[c];
-                    h->list_when[pos] = cl.next_when;
-                    h->list_ctime[pos] = cl.ctime;
-                    h->list_id[pos] = c;
-                    h->list_desc[pos] = cl.desc;
-                    h->list_size[pos] = w.S.size(cl.desc);
+        if (h->far_n > 0 && h->far_min < m + RING) {   // far timers now within the wheel: re-file them
+            if (lane == 0) {
+                int32_t c = h->far_head;
+                h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
+                h->k_done = m - 1;                     // windows before m are empty: wheel base = m
+                while (c >= 0) {
+                    int32_t nx = w.bnext[c];
+                    int32_t wk = timer_win(w, w.cl[c].next_when);
+                    if (wk - m < RING) {
+                        int32_t slot = wk & (RING - 1);
+                        w.bnext[c] = h->bhead[slot];
+                        h->bhead[slot] = c;
+                        h->bits[slot >> 5] |= 1u << (slot & 31);
+                    } else {
+                        w.bnext[c] = h->far_head;
+                        h->far_head = c;
+                        h->far_n++;
+                        h->far_min = min(h->far_min, wk);
+                    }
+                    c = nx;
                 }
             }
-            if (cand && !srv) w.blist[nb + __popc(ml & ((1u << lane) - 1))] = c;
-            if (cand) w.cwin[c] = WIN_NONE;
             __syncwarp();
-            if (lane == 0) { h->n_list = nl + __popc(ms); h->n_blist = nb + __popc(ml); }
-            __syncwarp();
+            continue;
         }
+        w.k = m;
+        w.E = (double)(m + 1) * w.W;
+        // pop the bucket: server events -> list, client-local events -> B-list
+        if (lane == 0) {
+            h->stats[OTF_ST_WINDOWS]++;
+            int32_t slot = m & (RING - 1);
+            int32_t c = h->bhead[slot];
+            h->bhead[slot] = -1;
+            h->bits[slot >> 5] &= ~(1u << (slot & 31));
+            int32_t nl = 0, nb = 0;
+            while (c >= 0) {
+                int32_t nx = w.bnext[c];
+                if (w.ckind[c] & K_SRV) { if (nl < LIST_CAP) h->list_id[nl] = c; nl++; }
+                else w.blist[nb++] = c;
+                c = nx;
+            }
+            h->n_list = nl;
+            h->n_blist = nb;
+        }
+        __syncwarp();
         if (h->n_list > LIST_CAP) {                    // too many simultaneous requests for this engine
             if (lane == 0) h->st.status |= OTF_S_TIE;
             __syncwarp();
             break;
         }
-        sort_list(h, lane);
+        for (int32_t i = lane; i < h->n_list; i += 32) {   // gather sort keys + request descriptors
+            const Client &cl = w.cl[h->list_id[i]];
+            int32_t d = cl.desc;
+            h->list_when[i] = cl.next_when;
+            h->list_ctime[i] = cl.ctime;
+            h->list_desc[i] = d;
+            h->list_size[i] = w.S.size(d);
+        }
         __syncwarp();
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
+        t0 = t1;
+        sort_list(h, lane);
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
+        t0 = t1;
         // ---- phase A: server lane ----
         if (lane == 0) {
-            for (int32_t i = 1; i < h->n_list; i++)    // equal (time, creation time): tick order unknown
+            for (int32_t i = 1; i < h->n_list; i++)    // equal (time, arm time): tick order unknown
                 if (h->list_when[i] == h->list_when[i - 1] && h->list_ctime[i] == h->list_ctime[i - 1])
                     h->st.status |= OTF_S_TIE;
             phase_a(w);
+            h->k_done = m;
         }
         __syncwarp();
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_SERVER] += t1 - t0;
+        t0 = t1;
         if (h->st.status & OTF_S_TIE) break;
         // ---- phase B: client lanes ----
         const int32_t nb = h->n_blist;
         for (int32_t i = lane; i < nb; i += 32) client_local(w, w.blist[i]);
         __syncwarp();
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_CLIENTS] += t1 - t0;
     }
+    if (lane == 0) h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
     if (!(h->st.status & OTF_S_TIE)) {

@@ -25,21 +25,38 @@ struct Trace {
     const double *starts;   // [n]
     const double *values;   // [n]
     double period, pbits;
+    double grid;            // > 0: starts[i] == i * grid exactly
     int32_t n;
 };
 
-// BandwidthTrace._drain_from (netem.py:77-95)
-OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
-    int32_t lo = 0, hi = tr.n;                 // bisect_right(starts, phase)
+// bisect_right(starts, phase) - 1, clamped at 0 (netem.py:80)
+OTF_HD int32_t trace_piece(const Trace &tr, double phase) {
+    if (tr.grid > 0) {
+        double q = phase / tr.grid;
+        int32_t i = q < (double)tr.n ? (int32_t)q : tr.n - 1;
+        if (i < 0) i = 0;
+        while (i + 1 < tr.n && (double)(i + 1) * tr.grid <= phase) i++;
+        while (i > 0 && (double)i * tr.grid > phase) i--;
+        return i;
+    }
+    int32_t lo = 0, hi = tr.n;
     while (lo < hi) {
         int32_t mid = (lo + hi) >> 1;
         if (phase < tr.starts[mid]) hi = mid; else lo = mid + 1;
     }
-    int32_t i = lo - 1;
-    if (i < 0) i = 0;
+    return lo > 0 ? lo - 1 : 0;
+}
+
+OTF_HD double piece_start(const Trace &tr, int32_t i) {
+    return tr.grid > 0 ? (double)i * tr.grid : tr.starts[i];
+}
+
+// BandwidthTrace._drain_from (netem.py:77-95)
+OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
+    int32_t i = trace_piece(tr, phase);
     double spent = 0.0, pos = phase;
     for (; i < tr.n; i++) {
-        double seg_end = (i + 1 < tr.n) ? tr.starts[i + 1] : tr.period;
+        double seg_end = (i + 1 < tr.n) ? piece_start(tr, i + 1) : tr.period;
         double width = seg_end - pos;
         if (width > 0) {
             double v = tr.values[i];

@@ -199,7 +199,8 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
                                 math.log(ne.median_bps), ne.sigma, decay, spread, ne.floor_bps, ne.cap_bps,
                                 values.ctypes.data_as(dp), pbits.ctypes.data_as(dp), threads)
         _lib.check(rc, "otf_build_traces")
-        trace_tab[key] = dict(n=n, period=period,
+        grid = float(ne.step_s) if all(x == float(i) * ne.step_s for i, x in enumerate(starts)) else 0.0
+        trace_tab[key] = dict(n=n, period=period, grid=grid,
                               starts=P.add("f64", starts_a), values=P.add("f64", values),
                               pbits=P.add("f64", pbits))
         input_bytes += values.nbytes + pbits.nbytes + starts_a.nbytes
@@ -278,6 +279,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.alpha, sc.headroom = float(cfg.client.ewma_alpha), float(cfg.client.headroom)
         sc.noise = float(cfg.noise_rel_std)
         sc.period = tt["period"]
+        sc.grid_step = tt["grid"]
         sc.off_sizes, sc.off_bitrates, sc.off_manifest, sc.off_segcount = o_sizes, o_bitrates, o_man, o_counts
         sc.off_seqdur, sc.off_segdur, sc.off_rho, sc.off_zipf = o_seqdur, o_segdur, o_rho, o_zipf
         sc.off_starts, sc.off_values, sc.off_pbits = tt["starts"], tt["values"], tt["pbits"]
