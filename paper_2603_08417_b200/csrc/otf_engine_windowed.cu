@@ -75,7 +75,7 @@ struct WinHeader {
     // the window's server events
     double list_when[LIST_CAP];
     double list_ctime[LIST_CAP];
-    int64_t list_size[LIST_CAP];
+    int32_t list_pack[LIST_CAP];         // rank | index << 8 | seq << 16
     int32_t list_id[LIST_CAP];
     int32_t list_desc[LIST_CAP];
 };
@@ -118,6 +118,10 @@ struct Win {
     JobEnt *jq;
     double W, H, E, now;
     int32_t k;
+    // lane 0's register copies of the hot server counters during phase A
+    int64_t req_counter, n_req;
+    int32_t n_blist;
+    bool wdirty;
 };
 
 // window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles)
@@ -221,12 +225,11 @@ __device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backe
     }
 }
 
-__device__ void maybe_speculate(Win &w, int32_t d) {                     // backend.py:135-154
+__device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, int32_t index) {  // backend.py:135-154
     int64_t *st = w.h->stats;
     if (!w.S.sc->spec_enabled) { st[OTF_ST_SKIP_DISABLED]++; return; }
-    int32_t seq = w.S.desc_seq(d), rank = w.S.desc_rank(d), index = w.S.desc_index(d);
-    if (index + 1 >= w.S.segcount(seq)) { st[OTF_ST_SKIP_EOS]++; return; }
-    if (w.S.stored(rank)) { st[OTF_ST_SKIP_STORED]++; return; }
+    if (index + 1 >= w.S.segcounts[seq]) { st[OTF_ST_SKIP_EOS]++; return; }
+    if ((w.S.sc->stored_mask >> rank) & 1u) { st[OTF_ST_SKIP_STORED]++; return; }
     int32_t nd = d + 1;                                // same (seq, rank), index + 1
     uint8_t f = w.dflags[nd];
     if (w.S.sc->cache_enabled && (f & D_CACHED)) { st[OTF_ST_SKIP_CACHED]++; return; }
@@ -235,58 +238,33 @@ __device__ void maybe_speculate(Win &w, int32_t d) {                     // back
     st[OTF_ST_SPEC_ENQUEUED]++;
 }
 
-// MediaServer.segment's record append at response time (server.py:76-77) +
-// handing the client back to the client lanes at instant `now`.
-__device__ void respond(Win &w, int32_t cid, int32_t d, int64_t size, int32_t path, int64_t req_id,
-                        double arrival) {
+// Response of MediaServer.segment (server.py:76-77): fix the record's slot
+// in response order and hand the client back to the client lanes at `now`.
+// The record itself and the request QoE are written by the client lane.
+__device__ __forceinline__ void respond(Win &w, int32_t cid) {
     Client &c = w.cl[cid];
-    int64_t r = w.h->st.n_req++;
-    const otf_scenario &sc = *w.S.sc;
-    if (w.S.records) {
-        if (r < sc.req_cap) {
-            int64_t o = sc.req_off + r;
-            w.S.b->req_id[o] = req_id;
-            w.S.b->req_seq[o] = w.S.desc_seq(d);
-            w.S.b->req_rep[o] = w.S.desc_rank(d);
-            w.S.b->req_index[o] = w.S.desc_index(d);
-            w.S.b->req_path[o] = path;
-            w.S.b->req_arrival[o] = arrival;
-            w.S.b->req_response[o] = w.now;
-            w.S.b->req_bytes[o] = size;
-        } else {
-            w.S.flag(OTF_S_RECORD_OVERFLOW);
-        }
-    }
-    double lat = w.now - arrival;
-    otf_qoe &q = w.h->q;
-    q.lat_hist[lat_bin(lat)]++;
-    q.path_count[path]++;
-    q.n_requests++;
-    q.latency_sum += lat;
+    c.req_slot = w.n_req++;
     c.pc = C_SEG_RESP;
     c.next_when = w.now;
-    c.size = size;
-    w.blist[w.h->n_blist++] = cid;
+    w.blist[w.n_blist++] = cid;
 }
 
 __device__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
     if (!(w.dflags[d] & D_INFLIGHT)) return;
     w.dflags[d] &= ~D_INFLIGHT;
-    int64_t size = w.S.size(d);
-    for (int32_t c = w.wq_head[d]; c >= 0;) {
-        Client &cl = w.cl[c];
-        int32_t nxt = cl.wait_next;
-        respond(w, c, d, size, cl.path, cl.req_id, cl.arrival);
+    int32_t c = w.wq_head[d];
+    while (c >= 0) {                                   // waiter Future callbacks, await order
+        int32_t nxt = w.bnext[c];
+        respond(w, c);
         c = nxt;
     }
-    w.wq_head[d] = -1;
-    w.wq_tail[d] = -1;
 }
 
-__device__ void add_waiter(Win &w, int32_t d, int32_t cid) {
-    w.cl[cid].wait_next = -1;
+// waiter links reuse bnext: a waiting client has no pending timer
+__device__ __forceinline__ void add_waiter(Win &w, int32_t d, int32_t cid) {
+    w.bnext[cid] = -1;
     int32_t t = w.wq_tail[d];
-    if (t >= 0) w.cl[t].wait_next = cid; else w.wq_head[d] = cid;
+    if (t >= 0) w.bnext[t] = cid; else w.wq_head[d] = cid;
     w.wq_tail[d] = cid;
 }
 
@@ -313,6 +291,7 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
             k.job = j;
             k.size = w.S.size(d);
             k.pc = W_SERVICE;
+            w.wdirty = true;
             return;
         }
         // next job: Queue.get on a non-empty queue does not yield (sim.py:242-244)
@@ -329,6 +308,7 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
         h->gq_n++;
         h->wk[wid].pc = W_GOT;
         h->wk[wid].win = WIN_NONE;
+        w.wdirty = true;
         return;
     }
 }
@@ -345,30 +325,27 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
 }
 
 // One client server event: MediaServer.segment + Backend.handle (server.py:61-78, backend.py:115-133)
-__device__ void server_request(Win &w, int32_t cid, int32_t d, int64_t size) {
+__device__ void server_request(Win &w, int32_t cid, int32_t d, int32_t rank, int32_t seq, int32_t index) {
     const otf_scenario &sc = *w.S.sc;
-    int64_t req_id = w.h->st.req_counter++;
-    double arrival = w.now;
-    int32_t rank = w.S.desc_rank(d);
-    if (w.S.stored(rank)) {
-        respond(w, cid, d, size, OTF_PATH_STORAGE, req_id, arrival);
+    Client &c = w.cl[cid];
+    c.req_id = w.req_counter++;
+    c.arrival = w.now;
+    if ((sc.stored_mask >> rank) & 1u) {
+        c.path = OTF_PATH_STORAGE;
+        respond(w, cid);
     } else if (sc.cache_enabled && cache_get(w, d)) {
-        maybe_speculate(w, d);
-        respond(w, cid, d, size, OTF_PATH_CACHE, req_id, arrival);
+        maybe_speculate(w, d, rank, seq, index);
+        c.path = OTF_PATH_CACHE;
+        respond(w, cid);
     } else {
-        Client &c = w.cl[cid];
-        int32_t path;
         if (w.dflags[d] & D_INFLIGHT) {
-            maybe_speculate(w, d);
-            path = OTF_PATH_WAITED;
+            maybe_speculate(w, d, rank, seq, index);
+            c.path = OTF_PATH_WAITED;
         } else {
             enqueue_job(w, d, OTF_ORIGIN_DEMAND);
-            maybe_speculate(w, d);
-            path = OTF_PATH_TRANSCODED;
+            maybe_speculate(w, d, rank, seq, index);
+            c.path = OTF_PATH_TRANSCODED;
         }
-        c.path = path;
-        c.req_id = req_id;
-        c.arrival = arrival;
         c.pc = C_SEG_WAIT;
         add_waiter(w, d, cid);
     }
@@ -379,6 +356,7 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
     WWorker &k = w.h->wk[wid];
     int32_t d = k.desc, j = k.job;
     k.win = WIN_NONE;
+    w.wdirty = true;
     w.S.job_finished(j, w.now);
     if (w.S.sc->cache_enabled) cache_put(w, d, k.size);
     resolve(w, d);
@@ -402,18 +380,27 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
 __device__ void phase_a(Win &w) {
     WinHeader *h = w.h;
     const int32_t K = w.S.sc->n_workers;
-    int32_t i = 0;
     const int32_t n = h->n_list;
+    w.req_counter = h->st.req_counter;
+    w.n_req = h->st.n_req;
+    w.n_blist = h->n_blist;
+    w.wdirty = true;
+    int32_t bw = -1;
+    int64_t pops = 0;
+    int32_t i = 0;
     for (;;) {
-        int32_t bw = -1;
-        for (int32_t q = 0; q < K; q++) {
-            const WWorker &x = h->wk[q];
-            if (x.win != w.k) continue;
-            if (bw < 0) { bw = q; continue; }
-            const WWorker &y = h->wk[bw];
-            if (x.when < y.when || (x.when == y.when && (x.ctime < y.ctime ||
-                                                         (x.ctime == y.ctime && x.seq < y.seq))))
-                bw = q;
+        if (w.wdirty) {                                // earliest worker timer in this window
+            bw = -1;
+            for (int32_t q = 0; q < K; q++) {
+                const WWorker &x = h->wk[q];
+                if (x.win != w.k) continue;
+                if (bw < 0) { bw = q; continue; }
+                const WWorker &y = h->wk[bw];
+                if (x.when < y.when || (x.when == y.when && (x.ctime < y.ctime ||
+                                                             (x.ctime == y.ctime && x.seq < y.seq))))
+                    bw = q;
+            }
+            w.wdirty = false;
         }
         bool take_worker;
         if (bw < 0 && i >= n) break;
@@ -430,17 +417,22 @@ __device__ void phase_a(Win &w) {
                 else { w.S.flag(OTF_S_TIE); take_worker = true; }
             }
         }
-        h->stats[OTF_ST_TIMER_POPS]++;
+        pops++;
         if (take_worker) {
             w.now = h->wk[bw].when;
             server_worker_done(w, bw);
         } else {
             w.now = h->list_when[i];
-            server_request(w, h->list_id[i], h->list_desc[i], h->list_size[i]);
+            int32_t pk = h->list_pack[i];
+            server_request(w, h->list_id[i], h->list_desc[i], pk & 0xff, pk >> 16, (pk >> 8) & 0xff);
             i++;
         }
-        drain_handoffs(w);
+        if (h->fq_n > 0) drain_handoffs(w);
     }
+    h->stats[OTF_ST_TIMER_POPS] += pops;
+    h->st.req_counter = w.req_counter;
+    h->st.n_req = w.n_req;
+    h->n_blist = w.n_blist;
 }
 
 // ---- client lanes ------------------------------------------------------------------
@@ -470,8 +462,46 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
     return false;
 }
 
+__device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid);
+
 __device__ void client_local(Win &w, int32_t cid) {
-    Client &c = w.cl[cid];
+    Client c = w.cl[cid];                              // one vectorised load; state lives in registers
+    client_local_body(w, c, cid);
+    w.cl[cid] = c;
+}
+
+// The response's record + QoE (server.py:76-77, metrics.py:67-78), written by the
+// client lane in parallel; the slot (response order) was fixed by the server lane.
+__device__ __forceinline__ void record_response(Win &w, const Client &c, double now) {
+    Scn &S = w.S;
+    const otf_scenario &sc = *S.sc;
+    int64_t size = S.size(c.desc);
+    if (S.records) {
+        int64_t r = c.req_slot;
+        if (r < sc.req_cap) {
+            int64_t o = sc.req_off + r;
+            S.b->req_id[o] = c.req_id;
+            S.b->req_seq[o] = c.seq;
+            S.b->req_rep[o] = c.rank;
+            S.b->req_index[o] = c.index;
+            S.b->req_path[o] = c.path;
+            S.b->req_arrival[o] = c.arrival;
+            S.b->req_response[o] = now;
+            S.b->req_bytes[o] = size;
+        } else {
+            S.flag(OTF_S_RECORD_OVERFLOW);
+        }
+    }
+    typedef unsigned long long ull;
+    double lat = now - c.arrival;
+    otf_qoe &q = w.h->q;
+    atomicAdd((ull *)&q.lat_hist[lat_bin(lat)], 1ull);
+    atomicAdd((ull *)&q.path_count[c.path], 1ull);
+    atomicAdd((ull *)&q.n_requests, 1ull);
+    atomicAdd(&q.latency_sum, lat);
+}
+
+__device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid) {
     Scn &S = w.S;
     const otf_scenario &sc = *S.sc;
     double now = c.next_when;
@@ -510,6 +540,8 @@ __device__ void client_local(Win &w, int32_t cid) {
             S.flag(OTF_S_INTERNAL);                    // zero latency never reaches this engine
             return;
         case C_SEG_RESP: {
+            record_response(w, c, now);
+            c.size = S.size(c.desc);
             c.xfer_start = now;
             double end = completion_time(S.trace(cid), now, c.size);
             if (!arm(w, c, cid, now, end - now, C_SEG_XFER)) return;
@@ -540,7 +572,7 @@ __device__ void sort_list(WinHeader *h, int lane) {
     const int32_t n = h->n_list;
     if (n <= 1) return;
     double my_w[LIST_CAP / 32], my_c[LIST_CAP / 32];
-    int64_t my_s[LIST_CAP / 32];
+    int32_t my_s[LIST_CAP / 32];
     int32_t my_id[LIST_CAP / 32], my_d[LIST_CAP / 32], my_r[LIST_CAP / 32];
     int32_t m = 0;
     for (int32_t i = lane; i < n; i += 32, m++) {
@@ -552,13 +584,13 @@ __device__ void sort_list(WinHeader *h, int lane) {
             r += (wj < wi) || (wj == wi && (cj < ci || (cj == ci && h->list_id[j] < idi)));
         }
         my_w[m] = wi; my_c[m] = ci; my_id[m] = idi; my_r[m] = r;
-        my_d[m] = h->list_desc[i]; my_s[m] = h->list_size[i];
+        my_d[m] = h->list_desc[i]; my_s[m] = h->list_pack[i];
     }
     __syncwarp();
     for (int32_t t = 0; t < m; t++) {
         int32_t r = my_r[t];
         h->list_when[r] = my_w[t]; h->list_ctime[r] = my_c[t]; h->list_id[r] = my_id[t];
-        h->list_desc[r] = my_d[t]; h->list_size[r] = my_s[t];
+        h->list_desc[r] = my_d[t]; h->list_pack[r] = my_s[t];
     }
     __syncwarp();
 }
@@ -747,11 +779,10 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         }
         for (int32_t i = lane; i < h->n_list; i += 32) {   // gather sort keys + request descriptors
             const Client &cl = w.cl[h->list_id[i]];
-            int32_t d = cl.desc;
             h->list_when[i] = cl.next_when;
             h->list_ctime[i] = cl.ctime;
-            h->list_desc[i] = d;
-            h->list_size[i] = w.S.size(d);
+            h->list_desc[i] = cl.desc;
+            h->list_pack[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
         }
         __syncwarp();
         t1 = clock64();

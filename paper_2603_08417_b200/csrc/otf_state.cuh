@@ -31,7 +31,7 @@ struct Client {
     Buffer buf;                 // 56 B
     double est, requested, arrival, xfer_start;
     double next_when, ctime;    // windowed engine: pending timer (fire time, arm time)
-    int64_t req_id, size;
+    int64_t req_id, size, req_slot;
     int32_t pc, seq, session, index, rank, has_est, buf_live, sess_open;
     int32_t path, desc, wait_next, pad;
     Pcg64 picks;                // sequence-pick stream SS([seed, 3, cid])
