@@ -24,13 +24,30 @@ struct EngineState {                 // first 256 B of every scenario arena
     int32_t pad;
 };
 
+// QoE accumulators: 32-bit counters (native shared/global atomics); the float
+// sums are accumulated per lane (Scn members) and reduced at the end.
+struct QoeAcc {
+    uint32_t lat_hist[OTF_LAT_BINS];
+    uint32_t path_count[4];
+    uint32_t stall_hist[OTF_STALL_BINS];
+    uint32_t rank_count[OTF_RANK_BINS];
+    uint32_t n_requests, n_sessions, n_segments, n_finished, n_started, pad[3];
+};
+
+__device__ __forceinline__ void qoe_zero(QoeAcc *a, int lane, int nlanes) {
+    uint32_t *p = (uint32_t *)a;
+    for (int i = lane; i < (int)(sizeof(QoeAcc) / 4); i += nlanes) p[i] = 0;
+}
+
 struct Scn {
     const otf_batch *b;              // shared memory (windowed) or a local copy (exact)
     const otf_scenario *sc;          // shared memory (windowed) or global (exact)
     int32_t s;
     EngineState *st;
     int64_t *stats;
-    otf_qoe *q;
+    otf_qoe *q;                      // final destination (global)
+    QoeAcc *qa;                      // counters while running (shared or scratch)
+    double lat_sum, stall_sum, startup_sum;   // this lane's float sums
     const int64_t *sizes, *bitrates, *manifest_b;
     const int32_t *segcounts;
     const double *seqdur, *segdur, *rho, *zipf, *starts, *values, *pbits, *arrivals, *eps;
@@ -65,8 +82,20 @@ struct Scn {
         z.lru_head = z.lru_tail = -1;
         *st = z;
         for (int i = 0; i < OTF_ST_NSLOTS; i++) stats[i] = 0;
-        int64_t *qq = (int64_t *)q;
-        for (size_t i = 0; i < sizeof(otf_qoe) / 8; i++) qq[i] = 0;
+        qoe_zero(qa, 0, 1);
+        lat_sum = stall_sum = startup_sum = 0.0;
+    }
+
+    // write the final otf_qoe (sums already reduced into this lane's members)
+    __device__ void flush_qoe() const {
+        for (int i = 0; i < OTF_LAT_BINS; i++) q->lat_hist[i] = qa->lat_hist[i];
+        for (int i = 0; i < 4; i++) q->path_count[i] = qa->path_count[i];
+        for (int i = 0; i < OTF_STALL_BINS; i++) q->stall_hist[i] = qa->stall_hist[i];
+        for (int i = 0; i < OTF_RANK_BINS; i++) q->rank_count[i] = qa->rank_count[i];
+        q->n_requests = qa->n_requests; q->n_sessions = qa->n_sessions; q->n_segments = qa->n_segments;
+        q->n_finished = qa->n_finished; q->n_started = qa->n_started; q->pad = 0;
+        q->latency_sum = lat_sum; q->stall_time_sum = stall_sum; q->startup_delay_sum = startup_sum;
+        q->pad2 = 0.0;
     }
 
     __device__ __forceinline__ int64_t &stat(int i) { return stats[i]; }
@@ -161,10 +190,10 @@ struct Scn {
             }
         }
         double lat = response - c.arrival;
-        q->lat_hist[lat_bin(lat)]++;
-        q->path_count[c.path]++;
-        q->n_requests++;
-        q->latency_sum += lat;
+        qa->lat_hist[lat_bin(lat)]++;
+        qa->path_count[c.path]++;
+        qa->n_requests++;
+        lat_sum += lat;
     }
 
     __device__ void sync_session(const Client &c, double now) {      // _sync_report (client.py:284-288)
@@ -178,18 +207,17 @@ struct Scn {
 
     // session QoE, once per session when its numbers are final
     __device__ void qoe_session(const Client &c, bool finished) {
-        typedef unsigned long long ull;
         int32_t stalls = c.buf_live ? c.buf.stall_events : 0;
-        atomicAdd((ull *)&q->n_sessions, 1ull);
-        atomicAdd((ull *)&q->stall_hist[stalls < OTF_STALL_BINS - 1 ? stalls : OTF_STALL_BINS - 1], 1ull);
+        atomicAdd(&qa->n_sessions, 1u);
+        atomicAdd(&qa->stall_hist[stalls < OTF_STALL_BINS - 1 ? stalls : OTF_STALL_BINS - 1], 1u);
         if (c.buf_live) {
-            atomicAdd(&q->stall_time_sum, c.buf.stall_time);
+            stall_sum += c.buf.stall_time;
             if (!isnan(c.buf.started_at)) {
-                atomicAdd((ull *)&q->n_started, 1ull);
-                atomicAdd(&q->startup_delay_sum, c.buf.started_at - c.buf.session_start);
+                atomicAdd(&qa->n_started, 1u);
+                startup_sum += c.buf.started_at - c.buf.session_start;
             }
         }
-        if (finished) atomicAdd((ull *)&q->n_finished, 1ull);
+        if (finished) atomicAdd(&qa->n_finished, 1u);
     }
 
     __device__ void finish() {
@@ -296,8 +324,8 @@ __device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
             S.flag(OTF_S_RECORD_OVERFLOW);
         }
     }
-    atomicAdd((unsigned long long *)&S.q->rank_count[c.rank < OTF_RANK_BINS ? c.rank : OTF_RANK_BINS - 1], 1ull);
-    atomicAdd((unsigned long long *)&S.q->n_segments, 1ull);
+    atomicAdd(&S.qa->rank_count[c.rank < OTF_RANK_BINS ? c.rank : OTF_RANK_BINS - 1], 1u);
+    atomicAdd(&S.qa->n_segments, 1u);
     S.sync_session(c, now);
     c.index++;
     if (c.index < S.segcount(c.seq)) return true;

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
     ExactWorld w;
     otf_batch bl = b;
     w.S.init(&bl, &b.scenarios[s], s);
+    w.S.qa = (QoeAcc *)(b.scratch + b.scenarios[s].scratch_off + 256);
     w.S.reset_outputs();
     const otf_scenario &sc = *w.S.sc;
     int64_t n_desc = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
     // harvest at the horizon (orchestrator.py:357-359, client.py:177-187)
     for (int32_t c = 0; c < sc.n_clients; c++) client_harvest(w.S, w.cl[c], w.now);
     w.S.finish();
+    w.S.flush_qoe();
 }
 
 }  // namespace otf

@@ -56,7 +56,7 @@ struct WinHeader {
     otf_scenario sc;
     EngineState st;
     int64_t stats[OTF_ST_NSLOTS];
-    otf_qoe q;
+    QoeAcc qa;
     WWorker wk[MAXK];
     int32_t gq[MAXK];
     int32_t fq_w[MAXK], fq_d[MAXK], fq_j[MAXK];
@@ -116,7 +116,7 @@ struct Win {
     Client *cl;
     int32_t *blist, *wq_head, *wq_tail;
     JobEnt *jq;
-    double W, H, E, now;
+    double W, invW, H, E, now;
     int32_t k;
     // lane 0's register copies of the hot server counters during phase A
     int64_t req_counter, n_req;
@@ -125,8 +125,8 @@ struct Win {
 };
 
 // window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles)
-__device__ __forceinline__ int32_t win_of(double when, double W) {
-    double q = floor(when / W);
+__device__ __forceinline__ int32_t win_of(double when, double W, double invW) {
+    double q = floor(when * invW);                     // estimate; the exact bounds decide
     int32_t k = q < 1.0e9 ? (int32_t)q : 1000000000;
     if (k < 0) k = 0;
     while (k > 0 && when < (double)k * W) k--;
@@ -136,7 +136,7 @@ __device__ __forceinline__ int32_t win_of(double when, double W) {
 
 __device__ __forceinline__ int32_t timer_win(const Win &w, double when) {
     if (!(when <= w.H)) return WIN_NONE;     // run_until(H) never fires it (sim.py:352)
-    int32_t k = win_of(when, w.W);
+    int32_t k = win_of(when, w.W, w.invW);
     return k < WIN_NONE ? k : WIN_NONE;
 }
 
@@ -492,13 +492,12 @@ __device__ __forceinline__ void record_response(Win &w, const Client &c, double 
             S.flag(OTF_S_RECORD_OVERFLOW);
         }
     }
-    typedef unsigned long long ull;
     double lat = now - c.arrival;
-    otf_qoe &q = w.h->q;
-    atomicAdd((ull *)&q.lat_hist[lat_bin(lat)], 1ull);
-    atomicAdd((ull *)&q.path_count[c.path], 1ull);
-    atomicAdd((ull *)&q.n_requests, 1ull);
-    atomicAdd(&q.latency_sum, lat);
+    QoeAcc &q = w.h->qa;
+    atomicAdd(&q.lat_hist[lat_bin(lat)], 1u);
+    atomicAdd(&q.path_count[c.path], 1u);
+    atomicAdd(&q.n_requests, 1u);
+    S.lat_sum += lat;
 }
 
 __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid) {
@@ -579,9 +578,11 @@ __device__ void sort_list(WinHeader *h, int lane) {
         double wi = h->list_when[i], ci = h->list_ctime[i];
         int32_t idi = h->list_id[i];
         int32_t r = 0;
-        for (int32_t j = 0; j < n; j++) {
+#pragma unroll 4
+        for (int32_t j = 0; j < n; j++) {              // branch-free lexicographic compare
             double wj = h->list_when[j], cj = h->list_ctime[j];
-            r += (wj < wi) || (wj == wi && (cj < ci || (cj == ci && h->list_id[j] < idi)));
+            int32_t idj = h->list_id[j];
+            r += (int32_t)((wj < wi) | ((wj == wi) & ((cj < ci) | ((cj == ci) & (idj < idi)))));
         }
         my_w[m] = wi; my_c[m] = ci; my_id[m] = idi; my_r[m] = r;
         my_d[m] = h->list_desc[i]; my_s[m] = h->list_pack[i];
@@ -649,8 +650,10 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     // counters, QoE and small tables live in shared memory
     w.S.st = &h->st;
     w.S.stats = h->stats;
-    w.S.q = &h->q;
+    w.S.qa = &h->qa;
+    w.S.lat_sum = w.S.stall_sum = w.S.startup_sum = 0.0;
     w.W = sc.latency * (1.0 - 0x1p-20);
+    w.invW = 1.0 / w.W;
     w.H = sc.horizon;
     w.k = -1;
 
@@ -662,8 +665,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         z.lru_head = z.lru_tail = -1;
         h->st = z;
         for (int i = 0; i < OTF_ST_NSLOTS; i++) h->stats[i] = 0;
-        int64_t *qq = (int64_t *)&h->q;
-        for (size_t i = 0; i < sizeof(otf_qoe) / 8; i++) qq[i] = 0;
+        qoe_zero(&h->qa, 0, 1);
         h->gq_head = 0; h->gq_n = K; h->fq_head = 0; h->fq_n = 0;
         h->jq_head = 0; h->jq_n = 0; h->jq_cap = (int32_t)(D + 1);
         h->n_list = 0; h->n_blist = 0; h->wseq = 0;
@@ -727,7 +729,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         m = min(m, warp_min(mw));
         m = min(m, h->far_min);
         if (m == WIN_NONE) break;
-        if (h->far_n > 0 && h->far_min < m + RING) {   // far timers now within the wheel: re-file them
+        if (h->far_n > 0 && h->far_min < m + RING / 2) {   // far timers close to the wheel: re-file them
             if (lane == 0) {
                 int32_t c = h->far_head;
                 h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
@@ -831,11 +833,13 @@ done:
         cnt[0] = h->st.n_req; cnt[1] = h->st.n_sess; cnt[2] = h->st.n_seg; cnt[3] = h->st.n_job;
         b.status[s] = h->st.status;
     }
-    {
-        const int64_t *src = (const int64_t *)&h->q;
-        int64_t *dst = (int64_t *)(b.qoe + s);
-        for (size_t i = lane; i < sizeof(otf_qoe) / 8; i += 32) dst[i] = src[i];
+    // float sums: fixed-order warp reduction, then lane 0 writes the QoE block
+    for (int o = 16; o > 0; o >>= 1) {
+        w.S.lat_sum += __shfl_down_sync(0xffffffffu, w.S.lat_sum, o);
+        w.S.stall_sum += __shfl_down_sync(0xffffffffu, w.S.stall_sum, o);
+        w.S.startup_sum += __shfl_down_sync(0xffffffffu, w.S.startup_sum, o);
     }
+    if (lane == 0) w.S.flush_qoe();
 }
 
 }  // namespace otf

@@ -76,6 +76,7 @@ OTF_HD ExactLayout exact_layout(int32_t n_clients, int32_t n_workers, int64_t n_
     int64_t n_tasks = (int64_t)n_clients + n_workers;
     int64_t o = 0;
     L.state = o; o += 256;                     // EngineState
+    o += 512;                                  // QoeAcc (at state + 256)
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
     L.workers = o; o += align256((int64_t)sizeof(Worker) * n_workers);
     L.heap = o;    o += align256((int64_t)sizeof(Timer) * (n_tasks + 1));
