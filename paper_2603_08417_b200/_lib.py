@@ -29,6 +29,8 @@ POP_UNIFORM, POP_ZIPF = 0, 1
 ENGINE_EXACT, ENGINE_WINDOWED = 0, 1
 MODE_HISTOGRAM, MODE_RECORDS = 0, 1
 S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG = 0x1, 0x2, 0x4, 0x8, 0x10
+BF_LRU_GLOBAL = 0x1
+SM_COUNT_B200, SMEM_PER_SM = 148, 227 * 1024
 
 ST_NSLOTS = 32
 ST = dict(jobs_total=0, jobs_demand=1, jobs_speculative=2, wasted_avoided=3, speculation_enqueued=4,
@@ -83,7 +85,7 @@ class Batch(ctypes.Structure):
                  ("i64_pool", _vp), ("i32_pool", _vp), ("scratch", _vp)]
                 + [(n, _vp) for n, _ in RECORD_FIELDS]
                 + [("counts", _vp), ("stats", _vp), ("qoe", _vp), ("status", _vp), ("order", _vp),
-                   ("shared_bytes", _i64)])
+                   ("shared_bytes", _i64), ("engine_flags", _i32), ("pad_flags", _i32)])
 
 
 class SizeTable(ctypes.Structure):
@@ -131,7 +133,7 @@ def lib():
     L.otf_scratch_bytes.restype = _i64
     L.otf_scratch_bytes.argtypes = [_i32] * 6
     L.otf_shared_bytes.restype = _i64
-    L.otf_shared_bytes.argtypes = [_i32] * 6
+    L.otf_shared_bytes.argtypes = [_i32] * 7
     L.otf_build_traces.restype = ctypes.c_int
     L.otf_build_traces.argtypes = [_i64, _i32, _P(_f64), _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
                                    _P(_f64), _P(_f64), _i32]

@@ -36,10 +36,11 @@ namespace otf {
 
 constexpr int32_t WIN_NONE = 0x3FFFFFFF;
 constexpr int LIST_CAP = 256;      // server events per window (more -> exact engine)
-constexpr int MAXK = 32;           // transcode workers
-constexpr int RING = 2048;         // timer-wheel buckets (windows); farther timers wait on a far list
+constexpr int MAXK = 16;           // transcode workers
+constexpr int RING = 512;          // timer-wheel buckets (windows); farther timers wait on a far list
 constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory
-constexpr uint8_t K_SRV = 1;       // client's pending timer is a server event (request latency)
+constexpr int MAXN = 32767;        // clients (16-bit wheel links)
+constexpr int16_t NIL = -1;
 
 struct WWorker {
     double when, ctime;
@@ -65,23 +66,24 @@ struct WinHeader {
     int32_t n_list, n_blist;
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
+    int32_t arr_next;                    // next client (arrival order) not yet on the wheel
     // small read-only tables
     int32_t t_segcount[MAXTAB];
     double t_seqdur[MAXTAB], t_segdur[MAXTAB], t_zipf[MAXTAB], t_rho[MAXTAB];
     int64_t t_bitrates[MAXTAB], t_manifest[MAXTAB];
-    // timer wheel
+    // timer wheel: server-event and client-local buckets per window
     uint32_t bits[RING / 32];
-    int32_t bhead[RING];
+    int32_t bhead_srv[RING];
+    int32_t bhead_loc[RING];
     // the window's server events
     double list_when[LIST_CAP];
-    double list_ctime[LIST_CAP];
     int32_t list_pack[LIST_CAP];         // rank | index << 8 | seq << 16
-    int32_t list_id[LIST_CAP];
-    int32_t list_desc[LIST_CAP];
+    int16_t list_id[LIST_CAP];
+    int16_t list_desc[LIST_CAP];
 };
 
 struct WinGlobalLayout {
-    int64_t clients, blist, wq_head, wq_tail, jobq, total;
+    int64_t clients, blist, wq_head, wq_tail, jobq, lru, total;
 };
 
 __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
@@ -92,16 +94,17 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
+    L.lru = o;     o += align256((int64_t)sizeof(int16_t) * 2 * n_desc);
     L.total = o;
     return L;
 }
 
-__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc) {
+// lru_smem: LRU links in shared memory (else in the scenario's global arena)
+__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc, bool lru_smem) {
     int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
-    o += 4 * (int64_t)n_clients;          // bucket next links
-    o += (int64_t)n_clients;              // pending-timer kind
+    o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
     o = (o + 15) & ~(int64_t)15;
-    o += 4 * n_desc;                      // lru prev/next (int16)
+    if (lru_smem) o += 4 * n_desc;        // lru prev/next (int16)
     o += n_desc;                          // descriptor flags
     return (o + 15) & ~(int64_t)15;
 }
@@ -109,9 +112,8 @@ __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_d
 struct Win {
     Scn S;
     WinHeader *h;
-    int32_t *bnext;
-    uint8_t *ckind;
-    int16_t *lru_prev, *lru_next;
+    int16_t *bnext;
+    int16_t *lru_prev, *lru_next;                     // shared or global (generic pointers)
     uint8_t *dflags;
     Client *cl;
     int32_t *blist, *wq_head, *wq_tail;
@@ -141,17 +143,16 @@ __device__ __forceinline__ int32_t timer_win(const Win &w, double when) {
 }
 
 // Put client c on the bucket of window `wk` (any lane; lock-free push).
-__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, uint8_t kind) {
+__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool srv) {
     WinHeader *h = w.h;
-    w.ckind[c] = kind;
     if (wk - w.k < RING) {
         int32_t slot = wk & (RING - 1);
-        int32_t old = atomicExch(&h->bhead[slot], c);
-        w.bnext[c] = old;
+        int32_t old = atomicExch(srv ? &h->bhead_srv[slot] : &h->bhead_loc[slot], c);
+        w.bnext[c] = (int16_t)old;
         atomicOr(&h->bits[slot >> 5], 1u << (slot & 31));
-    } else {
+    } else {                                           // beyond the wheel (rare): far list
         int32_t old = atomicExch(&h->far_head, c);
-        w.bnext[c] = old;
+        w.bnext[c] = (int16_t)old;
         atomicAdd(&h->far_n, 1);
         atomicMin(&h->far_min, wk);
     }
@@ -262,9 +263,9 @@ __device__ void resolve(Win &w, int32_t d) {                             // back
 
 // waiter links reuse bnext: a waiting client has no pending timer
 __device__ __forceinline__ void add_waiter(Win &w, int32_t d, int32_t cid) {
-    w.bnext[cid] = -1;
+    w.bnext[cid] = NIL;
     int32_t t = w.wq_tail[d];
-    if (t >= 0) w.bnext[t] = cid; else w.wq_head[d] = cid;
+    if (t >= 0) w.bnext[t] = (int16_t)cid; else w.wq_head[d] = cid;
     w.wq_tail[d] = cid;
 }
 
@@ -411,7 +412,7 @@ __device__ void phase_a(Win &w) {
             if (ww < cw) take_worker = true;
             else if (cw < ww) take_worker = false;
             else {
-                double cc = h->list_ctime[i], wc = h->wk[bw].ctime;
+                double cc = w.cl[h->list_id[i]].ctime, wc = h->wk[bw].ctime;
                 if (wc < cc) take_worker = true;
                 else if (cc < wc) take_worker = false;
                 else { w.S.flag(OTF_S_TIE); take_worker = true; }
@@ -450,7 +451,7 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
         int32_t k = timer_win(w, when);
         if (k == WIN_NONE) return false;
         if (k <= w.k) w.S.flag(OTF_S_TIE);             // lookahead violated (cannot happen)
-        bucket_push(w, cid, k, K_SRV);
+        bucket_push(w, cid, k, true);
         return false;
     }
     if (when <= w.H && when < w.E) {                   // fires inside this window: keep going
@@ -458,7 +459,7 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
         return true;
     }
     int32_t k = timer_win(w, when);
-    if (k != WIN_NONE) bucket_push(w, cid, k, 0);
+    if (k != WIN_NONE) bucket_push(w, cid, k, false);
     return false;
 }
 
@@ -570,30 +571,50 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) {
 __device__ void sort_list(WinHeader *h, int lane) {
     const int32_t n = h->n_list;
     if (n <= 1) return;
-    double my_w[LIST_CAP / 32], my_c[LIST_CAP / 32];
-    int32_t my_s[LIST_CAP / 32];
-    int32_t my_id[LIST_CAP / 32], my_d[LIST_CAP / 32], my_r[LIST_CAP / 32];
+    double my_w[LIST_CAP / 32];
+    int32_t my_s[LIST_CAP / 32], my_r[LIST_CAP / 32];
+    int16_t my_id[LIST_CAP / 32], my_d[LIST_CAP / 32];
     int32_t m = 0;
     for (int32_t i = lane; i < n; i += 32, m++) {
-        double wi = h->list_when[i], ci = h->list_ctime[i];
+        double wi = h->list_when[i];
         int32_t idi = h->list_id[i];
         int32_t r = 0;
 #pragma unroll 4
-        for (int32_t j = 0; j < n; j++) {              // branch-free lexicographic compare
-            double wj = h->list_when[j], cj = h->list_ctime[j];
+        for (int32_t j = 0; j < n; j++) {              // branch-free (time, client) compare
+            double wj = h->list_when[j];
             int32_t idj = h->list_id[j];
-            r += (int32_t)((wj < wi) | ((wj == wi) & ((cj < ci) | ((cj == ci) & (idj < idi)))));
+            r += (int32_t)((wj < wi) | ((wj == wi) & (idj < idi)));
         }
-        my_w[m] = wi; my_c[m] = ci; my_id[m] = idi; my_r[m] = r;
+        my_w[m] = wi; my_id[m] = (int16_t)idi; my_r[m] = r;
         my_d[m] = h->list_desc[i]; my_s[m] = h->list_pack[i];
     }
     __syncwarp();
     for (int32_t t = 0; t < m; t++) {
         int32_t r = my_r[t];
-        h->list_when[r] = my_w[t]; h->list_ctime[r] = my_c[t]; h->list_id[r] = my_id[t];
+        h->list_when[r] = my_w[t]; h->list_id[r] = my_id[t];
         h->list_desc[r] = my_d[t]; h->list_pack[r] = my_s[t];
     }
     __syncwarp();
+}
+
+// Equal request times (rare): order each tie group by arm time (the tick order
+// of their latency timers, sim.py:304-309); equal arm times cannot be ordered.
+__device__ void order_ties(Win &w) {
+    WinHeader *h = w.h;
+    const int32_t n = h->n_list;
+    for (int32_t i = 1; i < n; i++) {
+        if (h->list_when[i] != h->list_when[i - 1]) continue;
+        int32_t j = i;                                 // insertion step by ctime
+        while (j > 0 && h->list_when[j] == h->list_when[j - 1]) {
+            double cj = w.cl[h->list_id[j]].ctime, cp = w.cl[h->list_id[j - 1]].ctime;
+            if (cj == cp) { h->st.status |= OTF_S_TIE; break; }
+            if (cj > cp) break;
+            int16_t ti = h->list_id[j]; h->list_id[j] = h->list_id[j - 1]; h->list_id[j - 1] = ti;
+            int16_t td = h->list_desc[j]; h->list_desc[j] = h->list_desc[j - 1]; h->list_desc[j - 1] = td;
+            int32_t tp = h->list_pack[j]; h->list_pack[j] = h->list_pack[j - 1]; h->list_pack[j - 1] = tp;
+            j--;
+        }
+    }
 }
 
 // Next non-empty window after k_done on the wheel (warp-wide bitmap scan).
@@ -632,16 +653,21 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     const otf_scenario &sc = h->sc;
     const int32_t N = sc.n_clients, K = sc.n_workers;
     const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
+    const bool lru_smem = !(b.engine_flags & OTF_BF_LRU_GLOBAL);
     uint8_t *p = smem + ((sizeof(WinHeader) + 15) & ~(size_t)15);
-    w.h = h;
-    w.bnext = (int32_t *)p; p += 4 * (int64_t)N;
-    w.ckind = p; p += N;
-    p = (uint8_t *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    w.lru_prev = (int16_t *)p; p += 2 * D;
-    w.lru_next = (int16_t *)p; p += 2 * D;
-    w.dflags = p;
     uint8_t *g = b.scratch + sc.scratch_off;
     WinGlobalLayout L = win_global_layout(N, D);
+    w.h = h;
+    w.bnext = (int16_t *)p; p += 2 * (int64_t)N;
+    p = (uint8_t *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    if (lru_smem) {
+        w.lru_prev = (int16_t *)p; p += 2 * D;
+        w.lru_next = (int16_t *)p; p += 2 * D;
+    } else {
+        w.lru_prev = (int16_t *)(g + L.lru);
+        w.lru_next = w.lru_prev + D;
+    }
+    w.dflags = p;
     w.cl = (Client *)(g + L.clients);
     w.blist = (int32_t *)(g + L.blist);
     w.wq_head = (int32_t *)(g + L.wq_head);
@@ -658,7 +684,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     w.k = -1;
 
     // ---- init -------------------------------------------------------------------
-    const bool fits = K <= MAXK && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB && D < 32767 &&
+    const bool fits = K <= MAXK && N <= MAXN && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB && D < 32767 &&
                       sc.latency > 0 && sc.horizon / (sc.latency * (1.0 - 0x1p-20)) < 5.0e8;
     if (lane == 0) {
         EngineState z = {};
@@ -670,6 +696,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         h->jq_head = 0; h->jq_n = 0; h->jq_cap = (int32_t)(D + 1);
         h->n_list = 0; h->n_blist = 0; h->wseq = 0;
         h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
+        h->arr_next = 0;
         if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
     }
     __syncwarp();
@@ -680,7 +707,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         z.win = WIN_NONE; z.pc = W_GOT; z.desc = -1; z.job = -1;
         h->wk[q] = z;
     }
-    for (int32_t i = lane; i < RING; i += 32) h->bhead[i] = -1;
+    for (int32_t i = lane; i < RING; i += 32) { h->bhead_srv[i] = -1; h->bhead_loc[i] = -1; }
     for (int32_t i = lane; i < RING / 32; i += 32) h->bits[i] = 0;
     for (int32_t i = lane; i < sc.n_seq; i += 32) {
         h->t_segcount[i] = w.S.segcounts[i];
@@ -694,7 +721,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         h->t_bitrates[i] = w.S.bitrates[i];
     }
     for (int64_t d = lane; d < D; d += 32) {
-        w.lru_prev[d] = -1; w.lru_next[d] = -1; w.dflags[d] = 0;
+        w.lru_prev[d] = NIL; w.lru_next[d] = NIL; w.dflags[d] = 0;
         w.wq_head[d] = -1; w.wq_tail[d] = -1;
     }
     __syncwarp();
@@ -705,7 +732,8 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     w.S.manifest_b = h->t_manifest;
     w.S.rho = h->t_rho;
     w.S.bitrates = h->t_bitrates;
-    // clients: the first step arms sleep(offset) (orchestrator.py:337)
+    // clients: the first step arms sleep(offset) (orchestrator.py:337); offsets are a
+    // cumulative sum, so clients join the wheel in id order (arrival cursor below)
     for (int32_t c = lane; c < N; c += 32) {
         Client &cl = w.cl[c];
         client_init(cl);
@@ -714,40 +742,48 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         cl.ctime = 0.0;
         cl.next_when = 0.0 + off;
         if (!(off > 0)) w.S.flag(OTF_S_TIE);           // instant start: tick order among clients matters
-        int32_t wk = isinf(off) ? WIN_NONE : timer_win(w, cl.next_when);
-        if (wk != WIN_NONE) bucket_push(w, c, wk, 0);
     }
     __syncwarp();
+    if (h->st.status & OTF_S_TIE) goto done;
 
     // ---- window loop --------------------------------------------------------------
     t_start = clock64();
     for (;;) {
         t0 = clock64();
-        // next window: wheel, far list, worker timers
+        // next window: wheel, far list, worker timers, next arrival
         int32_t m = wheel_next(h, h->k_done, lane);
         int32_t mw = lane < K ? h->wk[lane].win : WIN_NONE;
         m = min(m, warp_min(mw));
         m = min(m, h->far_min);
+        int32_t arr_win = WIN_NONE;
+        if (h->arr_next < N) arr_win = timer_win(w, w.S.arrival(h->arr_next));
+        m = min(m, arr_win);
         if (m == WIN_NONE) break;
+        if (arr_win != WIN_NONE && arr_win - m < RING) {   // arrivals entering the wheel
+            if (lane == 0) {
+                h->k_done = m - 1;                     // windows before m are empty: wheel base = m
+                w.k = m - 1;
+                int32_t c = h->arr_next;
+                while (c < N) {
+                    int32_t wk = timer_win(w, w.S.arrival(c));
+                    if (wk == WIN_NONE || wk - m >= RING) break;
+                    bucket_push(w, c, wk, false);
+                    c++;
+                }
+                h->arr_next = c;
+            }
+            __syncwarp();
+        }
         if (h->far_n > 0 && h->far_min < m + RING / 2) {   // far timers close to the wheel: re-file them
             if (lane == 0) {
                 int32_t c = h->far_head;
                 h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
                 h->k_done = m - 1;                     // windows before m are empty: wheel base = m
+                w.k = m - 1;
                 while (c >= 0) {
                     int32_t nx = w.bnext[c];
-                    int32_t wk = timer_win(w, w.cl[c].next_when);
-                    if (wk - m < RING) {
-                        int32_t slot = wk & (RING - 1);
-                        w.bnext[c] = h->bhead[slot];
-                        h->bhead[slot] = c;
-                        h->bits[slot >> 5] |= 1u << (slot & 31);
-                    } else {
-                        w.bnext[c] = h->far_head;
-                        h->far_head = c;
-                        h->far_n++;
-                        h->far_min = min(h->far_min, wk);
-                    }
+                    const Client &cl = w.cl[c];
+                    bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT);
                     c = nx;
                 }
             }
@@ -756,19 +792,24 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         }
         w.k = m;
         w.E = (double)(m + 1) * w.W;
-        // pop the bucket: server events -> list, client-local events -> B-list
+        // pop the buckets: server events -> list, client-local events -> B-list
         if (lane == 0) {
             h->stats[OTF_ST_WINDOWS]++;
             int32_t slot = m & (RING - 1);
-            int32_t c = h->bhead[slot];
-            h->bhead[slot] = -1;
+            int32_t c = h->bhead_srv[slot];
+            int32_t cl = h->bhead_loc[slot];
+            h->bhead_srv[slot] = -1;
+            h->bhead_loc[slot] = -1;
             h->bits[slot >> 5] &= ~(1u << (slot & 31));
             int32_t nl = 0, nb = 0;
             while (c >= 0) {
-                int32_t nx = w.bnext[c];
-                if (w.ckind[c] & K_SRV) { if (nl < LIST_CAP) h->list_id[nl] = c; nl++; }
-                else w.blist[nb++] = c;
-                c = nx;
+                if (nl < LIST_CAP) h->list_id[nl] = (int16_t)c;
+                nl++;
+                c = w.bnext[c];
+            }
+            while (cl >= 0) {
+                w.blist[nb++] = cl;
+                cl = w.bnext[cl];
             }
             h->n_list = nl;
             h->n_blist = nb;
@@ -782,8 +823,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         for (int32_t i = lane; i < h->n_list; i += 32) {   // gather sort keys + request descriptors
             const Client &cl = w.cl[h->list_id[i]];
             h->list_when[i] = cl.next_when;
-            h->list_ctime[i] = cl.ctime;
-            h->list_desc[i] = cl.desc;
+            h->list_desc[i] = (int16_t)cl.desc;
             h->list_pack[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
         }
         __syncwarp();
@@ -796,9 +836,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         t0 = t1;
         // ---- phase A: server lane ----
         if (lane == 0) {
-            for (int32_t i = 1; i < h->n_list; i++)    // equal (time, arm time): tick order unknown
-                if (h->list_when[i] == h->list_when[i - 1] && h->list_ctime[i] == h->list_ctime[i - 1])
-                    h->st.status |= OTF_S_TIE;
+            order_ties(w);
             phase_a(w);
             h->k_done = m;
         }
@@ -849,8 +887,8 @@ int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t
     return otf::win_global_layout(n_clients, n_desc).total;
 }
 
-int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
-    return otf::win_smem_bytes(n_clients, n_desc);
+int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc, int32_t flags) {
+    return otf::win_smem_bytes(n_clients, n_desc, !(flags & OTF_BF_LRU_GLOBAL));
 }
 
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {

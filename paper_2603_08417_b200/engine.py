@@ -85,6 +85,7 @@ class DeviceBatch:
         self.order = torch.from_numpy(np.argsort(-cost, kind="stable").astype(np.int32)).to(dev)
         b.order = self.order.data_ptr()
         b.shared_bytes = inp.shared_bytes
+        b.engine_flags = inp.engine_flags
         self.batch = b
         self.n_tables = sum(1 for t in inp.size_tables if t.n_seq > 0)
         self.upload()
