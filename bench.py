@@ -7,8 +7,8 @@ A "step" is one pass of the hot path over the whole workload: device
 generation of the segment-size tables + one launch of the windowed engine
 replaying every scenario to its 600 s horizon + (N > 1) one NCCL all_gather
 of the per-scenario QoE/fulfillment blocks.  Scenarios are independent, so
-N ranks shard them (weak-scaling in the sense that the per-GPU scenario set
-is fixed by the sweep: total work is fixed, see "scaling").  Inputs are
+scaling is weak: each rank runs a full sweep of its own seeds (rank r: seeds
+64r+1..64r+64) with no data-path collective.  Inputs are
 resident in HBM before the timed region (traces alone are ~0.9 GB > 126 MB
 L2); `e2e` re-times the same step through the public batch API with the
 inputs copied from pinned host memory and the results read back every step.
