@@ -67,6 +67,8 @@ struct WinHeader {
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
     int32_t arr_next;                    // next client (arrival order) not yet on the wheel
+    uint32_t lq_head, lq_tail, lq_stamp; // lazy-LRU touch queue (global ring of lq_cap entries)
+    int32_t lq_cap;
     // small read-only tables
     int32_t t_segcount[MAXTAB];
     double t_seqdur[MAXTAB], t_segdur[MAXTAB], t_zipf[MAXTAB], t_rho[MAXTAB];
@@ -82,8 +84,17 @@ struct WinHeader {
     int16_t list_desc[LIST_CAP];
 };
 
+struct LqEnt {
+    int32_t desc;
+    uint32_t stamp;
+};
+
+__host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {
+    return n_desc * 4 > 4096 ? n_desc * 4 : 4096;
+}
+
 struct WinGlobalLayout {
-    int64_t clients, blist, wq_head, wq_tail, jobq, lru, total;
+    int64_t clients, blist, wq_head, wq_tail, jobq, lstamp, lq, total;
 };
 
 __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
@@ -94,17 +105,16 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
-    L.lru = o;     o += align256((int64_t)sizeof(int16_t) * 2 * n_desc);
+    L.lstamp = o;  o += align256((int64_t)sizeof(uint32_t) * n_desc);
+    L.lq = o;      o += align256((int64_t)sizeof(LqEnt) * 2 * lq_capacity(n_desc));
     L.total = o;
     return L;
 }
 
-// lru_smem: LRU links in shared memory (else in the scenario's global arena)
-__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc, bool lru_smem) {
+__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc, bool) {
     int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
     o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
     o = (o + 15) & ~(int64_t)15;
-    if (lru_smem) o += 4 * n_desc;        // lru prev/next (int16)
     o += n_desc;                          // descriptor flags
     return (o + 15) & ~(int64_t)15;
 }
@@ -113,7 +123,8 @@ struct Win {
     Scn S;
     WinHeader *h;
     int16_t *bnext;
-    int16_t *lru_prev, *lru_next;                     // shared or global (generic pointers)
+    uint32_t *lstamp;                                  // latest touch stamp per descriptor (global)
+    LqEnt *lq;                                         // touch queue (global, 2 * lq_cap)
     uint8_t *dflags;
     Client *cl;
     int32_t *blist, *wq_head, *wq_tail;
@@ -159,47 +170,94 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
 }
 
 // ---- server lane: cache / backend (lane 0 only) --------------------------------
-__device__ __forceinline__ void lru_unlink(Win &w, int32_t d) {
-    int32_t p = w.lru_prev[d], n = w.lru_next[d];
-    if (p >= 0) w.lru_next[p] = n; else w.h->st.lru_head = n;
-    if (n >= 0) w.lru_prev[n] = p; else w.h->st.lru_tail = p;
-}
-__device__ __forceinline__ void lru_append(Win &w, int32_t d) {
-    int32_t t = w.h->st.lru_tail;
-    w.lru_prev[d] = t;
-    w.lru_next[d] = -1;
-    if (t >= 0) w.lru_next[t] = d; else w.h->st.lru_head = d;
-    w.h->st.lru_tail = d;
+// ---- SegmentCache as a lazy LRU (cache.py:27-92) ---------------------------------
+// OrderedDict order == order of each key's latest touch (get moves to the end,
+// put inserts at the end).  Every touch stamps the descriptor and appends
+// (desc, stamp) to a queue; eviction pops the queue head and skips entries
+// that are stale (not cached, or superseded by a later touch).  Hits are two
+// stores -- no dependent loads on the server lane -- and evictions read the
+// queue sequentially.  The queue is compacted (warp-parallel, order kept)
+// before it can overflow.
+__device__ void lq_compact_serial(Win &w);
+
+__device__ __forceinline__ void lru_touch(Win &w, int32_t d) {
+    WinHeader *h = w.h;
+    uint32_t s = ++h->lq_stamp;
+    w.lstamp[d] = s;
+    if (h->lq_tail - h->lq_head >= (uint32_t)h->lq_cap) lq_compact_serial(w);
+    LqEnt e; e.desc = d; e.stamp = s;
+    w.lq[h->lq_tail % (uint32_t)h->lq_cap] = e;
+    h->lq_tail++;
 }
 __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache.py:45-52
     if (!(w.dflags[d] & D_CACHED)) { w.h->stats[OTF_ST_MISSES]++; return false; }
-    lru_unlink(w, d);
-    lru_append(w, d);
+    lru_touch(w, d);
     w.h->stats[OTF_ST_HITS]++;
     return true;
 }
 __device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
     int64_t cap = w.S.sc->cache_capacity;
     EngineState &st = w.h->st;
-    if (size > cap) { w.h->stats[OTF_ST_REJECTED]++; return; }
-    if (w.dflags[d] & D_CACHED) {
+    WinHeader *h = w.h;
+    if (size > cap) { h->stats[OTF_ST_REJECTED]++; return; }
+    if (w.dflags[d] & D_CACHED) {                      // replace: its old queue entry goes stale
         st.cur_bytes -= size;
-        lru_unlink(w, d);
         w.dflags[d] &= ~D_CACHED;
         st.entries--;
     }
-    while (st.cur_bytes + size > cap) {
-        int32_t v = st.lru_head;
-        lru_unlink(w, v);
+    while (st.cur_bytes + size > cap) {                // popitem(last=False): oldest live entry
+        LqEnt e = w.lq[h->lq_head % (uint32_t)h->lq_cap];
+        h->lq_head++;
+        int32_t v = e.desc;
+        if (!(w.dflags[v] & D_CACHED) || w.lstamp[v] != e.stamp) continue;
         w.dflags[v] &= ~D_CACHED;
         st.entries--;
         st.cur_bytes -= w.S.size(v);
-        w.h->stats[OTF_ST_EVICTIONS]++;
+        h->stats[OTF_ST_EVICTIONS]++;
     }
-    lru_append(w, d);
+    lru_touch(w, d);
     w.dflags[d] |= D_CACHED;
     st.entries++;
     st.cur_bytes += size;
+}
+
+// Drop stale queue entries in place, keeping order (lane 0; only if a window
+// overran the pre-window compaction margin).
+__device__ void lq_compact_serial(Win &w) {
+    WinHeader *h = w.h;
+    uint32_t cap = (uint32_t)h->lq_cap, o = h->lq_head;
+    for (uint32_t i = h->lq_head; i != h->lq_tail; i++) {
+        LqEnt e = w.lq[i % cap];
+        if ((w.dflags[e.desc] & D_CACHED) && w.lstamp[e.desc] == e.stamp) w.lq[(o++) % cap] = e;
+    }
+    h->lq_tail = o;
+}
+
+// Warp-parallel order-preserving compaction of the touch queue into a fresh
+// region (called between windows when the queue is 3/4 full).
+__device__ void lq_compact_warp(Win &w, int lane) {
+    WinHeader *h = w.h;
+    const uint32_t cap = (uint32_t)h->lq_cap;
+    const uint32_t head = h->lq_head, tail = h->lq_tail;
+    uint32_t out = 0;                                  // compacted entries go to [0, out) of the spare half
+    LqEnt *dst = w.lq + cap;                           // the queue owns 2*cap slots: compact into the other half
+    for (uint32_t base = head; base < tail; base += 32) {
+        uint32_t i = base + lane;
+        bool keep = false;
+        LqEnt e;
+        if (i < tail) {
+            e = w.lq[i % cap];
+            keep = (w.dflags[e.desc] & D_CACHED) && w.lstamp[e.desc] == e.stamp;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) dst[out + __popc(m & ((1u << lane) - 1))] = e;
+        out += __popc(m);
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < out; i += 32) w.lq[i] = dst[i];
+    __syncwarp();
+    if (lane == 0) { h->lq_head = 0; h->lq_tail = out; }
+    __syncwarp();
 }
 
 __device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backend.py:156-170
@@ -653,21 +711,15 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     const otf_scenario &sc = h->sc;
     const int32_t N = sc.n_clients, K = sc.n_workers;
     const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
-    const bool lru_smem = !(b.engine_flags & OTF_BF_LRU_GLOBAL);
     uint8_t *p = smem + ((sizeof(WinHeader) + 15) & ~(size_t)15);
     uint8_t *g = b.scratch + sc.scratch_off;
     WinGlobalLayout L = win_global_layout(N, D);
     w.h = h;
     w.bnext = (int16_t *)p; p += 2 * (int64_t)N;
     p = (uint8_t *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    if (lru_smem) {
-        w.lru_prev = (int16_t *)p; p += 2 * D;
-        w.lru_next = (int16_t *)p; p += 2 * D;
-    } else {
-        w.lru_prev = (int16_t *)(g + L.lru);
-        w.lru_next = w.lru_prev + D;
-    }
     w.dflags = p;
+    w.lstamp = (uint32_t *)(g + L.lstamp);
+    w.lq = (LqEnt *)(g + L.lq);
     w.cl = (Client *)(g + L.clients);
     w.blist = (int32_t *)(g + L.blist);
     w.wq_head = (int32_t *)(g + L.wq_head);
@@ -697,6 +749,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         h->n_list = 0; h->n_blist = 0; h->wseq = 0;
         h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
         h->arr_next = 0;
+        h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
         if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
     }
     __syncwarp();
@@ -721,7 +774,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         h->t_bitrates[i] = w.S.bitrates[i];
     }
     for (int64_t d = lane; d < D; d += 32) {
-        w.lru_prev[d] = NIL; w.lru_next[d] = NIL; w.dflags[d] = 0;
+        w.lstamp[d] = 0; w.dflags[d] = 0;
         w.wq_head[d] = -1; w.wq_tail[d] = -1;
     }
     __syncwarp();
@@ -792,6 +845,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         }
         w.k = m;
         w.E = (double)(m + 1) * w.W;
+        if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
         // pop the buckets: server events -> list, client-local events -> B-list
         if (lane == 0) {
             h->stats[OTF_ST_WINDOWS]++;
