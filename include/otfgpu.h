@@ -143,13 +143,9 @@ typedef struct otf_batch {
     const int32_t *order;             /* optional launch order (longest first), NULL = identity */
     int64_t shared_bytes;             /* windowed engine: dynamic shared memory per scenario
                                          (max of otf_shared_bytes over the batch) */
-    int32_t engine_flags;             /* OTF_BF_* */
+    int32_t engine_flags;             /* reserved, 0 */
     int32_t pad_flags;
 } otf_batch;
-
-/* otf_batch.engine_flags */
-#define OTF_BF_LRU_GLOBAL 0x1         /* windowed engine: cache LRU links in global scratch, not shared
-                                         memory (fewer shared bytes -> more scenarios resident per SM) */
 
 /* A segment-size table: Catalog.descriptor sizes (content.py:204-218) for one
  * catalog, generated on the device from SeedSequence([seed, key, rank, index]). */
@@ -176,7 +172,7 @@ int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, 
 
 /* Per-scenario dynamic shared memory of the windowed engine (host-side helper). */
 int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
-                         int32_t n_ranks, int32_t max_nseg, int32_t engine_flags);
+                         int32_t n_ranks, int32_t max_nseg);
 
 /* HOST function: synthetic traces (netem.py:179-202) + BandwidthTrace period
  * bits (netem.py:39-64) from numpy's standard-normal draws.  normals is

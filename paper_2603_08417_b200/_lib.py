@@ -29,7 +29,6 @@ POP_UNIFORM, POP_ZIPF = 0, 1
 ENGINE_EXACT, ENGINE_WINDOWED = 0, 1
 MODE_HISTOGRAM, MODE_RECORDS = 0, 1
 S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG = 0x1, 0x2, 0x4, 0x8, 0x10
-BF_LRU_GLOBAL = 0x1
 SM_COUNT_B200, SMEM_PER_SM = 148, 227 * 1024
 
 ST_NSLOTS = 32
@@ -133,7 +132,7 @@ def lib():
     L.otf_scratch_bytes.restype = _i64
     L.otf_scratch_bytes.argtypes = [_i32] * 6
     L.otf_shared_bytes.restype = _i64
-    L.otf_shared_bytes.argtypes = [_i32] * 7
+    L.otf_shared_bytes.argtypes = [_i32] * 6
     L.otf_build_traces.restype = ctypes.c_int
     L.otf_build_traces.argtypes = [_i64, _i32, _P(_f64), _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
                                    _P(_f64), _P(_f64), _i32]

@@ -15,7 +15,7 @@
 int otf_launch_exact(const otf_batch &b, cudaStream_t stream);
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream);
 int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc);
-int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc, int32_t flags);
+int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc);
 int otf_launch_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t *i64_pool,
                      const double *f64_pool, const int32_t *i32_pool, cudaStream_t stream);
 
@@ -50,10 +50,10 @@ int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, 
 }
 
 int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
-                         int32_t n_ranks, int32_t max_nseg, int32_t engine_flags) {
+                         int32_t n_ranks, int32_t max_nseg) {
     (void)n_workers;
     if (engine != OTF_ENGINE_WINDOWED) return 0;
-    return otf_windowed_shared_bytes(n_clients, (int64_t)n_seq * n_ranks * max_nseg, engine_flags);
+    return otf_windowed_shared_bytes(n_clients, (int64_t)n_seq * n_ranks * max_nseg);
 }
 
 // CPython >= 3.12 builtin sum() over floats: Neumaier-compensated.

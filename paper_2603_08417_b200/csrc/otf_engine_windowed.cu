@@ -111,7 +111,7 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     return L;
 }
 
-__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc, bool) {
+__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc) {
     int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
     o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
     o = (o + 15) & ~(int64_t)15;
@@ -941,8 +941,8 @@ int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t
     return otf::win_global_layout(n_clients, n_desc).total;
 }
 
-int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc, int32_t flags) {
-    return otf::win_smem_bytes(n_clients, n_desc, !(flags & OTF_BF_LRU_GLOBAL));
+int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
+    return otf::win_smem_bytes(n_clients, n_desc);
 }
 
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {

@@ -170,7 +170,6 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     totals = [0, 0, 0, 0]
     input_bytes = 0
     shared_bytes = 0
-    shared_lean = 0
 
     # -- traces: one table per (seed, netem), long enough for the largest N --
     trace_groups: dict = {}
@@ -289,9 +288,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.off_eps, sc.eps_stride = o_eps, eps_stride
         sc.scratch_off = scratch_off
         scratch_off += int(L.otf_scratch_bytes(engine, N, K, n_seq, n_ranks, max_nseg))
-        shared_bytes = max(shared_bytes, int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg, 0)))
-        shared_lean = max(shared_lean, int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg,
-                                                              _lib.BF_LRU_GLOBAL)))
+        shared_bytes = max(shared_bytes, int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg)))
         scratch_off = (scratch_off + 255) & ~255
         if mode == _lib.MODE_RECORDS:
             c = caps[si] if caps is not None else _default_caps(low)
@@ -308,17 +305,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         lowered=lows, scenarios=scen, size_tables=(_lib.SizeTable * max(1, len(tables)))(*tables),
         f64=P.concat("f64"), i64=P.concat("i64"), i32=P.concat("i32"),
         scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
-        engine=engine, mode=mode, input_bytes=input_bytes, **_placement(len(lows), shared_bytes, shared_lean))
-
-
-def _placement(n: int, full: int, lean: int) -> dict:
-    """Keep the cache LRU links in shared memory unless moving them out saves a wave."""
-    def waves(b):
-        per_sm = max(1, _lib.SMEM_PER_SM // (b + 1024)) if b > 0 else 32
-        return -(-n // (_lib.SM_COUNT_B200 * min(per_sm, 32)))
-    if full > 0 and (full > _lib.SMEM_PER_SM or waves(lean) < waves(full)):
-        return dict(shared_bytes=lean, engine_flags=_lib.BF_LRU_GLOBAL)
-    return dict(shared_bytes=full, engine_flags=0)
+        engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes)
 
 
 def n_size_tables(inp: BatchInputs) -> int:
