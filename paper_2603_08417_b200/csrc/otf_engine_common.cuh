@@ -99,7 +99,7 @@ struct Scn {
     }
 
     __device__ __forceinline__ int64_t &stat(int i) { return stats[i]; }
-    __device__ __forceinline__ void flag(int32_t bits) { st->status |= bits; }
+    __device__ __forceinline__ void flag(int32_t bits) { atomicOr(&st->status, bits); }
     __device__ __forceinline__ int32_t desc_id(int32_t seq, int32_t rank, int32_t index) const {
         return (seq * sc->n_ranks + (rank - 1)) * sc->max_nseg + index;
     }
