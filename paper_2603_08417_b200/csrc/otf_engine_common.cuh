@@ -243,7 +243,7 @@ __device__ __forceinline__ void client_init(Client &c) {
 }
 
 // orchestrator.py:338-340: the client's own pick stream
-static __device__ __noinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
+__device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
     uint32_t ent[8];
     int m = 0;
     m = push_words(ent, m, S.sc->seed);
@@ -253,7 +253,7 @@ static __device__ __noinline__ void client_arrive(Scn &S, Client &c, int32_t cid
 }
 
 // orchestrator.py:341-345 + client.py:237-239: pick a sequence, register a report
-static __device__ __noinline__ void client_new_session(Scn &S, Client &c, int32_t cid, double now) {
+__device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double now) {
     int32_t seq;
     if (S.sc->popularity == OTF_POP_ZIPF) {
         double u = pcg_next_double(c.picks);
@@ -304,7 +304,7 @@ __device__ __forceinline__ void client_select(Scn &S, Client &c) {
 
 // client.py:261-268; returns true when the session has more segments, else
 // leaves the buffer advanced for the final sleep(level) (client.py:270-271).
-static __device__ __noinline__ bool client_segment_done(Scn &S, Client &c, double now) {
+__device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
     double dt = now - c.xfer_start;                       // SegmentFetch.rate_bps
     double rate = dt > 0 ? ((double)c.size * 8.0) / dt : INFINITY;
     if (!c.has_est) { c.est = rate; c.has_est = 1; }
@@ -334,7 +334,7 @@ static __device__ __noinline__ bool client_segment_done(Scn &S, Client &c, doubl
 }
 
 // client.py:272-280 (+ the finally clause)
-static __device__ __noinline__ void client_finish_session(Scn &S, Client &c, double now) {
+__device__ inline void client_finish_session(Scn &S, Client &c, double now) {
     buf_advance(c.buf, now);
     c.buf.phase = PH_FINISHED;
     if (S.records && c.session < S.sc->sess_cap) S.b->sess_flags[S.sc->sess_off + c.session] |= 1;
@@ -345,7 +345,7 @@ static __device__ __noinline__ void client_finish_session(Scn &S, Client &c, dou
 }
 
 // SessionReport.harvest at the horizon (orchestrator.py:357-359, client.py:177-187)
-static __device__ __noinline__ void client_harvest(Scn &S, Client &c, double horizon) {
+__device__ inline void client_harvest(Scn &S, Client &c, double horizon) {
     if (c.pc == C_HUNG) S.flag(OTF_S_HUNG);
     if (!c.sess_open) return;
     if (c.buf_live) {

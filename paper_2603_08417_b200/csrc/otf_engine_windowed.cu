@@ -203,7 +203,7 @@ __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache
     w.h->stats[OTF_ST_HITS]++;
     return true;
 }
-__device__ __noinline__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
+__device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
     int64_t cap = w.S.sc->cache_capacity;
     EngineState &st = w.h->st;
     WinHeader *h = w.h;
@@ -231,7 +231,7 @@ __device__ __noinline__ void cache_put(Win &w, int32_t d, int64_t size) {       
 
 // Drop stale queue entries in place, keeping order (lane 0; only if a window
 // overran the pre-window compaction margin).
-__device__ __noinline__ void lq_compact_serial(Win &w) {
+__device__ void lq_compact_serial(Win &w) {
     WinHeader *h = w.h;
     uint32_t cap = (uint32_t)h->lq_cap, o = h->lq_head;
     for (uint32_t i = h->lq_head; i != h->lq_tail; i++) {
@@ -243,7 +243,7 @@ __device__ __noinline__ void lq_compact_serial(Win &w) {
 
 // Warp-parallel order-preserving compaction of the touch queue into a fresh
 // region (called between windows when the queue is 3/4 full).
-__device__ __noinline__ void lq_compact_warp(Win &w, int lane) {
+__device__ void lq_compact_warp(Win &w, int lane) {
     WinHeader *h = w.h;
     const uint32_t cap = (uint32_t)h->lq_cap;
     const uint32_t head = h->lq_head, tail = h->lq_tail;
@@ -268,7 +268,7 @@ __device__ __noinline__ void lq_compact_warp(Win &w, int lane) {
     __syncwarp();
 }
 
-__device__ __noinline__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backend.py:156-170
+__device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backend.py:156-170
     int32_t j = w.S.record_job(d, origin, w.now);
     w.dflags[d] |= D_INFLIGHT;
     w.wq_head[d] = -1;
@@ -292,7 +292,7 @@ __device__ __noinline__ void enqueue_job(Win &w, int32_t d, int32_t origin) {   
     }
 }
 
-__device__ __noinline__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, int32_t index) {  // backend.py:135-154
+__device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, int32_t index) {  // backend.py:135-154
     int64_t *st = w.h->stats;
     if (!w.S.sc->spec_enabled) { st[OTF_ST_SKIP_DISABLED]++; return; }
     if (index + 1 >= w.S.segcounts[seq]) { st[OTF_ST_SKIP_EOS]++; return; }
@@ -316,7 +316,7 @@ __device__ __forceinline__ void respond(Win &w, int32_t cid) {
     w.resp_cur[w.n_resp++] = cid;
 }
 
-__device__ __noinline__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
+__device__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
     if (!(w.dflags[d] & D_INFLIGHT)) return;
     w.dflags[d] &= ~D_INFLIGHT;
     int32_t c = w.wq_head[d];
@@ -336,7 +336,7 @@ __device__ __forceinline__ void add_waiter(Win &w, int32_t d, int32_t cid) {
 }
 
 // Backend._worker_loop body from "job dequeued" until the worker yields.
-__device__ __noinline__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
+__device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
     WinHeader *h = w.h;
     const otf_scenario &sc = *w.S.sc;
     for (;;) {
@@ -380,7 +380,7 @@ __device__ __noinline__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t 
     }
 }
 
-__device__ __noinline__ void drain_handoffs(Win &w) {            // ready-queue hops of handed-off jobs
+__device__ void drain_handoffs(Win &w) {            // ready-queue hops of handed-off jobs
     WinHeader *h = w.h;
     while (h->fq_n > 0) {
         int32_t wid = h->fq_w[h->fq_head], d = h->fq_d[h->fq_head], j = h->fq_j[h->fq_head];
@@ -419,7 +419,7 @@ __device__ void server_request(Win &w, int32_t cid, int32_t d, int32_t rank, int
 }
 
 // worker service timer fired (transcode.py:129-131, backend.py:205-207)
-__device__ __noinline__ void server_worker_done(Win &w, int32_t wid) {
+__device__ void server_worker_done(Win &w, int32_t wid) {
     WWorker &k = w.h->wk[wid];
     int32_t d = k.desc, j = k.job;
     k.win = WIN_NONE;
@@ -508,7 +508,7 @@ __device__ void phase_a(Win &w) {
 // Arm a sleep for client c at `now` (loop.sleep, sim.py:317-324): returns true
 // if the client keeps running inside this window (the timer fires before the
 // window ends), else files the timer on the wheel and returns false.
-__device__ __noinline__ bool arm(Win &w, Client &c, int32_t cid, double &now, double delay, int32_t next_pc) {
+__device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now, double delay, int32_t next_pc) {
     c.pc = next_pc;
     if (delay <= 0) return true;                       // resolved future: no yield (sim.py:320-321)
     if (isinf(delay)) { c.pc = C_HUNG; return false; } // never resolves (sim.py:322)
@@ -533,7 +533,7 @@ __device__ __noinline__ bool arm(Win &w, Client &c, int32_t cid, double &now, do
 
 __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid);
 
-__device__ __noinline__ void client_local(Win &w, int32_t cid) {
+__device__ void client_local(Win &w, int32_t cid) {
     Client c = w.cl[cid];                              // one vectorised load; state lives in registers
     client_local_body(w, c, cid);
     w.cl[cid] = c;
@@ -541,7 +541,7 @@ __device__ __noinline__ void client_local(Win &w, int32_t cid) {
 
 // The response's record + QoE (server.py:76-77, metrics.py:67-78), written by the
 // client lane in parallel; the slot (response order) was fixed by the server lane.
-__device__ __noinline__ void record_response(Win &w, const Client &c, double now) {
+__device__ __forceinline__ void record_response(Win &w, const Client &c, double now) {
     Scn &S = w.S;
     const otf_scenario &sc = *S.sc;
     int64_t size = S.size(c.desc);
@@ -636,7 +636,7 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) {
 
 // Order the window's server events by (time, arm time, client): each lane
 // ranks its entries against all others (ties are flagged afterwards).
-__device__ __noinline__ void sort_list(WinHeader *h, int lane) {
+__device__ void sort_list(WinHeader *h, int lane) {
     const int32_t n = h->n_list;
     if (n <= 1) return;
     double my_w[LIST_CAP / 32];
@@ -667,7 +667,7 @@ __device__ __noinline__ void sort_list(WinHeader *h, int lane) {
 
 // Equal request times (rare): order each tie group by arm time (the tick order
 // of their latency timers, sim.py:304-309); equal arm times cannot be ordered.
-__device__ __noinline__ void order_ties(Win &w) {
+__device__ void order_ties(Win &w) {
     WinHeader *h = w.h;
     const int32_t n = h->n_list;
     for (int32_t i = 1; i < n; i++) {
@@ -714,7 +714,7 @@ __device__ int32_t wheel_next(const uint32_t *bits, int32_t start, int lane) {
 // only depends on phase B(<= j-2); phase B(j-1) only depends on A(<= j-1).
 constexpr int NTHREADS = 64;
 
-__device__ __noinline__ void refile_far(Win &w, int32_t base) {     // server warp, lane 0
+__device__ void refile_far(Win &w, int32_t base) {     // server warp, lane 0
     WinHeader *h = w.h;
     int32_t c = h->far_head;
     h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
@@ -729,7 +729,7 @@ __device__ __noinline__ void refile_far(Win &w, int32_t base) {     // server wa
 
 // Server warp: choose the next iteration j (windows in between are empty for
 // both warps), feed arrivals / far timers that now fall on the wheel.
-__device__ __noinline__ void plan_next(Win &w, int lane) {
+__device__ void plan_next(Win &w, int lane) {
     WinHeader *h = w.h;
     const int32_t i = h->iter;
     const int32_t N = w.S.sc->n_clients, K = w.S.sc->n_workers;
@@ -770,7 +770,7 @@ __device__ __noinline__ void plan_next(Win &w, int lane) {
 }
 
 // Server warp: phase A of window j.
-__device__ __noinline__ void server_window(Win &w, int32_t j, int lane) {
+__device__ void server_window(Win &w, int32_t j, int lane) {
     WinHeader *h = w.h;
     long long t0 = clock64(), t1;
     w.k = j;
@@ -821,7 +821,7 @@ __device__ __noinline__ void server_window(Win &w, int32_t j, int lane) {
 }
 
 // Client warp: phase B of window j (its local timers + the responses of A(j)).
-__device__ __noinline__ void client_window(Win &w, int32_t j, int lane) {
+__device__ void client_window(Win &w, int32_t j, int lane) {
     WinHeader *h = w.h;
     long long t0 = clock64();
     w.k = j;

@@ -52,7 +52,7 @@ OTF_HD double piece_start(const Trace &tr, int32_t i) {
 }
 
 // BandwidthTrace._drain_from (netem.py:77-95)
-static __host__ __device__ __noinline__ void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
+OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
     int32_t i = trace_piece(tr, phase);
     double spent = 0.0, pos = phase;
     for (; i < tr.n; i++) {
@@ -73,7 +73,7 @@ static __host__ __device__ __noinline__ void drain_from(const Trace &tr, double 
 }
 
 // BandwidthTrace.completion_time for a looping trace (netem.py:97-118)
-static __host__ __device__ __noinline__ double completion_time(const Trace &tr, double start, int64_t nbytes) {
+OTF_HD double completion_time(const Trace &tr, double start, int64_t nbytes) {
     double bits = (double)nbytes * 8.0;
     if (bits <= 0) return start;
     if (tr.pbits <= 0) return INFINITY;
@@ -153,7 +153,7 @@ OTF_HD double seg_duration(double seqdur, double segdur, int32_t index) {
 OTF_HD double lat_edge(int k) {   // lower edge of bin 1 + k
     return ldexp(0.01 * (1.0 + 0.25 * (double)(k & 3)), k >> 2);
 }
-static __host__ __device__ __noinline__ int lat_bin(double lat) {
+OTF_HD int lat_bin(double lat) {
     if (lat < 0.010) return 0;
     int e;
     frexp(lat / 0.01, &e);                   // estimate, then fix up on the exact edges

@@ -34,8 +34,7 @@ OTF_HD int push_words(uint32_t *w, int n, uint64_t v) {
 }
 
 // SeedSequence(entropy words).generate_state(4, uint64) -> PCG64.__init__.
-// Out of line: runs once per stream and its unrolled mixing is large.
-static __host__ __device__ __noinline__ void pcg_seed(Pcg64 &g, const uint32_t *ent, int m) {
+OTF_HD void pcg_seed(Pcg64 &g, const uint32_t *ent, int m) {
     uint32_t pool[4];
     uint32_t hc = 0x43b0d7e5u;
     auto hashmix = [&](uint32_t v) -> uint32_t {
