@@ -63,11 +63,7 @@ struct WinHeader {
     int32_t fq_w[MAXK], fq_d[MAXK], fq_j[MAXK];
     int32_t gq_head, gq_n, fq_head, fq_n;
     int32_t jq_head, jq_n, jq_cap;
-    int32_t n_list;
-    int32_t n_resp[2];                   // responses per window parity (server warp -> client warp)
-    int32_t n_loc;                       // client-local events popped for the current window
-    int32_t iter, next_iter;             // last iteration / next one (set by the server warp)
-    int32_t done;
+    int32_t n_list, n_blist;
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
     int32_t arr_next;                    // next client (arrival order) not yet on the wheel
@@ -78,9 +74,7 @@ struct WinHeader {
     double t_seqdur[MAXTAB], t_segdur[MAXTAB], t_zipf[MAXTAB], t_rho[MAXTAB];
     int64_t t_bitrates[MAXTAB], t_manifest[MAXTAB];
     // timer wheel: server-event and client-local buckets per window
-    uint32_t bits_srv[RING / 32];
-    uint32_t bits_loc[RING / 32];
-    double red[3][2];                    // cross-warp reduction of the float sums
+    uint32_t bits[RING / 32];
     int32_t bhead_srv[RING];
     int32_t bhead_loc[RING];
     // the window's server events
@@ -100,15 +94,14 @@ __host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {
 }
 
 struct WinGlobalLayout {
-    int64_t clients, resp, loclist, wq_head, wq_tail, jobq, lstamp, lq, total;
+    int64_t clients, blist, wq_head, wq_tail, jobq, lstamp, lq, total;
 };
 
 __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
     WinGlobalLayout L;
     int64_t o = 0;
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
-    L.resp = o;    o += align256((int64_t)sizeof(int32_t) * 2 * (n_clients + 64));
-    L.loclist = o; o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
+    L.blist = o;   o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
     L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
@@ -134,14 +127,13 @@ struct Win {
     LqEnt *lq;                                         // touch queue (global, 2 * lq_cap)
     uint8_t *dflags;
     Client *cl;
-    int32_t *resp, *loclist, *wq_head, *wq_tail;     // resp: 2 x (N + 64), by window parity
+    int32_t *blist, *wq_head, *wq_tail;
     JobEnt *jq;
     double W, invW, H, E, now;
     int32_t k;
     // lane 0's register copies of the hot server counters during phase A
     int64_t req_counter, n_req;
-    int32_t n_resp;
-    int32_t *resp_cur;                                 // this window's response list
+    int32_t n_blist;
     bool wdirty;
 };
 
@@ -168,7 +160,7 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
         int32_t slot = wk & (RING - 1);
         int32_t old = atomicExch(srv ? &h->bhead_srv[slot] : &h->bhead_loc[slot], c);
         w.bnext[c] = (int16_t)old;
-        atomicOr(srv ? &h->bits_srv[slot >> 5] : &h->bits_loc[slot >> 5], 1u << (slot & 31));
+        atomicOr(&h->bits[slot >> 5], 1u << (slot & 31));
     } else {                                           // beyond the wheel (rare): far list
         int32_t old = atomicExch(&h->far_head, c);
         w.bnext[c] = (int16_t)old;
@@ -313,7 +305,7 @@ __device__ __forceinline__ void respond(Win &w, int32_t cid) {
     c.req_slot = w.n_req++;
     c.pc = C_SEG_RESP;
     c.next_when = w.now;
-    w.resp_cur[w.n_resp++] = cid;
+    w.blist[w.n_blist++] = cid;
 }
 
 __device__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
@@ -450,9 +442,7 @@ __device__ void phase_a(Win &w) {
     const int32_t n = h->n_list;
     w.req_counter = h->st.req_counter;
     w.n_req = h->st.n_req;
-    const int32_t par = w.k & 1;
-    w.resp_cur = w.resp + par * (w.S.sc->n_clients + 64);
-    w.n_resp = h->n_resp[par];
+    w.n_blist = h->n_blist;
     w.wdirty = true;
     int32_t bw = -1;
     int64_t pops = 0;
@@ -501,7 +491,7 @@ __device__ void phase_a(Win &w) {
     h->stats[OTF_ST_TIMER_POPS] += pops;
     h->st.req_counter = w.req_counter;
     h->st.n_req = w.n_req;
-    h->n_resp[par] = w.n_resp;
+    h->n_blist = w.n_blist;
 }
 
 // ---- client lanes ------------------------------------------------------------------
@@ -518,7 +508,7 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
     if (next_pc == C_SEG_LAT) {                        // a server event: always a later window
         int32_t k = timer_win(w, when);
         if (k == WIN_NONE) return false;
-        if (k <= w.k + 1) w.S.flag(OTF_S_TIE);         // lookahead violated (cannot happen)
+        if (k <= w.k) w.S.flag(OTF_S_TIE);             // lookahead violated (cannot happen)
         bucket_push(w, cid, k, true);
         return false;
     }
@@ -675,7 +665,7 @@ __device__ void order_ties(Win &w) {
         int32_t j = i;                                 // insertion step by ctime
         while (j > 0 && h->list_when[j] == h->list_when[j - 1]) {
             double cj = w.cl[h->list_id[j]].ctime, cp = w.cl[h->list_id[j - 1]].ctime;
-            if (cj == cp) { atomicOr(&h->st.status, OTF_S_TIE); break; }
+            if (cj == cp) { h->st.status |= OTF_S_TIE; break; }
             if (cj > cp) break;
             int16_t ti = h->list_id[j]; h->list_id[j] = h->list_id[j - 1]; h->list_id[j - 1] = ti;
             int16_t td = h->list_desc[j]; h->list_desc[j] = h->list_desc[j - 1]; h->list_desc[j - 1] = td;
@@ -685,20 +675,21 @@ __device__ void order_ties(Win &w) {
     }
 }
 
-// First non-empty window >= start on a wheel bitmap (warp-wide scan of RING slots).
-__device__ int32_t wheel_next(const uint32_t *bits, int32_t start, int lane) {
+// Next non-empty window after k_done on the wheel (warp-wide bitmap scan).
+__device__ int32_t wheel_next(WinHeader *h, int32_t k_done, int lane) {
+    const int32_t start = k_done + 1;
     const int32_t p0 = start & (RING - 1);
     const int32_t w0 = p0 >> 5;
     constexpr int32_t NW = RING / 32;
     int32_t best = WIN_NONE;
     // virtual words 0..NW: word 0 = first word from bit p0, word NW = its low bits (wrap)
     for (int32_t v = lane; v <= NW; v += 32) {
-        uint32_t x;
-        if (v == 0) x = bits[w0] & (0xffffffffu << (p0 & 31));
-        else if (v == NW) x = (p0 & 31) ? (bits[w0] & ((1u << (p0 & 31)) - 1)) : 0u;
-        else x = bits[(w0 + v) & (NW - 1)];
-        if (x) {
-            int32_t slot = ((v == NW ? w0 : (w0 + v) & (NW - 1)) << 5) + (__ffs(x) - 1);
+        uint32_t bits;
+        if (v == 0) bits = h->bits[w0] & (0xffffffffu << (p0 & 31));
+        else if (v == NW) bits = (p0 & 31) ? (h->bits[w0] & ((1u << (p0 & 31)) - 1)) : 0u;
+        else bits = h->bits[(w0 + v) & (NW - 1)];
+        if (bits) {
+            int32_t slot = (((v == NW ? w0 : (w0 + v) & (NW - 1))) << 5) + (__ffs(bits) - 1);
             int32_t dist = (slot - p0) & (RING - 1);
             if (v == NW && dist == 0) dist = RING;
             best = min(best, start + dist);
@@ -707,161 +698,14 @@ __device__ int32_t wheel_next(const uint32_t *bits, int32_t start, int lane) {
     return warp_min(best);
 }
 
-// Two warps per scenario.  Iteration j: the server warp replays window j's
-// server events (phase A) while the client warp runs window j-1's client
-// events (phase B).  With half-width windows W = latency(1-2^-20)/2, a server
-// event of window j was armed at least two windows earlier, so phase A(j)
-// only depends on phase B(<= j-2); phase B(j-1) only depends on A(<= j-1).
-constexpr int NTHREADS = 64;
-
-__device__ void refile_far(Win &w, int32_t base) {     // server warp, lane 0
-    WinHeader *h = w.h;
-    int32_t c = h->far_head;
-    h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
-    w.k = base;
-    while (c >= 0) {
-        int32_t nx = w.bnext[c];
-        const Client &cl = w.cl[c];
-        bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT);
-        c = nx;
-    }
-}
-
-// Server warp: choose the next iteration j (windows in between are empty for
-// both warps), feed arrivals / far timers that now fall on the wheel.
-__device__ void plan_next(Win &w, int lane) {
-    WinHeader *h = w.h;
-    const int32_t i = h->iter;
-    const int32_t N = w.S.sc->n_clients, K = w.S.sc->n_workers;
-    for (;;) {
-        int32_t srv = wheel_next(h->bits_srv, i + 1, lane);
-        srv = min(srv, warp_min(lane < K ? h->wk[lane].win : WIN_NONE));
-        int32_t loc = wheel_next(h->bits_loc, i < 0 ? 0 : i, lane);
-        if (i >= 0 && h->n_resp[i & 1] > 0) loc = min(loc, i);
-        int32_t arr = WIN_NONE;
-        if (h->arr_next < N) arr = timer_win(w, w.S.arrival(h->arr_next));
-        loc = min(loc, arr);
-        int32_t j = min(srv, loc == WIN_NONE ? WIN_NONE : loc + 1);
-        j = min(j, h->far_min);
-        if (j == WIN_NONE) { if (lane == 0) h->done = 1; break; }
-        if (h->far_n > 0 && h->far_min < j + RING / 2) {
-            if (lane == 0) refile_far(w, j - 1);
-            __syncwarp();
-            continue;
-        }
-        if (arr != WIN_NONE && arr - (j - 1) < RING - 1) {  // arrivals joining the wheel
-            if (lane == 0) {
-                w.k = j - 1;
-                int32_t c = h->arr_next;
-                while (c < N) {
-                    int32_t wk = timer_win(w, w.S.arrival(c));
-                    if (wk == WIN_NONE || wk - (j - 1) >= RING - 1) break;
-                    bucket_push(w, c, wk, false);
-                    c++;
-                }
-                h->arr_next = c;
-            }
-            __syncwarp();
-        }
-        if (lane == 0) h->next_iter = j;
-        break;
-    }
-    __syncwarp();
-}
-
-// Server warp: phase A of window j.
-__device__ void server_window(Win &w, int32_t j, int lane) {
-    WinHeader *h = w.h;
-    long long t0 = clock64(), t1;
-    w.k = j;
-    if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
-    const int32_t slot = j & (RING - 1);
-    const bool has_srv = (h->bits_srv[slot >> 5] >> (slot & 31)) & 1u;
-    if (lane == 0) {
-        int32_t nl = 0;
-        if (has_srv) {
-            int32_t c = h->bhead_srv[slot];
-            h->bhead_srv[slot] = -1;
-            atomicAnd(&h->bits_srv[slot >> 5], ~(1u << (slot & 31)));   // the client warp sets bits concurrently
-            while (c >= 0) {
-                if (nl < LIST_CAP) h->list_id[nl] = (int16_t)c;
-                nl++;
-                c = w.bnext[c];
-            }
-        }
-        h->n_list = nl;
-        h->stats[OTF_ST_WINDOWS]++;
-    }
-    __syncwarp();
-    if (h->n_list > LIST_CAP) {                        // too many simultaneous requests for this engine
-        if (lane == 0) { atomicOr(&h->st.status, OTF_S_TIE); h->n_list = 0; }
-        __syncwarp();
-        return;
-    }
-    for (int32_t i = lane; i < h->n_list; i += 32) {   // gather sort keys + request descriptors
-        const Client &cl = w.cl[h->list_id[i]];
-        h->list_when[i] = cl.next_when;
-        h->list_desc[i] = (int16_t)cl.desc;
-        h->list_pack[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
-    }
-    __syncwarp();
-    t1 = clock64();
-    if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
-    t0 = t1;
-    sort_list(h, lane);
-    t1 = clock64();
-    if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
-    t0 = t1;
-    if (lane == 0) {
-        order_ties(w);
-        phase_a(w);
-        h->stats[OTF_ST_CYC_SERVER] += clock64() - t0;
-    }
-    __syncwarp();
-}
-
-// Client warp: phase B of window j (its local timers + the responses of A(j)).
-__device__ void client_window(Win &w, int32_t j, int lane) {
-    WinHeader *h = w.h;
-    long long t0 = clock64();
-    w.k = j;
-    w.E = (double)(j + 1) * w.W;
-    const int32_t slot = j & (RING - 1);
-    const bool has_loc = (h->bits_loc[slot >> 5] >> (slot & 31)) & 1u;
-    if (lane == 0) {
-        int32_t nb = 0;
-        if (has_loc) {
-            int32_t c = h->bhead_loc[slot];
-            h->bhead_loc[slot] = -1;
-            atomicAnd(&h->bits_loc[slot >> 5], ~(1u << (slot & 31)));
-            while (c >= 0) {
-                w.loclist[nb++] = c;
-                c = w.bnext[c];
-            }
-        }
-        h->n_loc = nb;
-    }
-    __syncwarp();
-    const int32_t nb = h->n_loc;
-    const int32_t nr = h->n_resp[j & 1];
-    const int32_t *resp = w.resp + (j & 1) * (w.S.sc->n_clients + 64);
-    for (int32_t i = lane; i < nb + nr; i += 32) client_local(w, i < nb ? w.loclist[i] : resp[i - nb]);
-    __syncwarp();
-    if (lane == 0) {
-        h->n_resp[j & 1] = 0;
-        h->stats[OTF_ST_CYC_CLIENTS] += clock64() - t0;
-    }
-}
-
-__global__ void __launch_bounds__(NTHREADS, 8) windowed_kernel(const otf_batch b) {
+__global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const bool server_warp = tid < 32;
+    const int lane = threadIdx.x;
+    long long t_start = 0, t0 = 0, t1 = 0;
     const int32_t s = b.order ? b.order[blockIdx.x] : (int32_t)blockIdx.x;
     WinHeader *h = (WinHeader *)smem;
-    if (tid == 0) { h->b = b; h->sc = b.scenarios[s]; }
-    __syncthreads();
+    if (lane == 0) { h->b = b; h->sc = b.scenarios[s]; }
+    __syncwarp();
     Win w;
     w.S.init(&h->b, &h->sc, s);
     const otf_scenario &sc = h->sc;
@@ -877,25 +721,24 @@ __global__ void __launch_bounds__(NTHREADS, 8) windowed_kernel(const otf_batch b
     w.lstamp = (uint32_t *)(g + L.lstamp);
     w.lq = (LqEnt *)(g + L.lq);
     w.cl = (Client *)(g + L.clients);
-    w.resp = (int32_t *)(g + L.resp);
-    w.loclist = (int32_t *)(g + L.loclist);
+    w.blist = (int32_t *)(g + L.blist);
     w.wq_head = (int32_t *)(g + L.wq_head);
     w.wq_tail = (int32_t *)(g + L.wq_tail);
     w.jq = (JobEnt *)(g + L.jobq);
+    // counters, QoE and small tables live in shared memory
     w.S.st = &h->st;
     w.S.stats = h->stats;
     w.S.qa = &h->qa;
     w.S.lat_sum = w.S.stall_sum = w.S.startup_sum = 0.0;
-    w.W = sc.latency * (1.0 - 0x1p-20) * 0.5;
+    w.W = sc.latency * (1.0 - 0x1p-20);
     w.invW = 1.0 / w.W;
     w.H = sc.horizon;
     w.k = -1;
-    long long t_start = clock64();
 
     // ---- init -------------------------------------------------------------------
     const bool fits = K <= MAXK && N <= MAXN && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB && D < 32767 &&
-                      sc.latency > 0 && sc.horizon / (sc.latency * (1.0 - 0x1p-20) * 0.5) < 5.0e8;
-    if (tid == 0) {
+                      sc.latency > 0 && sc.horizon / (sc.latency * (1.0 - 0x1p-20)) < 5.0e8;
+    if (lane == 0) {
         EngineState z = {};
         z.lru_head = z.lru_tail = -1;
         h->st = z;
@@ -903,40 +746,48 @@ __global__ void __launch_bounds__(NTHREADS, 8) windowed_kernel(const otf_batch b
         qoe_zero(&h->qa, 0, 1);
         h->gq_head = 0; h->gq_n = K; h->fq_head = 0; h->fq_n = 0;
         h->jq_head = 0; h->jq_n = 0; h->jq_cap = (int32_t)(D + 1);
-        h->n_list = 0; h->n_resp[0] = h->n_resp[1] = 0; h->n_loc = 0; h->wseq = 0;
-        h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
-        h->arr_next = 0; h->iter = -1; h->next_iter = 0; h->done = 0;
+        h->n_list = 0; h->n_blist = 0; h->wseq = 0;
+        h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
+        h->arr_next = 0;
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
         if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
     }
-    __syncthreads();
+    __syncwarp();
     if (!fits) goto done;
-    for (int32_t q = tid; q < MAXK; q += NTHREADS) {
+    for (int32_t q = lane; q < MAXK; q += 32) {
         h->gq[q] = q;                                  // workers register as getters in id order
         WWorker z = {};
         z.win = WIN_NONE; z.pc = W_GOT; z.desc = -1; z.job = -1;
         h->wk[q] = z;
     }
-    for (int32_t i = tid; i < RING; i += NTHREADS) { h->bhead_srv[i] = -1; h->bhead_loc[i] = -1; }
-    for (int32_t i = tid; i < RING / 32; i += NTHREADS) { h->bits_srv[i] = 0; h->bits_loc[i] = 0; }
-    for (int32_t i = tid; i < sc.n_seq; i += NTHREADS) {
+    for (int32_t i = lane; i < RING; i += 32) { h->bhead_srv[i] = -1; h->bhead_loc[i] = -1; }
+    for (int32_t i = lane; i < RING / 32; i += 32) h->bits[i] = 0;
+    for (int32_t i = lane; i < sc.n_seq; i += 32) {
         h->t_segcount[i] = w.S.segcounts[i];
         h->t_seqdur[i] = w.S.seqdur[i];
         h->t_segdur[i] = w.S.segdur[i];
         h->t_zipf[i] = w.S.zipf[i];
         h->t_manifest[i] = w.S.manifest_b[i];
     }
-    for (int32_t i = tid; i < sc.n_ranks; i += NTHREADS) {
+    for (int32_t i = lane; i < sc.n_ranks; i += 32) {
         h->t_rho[i] = w.S.rho[i];
         h->t_bitrates[i] = w.S.bitrates[i];
     }
-    for (int64_t d = tid; d < D; d += NTHREADS) {
+    for (int64_t d = lane; d < D; d += 32) {
         w.lstamp[d] = 0; w.dflags[d] = 0;
         w.wq_head[d] = -1; w.wq_tail[d] = -1;
     }
+    __syncwarp();
+    w.S.segcounts = h->t_segcount;
+    w.S.seqdur = h->t_seqdur;
+    w.S.segdur = h->t_segdur;
+    w.S.zipf = h->t_zipf;
+    w.S.manifest_b = h->t_manifest;
+    w.S.rho = h->t_rho;
+    w.S.bitrates = h->t_bitrates;
     // clients: the first step arms sleep(offset) (orchestrator.py:337); offsets are a
-    // cumulative sum, so clients join the wheel in id order (arrival cursor)
-    for (int32_t c = tid; c < N; c += NTHREADS) {
+    // cumulative sum, so clients join the wheel in id order (arrival cursor below)
+    for (int32_t c = lane; c < N; c += 32) {
         Client &cl = w.cl[c];
         client_init(cl);
         double off = w.S.arrival(c);
@@ -945,57 +796,125 @@ __global__ void __launch_bounds__(NTHREADS, 8) windowed_kernel(const otf_batch b
         cl.next_when = 0.0 + off;
         if (!(off > 0)) w.S.flag(OTF_S_TIE);           // instant start: tick order among clients matters
     }
-    __syncthreads();
-    w.S.segcounts = h->t_segcount;
-    w.S.seqdur = h->t_seqdur;
-    w.S.segdur = h->t_segdur;
-    w.S.zipf = h->t_zipf;
-    w.S.manifest_b = h->t_manifest;
-    w.S.rho = h->t_rho;
-    w.S.bitrates = h->t_bitrates;
+    __syncwarp();
     if (h->st.status & OTF_S_TIE) goto done;
 
-    // ---- iterations -----------------------------------------------------------------
+    // ---- window loop --------------------------------------------------------------
+    t_start = clock64();
     for (;;) {
-        if (server_warp) plan_next(w, lane);
-        __syncthreads();
-        if (h->done) break;
-        const int32_t j = h->next_iter;
-        if (server_warp) server_window(w, j, lane);
-        else if (j >= 1) client_window(w, j - 1, lane);
-        __syncthreads();
+        t0 = clock64();
+        // next window: wheel, far list, worker timers, next arrival
+        int32_t m = wheel_next(h, h->k_done, lane);
+        int32_t mw = lane < K ? h->wk[lane].win : WIN_NONE;
+        m = min(m, warp_min(mw));
+        m = min(m, h->far_min);
+        int32_t arr_win = WIN_NONE;
+        if (h->arr_next < N) arr_win = timer_win(w, w.S.arrival(h->arr_next));
+        m = min(m, arr_win);
+        if (m == WIN_NONE) break;
+        if (arr_win != WIN_NONE && arr_win - m < RING) {   // arrivals entering the wheel
+            if (lane == 0) {
+                h->k_done = m - 1;                     // windows before m are empty: wheel base = m
+                w.k = m - 1;
+                int32_t c = h->arr_next;
+                while (c < N) {
+                    int32_t wk = timer_win(w, w.S.arrival(c));
+                    if (wk == WIN_NONE || wk - m >= RING) break;
+                    bucket_push(w, c, wk, false);
+                    c++;
+                }
+                h->arr_next = c;
+            }
+            __syncwarp();
+        }
+        if (h->far_n > 0 && h->far_min < m + RING / 2) {   // far timers close to the wheel: re-file them
+            if (lane == 0) {
+                int32_t c = h->far_head;
+                h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
+                h->k_done = m - 1;                     // windows before m are empty: wheel base = m
+                w.k = m - 1;
+                while (c >= 0) {
+                    int32_t nx = w.bnext[c];
+                    const Client &cl = w.cl[c];
+                    bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT);
+                    c = nx;
+                }
+            }
+            __syncwarp();
+            continue;
+        }
+        w.k = m;
+        w.E = (double)(m + 1) * w.W;
+        if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
+        // pop the buckets: server events -> list, client-local events -> B-list
+        if (lane == 0) {
+            h->stats[OTF_ST_WINDOWS]++;
+            int32_t slot = m & (RING - 1);
+            int32_t c = h->bhead_srv[slot];
+            int32_t cl = h->bhead_loc[slot];
+            h->bhead_srv[slot] = -1;
+            h->bhead_loc[slot] = -1;
+            h->bits[slot >> 5] &= ~(1u << (slot & 31));
+            int32_t nl = 0, nb = 0;
+            while (c >= 0) {
+                if (nl < LIST_CAP) h->list_id[nl] = (int16_t)c;
+                nl++;
+                c = w.bnext[c];
+            }
+            while (cl >= 0) {
+                w.blist[nb++] = cl;
+                cl = w.bnext[cl];
+            }
+            h->n_list = nl;
+            h->n_blist = nb;
+        }
+        __syncwarp();
+        if (h->n_list > LIST_CAP) {                    // too many simultaneous requests for this engine
+            if (lane == 0) h->st.status |= OTF_S_TIE;
+            __syncwarp();
+            break;
+        }
+        for (int32_t i = lane; i < h->n_list; i += 32) {   // gather sort keys + request descriptors
+            const Client &cl = w.cl[h->list_id[i]];
+            h->list_when[i] = cl.next_when;
+            h->list_desc[i] = (int16_t)cl.desc;
+            h->list_pack[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
+        }
+        __syncwarp();
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
+        t0 = t1;
+        sort_list(h, lane);
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
+        t0 = t1;
+        // ---- phase A: server lane ----
+        if (lane == 0) {
+            order_ties(w);
+            phase_a(w);
+            h->k_done = m;
+        }
+        __syncwarp();
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_SERVER] += t1 - t0;
+        t0 = t1;
         if (h->st.status & OTF_S_TIE) break;
-        if (tid == 0) h->iter = j;
+        // ---- phase B: client lanes ----
+        const int32_t nb = h->n_blist;
+        for (int32_t i = lane; i < nb; i += 32) client_local(w, w.blist[i]);
+        __syncwarp();
+        t1 = clock64();
+        if (lane == 0) h->stats[OTF_ST_CYC_CLIENTS] += t1 - t0;
     }
-    // the last responses (A(last)) still need their client step
-    if (!(h->st.status & OTF_S_TIE) && h->iter >= 0 && h->n_resp[h->iter & 1] > 0) {
-        if (!server_warp) client_window(w, h->iter, lane);
-        __syncthreads();
-    }
-    if (tid == 0) h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
+    if (lane == 0) h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
     if (!(h->st.status & OTF_S_TIE)) {
-        for (int32_t c = tid; c < N; c += NTHREADS) client_harvest(w.S, w.cl[c], sc.horizon);
+        for (int32_t c = lane; c < N; c += 32) client_harvest(w.S, w.cl[c], sc.horizon);
     }
-    __syncthreads();
+    __syncwarp();
 done:
-    // float sums: fixed-order reduction (per warp, then warp 0 + warp 1)
-    for (int o = 16; o > 0; o >>= 1) {
-        w.S.lat_sum += __shfl_down_sync(0xffffffffu, w.S.lat_sum, o);
-        w.S.stall_sum += __shfl_down_sync(0xffffffffu, w.S.stall_sum, o);
-        w.S.startup_sum += __shfl_down_sync(0xffffffffu, w.S.startup_sum, o);
-    }
     if (lane == 0) {
-        h->red[0][tid >> 5] = w.S.lat_sum;
-        h->red[1][tid >> 5] = w.S.stall_sum;
-        h->red[2][tid >> 5] = w.S.startup_sum;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        w.S.lat_sum = h->red[0][0] + h->red[0][1];
-        w.S.stall_sum = h->red[1][0] + h->red[1][1];
-        w.S.startup_sum = h->red[2][0] + h->red[2][1];
         int64_t *gs = b.stats + (int64_t)s * OTF_ST_NSLOTS;
         h->stats[OTF_ST_CACHE_CAPACITY] = sc.cache_capacity;
         h->stats[OTF_ST_CURRENT_BYTES] = h->st.cur_bytes;
@@ -1005,8 +924,14 @@ done:
         int64_t *cnt = b.counts + (int64_t)s * 4;
         cnt[0] = h->st.n_req; cnt[1] = h->st.n_sess; cnt[2] = h->st.n_seg; cnt[3] = h->st.n_job;
         b.status[s] = h->st.status;
-        w.S.flush_qoe();
     }
+    // float sums: fixed-order warp reduction, then lane 0 writes the QoE block
+    for (int o = 16; o > 0; o >>= 1) {
+        w.S.lat_sum += __shfl_down_sync(0xffffffffu, w.S.lat_sum, o);
+        w.S.stall_sum += __shfl_down_sync(0xffffffffu, w.S.stall_sum, o);
+        w.S.startup_sum += __shfl_down_sync(0xffffffffu, w.S.startup_sum, o);
+    }
+    if (lane == 0) w.S.flush_qoe();
 }
 
 }  // namespace otf
@@ -1026,6 +951,6 @@ int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
         cudaError_t e = cudaFuncSetAttribute(otf::windowed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return 1;
     }
-    otf::windowed_kernel<<<b.n_scenarios, otf::NTHREADS, smem, stream>>>(b);
+    otf::windowed_kernel<<<b.n_scenarios, 32, smem, stream>>>(b);
     return 0;
 }
