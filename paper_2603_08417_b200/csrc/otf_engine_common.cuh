@@ -48,6 +48,8 @@ struct Scn {
     otf_qoe *q;                      // final destination (global)
     QoeAcc *qa;                      // counters while running (shared or scratch)
     double lat_sum, stall_sum, startup_sum;   // this lane's float sums
+    uint64_t mag_g, mag_rg;                   // d / max_nseg, d / (n_ranks * max_nseg) by multiply-high
+    uint32_t div_g, div_rg;
     const int64_t *sizes, *bitrates, *manifest_b;
     const int32_t *segcounts;
     const double *seqdur, *segdur, *rho, *zipf, *starts, *values, *pbits, *arrivals, *eps;
@@ -74,6 +76,14 @@ struct Scn {
         arrivals = b->f64_pool + sc->off_arrivals;
         eps = b->f64_pool + sc->off_eps;
         records = b->mode == OTF_MODE_RECORDS;
+        div_g = (uint32_t)sc->max_nseg;
+        div_rg = (uint32_t)(sc->n_ranks * sc->max_nseg);
+        mag_g = 0xffffffffffffffffull / div_g + 1ull;
+        mag_rg = 0xffffffffffffffffull / div_rg + 1ull;
+    }
+    // floor(d / div) = umul64hi(d, floor((2^64-1)/div) + 1), exact for d, div < 2^31
+    __device__ __forceinline__ uint32_t qdiv(uint32_t d, uint64_t mag, uint32_t) const {
+        return (uint32_t)__umul64hi((uint64_t)d, mag);
     }
 
     // zero the scenario's outputs and counters (call once, single thread)
@@ -118,9 +128,13 @@ struct Scn {
         t.n = sc->n_samples;
         return t;
     }
-    __device__ __forceinline__ int32_t desc_seq(int32_t d) const { return d / (sc->n_ranks * sc->max_nseg); }
-    __device__ __forceinline__ int32_t desc_rank(int32_t d) const { return (d / sc->max_nseg) % sc->n_ranks + 1; }
-    __device__ __forceinline__ int32_t desc_index(int32_t d) const { return d % sc->max_nseg; }
+    __device__ __forceinline__ int32_t desc_seq(int32_t d) const { return (int32_t)qdiv(d, mag_rg, div_rg); }
+    __device__ __forceinline__ int32_t desc_rank(int32_t d) const {
+        return (int32_t)(qdiv(d, mag_g, div_g) - (uint32_t)desc_seq(d) * (uint32_t)sc->n_ranks) + 1;
+    }
+    __device__ __forceinline__ int32_t desc_index(int32_t d) const {
+        return (int32_t)((uint32_t)d - qdiv(d, mag_g, div_g) * div_g);
+    }
 
     // Backend._enqueue bookkeeping: TranscodeJob + jobs.append (backend.py:156-170)
     __device__ int32_t record_job(int32_t d, int32_t origin, double now) {

@@ -559,63 +559,75 @@ __device__ __forceinline__ void record_response(Win &w, const Client &c, double 
     S.lat_sum += lat;
 }
 
+// The client coroutine between two yields.  Every state computes either
+// "continue at the next state now" or (delay, next state); the single arm()
+// site and the single shaped-transfer site keep the hot code small.
 __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid) {
     Scn &S = w.S;
     const otf_scenario &sc = *S.sc;
     double now = c.next_when;
     for (;;) {
+        double delay = 0.0;
+        int64_t nbytes = 0;
+        int32_t next = C_DONE;
+        bool xfer = false;
         switch (c.pc) {
         case C_ARRIVED:
             client_arrive(S, c, cid);
             c.pc = C_SESSION;
-            break;
+            continue;
         case C_SESSION:
             if (!(now < sc.horizon)) { c.pc = C_DONE; return; }
             client_new_session(S, c, cid, now);
-            if (sc.latency > 0) { if (!arm(w, c, cid, now, sc.latency, C_MAN_LAT)) return; }
-            else c.pc = C_MAN_LAT;
+            delay = sc.latency;                        // manifest request latency (netem.py:138-139)
+            next = C_MAN_LAT;
             break;
-        case C_MAN_LAT: {
-            double end = completion_time(S.trace(cid), now, S.manifest(c.seq));
-            if (!arm(w, c, cid, now, end - now, C_MAN_XFER)) return;
+        case C_MAN_LAT:
+            nbytes = S.manifest(c.seq);
+            next = C_MAN_XFER;
+            xfer = true;
             break;
-        }
         case C_MAN_XFER:
             client_start_playback(c, now);
             c.pc = C_INDEX_HEAD;
-            break;
+            continue;
         case C_INDEX_HEAD:
         case C_TARGET_WAIT:
             buf_advance(c.buf, now);
             if (c.buf.phase == PH_PLAYING && c.buf.level >= sc.target) {
-                if (!arm(w, c, cid, now, c.buf.level - sc.target + 1e-9, C_TARGET_WAIT)) return;
+                delay = c.buf.level - sc.target + 1e-9;
+                next = C_TARGET_WAIT;
                 break;
             }
             client_select(S, c);
             c.requested = now;
             c.desc = S.desc_id(c.seq, c.rank, c.index);
-            if (!arm(w, c, cid, now, sc.latency, C_SEG_LAT)) return;
-            S.flag(OTF_S_INTERNAL);                    // zero latency never reaches this engine
-            return;
-        case C_SEG_RESP: {
+            delay = sc.latency;                        // request latency, then MediaServer.segment
+            next = C_SEG_LAT;
+            break;
+        case C_SEG_RESP:
             record_response(w, c, now);
             c.size = S.size(c.desc);
             c.xfer_start = now;
-            double end = completion_time(S.trace(cid), now, c.size);
-            if (!arm(w, c, cid, now, end - now, C_SEG_XFER)) return;
+            nbytes = c.size;
+            next = C_SEG_XFER;
+            xfer = true;
             break;
-        }
         case C_SEG_XFER:
-            if (client_segment_done(S, c, now)) { c.pc = C_INDEX_HEAD; break; }
-            if (!arm(w, c, cid, now, c.buf.level, C_PLAYOUT)) return;
+            if (client_segment_done(S, c, now)) { c.pc = C_INDEX_HEAD; continue; }
+            delay = c.buf.level;                       // play out the buffer (client.py:271)
+            next = C_PLAYOUT;
             break;
         case C_PLAYOUT:
             client_finish_session(S, c, now);
             c.pc = C_SESSION;
-            break;
+            continue;
         default:
             return;
         }
+        if (xfer) delay = completion_time(S.trace(cid), now, nbytes) - now;
+        if (!arm(w, c, cid, now, delay, next)) return;
+        if (next == C_SEG_LAT) { S.flag(OTF_S_INTERNAL); return; }   // zero latency never reaches this engine
     }
 }
 

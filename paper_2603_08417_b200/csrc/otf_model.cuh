@@ -10,6 +10,7 @@
 #pragma once
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "otfgpu.h"
 
@@ -18,6 +19,14 @@
 #endif
 
 namespace otf {
+
+#ifdef __CUDA_ARCH__
+OTF_HD double __longlong_as_double_hd(long long v) { return __longlong_as_double(v); }
+OTF_HD long long __double_as_longlong_hd(double v) { return __double_as_longlong(v); }
+#else
+OTF_HD double __longlong_as_double_hd(long long v) { double d; memcpy(&d, &v, 8); return d; }
+OTF_HD long long __double_as_longlong_hd(double v) { long long l; memcpy(&l, &v, 8); return l; }
+#endif
 
 enum { PH_STARTUP = 0, PH_PLAYING = 1, PH_STALLED = 2, PH_FINISHED = 3 };
 
@@ -72,21 +81,27 @@ OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent
     left_out = bits;
 }
 
-// BandwidthTrace.completion_time for a looping trace (netem.py:97-118)
+// BandwidthTrace.completion_time for a looping trace (netem.py:97-118).  The
+// two _drain_from calls share one loop so the walk is emitted once.
 OTF_HD double completion_time(const Trace &tr, double start, int64_t nbytes) {
     double bits = (double)nbytes * 8.0;
     if (bits <= 0) return start;
     if (tr.pbits <= 0) return INFINITY;
     double t = start, spent, left;
-    drain_from(tr, fmod(start, tr.period), bits, spent, left);
-    t += spent;
-    if (left <= 0) return t;
-    double whole = floor(left / tr.pbits);
-    t += whole * tr.period;
-    left -= whole * tr.pbits;
-    if (left <= 0) return t;
-    drain_from(tr, 0.0, left, spent, left);
-    return t + spent;
+    // fmod(start, period) == start for 0 <= start < period (exact)
+    double phase = (start >= 0.0 && start < tr.period) ? start : fmod(start, tr.period);
+    for (int pass = 0; pass < 2; pass++) {
+        drain_from(tr, phase, bits, spent, left);
+        t += spent;
+        if (left <= 0 || pass == 1) return t;
+        double whole = floor(left / tr.pbits);
+        t += whole * tr.period;
+        left -= whole * tr.pbits;
+        if (left <= 0) return t;
+        bits = left;
+        phase = 0.0;
+    }
+    return t;
 }
 
 struct Buffer {
@@ -149,16 +164,19 @@ OTF_HD double seg_duration(double seqdur, double segdur, int32_t index) {
 }
 
 // Latency histogram bin: 0 = instant (< 10 ms, metrics.py:38,77), then 4 bins
-// per octave with edges ldexp(0.01 * (1 + q/4), o).
-OTF_HD double lat_edge(int k) {   // lower edge of bin 1 + k
-    return ldexp(0.01 * (1.0 + 0.25 * (double)(k & 3)), k >> 2);
+// per octave with lower edges 0.01 * (1 + q/4) * 2^o (exact in double).
+OTF_HD double pow2i(int o) {                           // 2^o for 0 <= o < 1024, exact
+    return __longlong_as_double_hd((long long)(o + 1023) << 52);
+}
+OTF_HD double lat_edge(int k) {                        // lower edge of bin 1 + k
+    return (0.01 * (1.0 + 0.25 * (double)(k & 3))) * pow2i(k >> 2);
 }
 OTF_HD int lat_bin(double lat) {
     if (lat < 0.010) return 0;
-    int e;
-    frexp(lat / 0.01, &e);                   // estimate, then fix up on the exact edges
-    double r = ldexp(lat / 0.01, -(e - 1));
-    int k = (e - 1) * 4 + (int)((r - 1.0) * 4.0);
+    double x = lat * 100.0;                            // estimate of lat / 0.01; exact edges decide
+    long long bitsx = __double_as_longlong_hd(x);
+    int e = (int)((bitsx >> 52) & 0x7ff) - 1023;
+    int k = e * 4 + (int)((bitsx >> 50) & 3);
     if (k < 0) k = 0;
     if (k > OTF_LAT_BINS - 2) k = OTF_LAT_BINS - 2;
     while (k + 1 <= OTF_LAT_BINS - 2 && lat >= lat_edge(k + 1)) k++;

@@ -43,19 +43,21 @@ OTF_HD void pcg_seed(Pcg64 &g, const uint32_t *ent, int m) {
     auto mix = [](uint32_t x, uint32_t y) -> uint32_t {
         uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y; r ^= r >> 16; return r;
     };
-#pragma unroll
+    // loops kept rolled: this runs once per stream and code size matters more
+#pragma unroll 1
     for (int i = 0; i < 4; i++) pool[i] = hashmix(i < m ? ent[i] : 0u);
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < 4; s++)
-#pragma unroll
+#pragma unroll 1
         for (int d = 0; d < 4; d++)
             if (s != d) pool[d] = mix(pool[d], hashmix(pool[s]));
+#pragma unroll 1
     for (int s = 4; s < m; s++)
-#pragma unroll
+#pragma unroll 1
         for (int d = 0; d < 4; d++) pool[d] = mix(pool[d], hashmix(ent[s]));
     uint32_t st[8];
     uint32_t hb = 0x8b51f9ddu;
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < 8; i++) {
         uint32_t v = pool[i & 3];
         v ^= hb; hb *= 0x58f38dedu; v *= hb; v ^= v >> 16;
