@@ -89,8 +89,10 @@ struct LqEnt {
     uint32_t stamp;
 };
 
-__host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {
-    return n_desc * 4 > 4096 ? n_desc * 4 : 4096;
+__host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {   // power of two >= max(4D, 4096)
+    int64_t c = 4096;
+    while (c < 4 * n_desc) c <<= 1;
+    return c;
 }
 
 struct WinGlobalLayout {
@@ -135,6 +137,12 @@ struct Win {
     int64_t req_counter, n_req;
     int32_t n_blist;
     bool wdirty;
+    // server lane's register copies during phase A (loaded/stored around it)
+    uint32_t stored_mask, lq_head, lq_tail, lq_stamp, lq_mask;
+    bool cache_on, spec_on;
+    int64_t cur_bytes, entries, capacity;
+    uint32_t c_hits, c_miss, c_evict, c_reject, c_wasted, c_ready, c_spec, c_pops;
+    uint32_t c_skip[6];
 };
 
 // window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles)
@@ -181,56 +189,52 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
 __device__ void lq_compact_serial(Win &w);
 
 __device__ __forceinline__ void lru_touch(Win &w, int32_t d) {
-    WinHeader *h = w.h;
-    uint32_t s = ++h->lq_stamp;
+    uint32_t s = ++w.lq_stamp;
     w.lstamp[d] = s;
-    if (h->lq_tail - h->lq_head >= (uint32_t)h->lq_cap) lq_compact_serial(w);
+    if (w.lq_tail - w.lq_head > w.lq_mask) lq_compact_serial(w);
     LqEnt e; e.desc = d; e.stamp = s;
-    w.lq[h->lq_tail % (uint32_t)h->lq_cap] = e;
-    h->lq_tail++;
+    w.lq[w.lq_tail & w.lq_mask] = e;
+    w.lq_tail++;
 }
 __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache.py:45-52
-    if (!(w.dflags[d] & D_CACHED)) { w.h->stats[OTF_ST_MISSES]++; return false; }
+    if (!(w.dflags[d] & D_CACHED)) { w.c_miss++; return false; }
     lru_touch(w, d);
-    w.h->stats[OTF_ST_HITS]++;
+    w.c_hits++;
     return true;
 }
 __device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
-    int64_t cap = w.S.sc->cache_capacity;
-    EngineState &st = w.h->st;
-    WinHeader *h = w.h;
-    if (size > cap) { h->stats[OTF_ST_REJECTED]++; return; }
+    const int64_t cap = w.capacity;
+    if (size > cap) { w.c_reject++; return; }
     if (w.dflags[d] & D_CACHED) {                      // replace: its old queue entry goes stale
-        st.cur_bytes -= size;
+        w.cur_bytes -= size;
         w.dflags[d] &= ~D_CACHED;
-        st.entries--;
+        w.entries--;
     }
-    while (st.cur_bytes + size > cap) {                // popitem(last=False): oldest live entry
-        LqEnt e = w.lq[h->lq_head % (uint32_t)h->lq_cap];
-        h->lq_head++;
+    while (w.cur_bytes + size > cap) {                 // popitem(last=False): oldest live entry
+        LqEnt e = w.lq[w.lq_head & w.lq_mask];
+        w.lq_head++;
         int32_t v = e.desc;
         if (!(w.dflags[v] & D_CACHED) || w.lstamp[v] != e.stamp) continue;
         w.dflags[v] &= ~D_CACHED;
-        st.entries--;
-        st.cur_bytes -= w.S.size(v);
-        h->stats[OTF_ST_EVICTIONS]++;
+        w.entries--;
+        w.cur_bytes -= w.S.size(v);
+        w.c_evict++;
     }
     lru_touch(w, d);
     w.dflags[d] |= D_CACHED;
-    st.entries++;
-    st.cur_bytes += size;
+    w.entries++;
+    w.cur_bytes += size;
 }
 
 // Drop stale queue entries in place, keeping order (lane 0; only if a window
 // overran the pre-window compaction margin).
 __device__ void lq_compact_serial(Win &w) {
-    WinHeader *h = w.h;
-    uint32_t cap = (uint32_t)h->lq_cap, o = h->lq_head;
-    for (uint32_t i = h->lq_head; i != h->lq_tail; i++) {
-        LqEnt e = w.lq[i % cap];
-        if ((w.dflags[e.desc] & D_CACHED) && w.lstamp[e.desc] == e.stamp) w.lq[(o++) % cap] = e;
+    uint32_t o = w.lq_head;
+    for (uint32_t i = w.lq_head; i != w.lq_tail; i++) {
+        LqEnt e = w.lq[i & w.lq_mask];
+        if ((w.dflags[e.desc] & D_CACHED) && w.lstamp[e.desc] == e.stamp) w.lq[(o++) & w.lq_mask] = e;
     }
-    h->lq_tail = o;
+    w.lq_tail = o;
 }
 
 // Warp-parallel order-preserving compaction of the touch queue into a fresh
@@ -246,7 +250,7 @@ __device__ void lq_compact_warp(Win &w, int lane) {
         bool keep = false;
         LqEnt e;
         if (i < tail) {
-            e = w.lq[i % cap];
+            e = w.lq[i & (cap - 1)];
             keep = (w.dflags[e.desc] & D_CACHED) && w.lstamp[e.desc] == e.stamp;
         }
         unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -285,16 +289,15 @@ __device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backe
 }
 
 __device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, int32_t index) {  // backend.py:135-154
-    int64_t *st = w.h->stats;
-    if (!w.S.sc->spec_enabled) { st[OTF_ST_SKIP_DISABLED]++; return; }
-    if (index + 1 >= w.S.segcounts[seq]) { st[OTF_ST_SKIP_EOS]++; return; }
-    if ((w.S.sc->stored_mask >> rank) & 1u) { st[OTF_ST_SKIP_STORED]++; return; }
+    if (!w.spec_on) { w.c_skip[0]++; return; }
+    if (index + 1 >= w.S.segcounts[seq]) { w.c_skip[1]++; return; }
+    if ((w.stored_mask >> rank) & 1u) { w.c_skip[2]++; return; }
     int32_t nd = d + 1;                                // same (seq, rank), index + 1
     uint8_t f = w.dflags[nd];
-    if (w.S.sc->cache_enabled && (f & D_CACHED)) { st[OTF_ST_SKIP_CACHED]++; return; }
-    if (f & D_INFLIGHT) { st[OTF_ST_SKIP_INFLIGHT]++; return; }
+    if (w.cache_on && (f & D_CACHED)) { w.c_skip[3]++; return; }
+    if (f & D_INFLIGHT) { w.c_skip[4]++; return; }
     enqueue_job(w, nd, OTF_ORIGIN_SPECULATIVE);
-    st[OTF_ST_SPEC_ENQUEUED]++;
+    w.c_spec++;
 }
 
 // Response of MediaServer.segment (server.py:76-77): fix the record's slot
@@ -332,9 +335,9 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
     WinHeader *h = w.h;
     const otf_scenario &sc = *w.S.sc;
     for (;;) {
-        if (sc.cache_enabled && (w.dflags[d] & D_CACHED)) {   // dedup on dequeue (backend.py:193-198)
+        if (w.cache_on && (w.dflags[d] & D_CACHED)) {   // dedup on dequeue (backend.py:193-198)
             w.S.job_outcome(j, OTF_OUTCOME_DROPPED);
-            h->stats[OTF_ST_WASTED]++;
+            w.c_wasted++;
             resolve(w, d);
         } else {                                             // run_transcode (transcode.py:123-128)
             WWorker &k = h->wk[wid];
@@ -378,7 +381,7 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
         int32_t wid = h->fq_w[h->fq_head], d = h->fq_d[h->fq_head], j = h->fq_j[h->fq_head];
         h->fq_head = (h->fq_head + 1 == MAXK) ? 0 : h->fq_head + 1;
         h->fq_n--;
-        h->stats[OTF_ST_READY_CALLBACKS]++;
+        w.c_ready++;
         worker_run(w, wid, d, j);
     }
 }
@@ -389,10 +392,10 @@ __device__ void server_request(Win &w, int32_t cid, int32_t d, int32_t rank, int
     Client &c = w.cl[cid];
     c.req_id = w.req_counter++;
     c.arrival = w.now;
-    if ((sc.stored_mask >> rank) & 1u) {
+    if ((w.stored_mask >> rank) & 1u) {
         c.path = OTF_PATH_STORAGE;
         respond(w, cid);
-    } else if (sc.cache_enabled && cache_get(w, d)) {
+    } else if (w.cache_on && cache_get(w, d)) {
         maybe_speculate(w, d, rank, seq, index);
         c.path = OTF_PATH_CACHE;
         respond(w, cid);
@@ -417,7 +420,7 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
     k.win = WIN_NONE;
     w.wdirty = true;
     w.S.job_finished(j, w.now);
-    if (w.S.sc->cache_enabled) cache_put(w, d, k.size);
+    if (w.cache_on) cache_put(w, d, k.size);
     resolve(w, d);
     // next job
     WinHeader *h = w.h;
@@ -442,22 +445,34 @@ __device__ void phase_a(Win &w) {
     const int32_t n = h->n_list;
     w.req_counter = h->st.req_counter;
     w.n_req = h->st.n_req;
+    const otf_scenario &sc0 = *w.S.sc;
+    w.stored_mask = sc0.stored_mask;
+    w.cache_on = sc0.cache_enabled != 0;
+    w.spec_on = sc0.spec_enabled != 0;
+    w.capacity = sc0.cache_capacity;
+    w.cur_bytes = h->st.cur_bytes;
+    w.entries = h->st.entries;
+    w.lq_head = h->lq_head; w.lq_tail = h->lq_tail; w.lq_stamp = h->lq_stamp;
+    w.lq_mask = (uint32_t)h->lq_cap - 1u;
+    w.c_hits = w.c_miss = w.c_evict = w.c_reject = w.c_wasted = w.c_ready = w.c_spec = 0;
+    for (int q = 0; q < 6; q++) w.c_skip[q] = 0;
     w.n_blist = h->n_blist;
     w.wdirty = true;
     int32_t bw = -1;
+    double bw_when = 0.0, bw_ctime = 0.0;
     int64_t pops = 0;
     int32_t i = 0;
+    double cw = i < n ? h->list_when[0] : 0.0;
     for (;;) {
         if (w.wdirty) {                                // earliest worker timer in this window
             bw = -1;
             for (int32_t q = 0; q < K; q++) {
                 const WWorker &x = h->wk[q];
                 if (x.win != w.k) continue;
-                if (bw < 0) { bw = q; continue; }
-                const WWorker &y = h->wk[bw];
-                if (x.when < y.when || (x.when == y.when && (x.ctime < y.ctime ||
-                                                             (x.ctime == y.ctime && x.seq < y.seq))))
-                    bw = q;
+                if (bw < 0 || x.when < bw_when || (x.when == bw_when && (x.ctime < bw_ctime ||
+                                                       (x.ctime == bw_ctime && x.seq < h->wk[bw].seq)))) {
+                    bw = q; bw_when = x.when; bw_ctime = x.ctime;
+                }
             }
             w.wdirty = false;
         }
@@ -465,30 +480,39 @@ __device__ void phase_a(Win &w) {
         if (bw < 0 && i >= n) break;
         if (bw < 0) take_worker = false;
         else if (i >= n) take_worker = true;
+        else if (bw_when < cw) take_worker = true;
+        else if (cw < bw_when) take_worker = false;
         else {
-            double cw = h->list_when[i], ww = h->wk[bw].when;
-            if (ww < cw) take_worker = true;
-            else if (cw < ww) take_worker = false;
-            else {
-                double cc = w.cl[h->list_id[i]].ctime, wc = h->wk[bw].ctime;
-                if (wc < cc) take_worker = true;
-                else if (cc < wc) take_worker = false;
-                else { w.S.flag(OTF_S_TIE); take_worker = true; }
-            }
+            double cc = w.cl[h->list_id[i]].ctime;
+            if (bw_ctime < cc) take_worker = true;
+            else if (cc < bw_ctime) take_worker = false;
+            else { w.S.flag(OTF_S_TIE); take_worker = true; }
         }
         pops++;
         if (take_worker) {
-            w.now = h->wk[bw].when;
+            w.now = bw_when;
             server_worker_done(w, bw);
         } else {
-            w.now = h->list_when[i];
+            w.now = cw;
             int32_t pk = h->list_pack[i];
             server_request(w, h->list_id[i], h->list_desc[i], pk & 0xff, pk >> 16, (pk >> 8) & 0xff);
             i++;
+            if (i < n) cw = h->list_when[i];
         }
         if (h->fq_n > 0) drain_handoffs(w);
     }
     h->stats[OTF_ST_TIMER_POPS] += pops;
+    h->st.cur_bytes = w.cur_bytes;
+    h->st.entries = w.entries;
+    h->lq_head = w.lq_head; h->lq_tail = w.lq_tail; h->lq_stamp = w.lq_stamp;
+    h->stats[OTF_ST_HITS] += w.c_hits;
+    h->stats[OTF_ST_MISSES] += w.c_miss;
+    h->stats[OTF_ST_EVICTIONS] += w.c_evict;
+    h->stats[OTF_ST_REJECTED] += w.c_reject;
+    h->stats[OTF_ST_WASTED] += w.c_wasted;
+    h->stats[OTF_ST_READY_CALLBACKS] += w.c_ready;
+    h->stats[OTF_ST_SPEC_ENQUEUED] += w.c_spec;
+    for (int q = 0; q < 6; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += w.c_skip[q];
     h->st.req_counter = w.req_counter;
     h->st.n_req = w.n_req;
     h->n_blist = w.n_blist;
