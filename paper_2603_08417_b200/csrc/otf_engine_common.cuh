@@ -271,9 +271,12 @@ __device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double
     int32_t seq;
     if (S.sc->popularity == OTF_POP_ZIPF) {
         double u = pcg_next_double(c.picks);
-        seq = S.sc->n_seq - 1;
-        for (int32_t k = 0; k < S.sc->n_seq; k++)
-            if (u < S.zipf[k]) { seq = k; break; }
+        int32_t lo = 0, hi = S.sc->n_seq - 1;          // first k with u < cdf[k] (else the last)
+        while (lo < hi) {
+            int32_t mid = (lo + hi) >> 1;
+            if (u < S.zipf[mid]) hi = mid; else lo = mid + 1;
+        }
+        seq = lo;
     } else {
         seq = pcg_integers(c.picks, (uint32_t)S.sc->n_seq);
     }

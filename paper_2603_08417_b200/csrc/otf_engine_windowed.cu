@@ -63,7 +63,7 @@ struct WinHeader {
     int32_t fq_w[MAXK], fq_d[MAXK], fq_j[MAXK];
     int32_t gq_head, gq_n, fq_head, fq_n;
     int32_t jq_head, jq_n, jq_cap;
-    int32_t n_list, n_blist;
+    int32_t n_list, n_blist, n_ties;
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
     int32_t arr_next;                    // next client (arrival order) not yet on the wheel
@@ -136,6 +136,7 @@ struct Win {
     // lane 0's register copies of the hot server counters during phase A
     int64_t req_counter, n_req;
     int32_t n_blist;
+    int32_t fq_n;                                      // pending handed-off jobs (register mirror)
     bool wdirty;
     // server lane's register copies during phase A (loaded/stored around it)
     uint32_t stored_mask, lq_head, lq_tail, lq_stamp, lq_mask;
@@ -278,6 +279,7 @@ __device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backe
         if (pos >= MAXK) pos -= MAXK;
         h->fq_w[pos] = wid; h->fq_d[pos] = d; h->fq_j[pos] = j;
         h->fq_n++;
+        w.fq_n++;
     } else {
         if (h->jq_n >= h->jq_cap) { w.S.flag(OTF_S_INTERNAL); return; }
         int32_t pos = h->jq_head + h->jq_n;
@@ -381,6 +383,7 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
         int32_t wid = h->fq_w[h->fq_head], d = h->fq_d[h->fq_head], j = h->fq_j[h->fq_head];
         h->fq_head = (h->fq_head + 1 == MAXK) ? 0 : h->fq_head + 1;
         h->fq_n--;
+        w.fq_n--;
         w.c_ready++;
         worker_run(w, wid, d, j);
     }
@@ -457,6 +460,7 @@ __device__ void phase_a(Win &w) {
     w.c_hits = w.c_miss = w.c_evict = w.c_reject = w.c_wasted = w.c_ready = w.c_spec = 0;
     for (int q = 0; q < 6; q++) w.c_skip[q] = 0;
     w.n_blist = h->n_blist;
+    w.fq_n = h->fq_n;
     w.wdirty = true;
     int32_t bw = -1;
     double bw_when = 0.0, bw_ctime = 0.0;
@@ -499,7 +503,7 @@ __device__ void phase_a(Win &w) {
             i++;
             if (i < n) cw = h->list_when[i];
         }
-        if (h->fq_n > 0) drain_handoffs(w);
+        if (w.fq_n > 0) drain_handoffs(w);
     }
     h->stats[OTF_ST_TIMER_POPS] += pops;
     h->st.cur_bytes = w.cur_bytes;
@@ -664,7 +668,8 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) {
 // ranks its entries against all others (ties are flagged afterwards).
 __device__ void sort_list(WinHeader *h, int lane) {
     const int32_t n = h->n_list;
-    if (n <= 1) return;
+    if (lane == 0) h->n_ties = 0;
+    if (n <= 1) { __syncwarp(); return; }
     double my_w[LIST_CAP / 32];
     int32_t my_s[LIST_CAP / 32], my_r[LIST_CAP / 32];
     int16_t my_id[LIST_CAP / 32], my_d[LIST_CAP / 32];
@@ -688,6 +693,11 @@ __device__ void sort_list(WinHeader *h, int lane) {
         h->list_when[r] = my_w[t]; h->list_id[r] = my_id[t];
         h->list_desc[r] = my_d[t]; h->list_pack[r] = my_s[t];
     }
+    __syncwarp();
+    bool tie = false;                                  // any equal request times? (rare)
+    for (int32_t i = lane + 1; i < n; i += 32) tie |= h->list_when[i] == h->list_when[i - 1];
+    if (lane == 0) h->n_ties = __any_sync(0xffffffffu, tie) ? 1 : 0;
+    else __any_sync(0xffffffffu, tie);
     __syncwarp();
 }
 
@@ -926,7 +936,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
         t0 = t1;
         // ---- phase A: server lane ----
         if (lane == 0) {
-            order_ties(w);
+            if (h->n_ties) order_ties(w);
             phase_a(w);
             h->k_done = m;
         }
