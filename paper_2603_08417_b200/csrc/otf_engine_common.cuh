@@ -48,6 +48,7 @@ struct Scn {
     otf_qoe *q;                      // final destination (global)
     QoeAcc *qa;                      // counters while running (shared or scratch)
     double lat_sum, stall_sum, startup_sum;   // this lane's float sums
+    Pcg64 *picks;                             // [n_clients] sequence-pick streams (scratch)
     uint64_t mag_g, mag_rg;                   // d / max_nseg, d / (n_ranks * max_nseg) by multiply-high
     uint32_t div_g, div_rg;
     const int64_t *sizes, *bitrates, *manifest_b;
@@ -263,14 +264,14 @@ __device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
     m = push_words(ent, m, S.sc->seed);
     m = push_words(ent, m, 3u);
     m = push_words(ent, m, (uint64_t)cid);
-    pcg_seed(c.picks, ent, m);
+    pcg_seed(S.picks[cid], ent, m);
 }
 
 // orchestrator.py:341-345 + client.py:237-239: pick a sequence, register a report
 __device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double now) {
     int32_t seq;
     if (S.sc->popularity == OTF_POP_ZIPF) {
-        double u = pcg_next_double(c.picks);
+        double u = pcg_next_double(S.picks[cid]);
         int32_t lo = 0, hi = S.sc->n_seq - 1;          // first k with u < cdf[k] (else the last)
         while (lo < hi) {
             int32_t mid = (lo + hi) >> 1;
@@ -278,7 +279,7 @@ __device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double
         }
         seq = lo;
     } else {
-        seq = pcg_integers(c.picks, (uint32_t)S.sc->n_seq);
+        seq = pcg_integers(S.picks[cid], (uint32_t)S.sc->n_seq);
     }
     c.seq = seq;
     int64_t sid = atomicAdd((unsigned long long *)&S.st->n_sess, 1ull);

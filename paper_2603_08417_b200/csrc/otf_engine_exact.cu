@@ -228,11 +228,11 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
             if (sc.latency > 0 && do_sleep(w, c, task, sc.latency)) return;
             break;
         case C_SEG_LAT: {                   // MediaServer.segment + Backend.handle
-            c.req_id = w.S.st->req_counter++;
+            c.req_id = (int32_t)w.S.st->req_counter++;
             c.arrival = w.now;
             int32_t d = w.S.desc_id(c.seq, c.rank, c.index);
             c.desc = d;
-            c.size = w.S.size(d);
+            c.size = (int32_t)w.S.size(d);
             c.pc = C_SEG_WAIT;
             if (w.S.stored(c.rank)) {
                 c.path = OTF_PATH_STORAGE;
@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
     ExactLayout L = exact_layout(sc.n_clients, sc.n_workers, n_desc);
     uint8_t *base = b.scratch + sc.scratch_off;
     w.cl = (Client *)(base + L.clients);
+    w.S.picks = (Pcg64 *)(base + L.picks);
     w.wk = (Worker *)(base + L.workers);
     w.heap = (Timer *)(base + L.heap);
     w.ready = (ReadyEnt *)(base + L.ready);

@@ -96,13 +96,14 @@ __host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {   // power of t
 }
 
 struct WinGlobalLayout {
-    int64_t clients, blist, wq_head, wq_tail, jobq, lstamp, lq, total;
+    int64_t clients, picks, blist, wq_head, wq_tail, jobq, lstamp, lq, total;
 };
 
 __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
     WinGlobalLayout L;
     int64_t o = 0;
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
+    L.picks = o;   o += align256((int64_t)sizeof(Pcg64) * n_clients);
     L.blist = o;   o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
     L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
@@ -307,7 +308,7 @@ __device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, in
 // The record itself and the request QoE are written by the client lane.
 __device__ __forceinline__ void respond(Win &w, int32_t cid) {
     Client &c = w.cl[cid];
-    c.req_slot = w.n_req++;
+    c.req_slot = (int32_t)w.n_req++;
     c.pc = C_SEG_RESP;
     c.next_when = w.now;
     w.blist[w.n_blist++] = cid;
@@ -393,7 +394,7 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
 __device__ void server_request(Win &w, int32_t cid, int32_t d, int32_t rank, int32_t seq, int32_t index) {
     const otf_scenario &sc = *w.S.sc;
     Client &c = w.cl[cid];
-    c.req_id = w.req_counter++;
+    c.req_id = (int32_t)w.req_counter++;
     c.arrival = w.now;
     if ((w.stored_mask >> rank) & 1u) {
         c.path = OTF_PATH_STORAGE;
@@ -635,7 +636,7 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             break;
         case C_SEG_RESP:
             record_response(w, c, now);
-            c.size = S.size(c.desc);
+            c.size = (int32_t)S.size(c.desc);
             c.xfer_start = now;
             nbytes = c.size;
             next = C_SEG_XFER;
@@ -744,7 +745,7 @@ __device__ int32_t wheel_next(WinHeader *h, int32_t k_done, int lane) {
     return warp_min(best);
 }
 
-__global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
+__global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x;
     long long t_start = 0, t0 = 0, t1 = 0;
@@ -767,6 +768,7 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
     w.lstamp = (uint32_t *)(g + L.lstamp);
     w.lq = (LqEnt *)(g + L.lq);
     w.cl = (Client *)(g + L.clients);
+    w.S.picks = (Pcg64 *)(g + L.picks);
     w.blist = (int32_t *)(g + L.blist);
     w.wq_head = (int32_t *)(g + L.wq_head);
     w.wq_tail = (int32_t *)(g + L.wq_tail);
@@ -915,6 +917,11 @@ __global__ void __launch_bounds__(32) windowed_kernel(const otf_batch b) {
             h->n_blist = nb;
         }
         __syncwarp();
+        for (int32_t i = lane; i < h->n_blist; i += 32) {   // warm L2 with this window's client states
+            const char *ptr = (const char *)&w.cl[w.blist[i]];
+            asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
+            asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr + 128));
+        }
         if (h->n_list > LIST_CAP) {                    // too many simultaneous requests for this engine
             if (lane == 0) h->st.status |= OTF_S_TIE;
             __syncwarp();

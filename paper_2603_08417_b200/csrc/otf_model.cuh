@@ -105,7 +105,7 @@ OTF_HD double completion_time(const Trace &tr, double start, int64_t nbytes) {
 }
 
 struct Buffer {
-    double level, position, last_sync, stall_time, started_at, session_start;
+    double level, last_sync, stall_time, started_at, session_start;   // (position is never observed)
     int32_t phase, stall_events;
 };
 
@@ -117,10 +117,8 @@ OTF_HD void buf_advance(Buffer &b, double now) {
         if (b.level >= dt - 1e-9) {
             double l = b.level - dt;
             b.level = (l > 0.0) ? l : 0.0;
-            b.position += dt;
         } else {
             double played = b.level;
-            b.position += played;
             b.level = 0.0;
             b.phase = PH_STALLED;
             b.stall_events++;
@@ -144,7 +142,7 @@ OTF_HD void buf_on_segment(Buffer &b, double now, double duration, double startu
 }
 
 OTF_HD void buf_reset(Buffer &b, double now) {
-    b.level = 0.0; b.position = 0.0; b.last_sync = now; b.stall_time = 0.0;
+    b.level = 0.0; b.last_sync = now; b.stall_time = 0.0;
     b.started_at = NAN; b.session_start = now; b.phase = PH_STARTUP; b.stall_events = 0;
 }
 

@@ -27,15 +27,15 @@ enum {
     C_HUNG          // slept on an infinite delay; never wakes
 };
 
-struct Client {
-    Buffer buf;                 // 56 B
+struct Client {                 // 144 B: moved as a whole per event
+    Buffer buf;                 // 48 B
     double est, requested, arrival, xfer_start;
     double next_when, ctime;    // windowed engine: pending timer (fire time, arm time)
-    int64_t req_id, size, req_slot;
-    int32_t pc, seq, session, index, rank, has_est, buf_live, sess_open;
-    int32_t path, desc, wait_next, pad;
-    Pcg64 picks;                // sequence-pick stream SS([seed, 3, cid])
-};
+    int32_t req_id, size, req_slot;
+    int32_t pc, seq, session, index, rank;
+    int32_t path, desc, wait_next;
+    uint8_t has_est, buf_live, sess_open, pad;
+};                              // the pick stream lives in a separate (cold) array
 
 enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE };
 
@@ -68,7 +68,7 @@ struct JobEnt {
 OTF_HD int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
 struct ExactLayout {
-    int64_t state, clients, workers, heap, ready, descs, jobq, getq, total;
+    int64_t state, clients, picks, workers, heap, ready, descs, jobq, getq, total;
 };
 
 OTF_HD ExactLayout exact_layout(int32_t n_clients, int32_t n_workers, int64_t n_desc) {
@@ -78,6 +78,7 @@ OTF_HD ExactLayout exact_layout(int32_t n_clients, int32_t n_workers, int64_t n_
     L.state = o; o += 256;                     // EngineState
     o += 512;                                  // QoeAcc (at state + 256)
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
+    L.picks = o;   o += align256((int64_t)sizeof(Pcg64) * n_clients);
     L.workers = o; o += align256((int64_t)sizeof(Worker) * n_workers);
     L.heap = o;    o += align256((int64_t)sizeof(Timer) * (n_tasks + 1));
     L.ready = o;   o += align256((int64_t)sizeof(ReadyEnt) * (n_tasks + 1));
