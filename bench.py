@@ -202,13 +202,10 @@ def main():
     launches_per_step = 2 + (2 if exact_db is not None else 0)
     q_rows = db.qoe.shape[1]
 
-    def gather_qoe():
-        if world == 1:
-            return db.qoe
-        import torch.distributed as dist
-        out = [torch.empty_like(db.qoe) for _ in range(world)]
-        dist.all_gather(out, db.qoe)                           # the one collective: QoE blocks to every rank
-        return out
+    from paper_2603_08417_b200 import dist as odist
+
+    def gather_qoe():                                          # the one collective: QoE blocks to every rank
+        return odist.gather_blocks(db.qoe, world)
 
     def step():
         db.launch(stream, sizes=True)
@@ -257,13 +254,10 @@ def main():
     if exact_db is not None:
         ebr = exact_db.fetch()
         my_req += int(ebr.counts[:, 0].sum()) - int(br.counts[flagged, 0].sum())
-    stat = torch.tensor([elapsed_ms, float(my_req), statistics.mean(eng_ms)], dtype=torch.float64, device=dev)
     if world > 1:
-        mx = stat.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = stat.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        elapsed_ms, total_req, eng_ms_max = mx[0].item(), sm[1].item(), mx[2].item()
+        elapsed_ms = odist.all_max(elapsed_ms, dev)
+        total_req = odist.all_sum(float(my_req), dev)
+        eng_ms_max = odist.all_max(statistics.mean(eng_ms), dev)
     else:
         total_req, eng_ms_max = float(my_req), statistics.mean(eng_ms)
     value = total_req * args.steps / (elapsed_ms / 1e3)
@@ -284,11 +278,7 @@ def main():
     e2e_s = min(e2e_times)
     h2d = db.h2d_bytes + (exact_db.h2d_bytes if exact_db is not None else 0)
     d2h = sum(t.numel() * t.element_size() for t in out)
-    e2e_val = total_req / e2e_s if world == 1 else None
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_val = total_req / t.item()
+    e2e_val = total_req / (odist.all_max(e2e_s, dev) if world > 1 else e2e_s)
 
     if rank != 0:
         dist.destroy_process_group()

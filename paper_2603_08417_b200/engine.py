@@ -202,7 +202,7 @@ class BatchResult:
 
 
 def run_batch(configs, mode: str = "records", engine: str = "windowed", device=None,
-              max_retries: int = 4) -> list[ExperimentResult]:
+              max_retries: int = 4, _caps=None, _eps_scale: float = 1.0) -> list[ExperimentResult]:
     """Run every config on the GPU; returns one ExperimentResult per config.
 
     Scenarios whose record buffers or noise tables were too small are re-run
@@ -214,8 +214,8 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
     configs = list(configs)
     results: list = [None] * len(configs)
     todo = list(range(len(configs)))
-    caps = {}
-    eps_scale = {}
+    caps = {i: tuple(c) for i, c in enumerate(_caps)} if _caps is not None else {}   # test hook
+    eps_scale = {i: _eps_scale for i in todo} if _eps_scale != 1.0 else {}         # test hook
     engines = {i: eng for i in todo}
     for _attempt in range(max_retries + 1):
         if not todo:
@@ -252,6 +252,8 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                     nxt.append(i)
                 else:
                     results[i] = br.result(k)
+                    results[i].engine = "exact" if e == _lib.ENGINE_EXACT else "windowed"
+                    results[i].attempts = _attempt + 1
         todo = nxt
     if todo:
         raise _lib.OtfError(f"scenarios {todo} did not converge after {max_retries} retries")

@@ -156,7 +156,7 @@ def _eps_len(low: Lowered) -> int:
 
 
 def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.MODE_RECORDS,
-                 caps=None, eps_scale: int = 1, threads: int | None = None) -> BatchInputs:
+                 caps=None, eps_scale: float = 1, threads: int | None = None) -> BatchInputs:
     """Lower a list of ExperimentConfigs into one device batch (host arrays)."""
     L = _lib.lib()
     threads = threads or os.cpu_count() or 1
@@ -211,7 +211,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     for low in lows:
         key = (low.cfg.seed, low.cfg.noise_rel_std)
         k, e = eps_groups.get(key, (0, 0))
-        eps_groups[key] = (max(k, low.cfg.workers), max(e, _eps_len(low) * eps_scale))
+        eps_groups[key] = (max(k, low.cfg.workers), max(e, max(1, int(_eps_len(low) * eps_scale))))
     eps_tab = {}
     for (seed, noise), (kmax, elen) in eps_groups.items():
         if noise > 0:

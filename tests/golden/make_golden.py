@@ -34,6 +34,7 @@ import cases  # noqa: E402
 PATHS = {"storage": 0, "cache": 1, "waited_inflight": 2, "transcoded": 3}
 ORIGINS = {"demand": 0, "speculative": 1}
 OUTCOMES = {"pending": 0, "completed": 1, "dropped": 2, "failed": 3}
+CSV_CASES = {"grid_c4_k4_t2_T", "edge_two_clients", "edge_short_horizon"}
 
 
 def zipf_cdf(n, s):
@@ -158,6 +159,8 @@ def dump(name: str, cfg) -> None:
     }
     arrays["meta"] = np.frombuffer(json.dumps(meta, sort_keys=True).encode("utf-8"), dtype=np.uint8)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
+    if name in CSV_CASES:                               # the reference's own on-disk bundle
+        res.write(os.path.join(HERE, "csv", name))
     print(f"{name}: requests {len(R)} sessions {len(S)} jobs {len(J)}")
 
 

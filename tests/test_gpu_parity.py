@@ -147,3 +147,28 @@ def test_no_cpu_fallback_without_library(monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libotfgpu.so")
     with pytest.raises(_lib.OtfError):
         engine.run_experiment(workloads.c1())
+
+
+def test_fallback_and_retry_paths(golden):
+    """Windowed engine hands zero-latency scenarios to the exact engine; record and
+    noise-table overflows are re-run with exact sizes -- results stay bit-exact."""
+    want, meta = golden["edge_latency0"]
+    res = engine.run_batch([_cfg(meta)], mode="records", engine="windowed")[0]
+    assert res.engine == "exact"
+    _assert_parity(res, want, meta["backend_stats"])
+    want, meta = golden["grid_c24_k4_t2_TCP"]
+    res = engine.run_batch([_cfg(meta)], mode="records", _caps=[(10, 3, 10, 5)])[0]
+    assert res.attempts == 2 and res.engine == "windowed"
+    _assert_parity(res, want, meta["backend_stats"])
+    res = engine.run_batch([_cfg(meta)], mode="records", _eps_scale=0.02)[0]
+    assert res.attempts >= 2
+    _assert_parity(res, want, meta["backend_stats"])
+
+
+def test_run_sharded_single_rank():
+    from paper_2603_08417_b200 import dist as odist
+    cfgs = [workloads.c1(seed=s) for s in range(1, 5)]
+    blocks = odist.run_sharded(cfgs)
+    ref = engine.run_batch(cfgs, mode="histogram")
+    assert [int(b[0]) for b in blocks] == [0, 1, 2, 3]
+    assert [int(b[1]) for b in blocks] == [r.qoe["n_requests"] for r in ref]
