@@ -14,7 +14,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
-from paper_2603_08417_b200.config import ClientConfig, ExperimentConfig  # noqa: E402
+from paper_2603_08417_b200.config import ClientConfig, ExperimentConfig, NetemConfig  # noqa: E402
 from paper_2603_08417_b200 import workloads as W  # noqa: E402
 
 
@@ -45,8 +45,11 @@ def golden_cases():
                                                     horizon_s=120.0, seed=6)))
     out.append(("edge_tiny_cache", dataclasses.replace(base, variant="TCP", clients=16, cache_capacity_bytes=600_000,
                                                        horizon_s=120.0, seed=7)))
+    # the request latency lives in the netem section of the config document
+    # (orchestrator.py:133: ClientConfig.latency_s = netem.latency_s)
     out.append(("edge_latency0", dataclasses.replace(base, variant="TCP", clients=8, horizon_s=100.0, seed=8,
-                                                     client=ClientConfig(latency_s=0.0))))
+                                                     client=ClientConfig(latency_s=0.0),
+                                                     netem=NetemConfig(latency_s=0.0))))
     out.append(("edge_partial_seg", dataclasses.replace(
         base, variant="TCP", clients=10, horizon_s=150.0, seed=9,
         sequences=[{"id": "a", "duration_s": 9.5, "segment_duration_s": 2.0},
