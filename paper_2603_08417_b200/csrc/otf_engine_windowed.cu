@@ -63,9 +63,7 @@ struct WinHeader {
     int32_t fq_w[MAXK], fq_d[MAXK], fq_j[MAXK];
     int32_t gq_head, gq_n, fq_head, fq_n;
     int32_t jq_head, jq_n, jq_cap;
-    int32_t n_list, n_ties;
-    int32_t n_reg[4];                    // this window's client work by kind: 0 transfer done,
-                                         // 1 buffer-full wait, 2 other local, 3 server responses
+    int32_t n_list, n_blist, n_ties;
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
     int32_t arr_next;                    // next client (arrival order) not yet on the wheel
@@ -106,7 +104,7 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     int64_t o = 0;
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
     L.picks = o;   o += align256((int64_t)sizeof(Pcg64) * n_clients);
-    L.blist = o;   o += align256((int64_t)sizeof(int32_t) * 4 * (n_clients + 64));
+    L.blist = o;   o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
     L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
@@ -119,7 +117,6 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
 __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc) {
     int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
     o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
-    o += (int64_t)n_clients;              // kind of each client's pending local timer
     o = (o + 15) & ~(int64_t)15;
     o += n_desc;                          // descriptor flags
     return (o + 15) & ~(int64_t)15;
@@ -133,9 +130,7 @@ struct Win {
     LqEnt *lq;                                         // touch queue (global, 2 * lq_cap)
     uint8_t *dflags;
     Client *cl;
-    int32_t *blist, *wq_head, *wq_tail;               // blist: 4 regions of (N + 64), see n_reg
-    uint8_t *ckind;
-    int32_t breg;                                      // region stride
+    int32_t *blist, *wq_head, *wq_tail;
     JobEnt *jq;
     double W, invW, H, E, now;
     int32_t k;
@@ -169,13 +164,8 @@ __device__ __forceinline__ int32_t timer_win(const Win &w, double when) {
 }
 
 // Put client c on the bucket of window `wk` (any lane; lock-free push).
-__device__ __forceinline__ uint8_t local_kind(int32_t pc) {
-    return pc == C_SEG_XFER ? 0 : (pc == C_TARGET_WAIT ? 1 : 2);
-}
-
-__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool srv, int32_t pc) {
+__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool srv) {
     WinHeader *h = w.h;
-    if (!srv) w.ckind[c] = local_kind(pc);
     if (wk - w.k < RING) {
         int32_t slot = wk & (RING - 1);
         int32_t old = atomicExch(srv ? &h->bhead_srv[slot] : &h->bhead_loc[slot], c);
@@ -321,7 +311,7 @@ __device__ __forceinline__ void respond(Win &w, int32_t cid) {
     c.req_slot = (int32_t)w.n_req++;
     c.pc = C_SEG_RESP;
     c.next_when = w.now;
-    w.blist[3 * w.breg + w.n_blist++] = cid;
+    w.blist[w.n_blist++] = cid;
 }
 
 __device__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
@@ -470,7 +460,7 @@ __device__ void phase_a(Win &w) {
     w.lq_mask = (uint32_t)h->lq_cap - 1u;
     w.c_hits = w.c_miss = w.c_evict = w.c_reject = w.c_wasted = w.c_ready = w.c_spec = 0;
     for (int q = 0; q < 6; q++) w.c_skip[q] = 0;
-    w.n_blist = h->n_reg[3];
+    w.n_blist = h->n_blist;
     w.fq_n = h->fq_n;
     w.wdirty = true;
     int32_t bw = -1;
@@ -530,7 +520,7 @@ __device__ void phase_a(Win &w) {
     for (int q = 0; q < 6; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += w.c_skip[q];
     h->st.req_counter = w.req_counter;
     h->st.n_req = w.n_req;
-    h->n_reg[3] = w.n_blist;
+    h->n_blist = w.n_blist;
 }
 
 // ---- client lanes ------------------------------------------------------------------
@@ -548,7 +538,7 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
         int32_t k = timer_win(w, when);
         if (k == WIN_NONE) return false;
         if (k <= w.k) w.S.flag(OTF_S_TIE);             // lookahead violated (cannot happen)
-        bucket_push(w, cid, k, true, next_pc);
+        bucket_push(w, cid, k, true);
         return false;
     }
     if (when <= w.H && when < w.E) {                   // fires inside this window: keep going
@@ -556,7 +546,7 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
         return true;
     }
     int32_t k = timer_win(w, when);
-    if (k != WIN_NONE) bucket_push(w, cid, k, false, next_pc);
+    if (k != WIN_NONE) bucket_push(w, cid, k, false);
     return false;
 }
 
@@ -773,7 +763,6 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     WinGlobalLayout L = win_global_layout(N, D);
     w.h = h;
     w.bnext = (int16_t *)p; p += 2 * (int64_t)N;
-    w.ckind = p; p += N;
     p = (uint8_t *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
     w.dflags = p;
     w.lstamp = (uint32_t *)(g + L.lstamp);
@@ -781,7 +770,6 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     w.cl = (Client *)(g + L.clients);
     w.S.picks = (Pcg64 *)(g + L.picks);
     w.blist = (int32_t *)(g + L.blist);
-    w.breg = N + 64;
     w.wq_head = (int32_t *)(g + L.wq_head);
     w.wq_tail = (int32_t *)(g + L.wq_tail);
     w.jq = (JobEnt *)(g + L.jobq);
@@ -806,8 +794,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         qoe_zero(&h->qa, 0, 1);
         h->gq_head = 0; h->gq_n = K; h->fq_head = 0; h->fq_n = 0;
         h->jq_head = 0; h->jq_n = 0; h->jq_cap = (int32_t)(D + 1);
-        h->n_list = 0; h->wseq = 0;
-        for (int q = 0; q < 4; q++) h->n_reg[q] = 0;
+        h->n_list = 0; h->n_blist = 0; h->wseq = 0;
         h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
         h->arr_next = 0;
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
@@ -881,7 +868,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
                 while (c < N) {
                     int32_t wk = timer_win(w, w.S.arrival(c));
                     if (wk == WIN_NONE || wk - m >= RING) break;
-                    bucket_push(w, c, wk, false, C_ARRIVED);
+                    bucket_push(w, c, wk, false);
                     c++;
                 }
                 h->arr_next = c;
@@ -897,7 +884,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
                 while (c >= 0) {
                     int32_t nx = w.bnext[c];
                     const Client &cl = w.cl[c];
-                    bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT, cl.pc);
+                    bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT);
                     c = nx;
                 }
             }
@@ -916,29 +903,25 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
             h->bhead_srv[slot] = -1;
             h->bhead_loc[slot] = -1;
             h->bits[slot >> 5] &= ~(1u << (slot & 31));
-            int32_t nl = 0, n0 = 0, n1 = 0, n2 = 0;
+            int32_t nl = 0, nb = 0;
             while (c >= 0) {
                 if (nl < LIST_CAP) h->list_id[nl] = (int16_t)c;
                 nl++;
                 c = w.bnext[c];
             }
-            while (cl >= 0) {                          // group the window's local events by kind
-                uint8_t k = w.ckind[cl];
-                if (k == 0) w.blist[n0++] = cl;
-                else if (k == 1) w.blist[w.breg + n1++] = cl;
-                else w.blist[2 * w.breg + n2++] = cl;
+            while (cl >= 0) {
+                w.blist[nb++] = cl;
                 cl = w.bnext[cl];
             }
             h->n_list = nl;
-            h->n_reg[0] = n0; h->n_reg[1] = n1; h->n_reg[2] = n2; h->n_reg[3] = 0;
+            h->n_blist = nb;
         }
         __syncwarp();
-        for (int32_t r = 0; r < 3; r++)                // warm L2 with this window's client states
-            for (int32_t i = lane; i < h->n_reg[r]; i += 32) {
-                const char *ptr = (const char *)&w.cl[w.blist[r * w.breg + i]];
-                asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
-                asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr + 128));
-            }
+        for (int32_t i = lane; i < h->n_blist; i += 32) {   // warm L2 with this window's client states
+            const char *ptr = (const char *)&w.cl[w.blist[i]];
+            asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
+            asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr + 128));
+        }
         if (h->n_list > LIST_CAP) {                    // too many simultaneous requests for this engine
             if (lane == 0) h->st.status |= OTF_S_TIE;
             __syncwarp();
@@ -970,11 +953,8 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         t0 = t1;
         if (h->st.status & OTF_S_TIE) break;
         // ---- phase B: client lanes ----
-        for (int32_t r = 3; r >= 0; r--) {             // one kind at a time: converged lanes
-            const int32_t nr = h->n_reg[r];
-            const int32_t *lst = w.blist + r * w.breg;
-            for (int32_t i = lane; i < nr; i += 32) client_local(w, lst[i]);
-        }
+        const int32_t nb = h->n_blist;
+        for (int32_t i = lane; i < nb; i += 32) client_local(w, w.blist[i]);
         __syncwarp();
         t1 = clock64();
         if (lane == 0) h->stats[OTF_ST_CYC_CLIENTS] += t1 - t0;
