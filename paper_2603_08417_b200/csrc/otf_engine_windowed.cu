@@ -41,8 +41,6 @@ constexpr int RING = 512;          // timer-wheel buckets (windows); farther tim
 constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory
 constexpr int MAXN = 32767;        // clients (16-bit wheel links)
 constexpr int16_t NIL = -1;
-constexpr int FAST_N = 128;        // server events per window handled by the data-parallel path
-constexpr int FAST_PER_LANE = FAST_N / 32;
 
 struct WWorker {
     double when, ctime;
@@ -84,11 +82,6 @@ struct WinHeader {
     int32_t list_pack[LIST_CAP];         // rank | index << 8 | seq << 16
     int16_t list_id[LIST_CAP];
     int16_t list_desc[LIST_CAP];
-    // data-parallel phase A scratch: enqueue attempts in (request, demand-before-spec) order
-    int16_t at_tgt[2 * FAST_N];
-    int16_t at_ent[2 * FAST_N];
-    uint8_t at_ok[2 * FAST_N];
-    int32_t n_at;
 };
 
 struct LqEnt {
@@ -447,311 +440,6 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
         h->gq_n++;
         k.pc = W_GOT;
     }
-}
-
-// ---- data-parallel phase A ---------------------------------------------------------
-// In a window with no worker timer, cache contents cannot change (puts and
-// evictions happen only when a transcode finishes, cache.py:58-81 via
-// backend.py:205-207; a job handed to an idle worker is never dropped in the
-// step that enqueued it).  Each request's outcome is then a function of the
-// window-start flags and of "the first enqueue attempt on a descriptor wins"
-// (demand before speculation within a request, backend.py:130-133,
-// 156-170), so the warp resolves the whole window with ballots and prefix
-// sums.  If a worker started here would finish inside this window, nothing is
-// committed and the serial lane replays the window instead.
-enum { F_STORE = 0, F_HIT = 1, F_WAIT = 2, F_DEMAND = 3 };
-enum { S_NONE = 0, S_DISABLED, S_EOS, S_STORED, S_CACHED, S_INFLIGHT, S_CAND };
-
-__device__ __forceinline__ int32_t warp_excl_prefix(bool v, int lane, int32_t &total) {
-    unsigned m = __ballot_sync(0xffffffffu, v);
-    total = __popc(m);
-    return __popc(m & ((1u << lane) - 1));
-}
-
-__device__ bool phase_a_fast(Win &w, int lane) {
-    WinHeader *h = w.h;
-    const otf_scenario &sc = *w.S.sc;
-    const int32_t n = h->n_list;
-    const int32_t K = sc.n_workers;
-    if (n > FAST_N || h->n_ties) return false;
-    for (int32_t q = 0; q < K; q++) if (h->wk[q].win == w.k) return false;
-    const bool cache_on = sc.cache_enabled != 0, spec_on = sc.spec_enabled != 0;
-    const uint32_t stored_mask = sc.stored_mask;
-
-    // 1. classify each request with the window-start flags
-    int32_t cls[FAST_PER_LANE], spc[FAST_PER_LANE];
-    int32_t nat = 0;                                   // attempts are appended in entry order below
-#pragma unroll
-    for (int t = 0; t < FAST_PER_LANE; t++) {
-        int32_t i = lane + 32 * t;
-        cls[t] = F_STORE; spc[t] = S_NONE;
-        if (i < n) {
-            int32_t d = h->list_desc[i], pk = h->list_pack[i];
-            int32_t rank = pk & 0xff, index = (pk >> 8) & 0xff, seq = pk >> 16;
-            uint8_t f = w.dflags[d];
-            if ((stored_mask >> rank) & 1u) cls[t] = F_STORE;
-            else {
-                if (cache_on && (f & D_CACHED)) cls[t] = F_HIT;
-                else cls[t] = (f & D_INFLIGHT) ? F_WAIT : F_DEMAND;
-                if (!spec_on) spc[t] = S_DISABLED;
-                else if (index + 1 >= w.S.segcounts[seq]) spc[t] = S_EOS;
-                else if ((stored_mask >> rank) & 1u) spc[t] = S_STORED;
-                else {
-                    uint8_t g = w.dflags[d + 1];
-                    if (cache_on && (g & D_CACHED)) spc[t] = S_CACHED;
-                    else if (g & D_INFLIGHT) spc[t] = S_INFLIGHT;
-                    else spc[t] = S_CAND;
-                }
-            }
-        }
-    }
-    // 2. compact the enqueue attempts in (entry, demand, spec) order
-    for (int t = 0; t < FAST_PER_LANE; t++) {
-        int32_t i = lane + 32 * t;
-        bool dem = i < n && cls[t] == F_DEMAND;
-        bool spe = i < n && spc[t] == S_CAND;
-        int32_t tot;
-        // demand of entry i comes before its spec; entries of round t come in lane order
-        int32_t c = (dem ? 1 : 0) + (spe ? 1 : 0);
-        // exclusive prefix of c over lanes
-        int32_t pre = c;
-        for (int o = 1; o < 32; o <<= 1) {
-            int32_t v = __shfl_up_sync(0xffffffffu, pre, o);
-            if (lane >= o) pre += v;
-        }
-        tot = __shfl_sync(0xffffffffu, pre, 31);
-        pre -= c;
-        int32_t pos = nat + pre;
-        if (dem) { h->at_tgt[pos] = (int16_t)h->list_desc[i]; h->at_ent[pos] = (int16_t)(2 * i); pos++; }
-        if (spe) { h->at_tgt[pos] = (int16_t)(h->list_desc[i] + 1); h->at_ent[pos] = (int16_t)(2 * i + 1); }
-        nat += tot;
-    }
-    __syncwarp();
-    // 3. first attempt per target wins
-    for (int32_t a = lane; a < nat; a += 32) {
-        int16_t x = h->at_tgt[a];
-        bool first = true;
-        for (int32_t b = 0; b < a; b++) first &= (h->at_tgt[b] != x);
-        h->at_ok[a] = first ? 1 : 0;
-    }
-    __syncwarp();
-    // 4. jobs in attempt order; the first g go to idle workers (getter FIFO)
-    int32_t njobs_before = 0, njobs = 0;
-    for (int32_t base = 0; base < nat; base += 32) {
-        int32_t a = base + lane;
-        bool ok = a < nat && h->at_ok[a];
-        int32_t tot;
-        int32_t pre = warp_excl_prefix(ok, lane, tot);
-        if (ok) h->at_ok[a] = (uint8_t)(1 + 0);        // keep flag; rank recomputed below
-        (void)pre;
-        njobs += tot;
-    }
-    (void)njobs_before;
-    const int32_t g = h->gq_n < njobs ? h->gq_n : njobs;
-    // worker starts must not land inside this window (else: serial replay)
-    bool abort_fast = false;
-    {
-        int32_t rank_base = 0;
-        for (int32_t base = 0; base < nat; base += 32) {
-            int32_t a = base + lane;
-            bool ok = a < nat && h->at_ok[a];
-            int32_t tot;
-            int32_t r = rank_base + warp_excl_prefix(ok, lane, tot);
-            if (ok && r < g) {
-                int32_t wid = h->gq[(h->gq_head + r) % K];
-                int32_t ent = h->at_ent[a] >> 1;
-                int32_t x = h->at_tgt[a];
-                double now = h->list_when[ent];
-                const WWorker &k = h->wk[wid];
-                double e = 0.0;
-                if (sc.noise > 0) e = k.eps_pos < sc.eps_stride ? w.S.eps[(int64_t)wid * sc.eps_stride + k.eps_pos] : 0.0;
-                int32_t rank = w.S.desc_rank(x), seq = w.S.desc_seq(x), idx = w.S.desc_index(x);
-                double dur = seg_duration(w.S.seqdur[seq], w.S.segdur[seq], idx);
-                double svc = w.S.rho[rank - 1] * dur * (1.0 + e);
-                svc = (1e-9 > svc) ? 1e-9 : svc;
-                double when = now + svc;
-                if (timer_win(w, when) == w.k) abort_fast = true;
-            }
-            rank_base += tot;
-        }
-    }
-    if (__any_sync(0xffffffffu, abort_fast)) return false;
-
-    // ---- commit --------------------------------------------------------------------
-    const int64_t req0 = h->st.req_counter;
-    const int64_t slot0 = h->st.n_req;
-    const int32_t nb0 = h->n_blist;
-    const uint32_t stamp0 = h->lq_stamp;
-    const uint32_t lq_tail0 = h->lq_tail;
-    const uint32_t lq_mask = (uint32_t)h->lq_cap - 1u;
-    const int64_t job0 = h->st.n_job;
-    // per-entry outcome of the demand attempt
-    int32_t imm_base = 0, hit_base = 0;
-    uint32_t c_hit = 0, c_miss = 0, c_skip[6] = {0, 0, 0, 0, 0, 0}, c_spec = 0;
-    for (int t = 0; t < FAST_PER_LANE; t++) {
-        int32_t i = lane + 32 * t;
-        bool valid = i < n;
-        int32_t cl = valid ? cls[t] : F_STORE;
-        int32_t sp = valid ? spc[t] : S_NONE;
-        if (valid && cl == F_DEMAND) {                 // did this request's demand attempt win?
-            int32_t d = h->list_desc[i];
-            bool won = false;
-            for (int32_t a = 0; a < nat; a++)
-                if (h->at_ent[a] == 2 * i) { won = h->at_ok[a] != 0; break; }
-            if (!won) cl = F_WAIT;
-            (void)d;
-        }
-        if (valid && sp == S_CAND) {
-            bool won = false;
-            for (int32_t a = 0; a < nat; a++)
-                if (h->at_ent[a] == 2 * i + 1) { won = h->at_ok[a] != 0; break; }
-            sp = won ? S_CAND : S_INFLIGHT;
-        }
-        bool imm = valid && (cl == F_STORE || cl == F_HIT);
-        bool hit = valid && cl == F_HIT;
-        int32_t tot_imm, tot_hit;
-        int32_t pimm = warp_excl_prefix(imm, lane, tot_imm);
-        int32_t phit = warp_excl_prefix(hit, lane, tot_hit);
-        if (valid) {
-            int32_t cid = h->list_id[i];
-            int32_t d = h->list_desc[i];
-            Client &c = w.cl[cid];
-            double now = h->list_when[i];
-            c.req_id = (int32_t)(req0 + i);
-            c.arrival = now;
-            if (imm) {
-                c.path = cl == F_STORE ? OTF_PATH_STORAGE : OTF_PATH_CACHE;
-                c.req_slot = (int32_t)(slot0 + imm_base + pimm);
-                c.pc = C_SEG_RESP;
-                c.next_when = now;
-                w.blist[nb0 + imm_base + pimm] = cid;
-            } else {
-                c.path = cl == F_DEMAND ? OTF_PATH_TRANSCODED : OTF_PATH_WAITED;
-                c.pc = C_SEG_WAIT;
-            }
-            if (hit) {                                 // lazy-LRU touch in request order
-                uint32_t st = stamp0 + (uint32_t)(hit_base + phit) + 1u;
-                LqEnt e; e.desc = d; e.stamp = st;
-                w.lq[(lq_tail0 + (uint32_t)(hit_base + phit)) & lq_mask] = e;
-                bool last = true;                      // only the last touch of d stamps it
-                for (int32_t j = i + 1; j < n; j++)
-                    last &= !(h->list_desc[j] == d && !((stored_mask >> (h->list_pack[j] & 0xff)) & 1u) &&
-                              (w.dflags[d] & D_CACHED));
-                if (last) w.lstamp[d] = st;
-            }
-            if (cl != F_STORE && cache_on) { if (cl == F_HIT) c_hit++; else c_miss++; }
-            if (cl != F_STORE) {
-                if (sp == S_CAND) c_spec++;
-                else if (sp >= S_DISABLED && sp <= S_INFLIGHT) c_skip[sp - S_DISABLED]++;
-            }
-        }
-        imm_base += tot_imm;
-        hit_base += tot_hit;
-    }
-    // jobs: records, in-flight flags, waiter-list reset, handoffs / FIFO
-    int32_t rank_base = 0;
-    uint32_t c_dem = 0, c_spj = 0, c_ready = 0;
-    for (int32_t base = 0; base < nat; base += 32) {
-        int32_t a = base + lane;
-        bool ok = a < nat && h->at_ok[a];
-        int32_t tot;
-        int32_t r = rank_base + warp_excl_prefix(ok, lane, tot);
-        if (ok) {
-            int32_t ent = h->at_ent[a] >> 1;
-            int32_t origin = (h->at_ent[a] & 1) ? OTF_ORIGIN_SPECULATIVE : OTF_ORIGIN_DEMAND;
-            int32_t x = h->at_tgt[a];
-            double now = h->list_when[ent];
-            int64_t j = job0 + r;
-            if (origin == OTF_ORIGIN_DEMAND) c_dem++; else c_spj++;
-            if (w.S.records) {
-                if (j < sc.job_cap) {
-                    int64_t o = sc.job_off + j;
-                    w.S.b->job_seq[o] = w.S.desc_seq(x);
-                    w.S.b->job_rep[o] = w.S.desc_rank(x);
-                    w.S.b->job_index[o] = w.S.desc_index(x);
-                    w.S.b->job_origin[o] = origin;
-                    w.S.b->job_outcome[o] = OTF_OUTCOME_PENDING;
-                    w.S.b->job_enq[o] = now;
-                    w.S.b->job_start[o] = r < g ? now : NAN;
-                    w.S.b->job_fin[o] = NAN;
-                } else {
-                    w.S.flag(OTF_S_RECORD_OVERFLOW);
-                }
-            }
-            w.dflags[x] |= D_INFLIGHT;
-            w.wq_head[x] = -1;
-            w.wq_tail[x] = -1;
-            if (r < g) {                               // handed to the r-th idle worker: starts now
-                int32_t wid = h->gq[(h->gq_head + r) % K];
-                WWorker &k = h->wk[wid];
-                double e = 0.0;
-                if (sc.noise > 0) {
-                    if (k.eps_pos >= sc.eps_stride) w.S.flag(OTF_S_EPS_OVERFLOW);
-                    else e = w.S.eps[(int64_t)wid * sc.eps_stride + k.eps_pos];
-                    k.eps_pos++;
-                }
-                int32_t rank = w.S.desc_rank(x), seq = w.S.desc_seq(x), idx = w.S.desc_index(x);
-                double dur = seg_duration(w.S.seqdur[seq], w.S.segdur[seq], idx);
-                double svc = w.S.rho[rank - 1] * dur * (1.0 + e);
-                svc = (1e-9 > svc) ? 1e-9 : svc;
-                k.when = now + svc;
-                k.ctime = now;
-                k.seq = h->wseq + (uint32_t)r;
-                k.win = timer_win(w, k.when);
-                k.desc = x;
-                k.job = (int32_t)j;
-                k.size = w.S.size(x);
-                k.pc = W_SERVICE;
-                c_ready++;
-            } else {                                   // queued behind the busy workers
-                int32_t pos = (h->jq_head + h->jq_n + (r - g)) % h->jq_cap;
-                JobEnt e; e.desc = x; e.job = (int32_t)j;
-                w.jq[pos] = e;
-            }
-        }
-        rank_base += tot;
-    }
-    // warp totals of the counters
-    for (int o = 16; o > 0; o >>= 1) {
-        c_hit += __shfl_xor_sync(0xffffffffu, c_hit, o);
-        c_miss += __shfl_xor_sync(0xffffffffu, c_miss, o);
-        c_spec += __shfl_xor_sync(0xffffffffu, c_spec, o);
-        c_dem += __shfl_xor_sync(0xffffffffu, c_dem, o);
-        c_spj += __shfl_xor_sync(0xffffffffu, c_spj, o);
-        c_ready += __shfl_xor_sync(0xffffffffu, c_ready, o);
-        for (int q = 0; q < 5; q++) c_skip[q] += __shfl_xor_sync(0xffffffffu, c_skip[q], o);
-    }
-    __syncwarp();
-    if (lane == 0) {
-        // waiters join their descriptor's waiter list in request order (backend.py:125-133)
-        for (int32_t i = 0; i < n; i++) {
-            Client &c = w.cl[h->list_id[i]];
-            if (c.pc != C_SEG_WAIT) continue;
-            add_waiter(w, h->list_desc[i], h->list_id[i]);
-        }
-        int32_t jobs = c_dem + c_spj;
-        h->gq_head = (h->gq_head + g) % K;
-        h->gq_n -= g;
-        h->jq_n += jobs - g;
-        h->wseq += (uint32_t)g;
-        h->st.req_counter = req0 + n;
-        h->st.n_req = slot0 + imm_base;
-        h->st.n_job = job0 + jobs;
-        h->n_blist = nb0 + imm_base;
-        h->lq_stamp = stamp0 + (uint32_t)hit_base;
-        h->lq_tail = lq_tail0 + (uint32_t)hit_base;
-        h->stats[OTF_ST_HITS] += c_hit;
-        h->stats[OTF_ST_MISSES] += c_miss;
-        h->stats[OTF_ST_SPEC_ENQUEUED] += c_spec;
-        h->stats[OTF_ST_JOBS_TOTAL] += jobs;
-        h->stats[OTF_ST_JOBS_DEMAND] += c_dem;
-        h->stats[OTF_ST_JOBS_SPEC] += c_spj;
-        h->stats[OTF_ST_READY_CALLBACKS] += c_ready;
-        h->stats[OTF_ST_TIMER_POPS] += n;
-        for (int q = 0; q < 5; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += c_skip[q];
-    }
-    __syncwarp();
-    return true;
 }
 
 // Phase A: replay the window's server events in (time, creation, tick) order.
@@ -1253,12 +941,10 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         t1 = clock64();
         if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
         t0 = t1;
-        // ---- phase A: data-parallel when no worker event is due, else the serial lane ----
-        if (lane == 0 && h->n_ties) order_ties(w);
-        __syncwarp();
-        const bool fast = phase_a_fast(w, lane);
+        // ---- phase A: server lane ----
         if (lane == 0) {
-            if (!fast) phase_a(w);
+            if (h->n_ties) order_ties(w);
+            phase_a(w);
             h->k_done = m;
         }
         __syncwarp();
