@@ -188,12 +188,14 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
 // stores -- no dependent loads on the server lane -- and evictions read the
 // queue sequentially.  The queue is compacted (warp-parallel, order kept)
 // before it can overflow.
-__device__ void lq_compact_serial(Win &w);
+__device__ __noinline__ uint32_t lq_compact_serial(LqEnt *lq, const uint8_t *dflags, const uint32_t *lstamp,
+                                                   uint32_t head, uint32_t tail, uint32_t mask);
 
 __device__ __forceinline__ void lru_touch(Win &w, int32_t d) {
     uint32_t s = ++w.lq_stamp;
     w.lstamp[d] = s;
-    if (w.lq_tail - w.lq_head > w.lq_mask) lq_compact_serial(w);
+    if (w.lq_tail - w.lq_head > w.lq_mask)
+        w.lq_tail = lq_compact_serial(w.lq, w.dflags, w.lstamp, w.lq_head, w.lq_tail, w.lq_mask);
     LqEnt e; e.desc = d; e.stamp = s;
     w.lq[w.lq_tail & w.lq_mask] = e;
     w.lq_tail++;
@@ -230,13 +232,14 @@ __device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cach
 
 // Drop stale queue entries in place, keeping order (lane 0; only if a window
 // overran the pre-window compaction margin).
-__device__ void lq_compact_serial(Win &w) {
-    uint32_t o = w.lq_head;
-    for (uint32_t i = w.lq_head; i != w.lq_tail; i++) {
-        LqEnt e = w.lq[i & w.lq_mask];
-        if ((w.dflags[e.desc] & D_CACHED) && w.lstamp[e.desc] == e.stamp) w.lq[(o++) & w.lq_mask] = e;
+__device__ __noinline__ uint32_t lq_compact_serial(LqEnt *lq, const uint8_t *dflags, const uint32_t *lstamp,
+                                                   uint32_t head, uint32_t tail, uint32_t mask) {
+    uint32_t o = head;
+    for (uint32_t i = head; i != tail; i++) {
+        LqEnt e = lq[i & mask];
+        if ((dflags[e.desc] & D_CACHED) && lstamp[e.desc] == e.stamp) lq[(o++) & mask] = e;
     }
-    w.lq_tail = o;
+    return o;
 }
 
 // Warp-parallel order-preserving compaction of the touch queue into a fresh
@@ -745,6 +748,7 @@ __device__ int32_t wheel_next(WinHeader *h, int32_t k_done, int lane) {
     return warp_min(best);
 }
 
+template <bool RECORDS>
 __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x;
@@ -755,6 +759,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     __syncwarp();
     Win w;
     w.S.init(&h->b, &h->sc, s);
+    w.S.records = RECORDS;                             // compile-time: histogram kernels carry no record code
     const otf_scenario &sc = h->sc;
     const int32_t N = sc.n_clients, K = sc.n_workers;
     const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
@@ -1000,10 +1005,11 @@ int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
 
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
     int smem = (int)b.shared_bytes;
+    auto kern = b.mode == OTF_MODE_RECORDS ? otf::windowed_kernel<true> : otf::windowed_kernel<false>;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(otf::windowed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return 1;
     }
-    otf::windowed_kernel<<<b.n_scenarios, 32, smem, stream>>>(b);
+    kern<<<b.n_scenarios, 32, smem, stream>>>(b);
     return 0;
 }

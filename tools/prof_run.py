@@ -9,6 +9,9 @@ if which == "c5s":
     cfgs = [workloads.c5(seed=s, horizon_s=60.0) for s in range(1, 9)]
 elif which == "c5":
     cfgs = workloads.c5_sweep(seeds=range(1, 65))
+elif which == "c5h120":
+    import dataclasses
+    cfgs = [dataclasses.replace(c, horizon_s=120.0) for c in workloads.c5_sweep(seeds=range(1, 65))]
 else:
     cfgs = [workloads.c2(seed=s) for s in range(1, 65)]
 inp = inputs.build_inputs(cfgs, engine=eng, mode=_lib.MODE_HISTOGRAM)
