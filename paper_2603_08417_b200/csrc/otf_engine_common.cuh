@@ -258,29 +258,38 @@ __device__ __forceinline__ void client_init(Client &c) {
 }
 
 // orchestrator.py:338-340: the client's own pick stream
-__device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
+// Session-start RNG work runs once per session: kept out of line (plain
+// pointer/scalar arguments, so nothing is forced onto the stack).
+static __device__ __noinline__ void seed_picks(Pcg64 *g, uint64_t seed, int32_t cid) {
     uint32_t ent[8];
     int m = 0;
-    m = push_words(ent, m, S.sc->seed);
+    m = push_words(ent, m, seed);
     m = push_words(ent, m, 3u);
     m = push_words(ent, m, (uint64_t)cid);
-    pcg_seed(S.picks[cid], ent, m);
+    pcg_seed(*g, ent, m);
+}
+
+// orchestrator.py:342 picks.integers(n); Zipf extension: inverse CDF on picks.random()
+static __device__ __noinline__ int32_t draw_sequence(Pcg64 *g, int32_t n_seq, int32_t popularity, const double *zipf) {
+    if (popularity == OTF_POP_ZIPF) {
+        double u = pcg_next_double(*g);
+        int32_t lo = 0, hi = n_seq - 1;                // first k with u < cdf[k] (else the last)
+        while (lo < hi) {
+            int32_t mid = (lo + hi) >> 1;
+            if (u < zipf[mid]) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    }
+    return pcg_integers(*g, (uint32_t)n_seq);
+}
+
+__device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
+    seed_picks(&S.picks[cid], S.sc->seed, cid);
 }
 
 // orchestrator.py:341-345 + client.py:237-239: pick a sequence, register a report
 __device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double now) {
-    int32_t seq;
-    if (S.sc->popularity == OTF_POP_ZIPF) {
-        double u = pcg_next_double(S.picks[cid]);
-        int32_t lo = 0, hi = S.sc->n_seq - 1;          // first k with u < cdf[k] (else the last)
-        while (lo < hi) {
-            int32_t mid = (lo + hi) >> 1;
-            if (u < S.zipf[mid]) hi = mid; else lo = mid + 1;
-        }
-        seq = lo;
-    } else {
-        seq = pcg_integers(S.picks[cid], (uint32_t)S.sc->n_seq);
-    }
+    int32_t seq = draw_sequence(&S.picks[cid], S.sc->n_seq, S.sc->popularity, S.zipf);
     c.seq = seq;
     int64_t sid = atomicAdd((unsigned long long *)&S.st->n_sess, 1ull);
     c.session = (int32_t)sid;

@@ -147,8 +147,9 @@ struct Win {
     uint32_t c_skip[6];
 };
 
-// window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles)
-__device__ __forceinline__ int32_t win_of(double when, double W, double invW) {
+// window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles);
+// one out-of-line copy (scalar arguments) serves every call site
+__device__ __noinline__ int32_t win_of(double when, double W, double invW) {
     double q = floor(when * invW);                     // estimate; the exact bounds decide
     int32_t k = q < 1.0e9 ? (int32_t)q : 1000000000;
     if (k < 0) k = 0;
