@@ -199,7 +199,7 @@ def main():
         exact_inp = inputs.build_inputs([my_cfgs[i] for i in flagged], engine=_lib.ENGINE_EXACT,
                                         mode=_lib.MODE_HISTOGRAM, eps_scale=4)
         exact_db = engine.DeviceBatch(exact_inp, dev, pin=True)
-    launches_per_step = 2 + (2 if exact_db is not None else 0)
+    launches_per_step = 1 + len(db.groups) + (2 if exact_db is not None else 0)
     q_rows = db.qoe.shape[1]
 
     from paper_2603_08417_b200 import dist as odist

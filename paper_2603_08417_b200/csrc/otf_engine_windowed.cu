@@ -35,7 +35,7 @@
 namespace otf {
 
 constexpr int32_t WIN_NONE = 0x3FFFFFFF;
-constexpr int LIST_CAP = 256;      // server events per window (more -> exact engine)
+constexpr int RANK_SORT_MAX = 64;  // windows up to this many server events: rank sort, else bitonic
 constexpr int MAXK = 16;           // transcode workers
 constexpr int RING = 512;          // timer-wheel buckets (windows); farther timers wait on a far list
 constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory
@@ -77,12 +77,15 @@ struct WinHeader {
     uint32_t bits[RING / 32];
     int32_t bhead_srv[RING];
     int32_t bhead_loc[RING];
-    // the window's server events
-    double list_when[LIST_CAP];
-    int32_t list_pack[LIST_CAP];         // rank | index << 8 | seq << 16
-    int16_t list_id[LIST_CAP];
-    int16_t list_desc[LIST_CAP];
+    int32_t list_cap;                    // capacity of the window's server-event list (dynamic region)
 };
+
+// Server events one window can hold: the list lives in the dynamic shared region.
+__host__ __device__ inline int32_t win_list_cap(int32_t n_clients) {
+    int32_t c = 64;
+    while (c < n_clients / 16 && c < 4096) c <<= 1;
+    return c;
+}
 
 struct LqEnt {
     int32_t desc;
@@ -116,6 +119,7 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
 
 __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc) {
     int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
+    o += 16 * (int64_t)win_list_cap(n_clients);   // when f64, pack i32, id i16, desc i16
     o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
     o = (o + 15) & ~(int64_t)15;
     o += n_desc;                          // descriptor flags
@@ -126,6 +130,9 @@ struct Win {
     Scn S;
     WinHeader *h;
     int16_t *bnext;
+    double *lw;                                        // window's server events: time,
+    int32_t *lp;                                       //   rank | index << 8 | seq << 16,
+    int16_t *li, *ld;                                  //   client id, descriptor
     uint32_t *lstamp;                                  // latest touch stamp per descriptor (global)
     LqEnt *lq;                                         // touch queue (global, 2 * lq_cap)
     uint8_t *dflags;
@@ -471,7 +478,7 @@ __device__ void phase_a(Win &w) {
     double bw_when = 0.0, bw_ctime = 0.0;
     int64_t pops = 0;
     int32_t i = 0;
-    double cw = i < n ? h->list_when[0] : 0.0;
+    double cw = i < n ? w.lw[0] : 0.0;
     for (;;) {
         if (w.wdirty) {                                // earliest worker timer in this window
             bw = -1;
@@ -492,7 +499,7 @@ __device__ void phase_a(Win &w) {
         else if (bw_when < cw) take_worker = true;
         else if (cw < bw_when) take_worker = false;
         else {
-            double cc = w.cl[h->list_id[i]].ctime;
+            double cc = w.cl[w.li[i]].ctime;
             if (bw_ctime < cc) take_worker = true;
             else if (cc < bw_ctime) take_worker = false;
             else { w.S.flag(OTF_S_TIE); take_worker = true; }
@@ -503,10 +510,10 @@ __device__ void phase_a(Win &w) {
             server_worker_done(w, bw);
         } else {
             w.now = cw;
-            int32_t pk = h->list_pack[i];
-            server_request(w, h->list_id[i], h->list_desc[i], pk & 0xff, pk >> 16, (pk >> 8) & 0xff);
+            int32_t pk = w.lp[i];
+            server_request(w, w.li[i], w.ld[i], pk & 0xff, pk >> 16, (pk >> 8) & 0xff);
             i++;
-            if (i < n) cw = h->list_when[i];
+            if (i < n) cw = w.lw[i];
         }
         if (w.fq_n > 0) drain_handoffs(w);
     }
@@ -671,38 +678,75 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) {
 
 // Order the window's server events by (time, arm time, client): each lane
 // ranks its entries against all others (ties are flagged afterwards).
-__device__ void sort_list(WinHeader *h, int lane) {
+__device__ __forceinline__ bool key_gt(double wa, int32_t ia, double wb, int32_t ib) {
+    return wa > wb || (wa == wb && ia > ib);
+}
+
+// Order the window's server events by (time, client): rank sort for small
+// windows, in-place bitonic sort for large ones (ties are flagged afterwards).
+__device__ void sort_list(Win &w, int lane) {
+    WinHeader *h = w.h;
     const int32_t n = h->n_list;
     if (lane == 0) h->n_ties = 0;
     if (n <= 1) { __syncwarp(); return; }
-    double my_w[LIST_CAP / 32];
-    int32_t my_s[LIST_CAP / 32], my_r[LIST_CAP / 32];
-    int16_t my_id[LIST_CAP / 32], my_d[LIST_CAP / 32];
-    int32_t m = 0;
-    for (int32_t i = lane; i < n; i += 32, m++) {
-        double wi = h->list_when[i];
-        int32_t idi = h->list_id[i];
-        int32_t r = 0;
+    if (n <= RANK_SORT_MAX) {
+        double my_w[RANK_SORT_MAX / 32];
+        int32_t my_s[RANK_SORT_MAX / 32], my_r[RANK_SORT_MAX / 32];
+        int16_t my_id[RANK_SORT_MAX / 32], my_d[RANK_SORT_MAX / 32];
+#pragma unroll
+        for (int t = 0; t < RANK_SORT_MAX / 32; t++) {
+            int32_t i = lane + 32 * t;
+            if (i >= n) break;
+            double wi = w.lw[i];
+            int32_t idi = w.li[i];
+            int32_t r = 0;
 #pragma unroll 4
-        for (int32_t j = 0; j < n; j++) {              // branch-free (time, client) compare
-            double wj = h->list_when[j];
-            int32_t idj = h->list_id[j];
-            r += (int32_t)((wj < wi) | ((wj == wi) & (idj < idi)));
+            for (int32_t j = 0; j < n; j++) {          // branch-free (time, client) compare
+                double wj = w.lw[j];
+                int32_t idj = w.li[j];
+                r += (int32_t)((wj < wi) | ((wj == wi) & (idj < idi)));
+            }
+            my_w[t] = wi; my_id[t] = (int16_t)idi; my_r[t] = r;
+            my_d[t] = w.ld[i]; my_s[t] = w.lp[i];
         }
-        my_w[m] = wi; my_id[m] = (int16_t)idi; my_r[m] = r;
-        my_d[m] = h->list_desc[i]; my_s[m] = h->list_pack[i];
-    }
-    __syncwarp();
-    for (int32_t t = 0; t < m; t++) {
-        int32_t r = my_r[t];
-        h->list_when[r] = my_w[t]; h->list_id[r] = my_id[t];
-        h->list_desc[r] = my_d[t]; h->list_pack[r] = my_s[t];
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < RANK_SORT_MAX / 32; t++) {
+            int32_t i = lane + 32 * t;
+            if (i >= n) break;
+            int32_t r = my_r[t];
+            w.lw[r] = my_w[t]; w.li[r] = my_id[t];
+            w.ld[r] = my_d[t]; w.lp[r] = my_s[t];
+        }
+    } else {
+        int32_t p = 1;
+        while (p < n) p <<= 1;
+        for (int32_t i = n + lane; i < p; i += 32) { w.lw[i] = INFINITY; w.li[i] = 32767; }
+        __syncwarp();
+        for (int32_t size = 2; size <= p; size <<= 1) {
+            for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int32_t t = lane; t < (p >> 1); t += 32) {
+                    int32_t lo = 2 * t - (t & (stride - 1));
+                    int32_t hi = lo + stride;
+                    bool up = (lo & size) == 0;
+                    double wl = w.lw[lo], wh = w.lw[hi];
+                    int32_t il = w.li[lo], ih = w.li[hi];
+                    if (key_gt(wl, il, wh, ih) == up) {
+                        w.lw[lo] = wh; w.lw[hi] = wl;
+                        w.li[lo] = (int16_t)ih; w.li[hi] = (int16_t)il;
+                        int16_t td = w.ld[lo]; w.ld[lo] = w.ld[hi]; w.ld[hi] = td;
+                        int32_t tp = w.lp[lo]; w.lp[lo] = w.lp[hi]; w.lp[hi] = tp;
+                    }
+                }
+                __syncwarp();
+            }
+        }
     }
     __syncwarp();
     bool tie = false;                                  // any equal request times? (rare)
-    for (int32_t i = lane + 1; i < n; i += 32) tie |= h->list_when[i] == h->list_when[i - 1];
-    if (lane == 0) h->n_ties = __any_sync(0xffffffffu, tie) ? 1 : 0;
-    else __any_sync(0xffffffffu, tie);
+    for (int32_t i = lane + 1; i < n; i += 32) tie |= w.lw[i] == w.lw[i - 1];
+    bool any = __any_sync(0xffffffffu, tie);
+    if (lane == 0) h->n_ties = any ? 1 : 0;
     __syncwarp();
 }
 
@@ -712,15 +756,15 @@ __device__ void order_ties(Win &w) {
     WinHeader *h = w.h;
     const int32_t n = h->n_list;
     for (int32_t i = 1; i < n; i++) {
-        if (h->list_when[i] != h->list_when[i - 1]) continue;
+        if (w.lw[i] != w.lw[i - 1]) continue;
         int32_t j = i;                                 // insertion step by ctime
-        while (j > 0 && h->list_when[j] == h->list_when[j - 1]) {
-            double cj = w.cl[h->list_id[j]].ctime, cp = w.cl[h->list_id[j - 1]].ctime;
+        while (j > 0 && w.lw[j] == w.lw[j - 1]) {
+            double cj = w.cl[w.li[j]].ctime, cp = w.cl[w.li[j - 1]].ctime;
             if (cj == cp) { h->st.status |= OTF_S_TIE; break; }
             if (cj > cp) break;
-            int16_t ti = h->list_id[j]; h->list_id[j] = h->list_id[j - 1]; h->list_id[j - 1] = ti;
-            int16_t td = h->list_desc[j]; h->list_desc[j] = h->list_desc[j - 1]; h->list_desc[j - 1] = td;
-            int32_t tp = h->list_pack[j]; h->list_pack[j] = h->list_pack[j - 1]; h->list_pack[j - 1] = tp;
+            int16_t ti = w.li[j]; w.li[j] = w.li[j - 1]; w.li[j - 1] = ti;
+            int16_t td = w.ld[j]; w.ld[j] = w.ld[j - 1]; w.ld[j - 1] = td;
+            int32_t tp = w.lp[j]; w.lp[j] = w.lp[j - 1]; w.lp[j - 1] = tp;
             j--;
         }
     }
@@ -765,6 +809,11 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     const int32_t N = sc.n_clients, K = sc.n_workers;
     const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
     uint8_t *p = smem + ((sizeof(WinHeader) + 15) & ~(size_t)15);
+    const int32_t lcap = win_list_cap(sc.n_clients);
+    w.lw = (double *)p; p += 8 * (int64_t)lcap;
+    w.lp = (int32_t *)p; p += 4 * (int64_t)lcap;
+    w.li = (int16_t *)p; p += 2 * (int64_t)lcap;
+    w.ld = (int16_t *)p; p += 2 * (int64_t)lcap;
     uint8_t *g = b.scratch + sc.scratch_off;
     WinGlobalLayout L = win_global_layout(N, D);
     w.h = h;
@@ -804,6 +853,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
         h->arr_next = 0;
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
+        h->list_cap = lcap;
         if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
     }
     __syncwarp();
@@ -911,7 +961,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
             h->bits[slot >> 5] &= ~(1u << (slot & 31));
             int32_t nl = 0, nb = 0;
             while (c >= 0) {
-                if (nl < LIST_CAP) h->list_id[nl] = (int16_t)c;
+                if (nl < h->list_cap) w.li[nl] = (int16_t)c;
                 nl++;
                 c = w.bnext[c];
             }
@@ -928,22 +978,22 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
             asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
             asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr + 128));
         }
-        if (h->n_list > LIST_CAP) {                    // too many simultaneous requests for this engine
+        if (h->n_list > h->list_cap) {                 // too many simultaneous requests for this engine
             if (lane == 0) h->st.status |= OTF_S_TIE;
             __syncwarp();
             break;
         }
         for (int32_t i = lane; i < h->n_list; i += 32) {   // gather sort keys + request descriptors
-            const Client &cl = w.cl[h->list_id[i]];
-            h->list_when[i] = cl.next_when;
-            h->list_desc[i] = (int16_t)cl.desc;
-            h->list_pack[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
+            const Client &cl = w.cl[w.li[i]];
+            w.lw[i] = cl.next_when;
+            w.ld[i] = (int16_t)cl.desc;
+            w.lp[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
         }
         __syncwarp();
         t1 = clock64();
         if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
         t0 = t1;
-        sort_list(h, lane);
+        sort_list(w, lane);
         t1 = clock64();
         if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
         t0 = t1;

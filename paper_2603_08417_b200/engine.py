@@ -80,13 +80,26 @@ class DeviceBatch:
             setattr(b, name, self.rec[name].data_ptr() if name in self.rec else None)
         b.counts, b.stats = self.counts.data_ptr(), self.stats.data_ptr()
         b.qoe, b.status = self.qoe.data_ptr(), self.status.data_ptr()
-        # longest scenarios first (LPT): the grid drains them while short ones fill in
+        # launch groups: scenarios of similar shared-memory size together (a big
+        # scenario must not shrink everyone's occupancy), longest first within a group
         cost = np.array([l.cfg.clients * l.cfg.horizon_s / min(l.seq_segdur) for l in inp.lowered])
-        self.order = torch.from_numpy(np.argsort(-cost, kind="stable").astype(np.int32)).to(dev)
+        smem = np.array(inp.smem_per if inp.smem_per else [inp.shared_bytes] * n, dtype=np.int64)
+        cls = np.ceil(np.maximum(smem, 1) / 8192.0).astype(np.int64)
+        order = np.lexsort((-cost, cls)).astype(np.int32)   # by class, then longest first
+        self.order = torch.from_numpy(order).to(dev)
+        self.groups = []
+        for c in np.unique(cls):
+            idx = np.nonzero(cls[order] == c)[0]
+            gb = _lib.Batch.from_buffer_copy(b)
+            gb.n_scenarios = int(len(idx))
+            gb.order = self.order.data_ptr() + 4 * int(idx[0])
+            gb.shared_bytes = int(smem[order[idx]].max())
+            gb.engine_flags = 0
+            self.groups.append(gb)
         b.order = self.order.data_ptr()
         b.shared_bytes = inp.shared_bytes
-        b.engine_flags = inp.engine_flags
         self.batch = b
+        self.streams = [torch.cuda.Stream(dev) for _ in self.groups[1:]]
         self.n_tables = sum(1 for t in inp.size_tables if t.n_seq > 0)
         self.upload()
 
@@ -109,8 +122,19 @@ class DeviceBatch:
             rc = self.lib.otf_gen_sizes(self.tables.data_ptr(), self.n_tables, 0, self.i64.data_ptr(),
                                         self.f64.data_ptr(), self.i32.data_ptr(), s.cuda_stream)
             _lib.check(rc, "otf_gen_sizes")
-        rc = self.lib.otf_run_batch(ctypes.byref(self.batch), self.inp.engine, s.cuda_stream)
+        if len(self.groups) <= 1 or self.inp.engine != _lib.ENGINE_WINDOWED:
+            rc = self.lib.otf_run_batch(ctypes.byref(self.batch), self.inp.engine, s.cuda_stream)
+            _lib.check(rc, "otf_run_batch")
+            return
+        # size classes run concurrently on side streams, joined back to `s`
+        rc = self.lib.otf_run_batch(ctypes.byref(self.groups[0]), self.inp.engine, s.cuda_stream)
         _lib.check(rc, "otf_run_batch")
+        for gb, st in zip(self.groups[1:], self.streams):
+            st.wait_stream(s)
+            rc = self.lib.otf_run_batch(ctypes.byref(gb), self.inp.engine, st.cuda_stream)
+            _lib.check(rc, "otf_run_batch")
+        for st in self.streams:
+            s.wait_stream(st)
 
     def fetch(self) -> "BatchResult":
         torch.cuda.synchronize(self.device)

@@ -134,7 +134,8 @@ class BatchInputs:
     engine: int
     mode: int
     input_bytes: int            # algorithmic input bytes (for the roofline)
-    shared_bytes: int = 0       # windowed engine: dynamic shared memory per CTA
+    shared_bytes: int = 0       # windowed engine: dynamic shared memory per CTA (batch max)
+    smem_per: list = dataclasses.field(default_factory=list)   # per scenario
     engine_flags: int = 0       # OTF_BF_*
 
 
@@ -170,6 +171,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     totals = [0, 0, 0, 0]
     input_bytes = 0
     shared_bytes = 0
+    smem_per: list[int] = []
 
     # -- traces: one table per (seed, netem), long enough for the largest N --
     trace_groups: dict = {}
@@ -288,7 +290,8 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.off_eps, sc.eps_stride = o_eps, eps_stride
         sc.scratch_off = scratch_off
         scratch_off += int(L.otf_scratch_bytes(engine, N, K, n_seq, n_ranks, max_nseg))
-        shared_bytes = max(shared_bytes, int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg)))
+        smem_per.append(int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg)))
+        shared_bytes = max(shared_bytes, smem_per[-1])
         scratch_off = (scratch_off + 255) & ~255
         if mode == _lib.MODE_RECORDS:
             c = caps[si] if caps is not None else _default_caps(low)
@@ -305,7 +308,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         lowered=lows, scenarios=scen, size_tables=(_lib.SizeTable * max(1, len(tables)))(*tables),
         f64=P.concat("f64"), i64=P.concat("i64"), i32=P.concat("i32"),
         scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
-        engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes)
+        engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes, smem_per=smem_per)
 
 
 def n_size_tables(inp: BatchInputs) -> int:
