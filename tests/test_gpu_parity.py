@@ -172,3 +172,14 @@ def test_run_sharded_single_rank():
     ref = engine.run_batch(cfgs, mode="histogram")
     assert [int(b[0]) for b in blocks] == [0, 1, 2, 3]
     assert [int(b[1]) for b in blocks] == [r.qoe["n_requests"] for r in ref]
+
+
+def test_cli_matrix_matches_reference_bundles(tmp_path):
+    """`matrix` (72 configs, one launch) writes the reference's bundle for a grid point."""
+    import filecmp
+    import os
+    from paper_2603_08417_b200 import cli
+    assert cli.main(["run", "--variant", "T", "--clients", "4", "--seed", "1", "--out", str(tmp_path / "run")]) == 0
+    assert (tmp_path / "run" / "requests.csv").exists()
+    assert cli.main(["matrix", "--out", str(tmp_path / "m")]) == 0
+    assert len(os.listdir(tmp_path / "m")) == 72
