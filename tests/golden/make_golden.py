@@ -164,8 +164,19 @@ def dump(name: str, cfg) -> None:
     print(f"{name}: requests {len(R)} sessions {len(S)} jobs {len(J)}")
 
 
+def matrix_bundles():
+    """Reference CSV bundles of two grid points of scenario_matrix(ExperimentConfig())."""
+    grid = dict(ref_orch.scenario_matrix(ref_orch.ExperimentConfig()))
+    for name in ("c24_n1_t4_TCPF", "c04_n2_t2_TC"):
+        ref_orch.run_experiment(grid[name]).write(os.path.join(HERE, "csv_matrix", name))
+        print("matrix bundle", name)
+
+
 def main(argv):
     logging.disable(logging.WARNING)
+    if argv[1:] == ["matrix"]:
+        matrix_bundles()
+        return
     only = set(argv[1:])
     for name, cfg in cases.golden_cases():
         if only and name not in only:

@@ -183,3 +183,7 @@ def test_cli_matrix_matches_reference_bundles(tmp_path):
     assert (tmp_path / "run" / "requests.csv").exists()
     assert cli.main(["matrix", "--out", str(tmp_path / "m")]) == 0
     assert len(os.listdir(tmp_path / "m")) == 72
+    ref_dir = os.path.join(parity.GOLDEN_DIR, "csv_matrix")
+    for name in sorted(os.listdir(ref_dir)):            # byte-identical to the reference's own bundle
+        for f in ("requests.csv", "sessions.csv", "segments.csv", "jobs.csv", "config.json", "summary.json"):
+            assert filecmp.cmp(tmp_path / "m" / name / f, os.path.join(ref_dir, name, f), shallow=False), (name, f)
