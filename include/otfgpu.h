@@ -49,7 +49,7 @@ typedef enum {
 #define OTF_S_HUNG 0x10            /* a client slept forever (starved trace), informative */
 
 /* ---- enums shared with the host (values are part of the ABI) ---- */
-enum { OTF_PATH_STORAGE = 0, OTF_PATH_CACHE = 1, OTF_PATH_WAITED = 2, OTF_PATH_TRANSCODED = 3 };
+enum { OTF_PATH_STORAGE = 0, OTF_PATH_CACHE = 1, OTF_PATH_WAITED = 2, OTF_PATH_TRANSCODED = 3, OTF_PATH_ERROR = 4 };
 enum { OTF_ORIGIN_DEMAND = 0, OTF_ORIGIN_SPECULATIVE = 1 };
 enum { OTF_OUTCOME_PENDING = 0, OTF_OUTCOME_COMPLETED = 1, OTF_OUTCOME_DROPPED = 2 };
 enum { OTF_POP_UNIFORM = 0, OTF_POP_ZIPF = 1 };
@@ -75,8 +75,10 @@ enum {
 typedef struct otf_scenario {
     int32_t n_clients, n_workers, n_seq, n_ranks;
     int32_t max_nseg, n_samples, cache_enabled, spec_enabled;
-    int32_t popularity, pad0;
-    uint32_t stored_mask, pad1;       /* bit r set <=> rank r stored at origin (backend.py:76-82) */
+    int32_t popularity;
+    int32_t queue_bound;              /* BackendPolicy.queue_bound: 0 = unbounded (backend.py:56,160-166) */
+    uint32_t stored_mask;             /* bit r set <=> rank r stored at origin (backend.py:76-82) */
+    int32_t retries;                  /* ClientConfig.retries (client.py:291-305) */
     int64_t cache_capacity;           /* bytes (cache.py:27-30) */
     uint64_t seed;                    /* ExperimentConfig.seed: picks stream SS([seed, 3, cid]) */
     double horizon, latency;          /* horizon_s; ClientConfig.latency_s */
@@ -85,6 +87,7 @@ typedef struct otf_scenario {
     double noise;                     /* LatencyModel.noise_rel_std */
     double period;                    /* BandwidthTrace.period (shared timestamps) */
     double grid_step;                 /* > 0 when starts[i] == i * grid_step exactly (bisect-free lookup) */
+    double retry_backoff;             /* ClientConfig.retry_backoff_s */
     int64_t off_sizes;                /* i64: [n_seq][n_ranks][max_nseg] segment bytes */
     int64_t off_bitrates;             /* i64: [n_ranks] */
     int64_t off_manifest;             /* i64: [n_seq] manifest JSON bytes */
@@ -111,7 +114,7 @@ typedef struct otf_scenario {
 #define OTF_RANK_BINS 16     /* segments by representation rank */
 typedef struct otf_qoe {
     int64_t lat_hist[OTF_LAT_BINS];
-    int64_t path_count[4];
+    int64_t path_count[8];            /* by OTF_PATH_* */
     int64_t stall_hist[OTF_STALL_BINS];
     int64_t rank_count[OTF_RANK_BINS];
     int64_t n_requests, n_sessions, n_segments, n_finished, n_started;

@@ -30,7 +30,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
-PATHS = ("storage", "cache", "waited_inflight", "transcoded")
+PATHS = ("storage", "cache", "waited_inflight", "transcoded", "error")
 ORIGINS = ("demand", "speculative")
 OUTCOMES = ("pending", "completed", "dropped", "failed")
 SKIP_REASONS = ("disabled", "end-of-sequence", "stored", "cached", "in-flight", "overload")
@@ -66,6 +66,7 @@ class Scenario(ctypes.Structure):
         ("arrival_draws", _P(ctypes.c_double)), ("trace_normals", _P(ctypes.c_double)),
         ("zipf_cdf", _P(ctypes.c_double)), ("eps", _P(ctypes.c_double)),
         ("eps_per_worker", ctypes.c_int64),
+        ("queue_bound", ctypes.c_int32), ("retries", ctypes.c_int32), ("retry_backoff", ctypes.c_double),
     ]
 
 
@@ -239,6 +240,9 @@ class Prepared:
         sc.zipf_cdf = _ptr(self.zipf, ctypes.c_double)
         sc.eps = _ptr(self.eps, ctypes.c_double)
         sc.eps_per_worker = self.eps.shape[1]
+        sc.queue_bound = int(cfg.queue_bound)
+        sc.retries = int(cfg.client.retries)
+        sc.retry_backoff = float(cfg.client.retry_backoff_s)
         self.sc = sc
 
     def sizes(self):

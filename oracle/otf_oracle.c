@@ -208,7 +208,7 @@ enum { PH_STARTUP = 0, PH_PLAYING = 1, PH_STALLED = 2, PH_FINISHED = 3 };
 
 enum {
     C_START = 0, C_ARRIVED, C_SESSION, C_MAN_LAT, C_MAN_XFER, C_INDEX_HEAD, C_TARGET_WAIT,
-    C_SEG_LAT, C_SEG_WAIT, C_SEG_XFER, C_PLAYOUT, C_DONE, C_HUNG
+    C_SEG_LAT, C_SEG_WAIT, C_SEG_XFER, C_PLAYOUT, C_DONE, C_HUNG, C_RETRY
 };
 enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE };
 
@@ -223,6 +223,8 @@ typedef struct {
     double requested, arrival, xfer_start;
     int64_t req_id, size;
     int32_t path, desc;
+    int32_t attempt;                 /* _fetch_with_retry (client.py:291-305) */
+    double backoff;
     int32_t wait_next;
     pcg64_t picks;
     const double *values;
@@ -358,8 +360,11 @@ static void cache_put(world_t *w, int32_t d) {
 /* ---- backend (backend.py:135-216) ---- */
 static void set_overflow(world_t *w) { w->status = ORACLE_EOVERFLOW; }
 
-static void enqueue_job(world_t *w, int32_t d, int32_t origin) {
+/* Backend._enqueue (backend.py:156-170): returns 1 on OverloadError (queue at
+ * its bound and no idle worker: Queue.put_nowait raises QueueFull, sim.py:229-240). */
+static int enqueue_job(world_t *w, int32_t d, int32_t origin) {
     oracle_outputs *o = w->out;
+    if (w->gq_n == 0 && w->sc->queue_bound > 0 && w->jq_n >= w->sc->queue_bound) return 1;
     int64_t j = o->n_job++;
     if (j < o->job_cap) {
         int32_t per_seq = w->sc->n_ranks * w->sc->max_nseg;
@@ -386,10 +391,11 @@ static void enqueue_job(world_t *w, int32_t d, int32_t origin) {
         w->gq_n--;
         ready_push(w, wid, j);
     } else {
-        if (w->jq_n >= w->jq_cap) { set_overflow(w); return; }
+        if (w->jq_n >= w->jq_cap) { set_overflow(w); return 0; }
         w->jq[(w->jq_head + w->jq_n) % w->jq_cap] = (int32_t)j;
         w->jq_n++;
     }
+    return 0;
 }
 
 static void maybe_speculate(world_t *w, int32_t seq, int32_t rank, int32_t index) {
@@ -401,7 +407,7 @@ static void maybe_speculate(world_t *w, int32_t seq, int32_t rank, int32_t index
     int32_t d = desc_id(w, seq, rank, ni);
     if (w->sc->cache_enabled && w->present[d]) { st[ST_SKIP_CACHED]++; return; }
     if (w->inflight[d]) { st[ST_SKIP_INFLIGHT]++; return; }
-    enqueue_job(w, d, ORIGIN_SPEC);
+    if (enqueue_job(w, d, ORIGIN_SPEC)) { st[ST_SKIP_OVERLOAD]++; return; }
     st[ST_SPEC_ENQUEUED]++;
 }
 
@@ -606,6 +612,8 @@ static void client_step(world_t *w, int32_t cid) {
                 break;
             }
             if (c->index > 0) c->rank = select_quality(sc, c->level, c->rank, c->has_est, c->est);
+            c->attempt = 0;                  /* _fetch_with_retry (client.py:291-305) */
+            c->backoff = sc->retry_backoff;
             /* InProcessEndpoint.segment (client.py:218-226) */
             c->requested = w->now;
             c->pc = C_SEG_LAT;
@@ -631,8 +639,25 @@ static void client_step(world_t *w, int32_t cid) {
                     add_waiter(w, d, cid);
                     c->pc = C_SEG_WAIT;
                     return;
+                } else if (enqueue_job(w, d, ORIGIN_DEMAND)) {
+                    /* OverloadError: the server records an error (server.py:70-73), the
+                     * client backs off or gives up (client.py:291-305, 257-260) */
+                    c->path = PATH_ERROR;
+                    int64_t sz = c->size;
+                    c->size = 0;
+                    append_request(w, c, w->now);
+                    c->size = sz;
+                    if (c->attempt == sc->retries) {
+                        if (c->session < o->sess_cap) o->sess_flags[c->session] |= SESS_ABORTED;
+                        sync_report(w, c, w->now);
+                        c->buf_live = 0;
+                        c->pc = C_SESSION;
+                        break;
+                    }
+                    c->pc = C_RETRY;
+                    if (do_sleep(w, task, c->backoff, &hung)) { if (hung) c->pc = C_HUNG; return; }
+                    break;
                 } else {
-                    enqueue_job(w, d, ORIGIN_DEMAND);
                     maybe_speculate(w, c->seq, c->rank, c->index);
                     c->path = PATH_TRANSCODED;
                     add_waiter(w, d, cid);
@@ -677,6 +702,15 @@ static void client_step(world_t *w, int32_t cid) {
             if (do_sleep(w, task, c->level, &hung)) { if (hung) c->pc = C_HUNG; return; }
             break;
         }
+        case C_RETRY:                        /* after sleep(backoff): backoff *= 2, next attempt */
+            c->backoff *= 2.0;
+            c->attempt++;
+            c->requested = w->now;
+            c->pc = C_SEG_LAT;
+            if (sc->latency > 0) {
+                if (do_sleep(w, task, sc->latency, &hung)) { if (hung) c->pc = C_HUNG; return; }
+            }
+            break;
         case C_PLAYOUT: /* client.py:272-280 */
             buf_advance(c, w->now);
             c->phase = PH_FINISHED;

@@ -3,7 +3,7 @@
 #define OTF_ORACLE_H
 #include <stdint.h>
 
-enum { PATH_STORAGE = 0, PATH_CACHE = 1, PATH_WAITED = 2, PATH_TRANSCODED = 3 };
+enum { PATH_STORAGE = 0, PATH_CACHE = 1, PATH_WAITED = 2, PATH_TRANSCODED = 3, PATH_ERROR = 4 };
 enum { ORIGIN_DEMAND = 0, ORIGIN_SPEC = 1 };
 enum { OUT_PENDING = 0, OUT_COMPLETED = 1, OUT_DROPPED = 2, OUT_FAILED = 3 };
 enum { POP_UNIFORM = 0, POP_ZIPF = 1 };
@@ -40,6 +40,8 @@ typedef struct {
     const double *zipf_cdf;         /* [n_seq] */
     const double *eps;              /* [n_workers][eps_per_worker] */
     int64_t eps_per_worker;
+    int32_t queue_bound, retries;   /* BackendPolicy.queue_bound, ClientConfig.retries */
+    double retry_backoff;           /* ClientConfig.retry_backoff_s */
 } oracle_scenario;
 
 typedef struct {

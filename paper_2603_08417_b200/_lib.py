@@ -22,7 +22,7 @@ _vp = ctypes.c_void_p
 _i32, _u32, _i64, _u64, _f64 = ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
 
 # enums (values are part of the ABI)
-PATH_STORAGE, PATH_CACHE, PATH_WAITED, PATH_TRANSCODED = 0, 1, 2, 3
+PATH_STORAGE, PATH_CACHE, PATH_WAITED, PATH_TRANSCODED, PATH_ERROR = 0, 1, 2, 3, 4
 ORIGIN_DEMAND, ORIGIN_SPECULATIVE = 0, 1
 OUTCOME_PENDING, OUTCOME_COMPLETED, OUTCOME_DROPPED = 0, 1, 2
 POP_UNIFORM, POP_ZIPF = 0, 1
@@ -44,11 +44,11 @@ class Scenario(ctypes.Structure):
     _fields_ = [
         ("n_clients", _i32), ("n_workers", _i32), ("n_seq", _i32), ("n_ranks", _i32),
         ("max_nseg", _i32), ("n_samples", _i32), ("cache_enabled", _i32), ("spec_enabled", _i32),
-        ("popularity", _i32), ("pad0", _i32), ("stored_mask", _u32), ("pad1", _u32),
+        ("popularity", _i32), ("queue_bound", _i32), ("stored_mask", _u32), ("retries", _i32),
         ("cache_capacity", _i64), ("seed", _u64),
         ("horizon", _f64), ("latency", _f64),
         ("target", _f64), ("safe", _f64), ("panic", _f64), ("resume", _f64), ("startup", _f64),
-        ("alpha", _f64), ("headroom", _f64), ("noise", _f64), ("period", _f64), ("grid_step", _f64),
+        ("alpha", _f64), ("headroom", _f64), ("noise", _f64), ("period", _f64), ("grid_step", _f64), ("retry_backoff", _f64),
         ("off_sizes", _i64), ("off_bitrates", _i64), ("off_manifest", _i64), ("off_segcount", _i64),
         ("off_seqdur", _i64), ("off_segdur", _i64), ("off_rho", _i64), ("off_zipf", _i64),
         ("off_starts", _i64), ("off_values", _i64), ("off_pbits", _i64), ("off_arrivals", _i64),
@@ -60,7 +60,7 @@ class Scenario(ctypes.Structure):
 
 class Qoe(ctypes.Structure):
     _fields_ = [
-        ("lat_hist", _i64 * LAT_BINS), ("path_count", _i64 * 4), ("stall_hist", _i64 * STALL_BINS),
+        ("lat_hist", _i64 * LAT_BINS), ("path_count", _i64 * 8), ("stall_hist", _i64 * STALL_BINS),
         ("rank_count", _i64 * RANK_BINS),
         ("n_requests", _i64), ("n_sessions", _i64), ("n_segments", _i64), ("n_finished", _i64),
         ("n_started", _i64), ("pad", _i64),

@@ -399,8 +399,8 @@ class ExperimentConfig:
             raise ConfigError("netem.trace_dir (CSV traces) is not supported by the GPU engine yet")
         if self.clock != "virtual":
             raise ConfigError("the GPU engine runs the virtual clock only")
-        if self.queue_bound or self.demand_priority:
-            raise ConfigError("queue_bound / demand_priority are not supported by the GPU engine yet")
+        if self.demand_priority:
+            raise ConfigError("demand_priority is not supported by the GPU engine yet")
 
 
 def nominal_ladder_bytes(config: ExperimentConfig) -> float:

@@ -28,7 +28,7 @@ struct EngineState {                 // first 256 B of every scenario arena
 // sums are accumulated per lane (Scn members) and reduced at the end.
 struct QoeAcc {
     uint32_t lat_hist[OTF_LAT_BINS];
-    uint32_t path_count[4];
+    uint32_t path_count[8];
     uint32_t stall_hist[OTF_STALL_BINS];
     uint32_t rank_count[OTF_RANK_BINS];
     uint32_t n_requests, n_sessions, n_segments, n_finished, n_started, pad[3];
@@ -100,7 +100,7 @@ struct Scn {
     // write the final otf_qoe (sums already reduced into this lane's members)
     __device__ void flush_qoe() const {
         for (int i = 0; i < OTF_LAT_BINS; i++) q->lat_hist[i] = qa->lat_hist[i];
-        for (int i = 0; i < 4; i++) q->path_count[i] = qa->path_count[i];
+        for (int i = 0; i < 8; i++) q->path_count[i] = qa->path_count[i];
         for (int i = 0; i < OTF_STALL_BINS; i++) q->stall_hist[i] = qa->stall_hist[i];
         for (int i = 0; i < OTF_RANK_BINS; i++) q->rank_count[i] = qa->rank_count[i];
         q->n_requests = qa->n_requests; q->n_sessions = qa->n_sessions; q->n_segments = qa->n_segments;
@@ -367,6 +367,16 @@ __device__ inline void client_finish_session(Scn &S, Client &c, double now) {
     if (S.records && c.session < S.sc->sess_cap) S.b->sess_flags[S.sc->sess_off + c.session] |= 1;
     S.sync_session(c, now);
     S.qoe_session(c, true);
+    c.buf_live = 0;
+    c.sess_open = 0;
+}
+
+// Session given up after the last retry (client.py:257-260 + the finally
+// clause): flagged aborted, synced without advancing the buffer.
+__device__ inline void client_abort_session(Scn &S, Client &c, double now) {
+    if (S.records && c.session < S.sc->sess_cap) S.b->sess_flags[S.sc->sess_off + c.session] |= 2;
+    S.sync_session(c, now);
+    S.qoe_session(c, false);
     c.buf_live = 0;
     c.sess_open = 0;
 }

@@ -130,8 +130,10 @@ __device__ void cache_put(ExactWorld &w, int32_t d) {
 }
 
 // ---- backend (backend.py:135-216) --------------------------------------------
-// Backend._enqueue + Queue.put_nowait (backend.py:156-170, sim.py:229-240)
-__device__ void enqueue_job(ExactWorld &w, int32_t d, int32_t origin) {
+// Backend._enqueue + Queue.put_nowait (backend.py:156-170, sim.py:229-240).
+// Returns true on OverloadError: no idle worker and the queue at its bound.
+__device__ bool enqueue_job(ExactWorld &w, int32_t d, int32_t origin) {
+    if (w.gq_n == 0 && w.S.sc->queue_bound > 0 && w.jq_n >= w.S.sc->queue_bound) return true;
     int32_t j = w.S.record_job(d, origin, w.now);
     Desc &D = w.descs[d];
     D.flags |= D_INFLIGHT;
@@ -142,13 +144,14 @@ __device__ void enqueue_job(ExactWorld &w, int32_t d, int32_t origin) {
         w.gq_n--;
         ready_push(w, wid, d, j);
     } else {
-        if (w.jq_n >= w.jq_cap) { w.S.flag(OTF_S_INTERNAL); return; }
+        if (w.jq_n >= w.jq_cap) { w.S.flag(OTF_S_INTERNAL); return false; }
         int32_t pos = w.jq_head + w.jq_n;
         if (pos >= w.jq_cap) pos -= w.jq_cap;
         JobEnt e; e.desc = d; e.job = j;
         w.jq[pos] = e;
         w.jq_n++;
     }
+    return false;
 }
 
 // Backend.maybe_speculate (backend.py:135-154)
@@ -161,7 +164,7 @@ __device__ void maybe_speculate(ExactWorld &w, int32_t seq, int32_t rank, int32_
     int32_t f = w.descs[d].flags;
     if (w.S.sc->cache_enabled && (f & D_CACHED)) { w.S.stat(OTF_ST_SKIP_CACHED)++; return; }
     if (f & D_INFLIGHT) { w.S.stat(OTF_ST_SKIP_INFLIGHT)++; return; }
-    enqueue_job(w, d, OTF_ORIGIN_SPECULATIVE);
+    if (enqueue_job(w, d, OTF_ORIGIN_SPECULATIVE)) { w.S.stat(OTF_ST_SKIP_OVERLOAD)++; return; }
     w.S.stat(OTF_ST_SPEC_ENQUEUED)++;
 }
 
@@ -223,6 +226,8 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
                 break;
             }
             client_select(w.S, c);
+            c.attempt = 0;                  // _fetch_with_retry (client.py:291-305)
+            c.backoff = sc.retry_backoff;
             c.requested = w.now;            // InProcessEndpoint.segment (client.py:219-221)
             c.pc = C_SEG_LAT;
             if (sc.latency > 0 && do_sleep(w, c, task, sc.latency)) return;
@@ -244,8 +249,22 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
                 c.path = OTF_PATH_WAITED;
                 add_waiter(w, d, cid);
                 return;
+            } else if (enqueue_job(w, d, OTF_ORIGIN_DEMAND)) {
+                // OverloadError: error record (server.py:70-73), then retry or give up
+                c.path = OTF_PATH_ERROR;
+                int32_t sz = c.size;
+                c.size = 0;
+                w.S.record_request(c, w.now);
+                c.size = sz;
+                if (c.attempt == sc.retries) {
+                    client_abort_session(w.S, c, w.now);
+                    c.pc = C_SESSION;
+                    break;
+                }
+                c.pc = C_RETRY;
+                if (do_sleep(w, c, task, c.backoff)) return;
+                break;
             } else {
-                enqueue_job(w, d, OTF_ORIGIN_DEMAND);
                 maybe_speculate(w, c.seq, c.rank, c.index);
                 c.path = OTF_PATH_TRANSCODED;
                 add_waiter(w, d, cid);
@@ -269,6 +288,13 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
             }
             c.pc = C_PLAYOUT;
             if (do_sleep(w, c, task, c.buf.level)) return;
+            break;
+        case C_RETRY:                       // after sleep(backoff): backoff *= 2, next attempt
+            c.backoff *= 2.0;
+            c.attempt++;
+            c.requested = w.now;
+            c.pc = C_SEG_LAT;
+            if (sc.latency > 0 && do_sleep(w, c, task, sc.latency)) return;
             break;
         case C_PLAYOUT:                     // client.py:272-280
             client_finish_session(w.S, c, w.now);

@@ -277,7 +277,10 @@ __device__ void lq_compact_warp(Win &w, int lane) {
     __syncwarp();
 }
 
-__device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backend.py:156-170
+// Backend._enqueue (backend.py:156-170); true on OverloadError (no idle worker,
+// queue at its bound: Queue.put_nowait raises QueueFull, sim.py:229-240).
+__device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
+    if (w.h->gq_n == 0 && w.S.sc->queue_bound > 0 && w.h->jq_n >= w.S.sc->queue_bound) return true;
     int32_t j = w.S.record_job(d, origin, w.now);
     w.dflags[d] |= D_INFLIGHT;
     w.wq_head[d] = -1;
@@ -293,13 +296,14 @@ __device__ void enqueue_job(Win &w, int32_t d, int32_t origin) {        // backe
         h->fq_n++;
         w.fq_n++;
     } else {
-        if (h->jq_n >= h->jq_cap) { w.S.flag(OTF_S_INTERNAL); return; }
+        if (h->jq_n >= h->jq_cap) { w.S.flag(OTF_S_INTERNAL); return false; }
         int32_t pos = h->jq_head + h->jq_n;
         if (pos >= h->jq_cap) pos -= h->jq_cap;
         JobEnt e; e.desc = d; e.job = j;
         w.jq[pos] = e;
         h->jq_n++;
     }
+    return false;
 }
 
 __device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, int32_t index) {  // backend.py:135-154
@@ -310,7 +314,7 @@ __device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, in
     uint8_t f = w.dflags[nd];
     if (w.cache_on && (f & D_CACHED)) { w.c_skip[3]++; return; }
     if (f & D_INFLIGHT) { w.c_skip[4]++; return; }
-    enqueue_job(w, nd, OTF_ORIGIN_SPECULATIVE);
+    if (enqueue_job(w, nd, OTF_ORIGIN_SPECULATIVE)) { w.c_skip[5]++; return; }
     w.c_spec++;
 }
 
@@ -418,8 +422,12 @@ __device__ void server_request(Win &w, int32_t cid, int32_t d, int32_t rank, int
         if (w.dflags[d] & D_INFLIGHT) {
             maybe_speculate(w, d, rank, seq, index);
             c.path = OTF_PATH_WAITED;
+        } else if (enqueue_job(w, d, OTF_ORIGIN_DEMAND)) {
+            c.path = OTF_PATH_ERROR;                   // OverloadError: error record (server.py:70-73)
+            respond(w, cid);
+            c.pc = C_SEG_ERR;
+            return;
         } else {
-            enqueue_job(w, d, OTF_ORIGIN_DEMAND);
             maybe_speculate(w, d, rank, seq, index);
             c.path = OTF_PATH_TRANSCODED;
         }
@@ -574,7 +582,7 @@ __device__ void client_local(Win &w, int32_t cid) {
 __device__ __forceinline__ void record_response(Win &w, const Client &c, double now) {
     Scn &S = w.S;
     const otf_scenario &sc = *S.sc;
-    int64_t size = S.size(c.desc);
+    int64_t size = c.path == OTF_PATH_ERROR ? 0 : S.size(c.desc);
     if (S.records) {
         int64_t r = c.req_slot;
         if (r < sc.req_cap) {
@@ -640,6 +648,8 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
                 break;
             }
             client_select(S, c);
+            c.attempt = 0;                             // _fetch_with_retry (client.py:291-305)
+            c.backoff = sc.retry_backoff;
             c.requested = now;
             c.desc = S.desc_id(c.seq, c.rank, c.index);
             delay = sc.latency;                        // request latency, then MediaServer.segment
@@ -662,6 +672,23 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             client_finish_session(S, c, now);
             c.pc = C_SESSION;
             continue;
+        case C_SEG_ERR:                                // OverloadError response
+            record_response(w, c, now);
+            if (c.attempt == sc.retries) {             // give up: the session is aborted
+                client_abort_session(S, c, now);
+                c.pc = C_SESSION;
+                continue;
+            }
+            delay = c.backoff;
+            next = C_RETRY;
+            break;
+        case C_RETRY:                                  // after sleep(backoff): backoff *= 2
+            c.backoff *= 2.0;
+            c.attempt++;
+            c.requested = now;
+            delay = sc.latency;
+            next = C_SEG_LAT;
+            break;
         default:
             return;
         }

@@ -23,6 +23,8 @@ enum {
     C_SEG_RESP,     // response available (windowed engine): record + transfer
     C_SEG_XFER,     // shaped segment transfer
     C_PLAYOUT,      // final sleep(level)
+    C_SEG_ERR,      // OverloadError response (windowed engine): record, then retry or abort
+    C_RETRY,        // sleep(backoff) before the next attempt (client.py:297-300)
     C_DONE,         // client_proc returned (now >= horizon)
     C_HUNG          // slept on an infinite delay; never wakes
 };
@@ -34,6 +36,8 @@ struct Client {                 // 144 B: moved as a whole per event
     int32_t req_id, size, req_slot;
     int32_t pc, seq, session, index, rank;
     int32_t path, desc, wait_next;
+    int32_t attempt;            // _fetch_with_retry attempt (client.py:291-305)
+    double backoff;
     uint8_t has_est, buf_live, sess_open, pad;
 };                              // the pick stream lives in a separate (cold) array
 

@@ -170,7 +170,7 @@ def order_sessions(a: dict) -> None:
 def parse_qoe(row: np.ndarray) -> dict:
     q = _lib.Qoe.from_buffer_copy(row.tobytes())
     return {
-        "lat_hist": list(q.lat_hist), "path_count": list(q.path_count), "stall_hist": list(q.stall_hist),
+        "lat_hist": list(q.lat_hist), "path_count": list(q.path_count)[:5], "stall_hist": list(q.stall_hist),
         "rank_count": list(q.rank_count), "n_requests": q.n_requests, "n_sessions": q.n_sessions,
         "n_segments": q.n_segments, "n_finished": q.n_finished, "n_started": q.n_started,
         "latency_sum": q.latency_sum, "stall_time_sum": q.stall_time_sum,

@@ -24,7 +24,7 @@ __all__ = ["SegmentDescriptor", "RequestRecord", "SegmentRecord", "SessionReport
            "quality_proportions", "INSTANT_EPSILON_S", "SCHEMAS", "read_csv"]
 
 INSTANT_EPSILON_S = 0.010
-PATHS = ("storage", "cache", "waited_inflight", "transcoded")
+PATHS = ("storage", "cache", "waited_inflight", "transcoded", "error")
 ORIGINS = ("demand", "speculative")
 OUTCOMES = ("pending", "completed", "dropped", "failed")
 

@@ -62,4 +62,11 @@ def golden_cases():
     out.append(("edge_two_clients", dataclasses.replace(base, variant="TCP", clients=2, workers=2, horizon_s=60.0,
                                                         seed=12)))
     out.append(("c5_small", W.c5(seed=1, clients=60, horizon_s=60.0)))
+    # bounded job queue: OverloadError -> error records, client retry/backoff, aborted sessions
+    out.append(("knob_qbound_tcp", dataclasses.replace(base, variant="TCP", clients=40, workers=1, queue_bound=2,
+                                                       horizon_s=150.0, arrival_rate_per_s=1.0, seed=13)))
+    out.append(("knob_qbound_abort", dataclasses.replace(base, variant="TC", clients=30, workers=1, queue_bound=1,
+                                                         horizon_s=150.0, arrival_rate_per_s=1.0, seed=14,
+                                                         client=ClientConfig(retries=1, retry_backoff_s=0.25))))
+    out.append(("knob_qbound_c2", W.c2(seed=15, horizon_s=90.0, queue_bound=3, variant="TCPF")))
     return out

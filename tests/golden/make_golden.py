@@ -31,7 +31,7 @@ from otfstream import orchestrator as ref_orch  # noqa: E402
 
 import cases  # noqa: E402
 
-PATHS = {"storage": 0, "cache": 1, "waited_inflight": 2, "transcoded": 3}
+PATHS = {"storage": 0, "cache": 1, "waited_inflight": 2, "transcoded": 3, "error": 4}
 ORIGINS = {"demand": 0, "speculative": 1}
 OUTCOMES = {"pending": 0, "completed": 1, "dropped": 2, "failed": 3}
 CSV_CASES = {"grid_c4_k4_t2_T", "edge_two_clients", "edge_short_horizon"}
