@@ -130,7 +130,7 @@ def test_histogram_mode_matches_records():
         assert q["n_requests"] == len(a["req_id"])
         assert q["n_sessions"] == len(a["sess_client"])
         assert q["n_segments"] == len(a["seg_index"])
-        assert q["path_count"] == [int((a["req_path"] == p).sum()) for p in range(4)]
+        assert q["path_count"] == [int((a["req_path"] == p).sum()) for p in range(5)]
         lat = a["req_response"] - a["req_arrival"]
         assert q["lat_hist"][0] == int((lat < 0.010).sum())
         assert sum(q["lat_hist"]) == len(lat)
