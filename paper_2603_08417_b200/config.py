@@ -401,6 +401,8 @@ class ExperimentConfig:
             raise ConfigError("the GPU engine runs the virtual clock only")
         if self.demand_priority:
             raise ConfigError("demand_priority is not supported by the GPU engine yet")
+        if not 0 <= self.client.retries < 255:
+            raise ConfigError("client.retries must be in [0, 255) for the GPU engine")
 
 
 def nominal_ladder_bytes(config: ExperimentConfig) -> float:

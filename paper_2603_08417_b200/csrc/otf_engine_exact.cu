@@ -227,7 +227,6 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
             }
             client_select(w.S, c);
             c.attempt = 0;                  // _fetch_with_retry (client.py:291-305)
-            c.backoff = sc.retry_backoff;
             c.requested = w.now;            // InProcessEndpoint.segment (client.py:219-221)
             c.pc = C_SEG_LAT;
             if (sc.latency > 0 && do_sleep(w, c, task, sc.latency)) return;
@@ -262,7 +261,7 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
                     break;
                 }
                 c.pc = C_RETRY;
-                if (do_sleep(w, c, task, c.backoff)) return;
+                if (do_sleep(w, c, task, ldexp(sc.retry_backoff, c.attempt))) return;
                 break;
             } else {
                 maybe_speculate(w, c.seq, c.rank, c.index);
@@ -290,7 +289,6 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
             if (do_sleep(w, c, task, c.buf.level)) return;
             break;
         case C_RETRY:                       // after sleep(backoff): backoff *= 2, next attempt
-            c.backoff *= 2.0;
             c.attempt++;
             c.requested = w.now;
             c.pc = C_SEG_LAT;

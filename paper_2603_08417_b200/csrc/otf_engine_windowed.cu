@@ -649,7 +649,6 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             }
             client_select(S, c);
             c.attempt = 0;                             // _fetch_with_retry (client.py:291-305)
-            c.backoff = sc.retry_backoff;
             c.requested = now;
             c.desc = S.desc_id(c.seq, c.rank, c.index);
             delay = sc.latency;                        // request latency, then MediaServer.segment
@@ -679,11 +678,10 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
                 c.pc = C_SESSION;
                 continue;
             }
-            delay = c.backoff;
+            delay = ldexp(sc.retry_backoff, c.attempt);
             next = C_RETRY;
             break;
         case C_RETRY:                                  // after sleep(backoff): backoff *= 2
-            c.backoff *= 2.0;
             c.attempt++;
             c.requested = now;
             delay = sc.latency;

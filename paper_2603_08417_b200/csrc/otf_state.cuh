@@ -36,9 +36,9 @@ struct Client {                 // 144 B: moved as a whole per event
     int32_t req_id, size, req_slot;
     int32_t pc, seq, session, index, rank;
     int32_t path, desc, wait_next;
-    int32_t attempt;            // _fetch_with_retry attempt (client.py:291-305)
-    double backoff;
-    uint8_t has_est, buf_live, sess_open, pad;
+    uint8_t has_est, buf_live, sess_open;
+    uint8_t attempt;            // _fetch_with_retry attempt (client.py:291-305); the backoff is
+                                // retry_backoff_s * 2^attempt (repeated doubling is exact)
 };                              // the pick stream lives in a separate (cold) array
 
 enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE };
