@@ -88,6 +88,8 @@ typedef struct otf_scenario {
     double period;                    /* BandwidthTrace.period (shared timestamps) */
     double grid_step;                 /* > 0 when starts[i] == i * grid_step exactly (bisect-free lookup) */
     double retry_backoff;             /* ClientConfig.retry_backoff_s */
+    int32_t demand_priority;          /* BackendPolicy.demand_priority (backend.py:103-105,174-184) */
+    int32_t pad2;
     int64_t off_sizes;                /* i64: [n_seq][n_ranks][max_nseg] segment bytes */
     int64_t off_bitrates;             /* i64: [n_ranks] */
     int64_t off_manifest;             /* i64: [n_seq] manifest JSON bytes */

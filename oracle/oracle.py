@@ -67,6 +67,7 @@ class Scenario(ctypes.Structure):
         ("zipf_cdf", _P(ctypes.c_double)), ("eps", _P(ctypes.c_double)),
         ("eps_per_worker", ctypes.c_int64),
         ("queue_bound", ctypes.c_int32), ("retries", ctypes.c_int32), ("retry_backoff", ctypes.c_double),
+        ("demand_priority", ctypes.c_int32), ("pad2", ctypes.c_int32),
     ]
 
 
@@ -243,6 +244,7 @@ class Prepared:
         sc.queue_bound = int(cfg.queue_bound)
         sc.retries = int(cfg.client.retries)
         sc.retry_backoff = float(cfg.client.retry_backoff_s)
+        sc.demand_priority = int(bool(cfg.demand_priority))
         self.sc = sc
 
     def sizes(self):

@@ -210,7 +210,7 @@ enum {
     C_START = 0, C_ARRIVED, C_SESSION, C_MAN_LAT, C_MAN_XFER, C_INDEX_HEAD, C_TARGET_WAIT,
     C_SEG_LAT, C_SEG_WAIT, C_SEG_XFER, C_PLAYOUT, C_DONE, C_HUNG, C_RETRY
 };
-enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE };
+enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE, W_WOKEN };
 
 typedef struct {
     int pc;
@@ -253,6 +253,9 @@ typedef struct {
     /* job FIFO + getter FIFO (sim.py:215-247) */
     int32_t *jq; int64_t jq_head, jq_n, jq_cap;
     int32_t *gq; int64_t gq_head, gq_n;
+    /* demand-priority mode (backend.py:103-105,160-184): speculative FIFO + wakeup tokens */
+    int32_t *sq; int64_t sq_head, sq_n;
+    int64_t tokens;
     int64_t req_counter;
     const double *arrivals;
     int status;
@@ -364,7 +367,14 @@ static void set_overflow(world_t *w) { w->status = ORACLE_EOVERFLOW; }
  * its bound and no idle worker: Queue.put_nowait raises QueueFull, sim.py:229-240). */
 static int enqueue_job(world_t *w, int32_t d, int32_t origin) {
     oracle_outputs *o = w->out;
-    if (w->gq_n == 0 && w->sc->queue_bound > 0 && w->jq_n >= w->sc->queue_bound) return 1;
+    const int prio = w->sc->demand_priority;
+    if (prio) {
+        /* workers never wait on the job queues in this mode, so a bounded demand queue
+         * overflows on its own length (sim.py:238-239) */
+        if (origin == ORIGIN_DEMAND && w->sc->queue_bound > 0 && w->jq_n >= w->sc->queue_bound) return 1;
+    } else if (w->gq_n == 0 && w->sc->queue_bound > 0 && w->jq_n >= w->sc->queue_bound) {
+        return 1;
+    }
     int64_t j = o->n_job++;
     if (j < o->job_cap) {
         int32_t per_seq = w->sc->n_ranks * w->sc->max_nseg;
@@ -384,6 +394,25 @@ static int enqueue_job(world_t *w, int32_t d, int32_t origin) {
     w->inflight[d] = 1;
     w->wq_head[d] = -1;
     w->wq_tail[d] = -1;
+    if (prio) {
+        if (origin == ORIGIN_SPEC) {
+            w->sq[(w->sq_head + w->sq_n) % w->jq_cap] = (int32_t)j;
+            w->sq_n++;
+        } else {
+            w->jq[(w->jq_head + w->jq_n) % w->jq_cap] = (int32_t)j;
+            w->jq_n++;
+        }
+        /* _wakeup.put_nowait(None, force=True): wake the first idle worker or leave a token */
+        if (w->gq_n > 0) {
+            int32_t wid = w->gq[w->gq_head];
+            w->gq_head = (w->gq_head + 1) % w->n_workers;
+            w->gq_n--;
+            ready_push(w, wid, -1);
+        } else {
+            w->tokens++;
+        }
+        return 0;
+    }
     /* Queue.put_nowait: hand to the first waiting getter, else append. */
     if (w->gq_n > 0) {
         int32_t wid = w->gq[w->gq_head];
@@ -733,8 +762,26 @@ static void worker_step(world_t *w, int32_t wid, int64_t value) {
     int32_t job = (int32_t)value;
     for (;;) {
         switch (k->pc) {
+        case W_WOKEN:
         case W_START:
         case W_NEXT:
+            if (sc->demand_priority) {       /* Backend._next_job, priority mode (backend.py:174-184) */
+                if (w->jq_n > 0) {
+                    job = w->jq[w->jq_head]; w->jq_head = (w->jq_head + 1) % w->jq_cap; w->jq_n--;
+                    k->pc = W_GOT;
+                    break;
+                }
+                if (w->sq_n > 0) {
+                    job = w->sq[w->sq_head]; w->sq_head = (w->sq_head + 1) % w->jq_cap; w->sq_n--;
+                    k->pc = W_GOT;
+                    break;
+                }
+                if (w->tokens > 0) { w->tokens--; k->pc = W_NEXT; break; }   /* stale wakeup: no yield */
+                w->gq[(w->gq_head + w->gq_n) % w->n_workers] = wid;
+                w->gq_n++;
+                k->pc = W_WOKEN;
+                return;
+            }
             if (w->jq_n > 0) { /* Queue.get on a non-empty queue does not yield */
                 job = w->jq[w->jq_head];
                 w->jq_head = (w->jq_head + 1) % w->jq_cap;
@@ -900,6 +947,7 @@ int oracle_run(const oracle_scenario *sc, oracle_outputs *out) {
     w->jq_cap = w->n_desc + 1;   /* single-flight: <= one queued job per descriptor */
     w->jq = (int32_t *)malloc(sizeof(int32_t) * (size_t)w->jq_cap);
     w->gq = (int32_t *)malloc(sizeof(int32_t) * (size_t)w->n_workers);
+    w->sq = (int32_t *)malloc(sizeof(int32_t) * (size_t)w->jq_cap);
 
     /* spawn order: K workers (backend.py:110) then N clients (orchestrator.py:350-351) */
     for (int32_t k = 0; k < w->n_workers; k++) ready_push(w, k, 0);
@@ -936,6 +984,6 @@ int oracle_run(const oracle_scenario *sc, oracle_outputs *out) {
     free(w->sizes); free(w->seg_count); free(ts); free(vals); free(pb);
     free(w->cl); free(w->wk); free(w->heap); free(w->ready);
     free(w->present); free(w->inflight); free(w->lru_prev); free(w->lru_next);
-    free(w->wq_head); free(w->wq_tail); free(w->jq); free(w->gq); free(arr);
+    free(w->wq_head); free(w->wq_tail); free(w->jq); free(w->gq); free(w->sq); free(arr);
     return w->status;
 }

@@ -42,6 +42,7 @@ typedef struct {
     int64_t eps_per_worker;
     int32_t queue_bound, retries;   /* BackendPolicy.queue_bound, ClientConfig.retries */
     double retry_backoff;           /* ClientConfig.retry_backoff_s */
+    int32_t demand_priority, pad2;  /* BackendPolicy.demand_priority */
 } oracle_scenario;
 
 typedef struct {

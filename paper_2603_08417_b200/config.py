@@ -399,8 +399,6 @@ class ExperimentConfig:
             raise ConfigError("netem.trace_dir (CSV traces) is not supported by the GPU engine yet")
         if self.clock != "virtual":
             raise ConfigError("the GPU engine runs the virtual clock only")
-        if self.demand_priority:
-            raise ConfigError("demand_priority is not supported by the GPU engine yet")
         if not 0 <= self.client.retries < 255:
             raise ConfigError("client.retries must be in [0, 255) for the GPU engine")
 

@@ -22,10 +22,11 @@ struct ExactWorld {
     Timer *heap;
     ReadyEnt *ready;
     Desc *descs;
-    JobEnt *jq;
+    JobEnt *jq, *sq;                        // demand / speculative job FIFOs
     int32_t *gq;
     int32_t heap_n, rq_head, rq_n, rq_cap;
     int32_t jq_head, jq_n, jq_cap, gq_head, gq_n;
+    int32_t sq_head, sq_n, tokens;          // demand-priority mode (backend.py:103-105)
     uint32_t tick;
     double now;
 };
@@ -133,11 +134,35 @@ __device__ void cache_put(ExactWorld &w, int32_t d) {
 // Backend._enqueue + Queue.put_nowait (backend.py:156-170, sim.py:229-240).
 // Returns true on OverloadError: no idle worker and the queue at its bound.
 __device__ bool enqueue_job(ExactWorld &w, int32_t d, int32_t origin) {
-    if (w.gq_n == 0 && w.S.sc->queue_bound > 0 && w.jq_n >= w.S.sc->queue_bound) return true;
+    const bool prio = w.S.sc->demand_priority != 0;
+    if (prio) {                             // workers never wait on the job queues in this mode
+        if (origin == OTF_ORIGIN_DEMAND && w.S.sc->queue_bound > 0 && w.jq_n >= w.S.sc->queue_bound) return true;
+    } else if (w.gq_n == 0 && w.S.sc->queue_bound > 0 && w.jq_n >= w.S.sc->queue_bound) {
+        return true;
+    }
     int32_t j = w.S.record_job(d, origin, w.now);
     Desc &D = w.descs[d];
     D.flags |= D_INFLIGHT;
     D.wq_head = D.wq_tail = -1;
+    if (prio) {                             // separate FIFOs + _wakeup.put_nowait(None, force=True)
+        JobEnt e; e.desc = d; e.job = j;
+        if (origin == OTF_ORIGIN_SPECULATIVE) {
+            int32_t pos = w.sq_head + w.sq_n; if (pos >= w.jq_cap) pos -= w.jq_cap;
+            w.sq[pos] = e; w.sq_n++;
+        } else {
+            int32_t pos = w.jq_head + w.jq_n; if (pos >= w.jq_cap) pos -= w.jq_cap;
+            w.jq[pos] = e; w.jq_n++;
+        }
+        if (w.gq_n > 0) {
+            int32_t wid = w.gq[w.gq_head];
+            w.gq_head = (w.gq_head + 1 == w.S.sc->n_workers) ? 0 : w.gq_head + 1;
+            w.gq_n--;
+            ready_push(w, wid, -1, -1);
+        } else {
+            w.tokens++;
+        }
+        return false;
+    }
     if (w.gq_n > 0) {                         // hand to the first waiting getter
         int32_t wid = w.gq[w.gq_head];
         w.gq_head = (w.gq_head + 1 == w.S.sc->n_workers) ? 0 : w.gq_head + 1;
@@ -310,8 +335,26 @@ __device__ void worker_step(ExactWorld &w, int32_t wid, int32_t desc, int32_t jo
     Worker &k = w.wk[wid];
     for (;;) {
         switch (k.pc) {
+        case W_WOKEN:
         case W_START:
         case W_NEXT:
+            if (sc.demand_priority) {       // Backend._next_job, priority mode (backend.py:174-184)
+                if (w.jq_n > 0 || w.sq_n > 0) {
+                    JobEnt e;
+                    if (w.jq_n > 0) { e = w.jq[w.jq_head]; w.jq_head = (w.jq_head + 1 == w.jq_cap) ? 0 : w.jq_head + 1; w.jq_n--; }
+                    else { e = w.sq[w.sq_head]; w.sq_head = (w.sq_head + 1 == w.jq_cap) ? 0 : w.sq_head + 1; w.sq_n--; }
+                    desc = e.desc; job = e.job;
+                    k.pc = W_GOT;
+                    break;
+                }
+                if (w.tokens > 0) { w.tokens--; k.pc = W_NEXT; break; }   // stale wakeup: no yield
+                int32_t pos = w.gq_head + w.gq_n;
+                if (pos >= sc.n_workers) pos -= sc.n_workers;
+                w.gq[pos] = wid;
+                w.gq_n++;
+                k.pc = W_WOKEN;
+                return;
+            }
             if (w.jq_n > 0) {               // Queue.get on a non-empty queue: no yield
                 JobEnt e = w.jq[w.jq_head];
                 w.jq_head = (w.jq_head + 1 == w.jq_cap) ? 0 : w.jq_head + 1;
@@ -387,6 +430,8 @@ __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
     w.ready = (ReadyEnt *)(base + L.ready);
     w.descs = (Desc *)(base + L.descs);
     w.jq = (JobEnt *)(base + L.jobq);
+    w.sq = (JobEnt *)(base + L.specq);
+    w.sq_head = 0; w.sq_n = 0; w.tokens = 0;
     w.gq = (int32_t *)(base + L.getq);
     w.heap_n = 0; w.rq_head = 0; w.rq_n = 0;
     w.rq_cap = sc.n_clients + sc.n_workers + 1;

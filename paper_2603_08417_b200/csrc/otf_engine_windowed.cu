@@ -63,6 +63,7 @@ struct WinHeader {
     int32_t fq_w[MAXK], fq_d[MAXK], fq_j[MAXK];
     int32_t gq_head, gq_n, fq_head, fq_n;
     int32_t jq_head, jq_n, jq_cap;
+    int32_t sq_head, sq_n, tokens;       // demand-priority mode: speculative FIFO, wakeup tokens
     int32_t n_list, n_blist, n_ties;
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
@@ -99,7 +100,7 @@ __host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {   // power of t
 }
 
 struct WinGlobalLayout {
-    int64_t clients, picks, blist, wq_head, wq_tail, jobq, lstamp, lq, total;
+    int64_t clients, picks, blist, wq_head, wq_tail, jobq, specq, lstamp, lq, total;
 };
 
 __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
@@ -111,6 +112,7 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
+    L.specq = o;   o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.lstamp = o;  o += align256((int64_t)sizeof(uint32_t) * n_desc);
     L.lq = o;      o += align256((int64_t)sizeof(LqEnt) * 2 * lq_capacity(n_desc));
     L.total = o;
@@ -138,7 +140,7 @@ struct Win {
     uint8_t *dflags;
     Client *cl;
     int32_t *blist, *wq_head, *wq_tail;
-    JobEnt *jq;
+    JobEnt *jq, *sq;
     double W, invW, H, E, now;
     int32_t k;
     // lane 0's register copies of the hot server counters during phase A
@@ -280,12 +282,40 @@ __device__ void lq_compact_warp(Win &w, int lane) {
 // Backend._enqueue (backend.py:156-170); true on OverloadError (no idle worker,
 // queue at its bound: Queue.put_nowait raises QueueFull, sim.py:229-240).
 __device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
-    if (w.h->gq_n == 0 && w.S.sc->queue_bound > 0 && w.h->jq_n >= w.S.sc->queue_bound) return true;
+    WinHeader *h = w.h;
+    const bool prio = w.S.sc->demand_priority != 0;
+    if (prio) {                                        // workers never wait on the job queues
+        if (origin == OTF_ORIGIN_DEMAND && w.S.sc->queue_bound > 0 && h->jq_n >= w.S.sc->queue_bound) return true;
+    } else if (h->gq_n == 0 && w.S.sc->queue_bound > 0 && h->jq_n >= w.S.sc->queue_bound) {
+        return true;
+    }
     int32_t j = w.S.record_job(d, origin, w.now);
     w.dflags[d] |= D_INFLIGHT;
     w.wq_head[d] = -1;
     w.wq_tail[d] = -1;
-    WinHeader *h = w.h;
+    if (prio) {                                        // separate FIFOs + _wakeup.put_nowait(None, force=True)
+        JobEnt e; e.desc = d; e.job = j;
+        if (origin == OTF_ORIGIN_SPECULATIVE) {
+            int32_t pos = h->sq_head + h->sq_n; if (pos >= h->jq_cap) pos -= h->jq_cap;
+            w.sq[pos] = e; h->sq_n++;
+        } else {
+            int32_t pos = h->jq_head + h->jq_n; if (pos >= h->jq_cap) pos -= h->jq_cap;
+            w.jq[pos] = e; h->jq_n++;
+        }
+        if (h->gq_n > 0) {                             // wake the first idle worker (ready hop)
+            int32_t wid = h->gq[h->gq_head];
+            h->gq_head = (h->gq_head + 1 == w.S.sc->n_workers) ? 0 : h->gq_head + 1;
+            h->gq_n--;
+            int32_t pos = h->fq_head + h->fq_n;
+            if (pos >= MAXK) pos -= MAXK;
+            h->fq_w[pos] = wid; h->fq_d[pos] = -1; h->fq_j[pos] = -1;
+            h->fq_n++;
+            w.fq_n++;
+        } else {
+            h->tokens++;
+        }
+        return false;
+    }
     if (h->gq_n > 0) {                                 // Queue.put_nowait -> first getter
         int32_t wid = h->gq[h->gq_head];
         h->gq_head = (h->gq_head + 1 == w.S.sc->n_workers) ? 0 : h->gq_head + 1;
@@ -348,6 +378,40 @@ __device__ __forceinline__ void add_waiter(Win &w, int32_t d, int32_t cid) {
     w.wq_tail[d] = cid;
 }
 
+// Backend._next_job (backend.py:174-184): a job now (no yield), or the worker
+// becomes an idle getter (FIFO) and false is returned.
+__device__ bool take_job(Win &w, int32_t wid, int32_t &d, int32_t &j) {
+    WinHeader *h = w.h;
+    const otf_scenario &sc = *w.S.sc;
+    for (;;) {
+        if (h->jq_n > 0) {                             // Queue.get on a non-empty queue: no yield
+            JobEnt e = w.jq[h->jq_head];
+            h->jq_head = (h->jq_head + 1 == h->jq_cap) ? 0 : h->jq_head + 1;
+            h->jq_n--;
+            d = e.desc; j = e.job;
+            return true;
+        }
+        if (sc.demand_priority) {
+            if (h->sq_n > 0) {                         // speculative jobs only when no demand waits
+                JobEnt e = w.sq[h->sq_head];
+                h->sq_head = (h->sq_head + 1 == h->jq_cap) ? 0 : h->sq_head + 1;
+                h->sq_n--;
+                d = e.desc; j = e.job;
+                return true;
+            }
+            if (h->tokens > 0) { h->tokens--; continue; }   // stale wakeup token: no yield
+        }
+        int32_t pos = h->gq_head + h->gq_n;
+        if (pos >= sc.n_workers) pos -= sc.n_workers;
+        h->gq[pos] = wid;
+        h->gq_n++;
+        h->wk[wid].pc = W_GOT;
+        h->wk[wid].win = WIN_NONE;
+        w.wdirty = true;
+        return false;
+    }
+}
+
 // Backend._worker_loop body from "job dequeued" until the worker yields.
 __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
     WinHeader *h = w.h;
@@ -374,22 +438,7 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
             w.wdirty = true;
             return;
         }
-        // next job: Queue.get on a non-empty queue does not yield (sim.py:242-244)
-        if (h->jq_n > 0) {
-            JobEnt e = w.jq[h->jq_head];
-            h->jq_head = (h->jq_head + 1 == h->jq_cap) ? 0 : h->jq_head + 1;
-            h->jq_n--;
-            d = e.desc; j = e.job;
-            continue;
-        }
-        int32_t pos = h->gq_head + h->gq_n;
-        if (pos >= sc.n_workers) pos -= sc.n_workers;
-        h->gq[pos] = wid;
-        h->gq_n++;
-        h->wk[wid].pc = W_GOT;
-        h->wk[wid].win = WIN_NONE;
-        w.wdirty = true;
-        return;
+        if (!take_job(w, wid, d, j)) return;
     }
 }
 
@@ -401,6 +450,7 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
         h->fq_n--;
         w.fq_n--;
         w.c_ready++;
+        if (j < 0 && !take_job(w, wid, d, j)) continue;   // priority mode: a wakeup, not a job
         worker_run(w, wid, d, j);
     }
 }
@@ -445,20 +495,8 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
     w.S.job_finished(j, w.now);
     if (w.cache_on) cache_put(w, d, k.size);
     resolve(w, d);
-    // next job
-    WinHeader *h = w.h;
-    if (h->jq_n > 0) {
-        JobEnt e = w.jq[h->jq_head];
-        h->jq_head = (h->jq_head + 1 == h->jq_cap) ? 0 : h->jq_head + 1;
-        h->jq_n--;
-        worker_run(w, wid, e.desc, e.job);
-    } else {
-        int32_t pos = h->gq_head + h->gq_n;
-        if (pos >= w.S.sc->n_workers) pos -= w.S.sc->n_workers;
-        h->gq[pos] = wid;
-        h->gq_n++;
-        k.pc = W_GOT;
-    }
+    int32_t nd, nj;                                    // next job
+    if (take_job(w, wid, nd, nj)) worker_run(w, wid, nd, nj);
 }
 
 // Phase A: replay the window's server events in (time, creation, tick) order.
@@ -853,6 +891,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     w.wq_head = (int32_t *)(g + L.wq_head);
     w.wq_tail = (int32_t *)(g + L.wq_tail);
     w.jq = (JobEnt *)(g + L.jobq);
+    w.sq = (JobEnt *)(g + L.specq);
     // counters, QoE and small tables live in shared memory
     w.S.st = &h->st;
     w.S.stats = h->stats;
@@ -874,6 +913,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         qoe_zero(&h->qa, 0, 1);
         h->gq_head = 0; h->gq_n = K; h->fq_head = 0; h->fq_n = 0;
         h->jq_head = 0; h->jq_n = 0; h->jq_cap = (int32_t)(D + 1);
+        h->sq_head = 0; h->sq_n = 0; h->tokens = 0;
         h->n_list = 0; h->n_blist = 0; h->wseq = 0;
         h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
         h->arr_next = 0;

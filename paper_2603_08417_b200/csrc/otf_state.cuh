@@ -41,7 +41,7 @@ struct Client {                 // 144 B: moved as a whole per event
                                 // retry_backoff_s * 2^attempt (repeated doubling is exact)
 };                              // the pick stream lives in a separate (cold) array
 
-enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE };
+enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE, W_WOKEN };
 
 struct Worker {
     int32_t pc, desc, job, pad;
@@ -72,7 +72,7 @@ struct JobEnt {
 OTF_HD int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
 struct ExactLayout {
-    int64_t state, clients, picks, workers, heap, ready, descs, jobq, getq, total;
+    int64_t state, clients, picks, workers, heap, ready, descs, jobq, specq, getq, total;
 };
 
 OTF_HD ExactLayout exact_layout(int32_t n_clients, int32_t n_workers, int64_t n_desc) {
@@ -88,6 +88,7 @@ OTF_HD ExactLayout exact_layout(int32_t n_clients, int32_t n_workers, int64_t n_
     L.ready = o;   o += align256((int64_t)sizeof(ReadyEnt) * (n_tasks + 1));
     L.descs = o;   o += align256((int64_t)sizeof(Desc) * n_desc);
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
+    L.specq = o;   o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.getq = o;    o += align256((int64_t)sizeof(int32_t) * n_workers);
     L.total = o;
     return L;

@@ -286,6 +286,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.queue_bound = int(cfg.queue_bound)
         sc.retries = int(cfg.client.retries)
         sc.retry_backoff = float(cfg.client.retry_backoff_s)
+        sc.demand_priority = int(bool(cfg.demand_priority))
         sc.off_sizes, sc.off_bitrates, sc.off_manifest, sc.off_segcount = o_sizes, o_bitrates, o_man, o_counts
         sc.off_seqdur, sc.off_segdur, sc.off_rho, sc.off_zipf = o_seqdur, o_segdur, o_rho, o_zipf
         sc.off_starts, sc.off_values, sc.off_pbits = tt["starts"], tt["values"], tt["pbits"]

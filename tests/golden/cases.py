@@ -69,4 +69,11 @@ def golden_cases():
                                                          horizon_s=150.0, arrival_rate_per_s=1.0, seed=14,
                                                          client=ClientConfig(retries=1, retry_backoff_s=0.25))))
     out.append(("knob_qbound_c2", W.c2(seed=15, horizon_s=90.0, queue_bound=3, variant="TCPF")))
+    # demand-priority queues (speculative jobs only when no demand job waits)
+    out.append(("knob_prio_tcp", dataclasses.replace(base, variant="TCP", clients=30, workers=2, demand_priority=True,
+                                                     horizon_s=150.0, arrival_rate_per_s=1.0, seed=16)))
+    out.append(("knob_prio_qbound", dataclasses.replace(base, variant="TCPF", clients=40, workers=1,
+                                                        demand_priority=True, queue_bound=2, horizon_s=150.0,
+                                                        arrival_rate_per_s=1.0, seed=17)))
+    out.append(("knob_prio_c3", W.c3(seed=18, fraction=0.2, horizon_s=90.0, demand_priority=True)))
     return out
