@@ -90,6 +90,9 @@ typedef struct otf_scenario {
     double retry_backoff;             /* ClientConfig.retry_backoff_s */
     int32_t demand_priority;          /* BackendPolicy.demand_priority (backend.py:103-105,174-184) */
     int32_t pad2;
+    int64_t off_tr_i;                 /* CSV traces (netem.trace_dir): i64 [n_clients][3] = starts offset,
+                                         values offset, samples (f64 pool); -1 = synthetic traces */
+    int64_t off_tr_f;                 /* f64 [n_clients][3] = period, period bits, grid step */
     int64_t off_sizes;                /* i64: [n_seq][n_ranks][max_nseg] segment bytes */
     int64_t off_bitrates;             /* i64: [n_ranks] */
     int64_t off_manifest;             /* i64: [n_seq] manifest JSON bytes */

@@ -68,6 +68,9 @@ class Scenario(ctypes.Structure):
         ("eps_per_worker", ctypes.c_int64),
         ("queue_bound", ctypes.c_int32), ("retries", ctypes.c_int32), ("retry_backoff", ctypes.c_double),
         ("demand_priority", ctypes.c_int32), ("pad2", ctypes.c_int32),
+        ("tr_starts", _P(ctypes.c_double)), ("tr_values", _P(ctypes.c_double)),
+        ("tr_period", _P(ctypes.c_double)), ("tr_pbits", _P(ctypes.c_double)),
+        ("tr_off", _P(ctypes.c_int64)), ("tr_n", _P(ctypes.c_int32)),
     ]
 
 
@@ -141,6 +144,35 @@ def zipf_cdf(n: int, s: float) -> np.ndarray:
     return np.array([x / acc for x in c], dtype=np.float64)
 
 
+def load_trace_csv(path):
+    """netem.load_trace + BandwidthTrace.__init__ (netem.py:148-161, 39-64), restated."""
+    import csv
+    import statistics
+    samples = []
+    with open(path, newline="", encoding="utf-8") as fh:
+        for row in csv.reader(fh):
+            if not row or row[0].lstrip().startswith("#"):
+                continue
+            try:
+                ts, kbps = float(row[0]), float(row[1])
+            except ValueError:
+                continue
+            samples.append((ts, kbps * 1000.0))
+    if not samples:
+        raise ValueError(f"no samples in trace file {path}")
+    ts = [t for t, _ in samples]
+    if any(b - a <= 0 for a, b in zip(ts, ts[1:])) or ts[0] < 0 or any(bw < 0 for _, bw in samples):
+        raise ValueError(f"invalid trace {path}")
+    starts = list(ts)
+    values = [float(bw) for _, bw in samples]
+    if starts[0] > 0:
+        starts[0] = 0.0
+    gaps = [b - a for a, b in zip(ts, ts[1:])]
+    period = ts[-1] + (statistics.median(gaps) if gaps else 1.0)
+    pbits = sum(v * ((starts[i + 1] if i + 1 < len(starts) else period) - starts[i]) for i, v in enumerate(values))
+    return starts, values, period, pbits
+
+
 def _attr(cfg, name, default):
     return getattr(cfg, name, default)
 
@@ -191,8 +223,22 @@ class Prepared:
             t += ne.step_s
         self.n_samples = nsamp
         self.trace_normals = np.empty((N, nsamp + 1), dtype=np.float64)
-        for c in range(N):
-            self.trace_normals[c] = _gen([cfg.seed, 2, c]).standard_normal(nsamp + 1)
+        self.csv = None
+        if ne.trace_dir:                               # orchestrator.py:243-253
+            files = sorted(os.path.join(ne.trace_dir, f) for f in os.listdir(ne.trace_dir) if f.endswith(".csv"))
+            order = _gen([cfg.seed, 2]).permutation(len(files))
+            tabs = [load_trace_csv(f) for f in files]
+            st, vv, off, nn, per, pb = [], [], [], [], [], []
+            pos = 0
+            for c in range(N):
+                s_, v_, p_, b_ = tabs[order[c % len(files)]]
+                off.append(pos); nn.append(len(s_)); per.append(p_); pb.append(b_)
+                st.extend(s_); vv.extend(v_); pos += len(s_)
+            self.csv = (np.array(st), np.array(vv), np.array(per), np.array(pb),
+                        np.array(off, dtype=np.int64), np.array(nn, dtype=np.int32))
+        else:
+            for c in range(N):
+                self.trace_normals[c] = _gen([cfg.seed, 2, c]).standard_normal(nsamp + 1)
         pop = _attr(cfg, "popularity", "uniform")
         self.zipf = zipf_cdf(n_seq, float(_attr(cfg, "zipf_exponent", 0.8))) \
             if pop == "zipf" else np.zeros(n_seq)
@@ -245,6 +291,11 @@ class Prepared:
         sc.retries = int(cfg.client.retries)
         sc.retry_backoff = float(cfg.client.retry_backoff_s)
         sc.demand_priority = int(bool(cfg.demand_priority))
+        if self.csv is not None:
+            st, vv, per, pb, off, nn = self.csv
+            sc.tr_starts, sc.tr_values = _ptr(st, ctypes.c_double), _ptr(vv, ctypes.c_double)
+            sc.tr_period, sc.tr_pbits = _ptr(per, ctypes.c_double), _ptr(pb, ctypes.c_double)
+            sc.tr_off, sc.tr_n = _ptr(off, ctypes.c_int64), _ptr(nn, ctypes.c_int32)
         self.sc = sc
 
     def sizes(self):

@@ -227,8 +227,9 @@ typedef struct {
     double backoff;
     int32_t wait_next;
     pcg64_t picks;
-    const double *values;
-    double pbits;
+    const double *values, *starts;   /* the client's BandwidthTrace (netem.py:39-64) */
+    double pbits, period;
+    int32_t n_samples;
 } client_t;
 
 typedef struct { int pc; int32_t job; int64_t eps_pos; } worker_t;
@@ -523,17 +524,17 @@ static int32_t select_quality(const oracle_scenario *sc, double level, int32_t c
 }
 
 /* BandwidthTrace._drain_from (netem.py:77-95) */
-static void drain_from(const world_t *w, const double *values, double phase, double bits,
+static void drain_from(const client_t *c, const double *values, double phase, double bits,
                        double *spent_out, double *left_out) {
-    const double *st = w->starts;
-    int32_t n = w->n_samples;
+    const double *st = c->starts;
+    int32_t n = c->n_samples;
     int32_t lo = 0, hi = n;              /* bisect_right */
     while (lo < hi) { int32_t mid = (lo + hi) / 2; if (phase < st[mid]) hi = mid; else lo = mid + 1; }
     int32_t i = lo - 1;
     if (i < 0) i = 0;
     double spent = 0.0, pos = phase;
     for (; i < n; i++) {
-        double seg_end = (i + 1 < n) ? st[i + 1] : w->period;
+        double seg_end = (i + 1 < n) ? st[i + 1] : c->period;
         double width = seg_end - pos;
         if (width > 0) {
             double v = values[i];
@@ -555,14 +556,14 @@ static double completion_time(const world_t *w, const client_t *c, double start,
     if (bits <= 0) return start;
     if (c->pbits <= 0) return INFINITY;
     double t = start, spent, left;
-    drain_from(w, c->values, fmod(start, w->period), bits, &spent, &left);
+    drain_from(c, c->values, fmod(start, c->period), bits, &spent, &left);
     t += spent;
     if (left <= 0) return t;
     double whole = floor(left / c->pbits);
-    t += whole * w->period;
+    t += whole * c->period;
     left -= whole * c->pbits;
     if (left <= 0) return t;
-    drain_from(w, c->values, 0.0, left, &spent, &left);
+    drain_from(c, c->values, 0.0, left, &spent, &left);
     return t + spent;
 }
 
@@ -911,15 +912,18 @@ int oracle_run(const oracle_scenario *sc, oracle_outputs *out) {
     w->seg_count = (int32_t *)malloc(sizeof(int32_t) * (size_t)sc->n_seq);
     oracle_segment_sizes(sc, w->sizes, w->seg_count);
 
-    /* traces (one per client; timestamps shared) */
-    w->n_samples = sc->n_samples;
-    double *ts = (double *)malloc(sizeof(double) * (size_t)sc->n_samples);
-    oracle_sample_times(sc->trace_duration, sc->trace_step, ts, sc->n_samples);
-    if (ts[0] > 0) ts[0] = 0.0;
-    w->starts = ts;
-    double *vals = (double *)malloc(sizeof(double) * (size_t)sc->n_samples * (size_t)sc->n_clients);
+    /* traces: synthetic (one per client, timestamps shared) unless CSV tables are given */
+    const int csv = sc->tr_off != NULL;
+    w->n_samples = csv ? 1 : sc->n_samples;
+    double *ts = (double *)malloc(sizeof(double) * (size_t)w->n_samples);
+    double *vals = (double *)malloc(sizeof(double) * (size_t)w->n_samples * (size_t)(csv ? 1 : sc->n_clients));
     double *pb = (double *)malloc(sizeof(double) * (size_t)sc->n_clients);
-    oracle_build_traces(sc, vals, pb, &w->period);
+    if (!csv) {
+        oracle_sample_times(sc->trace_duration, sc->trace_step, ts, sc->n_samples);
+        if (ts[0] > 0) ts[0] = 0.0;
+        oracle_build_traces(sc, vals, pb, &w->period);
+    }
+    w->starts = ts;
 
     /* arrival offsets: list(np.cumsum(exponential draws)) (orchestrator.py:265-268) */
     double *arr = (double *)malloc(sizeof(double) * (size_t)sc->n_clients);
@@ -930,9 +934,21 @@ int oracle_run(const oracle_scenario *sc, oracle_outputs *out) {
     w->cl = (client_t *)calloc((size_t)sc->n_clients, sizeof(client_t));
     w->wk = (worker_t *)calloc((size_t)sc->n_workers, sizeof(worker_t));
     for (int32_t c = 0; c < sc->n_clients; c++) {
-        w->cl[c].values = vals + (int64_t)c * sc->n_samples;
-        w->cl[c].pbits = pb[c];
-        w->cl[c].wait_next = -1;
+        client_t *cl = &w->cl[c];
+        if (csv) {
+            cl->starts = sc->tr_starts + sc->tr_off[c];
+            cl->values = sc->tr_values + sc->tr_off[c];
+            cl->n_samples = sc->tr_n[c];
+            cl->period = sc->tr_period[c];
+            cl->pbits = sc->tr_pbits[c];
+        } else {
+            cl->starts = ts;
+            cl->values = vals + (int64_t)c * sc->n_samples;
+            cl->n_samples = sc->n_samples;
+            cl->period = w->period;
+            cl->pbits = pb[c];
+        }
+        cl->wait_next = -1;
     }
     w->heap = (timer_ent *)malloc(sizeof(timer_ent) * (size_t)(w->n_tasks + 1));
     w->rq_cap = w->n_tasks + 1;

@@ -43,6 +43,10 @@ typedef struct {
     int32_t queue_bound, retries;   /* BackendPolicy.queue_bound, ClientConfig.retries */
     double retry_backoff;           /* ClientConfig.retry_backoff_s */
     int32_t demand_priority, pad2;  /* BackendPolicy.demand_priority */
+    /* CSV traces (netem.trace_dir): per-client trace tables, else NULL (synthetic traces) */
+    const double *tr_starts, *tr_values, *tr_period, *tr_pbits;  /* tables; [N] period, pbits */
+    const int64_t *tr_off;          /* [N] offset of the client's trace in tr_starts/tr_values */
+    const int32_t *tr_n;            /* [N] samples */
 } oracle_scenario;
 
 typedef struct {

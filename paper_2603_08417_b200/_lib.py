@@ -49,7 +49,7 @@ class Scenario(ctypes.Structure):
         ("horizon", _f64), ("latency", _f64),
         ("target", _f64), ("safe", _f64), ("panic", _f64), ("resume", _f64), ("startup", _f64),
         ("alpha", _f64), ("headroom", _f64), ("noise", _f64), ("period", _f64), ("grid_step", _f64), ("retry_backoff", _f64),
-        ("demand_priority", _i32), ("pad2", _i32),
+        ("demand_priority", _i32), ("pad2", _i32), ("off_tr_i", _i64), ("off_tr_f", _i64),
         ("off_sizes", _i64), ("off_bitrates", _i64), ("off_manifest", _i64), ("off_segcount", _i64),
         ("off_seqdur", _i64), ("off_segdur", _i64), ("off_rho", _i64), ("off_zipf", _i64),
         ("off_starts", _i64), ("off_values", _i64), ("off_pbits", _i64), ("off_arrivals", _i64),

@@ -395,8 +395,6 @@ class ExperimentConfig:
             lm.rho(r)
         if policy.cache_enabled and policy.cache_capacity_bytes <= 0:
             raise ValueError("cache capacity must be positive")  # cache.py:29-30
-        if self.netem.trace_dir:
-            raise ConfigError("netem.trace_dir (CSV traces) is not supported by the GPU engine yet")
         if self.clock != "virtual":
             raise ConfigError("the GPU engine runs the virtual clock only")
         if not 0 <= self.client.retries < 255:

@@ -121,6 +121,17 @@ struct Scn {
     __device__ __forceinline__ int64_t manifest(int32_t seq) const { return manifest_b[seq]; }
     __device__ __forceinline__ Trace trace(int32_t cid) const {
         Trace t;
+        if (sc->off_tr_i >= 0) {                       // CSV traces: each client's own table
+            const int64_t *ti = b->i64_pool + sc->off_tr_i + 3 * (int64_t)cid;
+            const double *tf = b->f64_pool + sc->off_tr_f + 3 * (int64_t)cid;
+            t.starts = b->f64_pool + ti[0];
+            t.values = b->f64_pool + ti[1];
+            t.n = (int32_t)ti[2];
+            t.period = tf[0];
+            t.pbits = tf[1];
+            t.grid = tf[2];
+            return t;
+        }
         t.starts = starts;
         t.values = values + (int64_t)cid * sc->n_samples;
         t.period = sc->period;

@@ -51,6 +51,40 @@ def zipf_cdf(n: int, s: float) -> np.ndarray:
     return np.array([x / acc for x in c], dtype=np.float64)
 
 
+def load_trace_csv(path: str):
+    """netem.load_trace + BandwidthTrace.__init__ (netem.py:148-161, 39-64): the
+    (starts, values, period, period_bits) of one CSV trace (timestamp_s, kbps)."""
+    import csv
+    samples = []
+    with open(path, newline="", encoding="utf-8") as fh:
+        for row in csv.reader(fh):
+            if not row or row[0].lstrip().startswith("#"):
+                continue
+            try:
+                ts, kbps = float(row[0]), float(row[1])
+            except ValueError:
+                continue                               # header row
+            samples.append((ts, kbps * 1000.0))
+    if not samples:
+        raise ValueError(f"no samples in trace file {path}")
+    ts = [t for t, _ in samples]
+    if any(b - a <= 0 for a, b in zip(ts, ts[1:])):
+        raise ValueError("trace timestamps must strictly increase")
+    if ts[0] < 0:
+        raise ValueError("trace timestamps must be >= 0")
+    if any(bw < 0 for _, bw in samples):
+        raise ValueError("bandwidth must be >= 0")
+    starts = list(ts)
+    values = [float(bw) for _, bw in samples]
+    if starts[0] > 0:
+        starts[0] = 0.0
+    gaps = [b - a for a, b in zip(ts, ts[1:])]
+    period = ts[-1] + (statistics.median(gaps) if gaps else 1.0)
+    pbits = sum(v * ((starts[i + 1] if i + 1 < len(starts) else period) - starts[i])   # CPython 3.12 sum
+                for i, v in enumerate(values))
+    return starts, values, period, pbits
+
+
 def sample_times(duration: float, step: float) -> list[float]:
     """synthetic_trace's timestamps: t = 0; while t < duration: t += step (netem.py:195-201)."""
     ts, t = [], 0.0
@@ -176,6 +210,8 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     # -- traces: one table per (seed, netem), long enough for the largest N --
     trace_groups: dict = {}
     for low in lows:
+        if low.cfg.netem.trace_dir:
+            continue                                   # CSV traces: per-client tables below
         key = (low.cfg.seed, dataclasses.astuple(low.cfg.netem))
         prev = trace_groups.get(key, (0, low.cfg.netem))[0]
         trace_groups[key] = (max(prev, low.cfg.clients), low.cfg.netem)
@@ -264,7 +300,31 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
             P.add("f64", np.cumsum(draws), key=akey)                            # sequential cumsum
             input_bytes += 8 * N
         o_arr = P.memo[("f64", akey)]
-        tt = trace_tab[(cfg.seed, dataclasses.astuple(cfg.netem))]
+        if cfg.netem.trace_dir:                        # orchestrator.py:243-253
+            tdir = cfg.netem.trace_dir
+            files = sorted(os.path.join(tdir, f) for f in os.listdir(tdir) if f.endswith(".csv"))
+            if not files:
+                raise ConfigError(f"no trace CSVs in {tdir}")
+            order = _gen([cfg.seed, 2]).permutation(len(files))
+            ti, tf = [], []
+            for c in range(N):
+                f = files[order[c % len(files)]]
+                if ("f64", ("csv", f)) not in P.memo:
+                    st_, val_, per_, pb_ = load_trace_csv(f)
+                    grid_ = float(st_[1] - st_[0]) if len(st_) > 1 else 0.0
+                    if not (grid_ > 0 and all(x == float(i) * grid_ for i, x in enumerate(st_))):
+                        grid_ = 0.0
+                    o_st = P.add("f64", st_, key=("csv", f))
+                    o_val = P.add("f64", val_, key=("csvv", f))
+                    P.memo[("meta", f)] = (o_st, o_val, len(st_), per_, pb_, grid_)
+                    input_bytes += 16 * len(st_)
+                o_st, o_val, n_, per_, pb_, grid_ = P.memo[("meta", f)]
+                ti += [o_st, o_val, n_]
+                tf += [per_, pb_, grid_]
+            tt = dict(n=0, period=0.0, grid=0.0, starts=0, values=0, pbits=0,
+                      tr_i=P.add("i64", ti), tr_f=P.add("f64", tf))
+        else:
+            tt = trace_tab[(cfg.seed, dataclasses.astuple(cfg.netem))]
         o_eps, eps_stride = eps_tab[(cfg.seed, cfg.noise_rel_std)]
 
         sc = scen[si]
@@ -287,6 +347,8 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.retries = int(cfg.client.retries)
         sc.retry_backoff = float(cfg.client.retry_backoff_s)
         sc.demand_priority = int(bool(cfg.demand_priority))
+        sc.off_tr_i = tt.get("tr_i", -1)
+        sc.off_tr_f = tt.get("tr_f", -1)
         sc.off_sizes, sc.off_bitrates, sc.off_manifest, sc.off_segcount = o_sizes, o_bitrates, o_man, o_counts
         sc.off_seqdur, sc.off_segdur, sc.off_rho, sc.off_zipf = o_seqdur, o_segdur, o_rho, o_zipf
         sc.off_starts, sc.off_values, sc.off_pbits = tt["starts"], tt["values"], tt["pbits"]

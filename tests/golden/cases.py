@@ -76,4 +76,9 @@ def golden_cases():
                                                         demand_priority=True, queue_bound=2, horizon_s=150.0,
                                                         arrival_rate_per_s=1.0, seed=17)))
     out.append(("knob_prio_c3", W.c3(seed=18, fraction=0.2, horizon_s=90.0, demand_priority=True)))
+    # CSV bandwidth traces (netem.trace_dir): uneven steps, header/comment rows, a leading gap
+    tdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traces")
+    out.append(("knob_trace_dir", dataclasses.replace(base, variant="TCP", clients=9, horizon_s=200.0,
+                                                      arrival_rate_per_s=0.5, seed=19,
+                                                      netem=NetemConfig(trace_dir=tdir))))
     return out
