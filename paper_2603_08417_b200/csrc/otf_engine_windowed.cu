@@ -1015,27 +1015,29 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         w.k = m;
         w.E = (double)(m + 1) * w.W;
         if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
-        // pop the buckets: server events -> list, client-local events -> B-list
-        if (lane == 0) {
-            h->stats[OTF_ST_WINDOWS]++;
-            int32_t slot = m & (RING - 1);
-            int32_t c = h->bhead_srv[slot];
-            int32_t cl = h->bhead_loc[slot];
-            h->bhead_srv[slot] = -1;
-            h->bhead_loc[slot] = -1;
-            h->bits[slot >> 5] &= ~(1u << (slot & 31));
-            int32_t nl = 0, nb = 0;
+        // pop the buckets: lane 0 walks the server events into the list while lane 1
+        // walks the client-local events into the B-list (one converged loop)
+        if (lane < 2) {
+            const int32_t slot = m & (RING - 1);
+            int32_t c = lane == 0 ? h->bhead_srv[slot] : h->bhead_loc[slot];
+            int32_t n = 0;
+            const int32_t cap = lane == 0 ? h->list_cap : 0x7fffffff;
+            int32_t *dst = lane == 0 ? nullptr : w.blist;
             while (c >= 0) {
-                if (nl < h->list_cap) w.li[nl] = (int16_t)c;
-                nl++;
+                if (lane == 0) { if (n < cap) w.li[n] = (int16_t)c; }
+                else dst[n] = c;
+                n++;
                 c = w.bnext[c];
             }
-            while (cl >= 0) {
-                w.blist[nb++] = cl;
-                cl = w.bnext[cl];
+            if (lane == 0) {                           // each lane empties its own bucket
+                h->stats[OTF_ST_WINDOWS]++;
+                h->bhead_srv[slot] = -1;
+                h->bits[slot >> 5] &= ~(1u << (slot & 31));
+                h->n_list = n;
+            } else {
+                h->bhead_loc[slot] = -1;
+                h->n_blist = n;
             }
-            h->n_list = nl;
-            h->n_blist = nb;
         }
         __syncwarp();
         for (int32_t i = lane; i < h->n_blist; i += 32) {   // warm L2 with this window's client states
