@@ -76,8 +76,10 @@ struct WinHeader {
     int64_t t_bitrates[MAXTAB], t_manifest[MAXTAB];
     // timer wheel: server-event and client-local buckets per window
     uint32_t bits[RING / 32];
-    int32_t bhead_srv[RING];
-    int32_t bhead_loc[RING];
+    int32_t cnt_srv[RING];               // entries filed in each window's bucket arrays
+    int32_t cnt_loc[RING];
+    int32_t ovf_head, ovf_n, ovf_min;    // pushes past a full bucket (linked through bnext)
+    int32_t n_loc;                       // this window's client-local events (bucket array)
     int32_t list_cap;                    // capacity of the window's server-event list (dynamic region)
 };
 
@@ -100,8 +102,14 @@ __host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {   // power of t
 }
 
 struct WinGlobalLayout {
-    int64_t clients, picks, blist, wq_head, wq_tail, jobq, specq, lstamp, lq, total;
+    int64_t clients, picks, blist, wq_head, wq_tail, jobq, specq, lstamp, lq, bsrv, bloc, total;
 };
+
+// Per-window bucket arrays: server events up to the list capacity, client-local
+// events up to twice that; a push past a full bucket goes to the overflow list.
+__host__ __device__ inline int32_t win_list_cap(int32_t n_clients);
+__host__ __device__ inline int32_t bucket_cap_srv(int32_t n_clients) { return win_list_cap(n_clients); }
+__host__ __device__ inline int32_t bucket_cap_loc(int32_t n_clients) { return 2 * win_list_cap(n_clients); }
 
 __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
     WinGlobalLayout L;
@@ -115,6 +123,8 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     L.specq = o;   o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.lstamp = o;  o += align256((int64_t)sizeof(uint32_t) * n_desc);
     L.lq = o;      o += align256((int64_t)sizeof(LqEnt) * 2 * lq_capacity(n_desc));
+    L.bsrv = o;    o += align256((int64_t)sizeof(int32_t) * RING * bucket_cap_srv(n_clients));
+    L.bloc = o;    o += align256((int64_t)sizeof(int32_t) * RING * bucket_cap_loc(n_clients));
     L.total = o;
     return L;
 }
@@ -140,6 +150,8 @@ struct Win {
     uint8_t *dflags;
     Client *cl;
     int32_t *blist, *wq_head, *wq_tail;
+    int32_t *bsrv, *bloc;                              // bucket arrays [RING][cap]
+    int32_t scap, lcap;
     JobEnt *jq, *sq;
     double W, invW, H, E, now;
     int32_t k;
@@ -178,8 +190,16 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
     WinHeader *h = w.h;
     if (wk - w.k < RING) {
         int32_t slot = wk & (RING - 1);
-        int32_t old = atomicExch(srv ? &h->bhead_srv[slot] : &h->bhead_loc[slot], c);
-        w.bnext[c] = (int16_t)old;
+        const int32_t cap = srv ? w.scap : w.lcap;
+        int32_t pos = atomicAdd(srv ? &h->cnt_srv[slot] : &h->cnt_loc[slot], 1);
+        if (pos < cap) {
+            (srv ? w.bsrv : w.bloc)[(int64_t)slot * cap + pos] = c;
+        } else {                                       // bucket full (rare): overflow list
+            int32_t old = atomicExch(&h->ovf_head, c);
+            w.bnext[c] = (int16_t)old;
+            atomicAdd(&h->ovf_n, 1);
+            atomicMin(&h->ovf_min, wk);
+        }
         atomicOr(&h->bits[slot >> 5], 1u << (slot & 31));
     } else {                                           // beyond the wheel (rare): far list
         int32_t old = atomicExch(&h->far_head, c);
@@ -888,6 +908,10 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     w.cl = (Client *)(g + L.clients);
     w.S.picks = (Pcg64 *)(g + L.picks);
     w.blist = (int32_t *)(g + L.blist);
+    w.bsrv = (int32_t *)(g + L.bsrv);
+    w.bloc = (int32_t *)(g + L.bloc);
+    w.scap = bucket_cap_srv(N);
+    w.lcap = bucket_cap_loc(N);
     w.wq_head = (int32_t *)(g + L.wq_head);
     w.wq_tail = (int32_t *)(g + L.wq_tail);
     w.jq = (JobEnt *)(g + L.jobq);
@@ -917,6 +941,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         h->n_list = 0; h->n_blist = 0; h->wseq = 0;
         h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
         h->arr_next = 0;
+        h->ovf_head = -1; h->ovf_n = 0; h->ovf_min = WIN_NONE; h->n_loc = 0;
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
         h->list_cap = lcap;
         if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
@@ -929,7 +954,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         z.win = WIN_NONE; z.pc = W_GOT; z.desc = -1; z.job = -1;
         h->wk[q] = z;
     }
-    for (int32_t i = lane; i < RING; i += 32) { h->bhead_srv[i] = -1; h->bhead_loc[i] = -1; }
+    for (int32_t i = lane; i < RING; i += 32) { h->cnt_srv[i] = 0; h->cnt_loc[i] = 0; }
     for (int32_t i = lane; i < RING / 32; i += 32) h->bits[i] = 0;
     for (int32_t i = lane; i < sc.n_seq; i += 32) {
         h->t_segcount[i] = w.S.segcounts[i];
@@ -1015,48 +1040,72 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         w.k = m;
         w.E = (double)(m + 1) * w.W;
         if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
-        // pop the buckets: lane 0 walks the server events into the list while lane 1
-        // walks the client-local events into the B-list (one converged loop)
-        if (lane < 2) {
+        if (lane == 0) h->stats[28] += clock64() - t0;  // profile: next-window selection
+        long long tp = clock64();
+        {
+            // pop the buckets: the window's arrays are read by all lanes at once
             const int32_t slot = m & (RING - 1);
-            int32_t c = lane == 0 ? h->bhead_srv[slot] : h->bhead_loc[slot];
-            int32_t n = 0;
-            const int32_t cap = lane == 0 ? h->list_cap : 0x7fffffff;
-            int32_t *dst = lane == 0 ? nullptr : w.blist;
-            while (c >= 0) {
-                if (lane == 0) { if (n < cap) w.li[n] = (int16_t)c; }
-                else dst[n] = c;
-                n++;
-                c = w.bnext[c];
+            const int32_t ns = min(h->cnt_srv[slot], w.scap);
+            const int32_t nl = min(h->cnt_loc[slot], w.lcap);
+            int32_t n_ovf = 0, nb = 0;
+            if (h->ovf_n > 0 && h->ovf_min <= m) {     // overflowed pushes due now (rare)
+                if (lane == 0) {
+                    int32_t c = h->ovf_head, keep = -1, rem = WIN_NONE, kept = 0;
+                    while (c >= 0) {
+                        int32_t nx = w.bnext[c];
+                        const Client &cl = w.cl[c];
+                        int32_t wk = timer_win(w, cl.next_when);
+                        if (wk == m) {
+                            if (cl.pc == C_SEG_LAT) { if (ns + n_ovf < h->list_cap) w.li[ns + n_ovf] = (int16_t)c; n_ovf++; }
+                            else w.blist[nb++] = c;
+                        } else {
+                            w.bnext[c] = (int16_t)keep; keep = c; kept++;
+                            rem = min(rem, wk);
+                        }
+                        c = nx;
+                    }
+                    h->ovf_head = keep; h->ovf_n = kept; h->ovf_min = rem;
+                    h->n_list = ns + n_ovf;
+                    h->n_blist = nb;
+                }
+                __syncwarp();
+                n_ovf = h->n_list - ns;
+                nb = h->n_blist;
             }
-            if (lane == 0) {                           // each lane empties its own bucket
-                h->stats[OTF_ST_WINDOWS]++;
-                h->bhead_srv[slot] = -1;
-                h->bits[slot >> 5] &= ~(1u << (slot & 31));
-                h->n_list = n;
-            } else {
-                h->bhead_loc[slot] = -1;
-                h->n_blist = n;
+            const int32_t nlist = ns + n_ovf;
+            if (nlist > h->list_cap) {                 // too many simultaneous requests for this engine
+                if (lane == 0) h->st.status |= OTF_S_TIE;
+                __syncwarp();
+                break;
             }
-        }
-        __syncwarp();
-        for (int32_t i = lane; i < h->n_blist; i += 32) {   // warm L2 with this window's client states
-            const char *ptr = (const char *)&w.cl[w.blist[i]];
-            asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
-            asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr + 128));
-        }
-        if (h->n_list > h->list_cap) {                 // too many simultaneous requests for this engine
-            if (lane == 0) h->st.status |= OTF_S_TIE;
+            const int32_t *as = w.bsrv + (int64_t)slot * w.scap;
+            const int32_t *al = w.bloc + (int64_t)slot * w.lcap;
+            for (int32_t i = lane; i < nl; i += 32) {  // warm L2 with this window's client states
+                const char *ptr = (const char *)&w.cl[al[i]];
+                asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
+                asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr + 128));
+            }
+            if (lane == 0) h->stats[29] += clock64() - tp;  // profile: bucket pop
+            for (int32_t i = lane; i < nlist; i += 32) {   // gather sort keys + request descriptors
+                int32_t c = i < ns ? as[i] : w.li[i];
+                const Client &cl = w.cl[c];
+                w.li[i] = (int16_t)c;
+                w.lw[i] = cl.next_when;
+                w.ld[i] = (int16_t)cl.desc;
+                w.lp[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
+            }
             __syncwarp();
-            break;
+            if (lane == 0) {
+                h->stats[OTF_ST_WINDOWS]++;
+                h->cnt_srv[slot] = 0;
+                h->cnt_loc[slot] = 0;
+                h->bits[slot >> 5] &= ~(1u << (slot & 31));
+                h->n_list = nlist;
+                h->n_blist = nb;
+                h->n_loc = nl;
+            }
+            __syncwarp();
         }
-        for (int32_t i = lane; i < h->n_list; i += 32) {   // gather sort keys + request descriptors
-            const Client &cl = w.cl[w.li[i]];
-            w.lw[i] = cl.next_when;
-            w.ld[i] = (int16_t)cl.desc;
-            w.lp[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
-        }
-        __syncwarp();
         t1 = clock64();
         if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
         t0 = t1;
@@ -1076,8 +1125,11 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         t0 = t1;
         if (h->st.status & OTF_S_TIE) break;
         // ---- phase B: client lanes ----
-        const int32_t nb = h->n_blist;
-        for (int32_t i = lane; i < nb; i += 32) client_local(w, w.blist[i]);
+        {
+            const int32_t nl = h->n_loc, nb = h->n_blist;
+            const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
+            for (int32_t i = lane; i < nl + nb; i += 32) client_local(w, i < nl ? al[i] : w.blist[i - nl]);
+        }
         __syncwarp();
         t1 = clock64();
         if (lane == 0) h->stats[OTF_ST_CYC_CLIENTS] += t1 - t0;

@@ -22,7 +22,8 @@ def timeit(name, cfgs, eng, reps=2):
         tot = max(1, st[27])
         print("  windows/scn", st[22] / len(cfgs), "cycles/window", tot / max(1, st[22]),
               "scan %.2f sort %.2f server %.2f clients %.2f" % (st[23]/tot, st[24]/tot, st[25]/tot, st[26]/tot),
-              "pops/scn", st[20]/len(cfgs), "ready", st[21]/len(cfgs))
+              "pops/scn", st[20]/len(cfgs), "ready", st[21]/len(cfgs),
+              "| select %.2f pop %.2f" % (st[28]/tot, st[29]/tot))
     print(json.dumps(dict(name=name, engine=eng, scenarios=len(cfgs), build_s=round(t1-t0,2), ms=round(best,2),
                           requests=req, req_per_s=req/(best/1e3), status=int(br.status.max()))), flush=True)
 
