@@ -192,6 +192,35 @@ int otf_build_traces(int64_t n_traces, int32_t n_samples, const double *normals,
                      double period, double mu, double sigma, double decay, double spread,
                      double floor_bps, double cap_bps, double *values, double *pbits, int32_t n_threads);
 
+/* ---- HOST input generators: numpy Generator(PCG64(SeedSequence(entropy)))
+ * streams replayed bit-for-bit (numpy 2.3.5 SeedSequence, PCG64, ziggurat
+ * normal / exponential), multithreaded over independent streams.  They replace
+ * the reference's per-run numpy draws; host pointers. ---- */
+enum {
+    OTF_DRAW_STANDARD_NORMAL = 0,     /* Generator.standard_normal(n) */
+    OTF_DRAW_NORMAL = 1,              /* Generator.normal(loc, scale, n) */
+    OTF_DRAW_EXPONENTIAL = 2,         /* Generator.exponential(scale, n) */
+    OTF_DRAW_STANDARD_EXPONENTIAL = 3 /* Generator.standard_exponential(n) */
+};
+
+/* n draws of `kind` from Generator(PCG64(SeedSequence(entropy[0..n_entropy)))). */
+int otf_np_draws(int32_t kind, const uint64_t *entropy, int32_t n_entropy, double loc, double scale, int64_t n,
+                 double *out);
+
+/* ExperimentConfig.arrival_offsets (orchestrator.py:265-268):
+ * out = cumsum(SS([seed, 1]).exponential(scale, n)), sequential. */
+int otf_gen_arrivals(uint64_t seed, int64_t n, double scale, double *out);
+
+/* ServiceSampler noise (transcode.py:89-99): out[w][0..n) = SS([seed, w]).normal(0, noise, n). */
+int otf_gen_noise(uint64_t seed, int32_t n_workers, double noise, int64_t n, double *out, int32_t n_threads);
+
+/* ExperimentConfig.trace_for + synthetic_trace + BandwidthTrace (orchestrator.py:254-263,
+ * netem.py:179-202,39-64) for clients 0..n_traces-1 of `seed`: normals from
+ * SS([seed, 2, c]), then as otf_build_traces. */
+int otf_gen_traces(uint64_t seed, int64_t n_traces, int32_t n_samples, const double *starts, double period,
+                   double mu, double sigma, double decay, double spread, double floor_bps, double cap_bps,
+                   double *values, double *pbits, int32_t n_threads);
+
 /* DEVICE: fill segment-size tables (one thread per entry). */
 int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
                   int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream);

@@ -98,7 +98,9 @@ class SizeTable(ctypes.Structure):
 
 
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
-           "otf_scratch_bytes", "otf_shared_bytes", "otf_build_traces", "otf_gen_sizes", "otf_run_batch")
+           "otf_scratch_bytes", "otf_shared_bytes", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
+           "otf_gen_noise", "otf_gen_traces", "otf_gen_sizes", "otf_run_batch")
+DRAW_STANDARD_NORMAL, DRAW_NORMAL, DRAW_EXPONENTIAL, DRAW_STANDARD_EXPONENTIAL = 0, 1, 2, 3
 
 
 class OtfError(RuntimeError):
@@ -107,7 +109,7 @@ class OtfError(RuntimeError):
 
 def build(force: bool = False) -> str:
     """Compile libotfgpu.so for sm_100a in place (csrc/Makefile)."""
-    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", "Makefile"))]
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h", "Makefile"))]
     srcs.append(os.path.join(os.path.dirname(HERE), "include", "otfgpu.h"))
     stale = not os.path.exists(LIB_PATH) or any(os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in srcs)
     if force or stale:
@@ -137,6 +139,15 @@ def lib():
     L.otf_build_traces.restype = ctypes.c_int
     L.otf_build_traces.argtypes = [_i64, _i32, _P(_f64), _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
                                    _P(_f64), _P(_f64), _i32]
+    L.otf_np_draws.restype = ctypes.c_int
+    L.otf_np_draws.argtypes = [_i32, _P(ctypes.c_uint64), _i32, _f64, _f64, _i64, _P(_f64)]
+    L.otf_gen_arrivals.restype = ctypes.c_int
+    L.otf_gen_arrivals.argtypes = [ctypes.c_uint64, _i64, _f64, _P(_f64)]
+    L.otf_gen_noise.restype = ctypes.c_int
+    L.otf_gen_noise.argtypes = [ctypes.c_uint64, _i32, _f64, _i64, _P(_f64), _i32]
+    L.otf_gen_traces.restype = ctypes.c_int
+    L.otf_gen_traces.argtypes = [ctypes.c_uint64, _i64, _i32, _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
+                                 _P(_f64), _P(_f64), _i32]
     L.otf_gen_sizes.restype = ctypes.c_int
     L.otf_gen_sizes.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp, _vp]
     L.otf_run_batch.restype = ctypes.c_int

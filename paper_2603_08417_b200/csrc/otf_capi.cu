@@ -26,6 +26,8 @@ static int fail(int code, const std::string &msg) {
     return code;
 }
 
+int otf_fail(int code, const std::string &msg) { return fail(code, msg); }   // for otf_hostgen.cu
+
 static int check_cuda(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(OTF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -54,62 +56,6 @@ int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, i
     (void)n_workers;
     if (engine != OTF_ENGINE_WINDOWED) return 0;
     return otf_windowed_shared_bytes(n_clients, (int64_t)n_seq * n_ranks * max_nseg);
-}
-
-// CPython >= 3.12 builtin sum() over floats: Neumaier-compensated.
-static double py_sum(const double *xs, int n) {
-    double f = 0.0, c = 0.0;
-    for (int i = 0; i < n; i++) {
-        double x = xs[i];
-        double t = f + x;
-        if (fabs(f) >= fabs(x)) c += (f - t) + x;
-        else c += (x - t) + f;
-        f = t;
-    }
-    if (c != 0.0 && std::isfinite(c)) f += c;
-    return f;
-}
-
-int otf_build_traces(int64_t n_traces, int32_t n_samples, const double *normals, const double *starts,
-                     double period, double mu, double sigma, double decay, double spread,
-                     double floor_bps, double cap_bps, double *values, double *pbits, int32_t n_threads) {
-    if (n_traces < 0 || n_samples <= 0 || !normals || !starts || !values || !pbits)
-        return fail(OTF_EINVAL, "otf_build_traces: bad arguments");
-    auto work = [&](int64_t lo, int64_t hi) {
-        std::vector<double> terms((size_t)n_samples);
-        for (int64_t t = lo; t < hi; t++) {
-            const double *z = normals + t * (int64_t)(n_samples + 1);
-            double *v = values + t * (int64_t)n_samples;
-            // synthetic_trace (netem.py:190-201)
-            double x = mu + sigma * z[0];
-            for (int32_t i = 0; i < n_samples; i++) {
-                double e = exp(x);                       // glibc exp == math.exp
-                double bw = e > floor_bps ? e : floor_bps;
-                bw = cap_bps < bw ? cap_bps : bw;
-                v[i] = bw;
-                x = mu + (x - mu) * decay + spread * z[i + 1];
-            }
-            // BandwidthTrace._period_bits (netem.py:61-64)
-            for (int32_t i = 0; i < n_samples; i++) {
-                double end = (i + 1 < n_samples) ? starts[i + 1] : period;
-                terms[(size_t)i] = v[i] * (end - starts[i]);
-            }
-            pbits[t] = py_sum(terms.data(), n_samples);
-        }
-    };
-    int nt = std::max(1, std::min<int>(n_threads > 0 ? n_threads : 1, (int)std::max<int64_t>(1, n_traces / 64)));
-    if (nt == 1) {
-        work(0, n_traces);
-    } else {
-        std::vector<std::thread> th;
-        int64_t chunk = (n_traces + nt - 1) / nt;
-        for (int i = 0; i < nt; i++) {
-            int64_t lo = i * chunk, hi = std::min(n_traces, lo + chunk);
-            if (lo < hi) th.emplace_back(work, lo, hi);
-        }
-        for (auto &t : th) t.join();
-    }
-    return OTF_OK;
 }
 
 int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,

@@ -55,7 +55,9 @@ class DeviceBatch:
         self.h_i32 = torch.from_numpy(inp.i32)
         if pin:
             self.h_scen, self.h_tables = self.h_scen.pin_memory(), self.h_tables.pin_memory()
-            self.h_f64, self.h_i64, self.h_i32 = self.h_f64.pin_memory(), self.h_i64.pin_memory(), self.h_i32.pin_memory()
+            if not inp.pinned:
+                self.h_f64, self.h_i64, self.h_i32 = (self.h_f64.pin_memory(), self.h_i64.pin_memory(),
+                                                      self.h_i32.pin_memory())
         self.scen = torch.empty_like(self.h_scen, device=dev)
         self.tables = torch.empty_like(self.h_tables, device=dev)
         self.f64 = torch.empty_like(self.h_f64, device=dev)
@@ -254,8 +256,8 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
             if any(c is not None for c in cap_list):
                 inp0 = build_inputs([configs[i] for i in idx], engine=e, mode=m, eps_scale=es)
                 use_caps = [c if c is not None else tuple(inp0.caps[k]) for k, c in enumerate(cap_list)]
-            inp = build_inputs([configs[i] for i in idx], engine=e, mode=m, caps=use_caps, eps_scale=es)
-            db = DeviceBatch(inp, device)
+            inp = build_inputs([configs[i] for i in idx], engine=e, mode=m, caps=use_caps, eps_scale=es, pin=True)
+            db = DeviceBatch(inp, device, pin=True)
             db.launch()
             br = db.fetch()
             for k, i in enumerate(idx):

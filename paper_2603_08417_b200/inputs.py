@@ -1,11 +1,13 @@
 """Host input builder: lowers ExperimentConfigs to otf_scenario structs + shared pools.
 
 Everything a scenario reads is derived here from the reference's own seeded
-streams, drawn with numpy exactly where the reference draws them:
+streams.  The numpy Generator streams are replayed bit-for-bit by the host
+generators of libotfgpu (csrc/otf_hostgen.cu: SeedSequence + PCG64 + numpy's
+ziggurats, multithreaded), where the reference draws them:
 
 * arrival offsets  list(np.cumsum(exponential(1/rate, N)))  SS([seed, 1])   orchestrator.py:265-268
 * trace normals    standard_normal per client               SS([seed, 2, c]) orchestrator.py:254-263
-                   -> values/period-bits in C++ (glibc exp, CPython 3.12 sum)  netem.py:39-64,179-202
+                   -> values/period-bits (glibc exp, CPython 3.12 sum)  netem.py:39-64,179-202
 * worker noise     normal(0, noise) per worker              SS([seed, w])    transcode.py:89-99
 * sequence keys    sha256(id)[:8] big-endian                                  content.py:165-166
 * manifest bytes   len(json.dumps(manifest_for(seq), sort_keys=True))         server.py:58-59
@@ -146,11 +148,34 @@ class _Pools:
     def reserve(self, kind: str, n: int, key=None) -> int:
         return self.add(kind, np.zeros(n), key)
 
-    def concat(self, kind: str) -> np.ndarray:
+    def defer(self, kind: str, n: int, fill) -> int:
+        """Reserve n elements that fill(view) writes in place when the pool is laid out."""
+        off = self.size[kind]
+        self.parts[kind].append((int(n), fill))
+        self.size[kind] += int(n)
+        return off
+
+    def concat(self, kind: str, pin: bool = False) -> np.ndarray:
+        """The pool as one array (page-locked when pin, so the H2D copy is a single DMA)."""
         dt = {"f64": np.float64, "i64": np.int64, "i32": np.int32}[kind]
-        if not self.parts[kind]:
-            return np.zeros(1, dtype=dt)
-        return np.concatenate(self.parts[kind])
+        total = max(1, self.size[kind])
+        if pin:
+            import torch
+            tt = {"f64": torch.float64, "i64": torch.int64, "i32": torch.int32}[kind]
+            out = torch.empty(total, dtype=tt, pin_memory=True).numpy()
+        else:
+            out = np.empty(total, dtype=dt)
+        pos = 0
+        for part in self.parts[kind]:
+            if isinstance(part, tuple):
+                n, fill = part
+                fill(out[pos:pos + n])
+            else:
+                n = part.size
+                out[pos:pos + n] = part
+            pos += n
+        out[pos:] = 0
+        return out
 
 
 @dataclasses.dataclass
@@ -171,6 +196,7 @@ class BatchInputs:
     shared_bytes: int = 0       # windowed engine: dynamic shared memory per CTA (batch max)
     smem_per: list = dataclasses.field(default_factory=list)   # per scenario
     engine_flags: int = 0       # OTF_BF_*
+    pinned: bool = False        # pools allocated page-locked (torch pinned memory)
 
 
 def _default_caps(low: Lowered) -> tuple[int, int, int, int]:
@@ -191,8 +217,8 @@ def _eps_len(low: Lowered) -> int:
 
 
 def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.MODE_RECORDS,
-                 caps=None, eps_scale: float = 1, threads: int | None = None) -> BatchInputs:
-    """Lower a list of ExperimentConfigs into one device batch (host arrays)."""
+                 caps=None, eps_scale: float = 1, threads: int | None = None, pin: bool = False) -> BatchInputs:
+    """Lower a list of ExperimentConfigs into one device batch (host arrays; page-locked if pin)."""
     L = _lib.lib()
     threads = threads or os.cpu_count() or 1
     lows = [lower(ExperimentConfig.from_reference(c)) for c in configs]
@@ -225,24 +251,25 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         period = ts[-1] + (statistics.median(gaps) if gaps else 1.0)
         starts = list(ts)
         n = len(ts)
-        normals = np.empty((nmax, n + 1), dtype=np.float64)
-        for c in range(nmax):
-            normals[c] = _gen([seed, 2, c]).standard_normal(n + 1)
-        values = np.empty((nmax, n), dtype=np.float64)
-        pbits = np.empty(nmax, dtype=np.float64)
         starts_a = np.asarray(starts, dtype=np.float64)
         decay = math.exp(-ne.theta_per_s * ne.step_s)
         spread = ne.sigma * math.sqrt(1.0 - decay * decay)
-        dp = ctypes.POINTER(ctypes.c_double)
-        rc = L.otf_build_traces(nmax, n, normals.ctypes.data_as(dp), starts_a.ctypes.data_as(dp), period,
-                                math.log(ne.median_bps), ne.sigma, decay, spread, ne.floor_bps, ne.cap_bps,
-                                values.ctypes.data_as(dp), pbits.ctypes.data_as(dp), threads)
-        _lib.check(rc, "otf_build_traces")
+        pbits = np.empty(nmax, dtype=np.float64)
+
+        def fill_values(view, seed=seed, nmax=nmax, n=n, starts_a=starts_a, period=period, ne=ne, decay=decay,
+                        spread=spread, pbits=pbits):
+            # generated straight into the (pinned) pool: no intermediate copy
+            dp = ctypes.POINTER(ctypes.c_double)
+            rc = L.otf_gen_traces(seed, nmax, n, starts_a.ctypes.data_as(dp), period, math.log(ne.median_bps),
+                                  ne.sigma, decay, spread, ne.floor_bps, ne.cap_bps, view.ctypes.data_as(dp),
+                                  pbits.ctypes.data_as(dp), threads)
+            _lib.check(rc, "otf_gen_traces")
+
         grid = float(ne.step_s) if all(x == float(i) * ne.step_s for i, x in enumerate(starts)) else 0.0
         trace_tab[key] = dict(n=n, period=period, grid=grid,
-                              starts=P.add("f64", starts_a), values=P.add("f64", values),
-                              pbits=P.add("f64", pbits))
-        input_bytes += values.nbytes + pbits.nbytes + starts_a.nbytes
+                              starts=P.add("f64", starts_a), values=P.defer("f64", nmax * n, fill_values),
+                              pbits=P.defer("f64", nmax, lambda view, pbits=pbits: np.copyto(view, pbits)))
+        input_bytes += 8 * (nmax * n + nmax) + starts_a.nbytes
 
     # -- worker noise: one table per (seed, noise), longest draw count --
     eps_groups: dict = {}
@@ -253,7 +280,9 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     eps_tab = {}
     for (seed, noise), (kmax, elen) in eps_groups.items():
         if noise > 0:
-            eps = np.stack([_gen([seed, w]).normal(0.0, noise, size=elen) for w in range(kmax)])
+            eps = np.empty((kmax, elen), dtype=np.float64)
+            _lib.check(L.otf_gen_noise(seed, kmax, noise, elen, eps.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       threads), "otf_gen_noise")
         else:
             eps = np.zeros((kmax, 1))
         eps_tab[(seed, noise)] = (P.add("f64", eps), eps.shape[1])
@@ -282,13 +311,15 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
             tables.append(t)
             input_bytes += 8 * n_seq * n_ranks * max_nseg
         o_sizes = P.memo[("i64", ("sizes", cat_key))]
-        man = []
-        for sid, dur, segdur, cnt in zip(low.seq_ids, low.seq_dur, low.seq_segdur, low.counts):
-            m = {"sequence": sid, "duration_s": dur, "segment_duration_s": segdur, "segment_count": cnt,
-                 "representations": [{"rank": r, "bitrate_bps": b} for r, b in ladder],
-                 "url_template": URL_TEMPLATE}
-            man.append(len(json.dumps(m, sort_keys=True).encode("utf-8")))   # server.py:58-59
-        o_man = P.add("i64", man, key=("manifest", cat_key))
+        if ("i64", ("manifest", cat_key)) not in P.memo:
+            man = []
+            for sid, dur, segdur, cnt in zip(low.seq_ids, low.seq_dur, low.seq_segdur, low.counts):
+                m = {"sequence": sid, "duration_s": dur, "segment_duration_s": segdur, "segment_count": cnt,
+                     "representations": [{"rank": r, "bitrate_bps": b} for r, b in ladder],
+                     "url_template": URL_TEMPLATE}
+                man.append(len(json.dumps(m, sort_keys=True).encode("utf-8")))   # server.py:58-59
+            P.add("i64", man, key=("manifest", cat_key))
+        o_man = P.memo[("i64", ("manifest", cat_key))]
         rho_map = cfg.per_rank_rho or {r: cfg.rho for r, _ in ladder}
         o_rho = P.add("f64", [float(rho_map[r]) for r, _ in ladder], key=("rho", tuple(sorted(rho_map.items()))))
         pop = 1 if cfg.popularity == "zipf" else 0
@@ -296,8 +327,10 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
                        key=("zipf", n_seq, pop, cfg.zipf_exponent))
         akey = ("arrivals", cfg.seed, N, cfg.arrival_rate_per_s)
         if ("f64", akey) not in P.memo:
-            draws = _gen([cfg.seed, 1]).exponential(1.0 / cfg.arrival_rate_per_s, size=N)
-            P.add("f64", np.cumsum(draws), key=akey)                            # sequential cumsum
+            arr = np.empty(N, dtype=np.float64)                                  # cumsum(exponential), sequential
+            _lib.check(L.otf_gen_arrivals(cfg.seed, N, 1.0 / cfg.arrival_rate_per_s,
+                                          arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "otf_gen_arrivals")
+            P.add("f64", arr, key=akey)
             input_bytes += 8 * N
         o_arr = P.memo[("f64", akey)]
         if cfg.netem.trace_dir:                        # orchestrator.py:243-253
@@ -372,7 +405,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
 
     return BatchInputs(
         lowered=lows, scenarios=scen, size_tables=(_lib.SizeTable * max(1, len(tables)))(*tables),
-        f64=P.concat("f64"), i64=P.concat("i64"), i32=P.concat("i32"),
+        f64=P.concat("f64", pin), i64=P.concat("i64", pin), i32=P.concat("i32", pin), pinned=pin,
         scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
         engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes, smem_per=smem_per)
 

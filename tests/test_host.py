@@ -157,3 +157,63 @@ def test_c5_sweep_shape():
     sweep = workloads.c5_sweep(seeds=range(1, 3))
     assert len(sweep) == 2 * 16
     assert all(len(c.ladder) == 10 for c in sweep)
+
+
+def _np_gen(ent):
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence(ent)))
+
+
+@pytest.mark.parametrize("ent", [[7, 2, 0], [1, 2, 2799], [123456789012, 1], [0], [5, 0], [2**40 + 3, 2, 17]])
+def test_host_generator_replays_numpy_streams(ent):
+    """otf_np_draws (SeedSequence + PCG64 + numpy's ziggurats, csrc/otf_hostgen.cu) is
+    bit-identical to numpy 2.3.5's Generator -- 400k draws per kind, so the
+    rejection and tail branches of both ziggurats are exercised."""
+    L = _lib.lib()
+    dp = ctypes.POINTER(ctypes.c_double)
+    e = (ctypes.c_uint64 * len(ent))(*ent)
+    n = 400_000
+    cases = [(_lib.DRAW_STANDARD_NORMAL, 0.0, 1.0, lambda g: g.standard_normal(n)),
+             (_lib.DRAW_NORMAL, 0.0, 0.05, lambda g: g.normal(0.0, 0.05, n)),
+             (_lib.DRAW_EXPONENTIAL, 0.0, 0.37, lambda g: g.exponential(0.37, n)),
+             (_lib.DRAW_STANDARD_EXPONENTIAL, 0.0, 1.0, lambda g: g.standard_exponential(n))]
+    for kind, loc, scale, ref in cases:
+        out = np.empty(n)
+        _lib.check(L.otf_np_draws(kind, e, len(ent), loc, scale, n, out.ctypes.data_as(dp)), "otf_np_draws")
+        want = ref(_np_gen(ent))
+        assert np.array_equal(out.view(np.int64), want.view(np.int64)), kind
+    z = _np_gen(ent).standard_normal(n)
+    assert (np.abs(z) > 3.6541528853610088).sum() > 0      # the tail branch was exercised
+
+
+def test_host_noise_and_arrivals_tables():
+    """otf_gen_noise / otf_gen_arrivals == transcode.py:89-99 / orchestrator.py:265-268 streams."""
+    L = _lib.lib()
+    dp = ctypes.POINTER(ctypes.c_double)
+    eps = np.empty((4, 5000))
+    _lib.check(L.otf_gen_noise(11, 4, 0.05, 5000, eps.ctypes.data_as(dp), 3), "otf_gen_noise")
+    for w in range(4):
+        want = _np_gen([11, w]).normal(0.0, 0.05, size=5000)
+        assert np.array_equal(eps[w].view(np.int64), want.view(np.int64))
+    arr = np.empty(2800)
+    _lib.check(L.otf_gen_arrivals(11, 2800, 1 / 46.0, arr.ctypes.data_as(dp)), "otf_gen_arrivals")
+    want = np.cumsum(_np_gen([11, 1]).exponential(1 / 46.0, size=2800))
+    assert np.array_equal(arr.view(np.int64), want.view(np.int64))
+
+
+def test_trace_tables_many_clients_threaded():
+    """Multithreaded otf_gen_traces == per-client numpy normals + otf_build_traces."""
+    L = _lib.lib()
+    dp = ctypes.POINTER(ctypes.c_double)
+    n, nc = 600, 300
+    starts = np.arange(n, dtype=np.float64)
+    mu, sigma, decay = math.log(17e6), 0.35, math.exp(-0.08)
+    spread = sigma * math.sqrt(1 - decay * decay)
+    v1, p1 = np.empty((nc, n)), np.empty(nc)
+    _lib.check(L.otf_gen_traces(9, nc, n, starts.ctypes.data_as(dp), 600.0, mu, sigma, decay, spread, 2e6, 400e6,
+                                v1.ctypes.data_as(dp), p1.ctypes.data_as(dp), 8), "otf_gen_traces")
+    z = np.stack([_np_gen([9, 2, c]).standard_normal(n + 1) for c in range(nc)])
+    v2, p2 = np.empty((nc, n)), np.empty(nc)
+    _lib.check(L.otf_build_traces(nc, n, z.ctypes.data_as(dp), starts.ctypes.data_as(dp), 600.0, mu, sigma, decay,
+                                  spread, 2e6, 400e6, v2.ctypes.data_as(dp), p2.ctypes.data_as(dp), 1), "b")
+    assert np.array_equal(v1.view(np.int64), v2.view(np.int64))
+    assert np.array_equal(p1.view(np.int64), p2.view(np.int64))
