@@ -67,6 +67,7 @@ enum {
     OTF_ST_STATUS, OTF_ST_HUNG, OTF_ST_TIMER_POPS, OTF_ST_READY_CALLBACKS, OTF_ST_WINDOWS,
     /* windowed engine profile: SM cycles spent per phase (lane 0's clock) */
     OTF_ST_CYC_SCAN, OTF_ST_CYC_SORT, OTF_ST_CYC_SERVER, OTF_ST_CYC_CLIENTS, OTF_ST_CYC_TOTAL,
+    OTF_ST_CYC_LOCAL,   /* client-local phase run concurrently with the server lane */
     OTF_ST_NSLOTS = 32
 };
 

@@ -14,7 +14,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB_PATH = os.path.join(HERE, "libotfgpu.so")
+LIB_PATH = os.environ.get("OTFGPU_LIB_OVERRIDE") or os.path.join(HERE, "libotfgpu.so")   # override: tools/ experiments
 ABI_VERSION = 1
 
 _P = ctypes.POINTER

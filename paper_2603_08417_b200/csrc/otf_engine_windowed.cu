@@ -39,8 +39,22 @@ constexpr int RANK_SORT_MAX = 64;  // windows up to this many server events: ran
 constexpr int MAXK = 16;           // transcode workers
 constexpr int RING = 512;          // timer-wheel buckets (windows); farther timers wait on a far list
 constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory
-constexpr int MAXN = 32767;        // clients (16-bit wheel links)
+constexpr int MAXN = 32766;        // clients (16-bit wheel links; 0x7FFE/0x7FFF are descriptor states)
+
+// Descriptor word (16 bits, shared memory): bit 15 = cached; bits 0-14 = the
+// in-flight state: DF_IDLE (no job), DF_NOWAIT (job, no waiter yet) or the
+// client id at the TAIL of the job's waiter list.  Waiters form a circular
+// list through bnext (tail.next = head), so the whole Future-callback list of
+// an in-flight descriptor lives in shared memory (backend.py:123-133,209-216).
+constexpr uint16_t DF_CACHED = 0x8000;
+constexpr uint16_t DF_IDLE = 0x7FFF;
+constexpr uint16_t DF_NOWAIT = 0x7FFE;
+__device__ __forceinline__ bool df_inflight(uint16_t f) { return (f & 0x7FFF) != DF_IDLE; }
 constexpr int16_t NIL = -1;
+#ifndef WIN_WARPS
+#define WIN_WARPS 1
+#endif
+constexpr int WIN_THREADS = 32 * WIN_WARPS;   // threads per scenario (see windowed_kernel)
 
 struct WWorker {
     double when, ctime;
@@ -81,6 +95,8 @@ struct WinHeader {
     int32_t ovf_head, ovf_n, ovf_min;    // pushes past a full bucket (linked through bnext)
     int32_t n_loc;                       // this window's client-local events (bucket array)
     int32_t list_cap;                    // capacity of the window's server-event list (dynamic region)
+    int32_t ctl, cur_m;                  // window-loop control word + the window being run
+    double wsum[WIN_WARPS][3];           // per-warp float sums (fixed-order final reduction)
 };
 
 // Server events one window can hold: the list lives in the dynamic shared region.
@@ -102,7 +118,7 @@ __host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {   // power of t
 }
 
 struct WinGlobalLayout {
-    int64_t clients, picks, blist, wq_head, wq_tail, jobq, specq, lstamp, lq, bsrv, bloc, total;
+    int64_t clients, picks, blist, jobq, specq, lstamp, lq, bsrv, bloc, total;
 };
 
 // Per-window bucket arrays: server events up to the list capacity, client-local
@@ -117,8 +133,6 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
     L.picks = o;   o += align256((int64_t)sizeof(Pcg64) * n_clients);
     L.blist = o;   o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
-    L.wq_head = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
-    L.wq_tail = o; o += align256((int64_t)sizeof(int32_t) * n_desc);
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.specq = o;   o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.lstamp = o;  o += align256((int64_t)sizeof(uint32_t) * n_desc);
@@ -134,7 +148,7 @@ __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_d
     o += 16 * (int64_t)win_list_cap(n_clients);   // when f64, pack i32, id i16, desc i16
     o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
     o = (o + 15) & ~(int64_t)15;
-    o += n_desc;                          // descriptor flags
+    o += 2 * n_desc;                      // descriptor words (DF_*)
     return (o + 15) & ~(int64_t)15;
 }
 
@@ -147,9 +161,9 @@ struct Win {
     int16_t *li, *ld;                                  //   client id, descriptor
     uint32_t *lstamp;                                  // latest touch stamp per descriptor (global)
     LqEnt *lq;                                         // touch queue (global, 2 * lq_cap)
-    uint8_t *dflags;
+    uint16_t *dflags;                                  // descriptor words (DF_*), shared
     Client *cl;
-    int32_t *blist, *wq_head, *wq_tail;
+    int32_t *blist;
     int32_t *bsrv, *bloc;                              // bucket arrays [RING][cap]
     int32_t scap, lcap;
     JobEnt *jq, *sq;
@@ -159,7 +173,8 @@ struct Win {
     int64_t req_counter, n_req;
     int32_t n_blist;
     int32_t fq_n;                                      // pending handed-off jobs (register mirror)
-    bool wdirty;
+    bool wdirty;                                       // `due` changed: recompute the earliest due worker
+    uint32_t due;                                      // workers whose service timer fires in this window
     // server lane's register copies during phase A (loaded/stored around it)
     uint32_t stored_mask, lq_head, lq_tail, lq_stamp, lq_mask;
     bool cache_on, spec_on;
@@ -218,7 +233,7 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
 // stores -- no dependent loads on the server lane -- and evictions read the
 // queue sequentially.  The queue is compacted (warp-parallel, order kept)
 // before it can overflow.
-__device__ __noinline__ uint32_t lq_compact_serial(LqEnt *lq, const uint8_t *dflags, const uint32_t *lstamp,
+__device__ __noinline__ uint32_t lq_compact_serial(LqEnt *lq, const uint16_t *dflags, const uint32_t *lstamp,
                                                    uint32_t head, uint32_t tail, uint32_t mask);
 
 __device__ __forceinline__ void lru_touch(Win &w, int32_t d) {
@@ -231,7 +246,7 @@ __device__ __forceinline__ void lru_touch(Win &w, int32_t d) {
     w.lq_tail++;
 }
 __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache.py:45-52
-    if (!(w.dflags[d] & D_CACHED)) { w.c_miss++; return false; }
+    if (!(w.dflags[d] & DF_CACHED)) { w.c_miss++; return false; }
     lru_touch(w, d);
     w.c_hits++;
     return true;
@@ -239,35 +254,35 @@ __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache
 __device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
     const int64_t cap = w.capacity;
     if (size > cap) { w.c_reject++; return; }
-    if (w.dflags[d] & D_CACHED) {                      // replace: its old queue entry goes stale
+    if (w.dflags[d] & DF_CACHED) {                     // replace: its old queue entry goes stale
         w.cur_bytes -= size;
-        w.dflags[d] &= ~D_CACHED;
+        w.dflags[d] &= (uint16_t)~DF_CACHED;
         w.entries--;
     }
     while (w.cur_bytes + size > cap) {                 // popitem(last=False): oldest live entry
         LqEnt e = w.lq[w.lq_head & w.lq_mask];
         w.lq_head++;
         int32_t v = e.desc;
-        if (!(w.dflags[v] & D_CACHED) || w.lstamp[v] != e.stamp) continue;
-        w.dflags[v] &= ~D_CACHED;
+        if (!(w.dflags[v] & DF_CACHED) || w.lstamp[v] != e.stamp) continue;
+        w.dflags[v] &= (uint16_t)~DF_CACHED;
         w.entries--;
         w.cur_bytes -= w.S.size(v);
         w.c_evict++;
     }
     lru_touch(w, d);
-    w.dflags[d] |= D_CACHED;
+    w.dflags[d] |= DF_CACHED;
     w.entries++;
     w.cur_bytes += size;
 }
 
 // Drop stale queue entries in place, keeping order (lane 0; only if a window
 // overran the pre-window compaction margin).
-__device__ __noinline__ uint32_t lq_compact_serial(LqEnt *lq, const uint8_t *dflags, const uint32_t *lstamp,
+__device__ __noinline__ uint32_t lq_compact_serial(LqEnt *lq, const uint16_t *dflags, const uint32_t *lstamp,
                                                    uint32_t head, uint32_t tail, uint32_t mask) {
     uint32_t o = head;
     for (uint32_t i = head; i != tail; i++) {
         LqEnt e = lq[i & mask];
-        if ((dflags[e.desc] & D_CACHED) && lstamp[e.desc] == e.stamp) lq[(o++) & mask] = e;
+        if ((dflags[e.desc] & DF_CACHED) && lstamp[e.desc] == e.stamp) lq[(o++) & mask] = e;
     }
     return o;
 }
@@ -286,7 +301,7 @@ __device__ void lq_compact_warp(Win &w, int lane) {
         LqEnt e;
         if (i < tail) {
             e = w.lq[i & (cap - 1)];
-            keep = (w.dflags[e.desc] & D_CACHED) && w.lstamp[e.desc] == e.stamp;
+            keep = (w.dflags[e.desc] & DF_CACHED) && w.lstamp[e.desc] == e.stamp;
         }
         unsigned m = __ballot_sync(0xffffffffu, keep);
         if (keep) dst[out + __popc(m & ((1u << lane) - 1))] = e;
@@ -310,9 +325,7 @@ __device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
         return true;
     }
     int32_t j = w.S.record_job(d, origin, w.now);
-    w.dflags[d] |= D_INFLIGHT;
-    w.wq_head[d] = -1;
-    w.wq_tail[d] = -1;
+    w.dflags[d] = (uint16_t)((w.dflags[d] & DF_CACHED) | DF_NOWAIT);   // in flight, no waiter yet
     if (prio) {                                        // separate FIFOs + _wakeup.put_nowait(None, force=True)
         JobEnt e; e.desc = d; e.job = j;
         if (origin == OTF_ORIGIN_SPECULATIVE) {
@@ -361,9 +374,9 @@ __device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, in
     if (index + 1 >= w.S.segcounts[seq]) { w.c_skip[1]++; return; }
     if ((w.stored_mask >> rank) & 1u) { w.c_skip[2]++; return; }
     int32_t nd = d + 1;                                // same (seq, rank), index + 1
-    uint8_t f = w.dflags[nd];
-    if (w.cache_on && (f & D_CACHED)) { w.c_skip[3]++; return; }
-    if (f & D_INFLIGHT) { w.c_skip[4]++; return; }
+    uint16_t f = w.dflags[nd];
+    if (w.cache_on && (f & DF_CACHED)) { w.c_skip[3]++; return; }
+    if (df_inflight(f)) { w.c_skip[4]++; return; }
     if (enqueue_job(w, nd, OTF_ORIGIN_SPECULATIVE)) { w.c_skip[5]++; return; }
     w.c_spec++;
 }
@@ -380,22 +393,31 @@ __device__ __forceinline__ void respond(Win &w, int32_t cid) {
 }
 
 __device__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
-    if (!(w.dflags[d] & D_INFLIGHT)) return;
-    w.dflags[d] &= ~D_INFLIGHT;
-    int32_t c = w.wq_head[d];
-    while (c >= 0) {                                   // waiter Future callbacks, await order
-        int32_t nxt = w.bnext[c];
+    const uint16_t f = w.dflags[d];
+    if (!df_inflight(f)) return;
+    w.dflags[d] = (uint16_t)((f & DF_CACHED) | DF_IDLE);
+    const int32_t t = f & 0x7FFF;
+    if (t == DF_NOWAIT) return;
+    int32_t c = w.bnext[t];                            // head: waiter Future callbacks, await order
+    for (;;) {
+        const int32_t nxt = w.bnext[c];
         respond(w, c);
+        if (c == t) break;
         c = nxt;
     }
 }
 
-// waiter links reuse bnext: a waiting client has no pending timer
+// Append a waiter (waiter links reuse bnext: a waiting client has no pending timer).
 __device__ __forceinline__ void add_waiter(Win &w, int32_t d, int32_t cid) {
-    w.bnext[cid] = NIL;
-    int32_t t = w.wq_tail[d];
-    if (t >= 0) w.bnext[t] = (int16_t)cid; else w.wq_head[d] = cid;
-    w.wq_tail[d] = cid;
+    const uint16_t f = w.dflags[d];
+    const int32_t t = f & 0x7FFF;
+    if (t == DF_NOWAIT) {
+        w.bnext[cid] = (int16_t)cid;
+    } else {
+        w.bnext[cid] = w.bnext[t];
+        w.bnext[t] = (int16_t)cid;
+    }
+    w.dflags[d] = (uint16_t)((f & DF_CACHED) | cid);
 }
 
 // Backend._next_job (backend.py:174-184): a job now (no yield), or the worker
@@ -427,7 +449,7 @@ __device__ bool take_job(Win &w, int32_t wid, int32_t &d, int32_t &j) {
         h->gq_n++;
         h->wk[wid].pc = W_GOT;
         h->wk[wid].win = WIN_NONE;
-        w.wdirty = true;
+        if (w.due & (1u << wid)) { w.due &= ~(1u << wid); w.wdirty = true; }
         return false;
     }
 }
@@ -437,7 +459,7 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
     WinHeader *h = w.h;
     const otf_scenario &sc = *w.S.sc;
     for (;;) {
-        if (w.cache_on && (w.dflags[d] & D_CACHED)) {   // dedup on dequeue (backend.py:193-198)
+        if (w.cache_on && (w.dflags[d] & DF_CACHED)) {  // dedup on dequeue (backend.py:193-198)
             w.S.job_outcome(j, OTF_OUTCOME_DROPPED);
             w.c_wasted++;
             resolve(w, d);
@@ -455,7 +477,7 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
             k.job = j;
             k.size = w.S.size(d);
             k.pc = W_SERVICE;
-            w.wdirty = true;
+            if (k.win == w.k) { w.due |= 1u << wid; w.wdirty = true; }   // fires in this window (rare)
             return;
         }
         if (!take_job(w, wid, d, j)) return;
@@ -489,20 +511,21 @@ __device__ void server_request(Win &w, int32_t cid, int32_t d, int32_t rank, int
         c.path = OTF_PATH_CACHE;
         respond(w, cid);
     } else {
-        if (w.dflags[d] & D_INFLIGHT) {
+        if (df_inflight(w.dflags[d])) {
             maybe_speculate(w, d, rank, seq, index);
             c.path = OTF_PATH_WAITED;
+            c.pc = C_SEG_WAIT;
+            add_waiter(w, d, cid);
         } else if (enqueue_job(w, d, OTF_ORIGIN_DEMAND)) {
             c.path = OTF_PATH_ERROR;                   // OverloadError: error record (server.py:70-73)
             respond(w, cid);
             c.pc = C_SEG_ERR;
-            return;
         } else {
             maybe_speculate(w, d, rank, seq, index);
             c.path = OTF_PATH_TRANSCODED;
+            c.pc = C_SEG_WAIT;
+            add_waiter(w, d, cid);
         }
-        c.pc = C_SEG_WAIT;
-        add_waiter(w, d, cid);
     }
 }
 
@@ -511,6 +534,7 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
     WWorker &k = w.h->wk[wid];
     int32_t d = k.desc, j = k.job;
     k.win = WIN_NONE;
+    w.due &= ~(1u << wid);
     w.wdirty = true;
     w.S.job_finished(j, w.now);
     if (w.cache_on) cache_put(w, d, k.size);
@@ -539,6 +563,9 @@ __device__ void phase_a(Win &w) {
     for (int q = 0; q < 6; q++) w.c_skip[q] = 0;
     w.n_blist = h->n_blist;
     w.fq_n = h->fq_n;
+    uint32_t due = 0;
+    for (int32_t q = 0; q < K; q++) due |= (h->wk[q].win == w.k ? 1u : 0u) << q;
+    w.due = due;
     w.wdirty = true;
     int32_t bw = -1;
     double bw_when = 0.0, bw_ctime = 0.0;
@@ -548,9 +575,9 @@ __device__ void phase_a(Win &w) {
     for (;;) {
         if (w.wdirty) {                                // earliest worker timer in this window
             bw = -1;
-            for (int32_t q = 0; q < K; q++) {
+            for (uint32_t mm = w.due; mm; mm &= mm - 1) {
+                const int32_t q = __ffs(mm) - 1;
                 const WWorker &x = h->wk[q];
-                if (x.win != w.k) continue;
                 if (bw < 0 || x.when < bw_when || (x.when == bw_when && (x.ctime < bw_ctime ||
                                                        (x.ctime == bw_ctime && x.seq < h->wk[bw].seq)))) {
                     bw = q; bw_when = x.when; bw_ctime = x.ctime;
@@ -571,17 +598,32 @@ __device__ void phase_a(Win &w) {
             else { w.S.flag(OTF_S_TIE); take_worker = true; }
         }
         pops++;
+#ifdef WIN_DIAG
+        long long dg0 = clock64();
+#endif
         if (take_worker) {
             w.now = bw_when;
             server_worker_done(w, bw);
+#ifdef WIN_DIAG
+            h->stats[30] += clock64() - dg0;
+#endif
         } else {
             w.now = cw;
             int32_t pk = w.lp[i];
             server_request(w, w.li[i], w.ld[i], pk & 0xff, pk >> 16, (pk >> 8) & 0xff);
             i++;
             if (i < n) cw = w.lw[i];
+#ifdef WIN_DIAG
+            h->stats[29] += clock64() - dg0;
+#endif
         }
+#ifdef WIN_DIAG
+        long long dg1 = clock64();
+#endif
         if (w.fq_n > 0) drain_handoffs(w);
+#ifdef WIN_DIAG
+        h->stats[31] += clock64() - dg1;
+#endif
     }
     h->stats[OTF_ST_TIMER_POPS] += pops;
     h->st.cur_bytes = w.cur_bytes;
@@ -843,7 +885,7 @@ __device__ void order_ties(Win &w) {
         int32_t j = i;                                 // insertion step by ctime
         while (j > 0 && w.lw[j] == w.lw[j - 1]) {
             double cj = w.cl[w.li[j]].ctime, cp = w.cl[w.li[j - 1]].ctime;
-            if (cj == cp) { h->st.status |= OTF_S_TIE; break; }
+            if (cj == cp) { atomicOr(&h->st.status, OTF_S_TIE); break; }
             if (cj > cp) break;
             int16_t ti = w.li[j]; w.li[j] = w.li[j - 1]; w.li[j - 1] = ti;
             int16_t td = w.ld[j]; w.ld[j] = w.ld[j - 1]; w.ld[j - 1] = td;
@@ -876,15 +918,33 @@ __device__ int32_t wheel_next(WinHeader *h, int32_t k_done, int lane) {
     return warp_min(best);
 }
 
+// Window-loop control word (shared): what both warps do after the selection step.
+enum { CTL_RUN = 0, CTL_REFILE = 1, CTL_STOP = 2 };
+
+// Two warps per scenario.  Warp 0 selects the next window, pops its buckets and
+// sorts the server events; then, concurrently, lane 0 of warp 0 replays the
+// server events (phase A) while warp 1 runs the window's client-local timers
+// (clients with a local timer due are never touched by phase A: they are not
+// waiting on the backend and have no pending request).  Finally both warps run
+// the clients phase A responded to.
 template <bool RECORDS>
-__global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
+// 7 CTAs per SM run 1,024 scenarios on 148 SMs in one wave.  The register file
+// is split over the 4 SM sub-partitions (16k each), so 2 warps per CTA cap the
+// kernel at 128 registers; one warp per CTA leaves it ~210.
+#if WIN_WARPS == 1
+#define WIN_BOUNDS __launch_bounds__(32, 8)
+#else
+#define WIN_BOUNDS __launch_bounds__(WIN_THREADS, 7)
+#endif
+__global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     long long t_start = 0, t0 = 0, t1 = 0;
     const int32_t s = b.order ? b.order[blockIdx.x] : (int32_t)blockIdx.x;
     WinHeader *h = (WinHeader *)smem;
-    if (lane == 0) { h->b = b; h->sc = b.scenarios[s]; }
-    __syncwarp();
+    if (tid == 0) { h->b = b; h->sc = b.scenarios[s]; }
+    __syncthreads();
     Win w;
     w.S.init(&h->b, &h->sc, s);
     w.S.records = RECORDS;                             // compile-time: histogram kernels carry no record code
@@ -902,7 +962,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     w.h = h;
     w.bnext = (int16_t *)p; p += 2 * (int64_t)N;
     p = (uint8_t *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    w.dflags = p;
+    w.dflags = (uint16_t *)p;
     w.lstamp = (uint32_t *)(g + L.lstamp);
     w.lq = (LqEnt *)(g + L.lq);
     w.cl = (Client *)(g + L.clients);
@@ -912,8 +972,6 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     w.bloc = (int32_t *)(g + L.bloc);
     w.scap = bucket_cap_srv(N);
     w.lcap = bucket_cap_loc(N);
-    w.wq_head = (int32_t *)(g + L.wq_head);
-    w.wq_tail = (int32_t *)(g + L.wq_tail);
     w.jq = (JobEnt *)(g + L.jobq);
     w.sq = (JobEnt *)(g + L.specq);
     // counters, QoE and small tables live in shared memory
@@ -929,7 +987,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     // ---- init -------------------------------------------------------------------
     const bool fits = K <= MAXK && N <= MAXN && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB && D < 32767 &&
                       sc.latency > 0 && sc.horizon / (sc.latency * (1.0 - 0x1p-20)) < 5.0e8;
-    if (lane == 0) {
+    if (tid == 0) {
         EngineState z = {};
         z.lru_head = z.lru_tail = -1;
         h->st = z;
@@ -944,34 +1002,34 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         h->ovf_head = -1; h->ovf_n = 0; h->ovf_min = WIN_NONE; h->n_loc = 0;
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
         h->list_cap = lcap;
+        h->ctl = CTL_RUN; h->cur_m = 0;
         if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
     }
-    __syncwarp();
+    __syncthreads();
     if (!fits) goto done;
-    for (int32_t q = lane; q < MAXK; q += 32) {
+    for (int32_t q = tid; q < MAXK; q += WIN_THREADS) {
         h->gq[q] = q;                                  // workers register as getters in id order
         WWorker z = {};
         z.win = WIN_NONE; z.pc = W_GOT; z.desc = -1; z.job = -1;
         h->wk[q] = z;
     }
-    for (int32_t i = lane; i < RING; i += 32) { h->cnt_srv[i] = 0; h->cnt_loc[i] = 0; }
-    for (int32_t i = lane; i < RING / 32; i += 32) h->bits[i] = 0;
-    for (int32_t i = lane; i < sc.n_seq; i += 32) {
+    for (int32_t i = tid; i < RING; i += WIN_THREADS) { h->cnt_srv[i] = 0; h->cnt_loc[i] = 0; }
+    for (int32_t i = tid; i < RING / 32; i += WIN_THREADS) h->bits[i] = 0;
+    for (int32_t i = tid; i < sc.n_seq; i += WIN_THREADS) {
         h->t_segcount[i] = w.S.segcounts[i];
         h->t_seqdur[i] = w.S.seqdur[i];
         h->t_segdur[i] = w.S.segdur[i];
         h->t_zipf[i] = w.S.zipf[i];
         h->t_manifest[i] = w.S.manifest_b[i];
     }
-    for (int32_t i = lane; i < sc.n_ranks; i += 32) {
+    for (int32_t i = tid; i < sc.n_ranks; i += WIN_THREADS) {
         h->t_rho[i] = w.S.rho[i];
         h->t_bitrates[i] = w.S.bitrates[i];
     }
-    for (int64_t d = lane; d < D; d += 32) {
-        w.lstamp[d] = 0; w.dflags[d] = 0;
-        w.wq_head[d] = -1; w.wq_tail[d] = -1;
+    for (int64_t d = tid; d < D; d += WIN_THREADS) {
+        w.lstamp[d] = 0; w.dflags[d] = DF_IDLE;
     }
-    __syncwarp();
+    __syncthreads();
     w.S.segcounts = h->t_segcount;
     w.S.seqdur = h->t_seqdur;
     w.S.segdur = h->t_segdur;
@@ -981,7 +1039,7 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
     w.S.bitrates = h->t_bitrates;
     // clients: the first step arms sleep(offset) (orchestrator.py:337); offsets are a
     // cumulative sum, so clients join the wheel in id order (arrival cursor below)
-    for (int32_t c = lane; c < N; c += 32) {
+    for (int32_t c = tid; c < N; c += WIN_THREADS) {
         Client &cl = w.cl[c];
         client_init(cl);
         double off = w.S.arrival(c);
@@ -990,159 +1048,174 @@ __global__ void __launch_bounds__(32, 8) windowed_kernel(const otf_batch b) {
         cl.next_when = 0.0 + off;
         if (!(off > 0)) w.S.flag(OTF_S_TIE);           // instant start: tick order among clients matters
     }
-    __syncwarp();
+    __syncthreads();
     if (h->st.status & OTF_S_TIE) goto done;
 
     // ---- window loop --------------------------------------------------------------
     t_start = clock64();
     for (;;) {
-        t0 = clock64();
-        // next window: wheel, far list, worker timers, next arrival
-        int32_t m = wheel_next(h, h->k_done, lane);
-        int32_t mw = lane < K ? h->wk[lane].win : WIN_NONE;
-        m = min(m, warp_min(mw));
-        m = min(m, h->far_min);
-        int32_t arr_win = WIN_NONE;
-        if (h->arr_next < N) arr_win = timer_win(w, w.S.arrival(h->arr_next));
-        m = min(m, arr_win);
-        if (m == WIN_NONE) break;
-        if (arr_win != WIN_NONE && arr_win - m < RING) {   // arrivals entering the wheel
-            if (lane == 0) {
-                h->k_done = m - 1;                     // windows before m are empty: wheel base = m
-                w.k = m - 1;
-                int32_t c = h->arr_next;
-                while (c < N) {
-                    int32_t wk = timer_win(w, w.S.arrival(c));
-                    if (wk == WIN_NONE || wk - m >= RING) break;
-                    bucket_push(w, c, wk, false);
-                    c++;
+        if (warp == 0) {
+            t0 = clock64();
+            // next window: wheel, far list, worker timers, next arrival
+            int32_t m = wheel_next(h, h->k_done, lane);
+            int32_t mw = lane < K ? h->wk[lane].win : WIN_NONE;
+            m = min(m, warp_min(mw));
+            m = min(m, h->far_min);
+            int32_t arr_win = WIN_NONE;
+            if (h->arr_next < N) arr_win = timer_win(w, w.S.arrival(h->arr_next));
+            m = min(m, arr_win);
+            int32_t ctl = CTL_RUN;
+            if (m == WIN_NONE) {
+                ctl = CTL_STOP;
+            } else {
+                if (arr_win != WIN_NONE && arr_win - m < RING) {   // arrivals entering the wheel
+                    if (lane == 0) {
+                        h->k_done = m - 1;                 // windows before m are empty: wheel base = m
+                        w.k = m - 1;
+                        int32_t c = h->arr_next;
+                        while (c < N) {
+                            int32_t wk = timer_win(w, w.S.arrival(c));
+                            if (wk == WIN_NONE || wk - m >= RING) break;
+                            bucket_push(w, c, wk, false);
+                            c++;
+                        }
+                        h->arr_next = c;
+                    }
+                    __syncwarp();
                 }
-                h->arr_next = c;
-            }
-            __syncwarp();
-        }
-        if (h->far_n > 0 && h->far_min < m + RING / 2) {   // far timers close to the wheel: re-file them
-            if (lane == 0) {
-                int32_t c = h->far_head;
-                h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
-                h->k_done = m - 1;                     // windows before m are empty: wheel base = m
-                w.k = m - 1;
-                while (c >= 0) {
-                    int32_t nx = w.bnext[c];
-                    const Client &cl = w.cl[c];
-                    bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT);
-                    c = nx;
+                if (h->far_n > 0 && h->far_min < m + RING / 2) {   // far timers close to the wheel: re-file
+                    if (lane == 0) {
+                        int32_t c = h->far_head;
+                        h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE;
+                        h->k_done = m - 1;                 // windows before m are empty: wheel base = m
+                        w.k = m - 1;
+                        while (c >= 0) {
+                            int32_t nx = w.bnext[c];
+                            const Client &cl = w.cl[c];
+                            bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT);
+                            c = nx;
+                        }
+                    }
+                    __syncwarp();
+                    ctl = CTL_REFILE;
                 }
             }
-            __syncwarp();
-            continue;
+            if (ctl == CTL_RUN) {
+                w.k = m;
+                w.E = (double)(m + 1) * w.W;
+                if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
+                // pop the buckets: the window's arrays are read by all lanes at once
+                const int32_t slot = m & (RING - 1);
+                const int32_t ns = min(h->cnt_srv[slot], w.scap);
+                const int32_t nl = min(h->cnt_loc[slot], w.lcap);
+                int32_t n_ovf = 0, nb = 0;
+                if (h->ovf_n > 0 && h->ovf_min <= m) {     // overflowed pushes due now (rare)
+                    if (lane == 0) {
+                        int32_t c = h->ovf_head, keep = -1, rem = WIN_NONE, kept = 0;
+                        while (c >= 0) {
+                            int32_t nx = w.bnext[c];
+                            const Client &cl = w.cl[c];
+                            int32_t wk = timer_win(w, cl.next_when);
+                            if (wk == m) {
+                                if (cl.pc == C_SEG_LAT) { if (ns + n_ovf < h->list_cap) w.li[ns + n_ovf] = (int16_t)c; n_ovf++; }
+                                else w.blist[nb++] = c;
+                            } else {
+                                w.bnext[c] = (int16_t)keep; keep = c; kept++;
+                                rem = min(rem, wk);
+                            }
+                            c = nx;
+                        }
+                        h->ovf_head = keep; h->ovf_n = kept; h->ovf_min = rem;
+                        h->n_list = ns + n_ovf;
+                        h->n_blist = nb;
+                    }
+                    __syncwarp();
+                    n_ovf = h->n_list - ns;
+                    nb = h->n_blist;
+                }
+                const int32_t nlist = ns + n_ovf;
+                if (nlist > h->list_cap) {                 // too many simultaneous requests for this engine
+                    if (lane == 0) atomicOr(&h->st.status, OTF_S_TIE);
+                    ctl = CTL_STOP;
+                } else {
+                    const int32_t *as = w.bsrv + (int64_t)slot * w.scap;
+                    for (int32_t i = lane; i < nlist; i += 32) {   // gather sort keys + request descriptors
+                        int32_t c = i < ns ? as[i] : w.li[i];
+                        const Client &cl = w.cl[c];
+                        w.li[i] = (int16_t)c;
+                        w.lw[i] = cl.next_when;
+                        w.ld[i] = (int16_t)cl.desc;
+                        w.lp[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        h->stats[OTF_ST_WINDOWS]++;
+                        h->cnt_srv[slot] = 0;
+                        h->cnt_loc[slot] = 0;
+                        h->bits[slot >> 5] &= ~(1u << (slot & 31));
+                        h->n_list = nlist;
+                        h->n_blist = nb;
+                        h->n_loc = nl;
+                        h->cur_m = m;
+                    }
+                    __syncwarp();
+                    t1 = clock64();
+                    if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
+                    t0 = t1;
+                    sort_list(w, lane);
+                    t1 = clock64();
+                    if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
+                }
+            }
+            if (lane == 0) h->ctl = ctl;
         }
+        __syncthreads();
+        const int32_t ctl = h->ctl;
+        if (ctl == CTL_STOP) break;
+        if (ctl == CTL_REFILE) continue;
+        const int32_t m = h->cur_m;
         w.k = m;
         w.E = (double)(m + 1) * w.W;
-        if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
-        if (lane == 0) h->stats[28] += clock64() - t0;  // profile: next-window selection
-        long long tp = clock64();
-        {
-            // pop the buckets: the window's arrays are read by all lanes at once
-            const int32_t slot = m & (RING - 1);
-            const int32_t ns = min(h->cnt_srv[slot], w.scap);
-            const int32_t nl = min(h->cnt_loc[slot], w.lcap);
-            int32_t n_ovf = 0, nb = 0;
-            if (h->ovf_n > 0 && h->ovf_min <= m) {     // overflowed pushes due now (rare)
-                if (lane == 0) {
-                    int32_t c = h->ovf_head, keep = -1, rem = WIN_NONE, kept = 0;
-                    while (c >= 0) {
-                        int32_t nx = w.bnext[c];
-                        const Client &cl = w.cl[c];
-                        int32_t wk = timer_win(w, cl.next_when);
-                        if (wk == m) {
-                            if (cl.pc == C_SEG_LAT) { if (ns + n_ovf < h->list_cap) w.li[ns + n_ovf] = (int16_t)c; n_ovf++; }
-                            else w.blist[nb++] = c;
-                        } else {
-                            w.bnext[c] = (int16_t)keep; keep = c; kept++;
-                            rem = min(rem, wk);
-                        }
-                        c = nx;
-                    }
-                    h->ovf_head = keep; h->ovf_n = kept; h->ovf_min = rem;
-                    h->n_list = ns + n_ovf;
-                    h->n_blist = nb;
-                }
-                __syncwarp();
-                n_ovf = h->n_list - ns;
-                nb = h->n_blist;
-            }
-            const int32_t nlist = ns + n_ovf;
-            if (nlist > h->list_cap) {                 // too many simultaneous requests for this engine
-                if (lane == 0) h->st.status |= OTF_S_TIE;
-                __syncwarp();
-                break;
-            }
-            const int32_t *as = w.bsrv + (int64_t)slot * w.scap;
-            const int32_t *al = w.bloc + (int64_t)slot * w.lcap;
-            for (int32_t i = lane; i < nl; i += 32) {  // warm L2 with this window's client states
-                const char *ptr = (const char *)&w.cl[al[i]];
-                asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
-                asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr + 128));
-            }
-            if (lane == 0) h->stats[29] += clock64() - tp;  // profile: bucket pop
-            for (int32_t i = lane; i < nlist; i += 32) {   // gather sort keys + request descriptors
-                int32_t c = i < ns ? as[i] : w.li[i];
-                const Client &cl = w.cl[c];
-                w.li[i] = (int16_t)c;
-                w.lw[i] = cl.next_when;
-                w.ld[i] = (int16_t)cl.desc;
-                w.lp[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                h->stats[OTF_ST_WINDOWS]++;
-                h->cnt_srv[slot] = 0;
-                h->cnt_loc[slot] = 0;
-                h->bits[slot >> 5] &= ~(1u << (slot & 31));
-                h->n_list = nlist;
-                h->n_blist = nb;
-                h->n_loc = nl;
-            }
-            __syncwarp();
-        }
-        t1 = clock64();
-        if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
-        t0 = t1;
-        sort_list(w, lane);
-        t1 = clock64();
-        if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
-        t0 = t1;
-        // ---- phase A: server lane ----
-        if (lane == 0) {
+        t0 = clock64();
+        // thread 0 = the server lane; with two warps, warp 1 runs the local timers meanwhile
+        if (tid == 0) {
+            // ---- phase A: server lane ----
             if (h->n_ties) order_ties(w);
             phase_a(w);
             h->k_done = m;
+            h->stats[OTF_ST_CYC_SERVER] += clock64() - t0;
         }
-        __syncwarp();
-        t1 = clock64();
-        if (lane == 0) h->stats[OTF_ST_CYC_SERVER] += t1 - t0;
-        t0 = t1;
-        if (h->st.status & OTF_S_TIE) break;
-        // ---- phase B: client lanes ----
-        {
-            const int32_t nl = h->n_loc, nb = h->n_blist;
+        if (WIN_WARPS == 1) __syncwarp();
+        if (WIN_WARPS == 1 || warp > 0) {
+            // ---- phase B1: the window's client-local timers (concurrent with phase A on 2 warps) ----
+            constexpr int B1_THREADS = WIN_WARPS == 1 ? 32 : WIN_THREADS - 32;
+            const int b1 = WIN_WARPS == 1 ? tid : tid - 32;
+            const long long tb = clock64();
+            const int32_t nl = h->n_loc;
             const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
-            for (int32_t i = lane; i < nl + nb; i += 32) client_local(w, i < nl ? al[i] : w.blist[i - nl]);
+            for (int32_t i = b1; i < nl; i += B1_THREADS) client_local(w, al[i]);
+            if (b1 == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
         }
-        __syncwarp();
-        t1 = clock64();
-        if (lane == 0) h->stats[OTF_ST_CYC_CLIENTS] += t1 - t0;
+        __syncthreads();
+        if (h->st.status & OTF_S_TIE) break;
+        // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
+        t0 = clock64();
+        {
+            const int32_t nb = h->n_blist;
+            for (int32_t i = tid; i < nb; i += WIN_THREADS) client_local(w, w.blist[i]);
+        }
+        __syncthreads();
+        if (tid == 0) h->stats[OTF_ST_CYC_CLIENTS] += clock64() - t0;
     }
-    if (lane == 0) h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
+    if (tid == 0) h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
     if (!(h->st.status & OTF_S_TIE)) {
-        for (int32_t c = lane; c < N; c += 32) client_harvest(w.S, w.cl[c], sc.horizon);
+        for (int32_t c = tid; c < N; c += WIN_THREADS) client_harvest(w.S, w.cl[c], sc.horizon);
     }
-    __syncwarp();
+    __syncthreads();
 done:
-    if (lane == 0) {
+    if (tid == 0) {
         int64_t *gs = b.stats + (int64_t)s * OTF_ST_NSLOTS;
         h->stats[OTF_ST_CACHE_CAPACITY] = sc.cache_capacity;
         h->stats[OTF_ST_CURRENT_BYTES] = h->st.cur_bytes;
@@ -1153,13 +1226,26 @@ done:
         cnt[0] = h->st.n_req; cnt[1] = h->st.n_sess; cnt[2] = h->st.n_seg; cnt[3] = h->st.n_job;
         b.status[s] = h->st.status;
     }
-    // float sums: fixed-order warp reduction, then lane 0 writes the QoE block
+    // float sums: fixed-order reduction (lanes, then warps), then thread 0 writes the QoE block
     for (int o = 16; o > 0; o >>= 1) {
         w.S.lat_sum += __shfl_down_sync(0xffffffffu, w.S.lat_sum, o);
         w.S.stall_sum += __shfl_down_sync(0xffffffffu, w.S.stall_sum, o);
         w.S.startup_sum += __shfl_down_sync(0xffffffffu, w.S.startup_sum, o);
     }
-    if (lane == 0) w.S.flush_qoe();
+    if (lane == 0 && warp > 0) {
+        h->wsum[warp - 1][0] = w.S.lat_sum;
+        h->wsum[warp - 1][1] = w.S.stall_sum;
+        h->wsum[warp - 1][2] = w.S.startup_sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int q = 1; q < WIN_WARPS; q++) {
+            w.S.lat_sum += h->wsum[q - 1][0];
+            w.S.stall_sum += h->wsum[q - 1][1];
+            w.S.startup_sum += h->wsum[q - 1][2];
+        }
+        w.S.flush_qoe();
+    }
 }
 
 }  // namespace otf
@@ -1180,6 +1266,6 @@ int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return 1;
     }
-    kern<<<b.n_scenarios, 32, smem, stream>>>(b);
+    kern<<<b.n_scenarios, otf::WIN_THREADS, smem, stream>>>(b);
     return 0;
 }

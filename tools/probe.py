@@ -23,7 +23,19 @@ def timeit(name, cfgs, eng, reps=2):
         print("  windows/scn", st[22] / len(cfgs), "cycles/window", tot / max(1, st[22]),
               "scan %.2f sort %.2f server %.2f clients %.2f" % (st[23]/tot, st[24]/tot, st[25]/tot, st[26]/tot),
               "pops/scn", st[20]/len(cfgs), "ready", st[21]/len(cfgs),
-              "| select %.2f pop %.2f" % (st[28]/tot, st[29]/tot))
+              "| local(concurrent) %.2f" % (st[28]/tot))
+        if os.environ.get("OTF_DIAG"):
+            for name, rows in (("all", slice(None)), ("TCP", [i for i in range(len(cfgs)) if i % 16 in (4, 5, 6, 7)])):
+                S = br.stats[rows].sum(0).astype(float)
+                print("  diag[%s]: per window: server %.0f requests %.0f workers %.0f handoffs %.0f clients %.0f local %.0f "
+                      "scan %.0f sort %.0f cycles; requests/window %.1f" % (name,
+                      S[25] / S[22], S[29] / S[22], S[30] / S[22], S[31] / S[22], S[26] / S[22], S[28] / S[22],
+                      S[23] / S[22], S[24] / S[22], br.counts[rows, 0].sum() / S[22]))
+        per = br.stats[:, 27].astype(float)
+        print("  scenario cycles: mean %.3g max %.3g (max/mean %.3f), max at %d" % (per.mean(), per.max(), per.max() / per.mean(), per.argmax()))
+        if len(cfgs) % 16 == 0:
+            g = per.reshape(-1, 16).mean(0)
+            print("  by (variant, fraction) slot:", " ".join("%.3g" % x for x in g))
     print(json.dumps(dict(name=name, engine=eng, scenarios=len(cfgs), build_s=round(t1-t0,2), ms=round(best,2),
                           requests=req, req_per_s=req/(best/1e3), status=int(br.status.max()))), flush=True)
 
