@@ -148,7 +148,7 @@ __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_d
     o += 16 * (int64_t)win_list_cap(n_clients);   // when f64, pack i32, id i16, desc i16
     o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
     o = (o + 15) & ~(int64_t)15;
-    o += 2 * n_desc;                      // descriptor words (DF_*)
+    o += 2 * (n_desc + 1);                // descriptor words (DF_*), +1: the server lane reads d + 1 early
     return (o + 15) & ~(int64_t)15;
 }
 
@@ -369,18 +369,6 @@ __device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
     return false;
 }
 
-__device__ void maybe_speculate(Win &w, int32_t d, int32_t rank, int32_t seq, int32_t index) {  // backend.py:135-154
-    if (!w.spec_on) { w.c_skip[0]++; return; }
-    if (index + 1 >= w.S.segcounts[seq]) { w.c_skip[1]++; return; }
-    if ((w.stored_mask >> rank) & 1u) { w.c_skip[2]++; return; }
-    int32_t nd = d + 1;                                // same (seq, rank), index + 1
-    uint16_t f = w.dflags[nd];
-    if (w.cache_on && (f & DF_CACHED)) { w.c_skip[3]++; return; }
-    if (df_inflight(f)) { w.c_skip[4]++; return; }
-    if (enqueue_job(w, nd, OTF_ORIGIN_SPECULATIVE)) { w.c_skip[5]++; return; }
-    w.c_spec++;
-}
-
 // Response of MediaServer.segment (server.py:76-77): fix the record's slot
 // in response order and hand the client back to the client lanes at `now`.
 // The record itself and the request QoE are written by the client lane.
@@ -497,35 +485,58 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
     }
 }
 
-// One client server event: MediaServer.segment + Backend.handle (server.py:61-78, backend.py:115-133)
-__device__ void server_request(Win &w, int32_t cid, int32_t d, int32_t rank, int32_t seq, int32_t index) {
-    const otf_scenario &sc = *w.S.sc;
+// Backend.maybe_speculate (backend.py:135-154) for a request on d whose rank is
+// not stored, with the next descriptor's word `fn` and the sequence's segment
+// count already loaded.
+__device__ __forceinline__ void speculate_next(Win &w, int32_t d, int32_t index, int32_t segc, uint16_t fn) {
+    if (!w.spec_on) { w.c_skip[0]++; return; }
+    if (index + 1 >= segc) { w.c_skip[1]++; return; }
+    if (w.cache_on && (fn & DF_CACHED)) { w.c_skip[3]++; return; }
+    if (df_inflight(fn)) { w.c_skip[4]++; return; }
+    if (enqueue_job(w, d + 1, OTF_ORIGIN_SPECULATIVE)) { w.c_skip[5]++; return; }
+    w.c_spec++;
+}
+
+// One client server event: MediaServer.segment + Backend.handle (server.py:61-78,
+// backend.py:115-133), with every shared-memory word it branches on loaded up front
+// (the descriptor's word f, the next descriptor's word fn, the sequence's
+// segment count), so the server lane pays one shared-memory round trip per
+// request instead of a chain of them.
+__device__ __forceinline__ void server_request_fast(Win &w, int32_t cid, int32_t d, int32_t pk, uint16_t f,
+                                                    uint16_t fn, int32_t segc) {
+    const int32_t rank = pk & 0xff, index = (pk >> 8) & 0xff;
     Client &c = w.cl[cid];
     c.req_id = (int32_t)w.req_counter++;
     c.arrival = w.now;
     if ((w.stored_mask >> rank) & 1u) {
         c.path = OTF_PATH_STORAGE;
         respond(w, cid);
-    } else if (w.cache_on && cache_get(w, d)) {
-        maybe_speculate(w, d, rank, seq, index);
-        c.path = OTF_PATH_CACHE;
-        respond(w, cid);
-    } else {
-        if (df_inflight(w.dflags[d])) {
-            maybe_speculate(w, d, rank, seq, index);
-            c.path = OTF_PATH_WAITED;
-            c.pc = C_SEG_WAIT;
-            add_waiter(w, d, cid);
-        } else if (enqueue_job(w, d, OTF_ORIGIN_DEMAND)) {
-            c.path = OTF_PATH_ERROR;                   // OverloadError: error record (server.py:70-73)
+        return;
+    }
+    if (w.cache_on) {                                  // SegmentCache.get (cache.py:45-52)
+        if (f & DF_CACHED) {
+            lru_touch(w, d);
+            w.c_hits++;
+            speculate_next(w, d, index, segc, fn);
+            c.path = OTF_PATH_CACHE;
             respond(w, cid);
-            c.pc = C_SEG_ERR;
-        } else {
-            maybe_speculate(w, d, rank, seq, index);
-            c.path = OTF_PATH_TRANSCODED;
-            c.pc = C_SEG_WAIT;
-            add_waiter(w, d, cid);
+            return;
         }
+        w.c_miss++;
+    }
+    c.pc = C_SEG_WAIT;
+    if (df_inflight(f)) {
+        speculate_next(w, d, index, segc, fn);
+        c.path = OTF_PATH_WAITED;
+        add_waiter(w, d, cid);
+    } else if (enqueue_job(w, d, OTF_ORIGIN_DEMAND)) {
+        c.path = OTF_PATH_ERROR;                       // OverloadError: error record (server.py:70-73)
+        respond(w, cid);
+        c.pc = C_SEG_ERR;
+    } else {
+        speculate_next(w, d, index, segc, fn);
+        c.path = OTF_PATH_TRANSCODED;
+        add_waiter(w, d, cid);
     }
 }
 
@@ -571,7 +582,10 @@ __device__ void phase_a(Win &w) {
     double bw_when = 0.0, bw_ctime = 0.0;
     int64_t pops = 0;
     int32_t i = 0;
-    double cw = i < n ? w.lw[0] : 0.0;
+    double cw = 0.0;                                   // next request, loaded one event ahead
+    int32_t ncid = 0, nd = 0, npk = 0;
+    if (n > 0) { cw = w.lw[0]; ncid = w.li[0]; nd = w.ld[0]; npk = w.lp[0]; }
+    const int32_t *segcount = w.S.segcounts;
     for (;;) {
         if (w.wdirty) {                                // earliest worker timer in this window
             bw = -1;
@@ -609,10 +623,12 @@ __device__ void phase_a(Win &w) {
 #endif
         } else {
             w.now = cw;
-            int32_t pk = w.lp[i];
-            server_request(w, w.li[i], w.ld[i], pk & 0xff, pk >> 16, (pk >> 8) & 0xff);
+            const int32_t cid = ncid, d = nd, pk = npk;
+            const uint16_t f = w.dflags[d], fn = w.dflags[d + 1];
+            const int32_t segc = segcount[pk >> 16];
             i++;
-            if (i < n) cw = w.lw[i];
+            if (i < n) { cw = w.lw[i]; ncid = w.li[i]; nd = w.ld[i]; npk = w.lp[i]; }
+            server_request_fast(w, cid, d, pk, f, fn, segc);
 #ifdef WIN_DIAG
             h->stats[29] += clock64() - dg0;
 #endif
