@@ -37,7 +37,7 @@ namespace otf {
 constexpr int32_t WIN_NONE = 0x3FFFFFFF;
 constexpr int RANK_SORT_MAX = 64;  // windows up to this many server events: rank sort, else bitonic
 constexpr int MAXK = 16;           // transcode workers
-constexpr int RING = 512;          // timer-wheel buckets (windows); farther timers wait on a far list
+constexpr int RING = 1024;         // timer-wheel buckets (windows, ~20 s at 20 ms); farther timers wait on a far list
 constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory
 constexpr int MAXN = 32766;        // clients (16-bit wheel links; 0x7FFE/0x7FFF are descriptor states)
 
@@ -82,6 +82,7 @@ struct WinHeader {
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
     int32_t arr_next;                    // next client (arrival order) not yet on the wheel
+    int32_t arr_win;                     // its window (WIN_NONE when every client is on the wheel)
     uint32_t lq_head, lq_tail, lq_stamp; // lazy-LRU touch queue (global ring of lq_cap entries)
     int32_t lq_cap;
     // small read-only tables
@@ -90,8 +91,8 @@ struct WinHeader {
     int64_t t_bitrates[MAXTAB], t_manifest[MAXTAB];
     // timer wheel: server-event and client-local buckets per window
     uint32_t bits[RING / 32];
-    int32_t cnt_srv[RING];               // entries filed in each window's bucket arrays
-    int32_t cnt_loc[RING];
+    uint32_t cnt_srv[RING / 2];          // entries filed in each window's bucket arrays:
+    uint32_t cnt_loc[RING / 2];          //   16-bit counts, two windows per word
     int32_t ovf_head, ovf_n, ovf_min;    // pushes past a full bucket (linked through bnext)
     int32_t n_loc;                       // this window's client-local events (bucket array)
     int32_t list_cap;                    // capacity of the window's server-event list (dynamic region)
@@ -206,7 +207,8 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
     if (wk - w.k < RING) {
         int32_t slot = wk & (RING - 1);
         const int32_t cap = srv ? w.scap : w.lcap;
-        int32_t pos = atomicAdd(srv ? &h->cnt_srv[slot] : &h->cnt_loc[slot], 1);
+        const uint32_t sh = (slot & 1) << 4;
+        int32_t pos = (int32_t)((atomicAdd(srv ? &h->cnt_srv[slot >> 1] : &h->cnt_loc[slot >> 1], 1u << sh) >> sh) & 0xffffu);
         if (pos < cap) {
             (srv ? w.bsrv : w.bloc)[(int64_t)slot * cap + pos] = c;
         } else {                                       // bucket full (rare): overflow list
@@ -736,8 +738,7 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
         int32_t next = C_DONE;
         bool xfer = false;
         switch (c.pc) {
-        case C_ARRIVED:
-            client_arrive(S, c, cid);
+        case C_ARRIVED:                                // pick stream already seeded at init
             c.pc = C_SESSION;
             continue;
         case C_SESSION:
@@ -1015,6 +1016,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
         h->n_list = 0; h->n_blist = 0; h->wseq = 0;
         h->far_head = -1; h->far_n = 0; h->far_min = WIN_NONE; h->k_done = -1;
         h->arr_next = 0;
+        h->arr_win = (fits && N > 0) ? timer_win(w, w.S.arrival(0)) : WIN_NONE;   // W > 0 only if fits
         h->ovf_head = -1; h->ovf_n = 0; h->ovf_min = WIN_NONE; h->n_loc = 0;
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
         h->list_cap = lcap;
@@ -1029,7 +1031,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
         z.win = WIN_NONE; z.pc = W_GOT; z.desc = -1; z.job = -1;
         h->wk[q] = z;
     }
-    for (int32_t i = tid; i < RING; i += WIN_THREADS) { h->cnt_srv[i] = 0; h->cnt_loc[i] = 0; }
+    for (int32_t i = tid; i < RING / 2; i += WIN_THREADS) { h->cnt_srv[i] = 0; h->cnt_loc[i] = 0; }
     for (int32_t i = tid; i < RING / 32; i += WIN_THREADS) h->bits[i] = 0;
     for (int32_t i = tid; i < sc.n_seq; i += WIN_THREADS) {
         h->t_segcount[i] = w.S.segcounts[i];
@@ -1063,6 +1065,9 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
         cl.ctime = 0.0;
         cl.next_when = 0.0 + off;
         if (!(off > 0)) w.S.flag(OTF_S_TIE);           // instant start: tick order among clients matters
+        // the client's pick stream (orchestrator.py:338-340), seeded here in parallel rather
+        // than by one lane at the arrival: it is first drawn from after the arrival
+        seed_picks(&w.S.picks[c], sc.seed, c);
     }
     __syncthreads();
     if (h->st.status & OTF_S_TIE) goto done;
@@ -1078,7 +1083,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
             m = min(m, warp_min(mw));
             m = min(m, h->far_min);
             int32_t arr_win = WIN_NONE;
-            if (h->arr_next < N) arr_win = timer_win(w, w.S.arrival(h->arr_next));
+            arr_win = h->arr_win;
             m = min(m, arr_win);
             int32_t ctl = CTL_RUN;
             if (m == WIN_NONE) {
@@ -1096,6 +1101,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
                             c++;
                         }
                         h->arr_next = c;
+                        h->arr_win = c < N ? timer_win(w, w.S.arrival(c)) : WIN_NONE;
                     }
                     __syncwarp();
                 }
@@ -1122,8 +1128,9 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
                 if (h->lq_tail - h->lq_head > (uint32_t)(h->lq_cap / 4 * 3)) lq_compact_warp(w, lane);
                 // pop the buckets: the window's arrays are read by all lanes at once
                 const int32_t slot = m & (RING - 1);
-                const int32_t ns = min(h->cnt_srv[slot], w.scap);
-                const int32_t nl = min(h->cnt_loc[slot], w.lcap);
+                const uint32_t csh = (slot & 1) << 4;
+                const int32_t ns = min((int32_t)((h->cnt_srv[slot >> 1] >> csh) & 0xffffu), w.scap);
+                const int32_t nl = min((int32_t)((h->cnt_loc[slot >> 1] >> csh) & 0xffffu), w.lcap);
                 int32_t n_ovf = 0, nb = 0;
                 if (h->ovf_n > 0 && h->ovf_min <= m) {     // overflowed pushes due now (rare)
                     if (lane == 0) {
@@ -1166,8 +1173,8 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
                     __syncwarp();
                     if (lane == 0) {
                         h->stats[OTF_ST_WINDOWS]++;
-                        h->cnt_srv[slot] = 0;
-                        h->cnt_loc[slot] = 0;
+                        h->cnt_srv[slot >> 1] &= ~(0xffffu << csh);
+                        h->cnt_loc[slot >> 1] &= ~(0xffffu << csh);
                         h->bits[slot >> 5] &= ~(1u << (slot & 31));
                         h->n_list = nlist;
                         h->n_blist = nb;
