@@ -1208,26 +1208,34 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
             h->k_done = m;
             h->stats[OTF_ST_CYC_SERVER] += clock64() - t0;
         }
-        if (WIN_WARPS == 1) __syncwarp();
-        if (WIN_WARPS == 1 || warp > 0) {
-            // ---- phase B1: the window's client-local timers (concurrent with phase A on 2 warps) ----
-            constexpr int B1_THREADS = WIN_WARPS == 1 ? 32 : WIN_THREADS - 32;
-            const int b1 = WIN_WARPS == 1 ? tid : tid - 32;
-            const long long tb = clock64();
-            const int32_t nl = h->n_loc;
+        if constexpr (WIN_WARPS == 1) {
+            // ---- phase B: the window's local timers, then the clients phase A responded
+            // to, in ONE loop: a single inlined copy of the client state machine ----
+            __syncwarp();
+            t0 = clock64();
+            const int32_t nl = h->n_loc, nb = h->n_blist;
             const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
-            for (int32_t i = b1; i < nl; i += B1_THREADS) client_local(w, al[i]);
-            if (b1 == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
-        }
-        __syncthreads();
-        if (h->st.status & OTF_S_TIE) break;
-        // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
-        t0 = clock64();
-        {
+            for (int32_t i = lane; i < nl + nb; i += 32) client_local(w, i < nl ? al[i] : w.blist[i - nl]);
+            __syncwarp();
+            if (h->st.status & OTF_S_TIE) break;
+        } else {
+            if (warp > 0) {
+                // ---- phase B1: the window's client-local timers, concurrent with phase A ----
+                const int b1 = tid - 32;
+                const long long tb = clock64();
+                const int32_t nl = h->n_loc;
+                const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
+                for (int32_t i = b1; i < nl; i += WIN_THREADS - 32) client_local(w, al[i]);
+                if (b1 == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
+            }
+            __syncthreads();
+            if (h->st.status & OTF_S_TIE) break;
+            // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
+            t0 = clock64();
             const int32_t nb = h->n_blist;
             for (int32_t i = tid; i < nb; i += WIN_THREADS) client_local(w, w.blist[i]);
+            __syncthreads();
         }
-        __syncthreads();
         if (tid == 0) h->stats[OTF_ST_CYC_CLIENTS] += clock64() - t0;
     }
     if (tid == 0) h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
