@@ -671,19 +671,15 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
     double when = now + delay;
     c.ctime = now;
     c.next_when = when;
-    if (next_pc == C_SEG_LAT) {                        // a server event: always a later window
-        int32_t k = timer_win(w, when);
-        if (k == WIN_NONE) return false;
-        if (k <= w.k) w.S.flag(OTF_S_TIE);             // lookahead violated (cannot happen)
-        bucket_push(w, cid, k, true);
-        return false;
-    }
-    if (when <= w.H && when < w.E) {                   // fires inside this window: keep going
+    const bool srv = next_pc == C_SEG_LAT;             // a server event: always a later window
+    if (!srv && when <= w.H && when < w.E) {           // fires inside this window: keep going
         now = when;
         return true;
     }
-    int32_t k = timer_win(w, when);
-    if (k != WIN_NONE) bucket_push(w, cid, k, false);
+    const int32_t k = timer_win(w, when);
+    if (k == WIN_NONE) return false;
+    if (srv && k <= w.k) w.S.flag(OTF_S_TIE);          // lookahead violated (cannot happen)
+    bucket_push(w, cid, k, srv);                       // the single push site (code size)
     return false;
 }
 
