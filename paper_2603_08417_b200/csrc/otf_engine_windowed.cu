@@ -1211,7 +1211,22 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
             t0 = clock64();
             const int32_t nl = h->n_loc, nb = h->n_blist;
             const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
-            for (int32_t i = lane; i < nl + nb; i += 32) client_local(w, i < nl ? al[i] : w.blist[i - nl]);
+            // software-pipelined: the next event's client state is loaded (into registers)
+            // while this one runs -- each client appears once per window and client events
+            // touch only their own client, so the early load cannot be stale
+            const int32_t total = nl + nb;
+            int32_t i = lane;
+            int32_t ncid = 0;
+            Client nc;
+            if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; nc = w.cl[ncid]; }
+            while (i < total) {
+                const int32_t cid = ncid;
+                Client c = nc;
+                i += 32;
+                if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; nc = w.cl[ncid]; }
+                client_local_body(w, c, cid);
+                w.cl[cid] = c;
+            }
             __syncwarp();
             if (h->st.status & OTF_S_TIE) break;
         } else {
