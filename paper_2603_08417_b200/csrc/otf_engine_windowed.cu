@@ -182,6 +182,7 @@ struct Win {
     int64_t cur_bytes, entries, capacity;
     uint32_t c_hits, c_miss, c_evict, c_reject, c_wasted, c_ready, c_spec, c_pops;
     uint32_t c_skip[6];
+    int64_t pops;
 };
 
 // window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles);
@@ -556,38 +557,77 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
     if (take_job(w, wid, nd, nj)) worker_run(w, wid, nd, nj);
 }
 
-// Phase A: replay the window's server events in (time, creation, tick) order.
-__device__ void phase_a(Win &w) {
+// The server lane's scalar state stays in lane 0's registers for the whole run
+// (loaded once by server_begin, flushed by server_end); per window only the
+// queue cursors shared with the compaction step are exchanged.
+__device__ void server_begin(Win &w) {
     WinHeader *h = w.h;
-    const int32_t K = w.S.sc->n_workers;
-    const int32_t n = h->n_list;
+    const otf_scenario &sc0 = *w.S.sc;
     w.req_counter = h->st.req_counter;
     w.n_req = h->st.n_req;
-    const otf_scenario &sc0 = *w.S.sc;
     w.stored_mask = sc0.stored_mask;
     w.cache_on = sc0.cache_enabled != 0;
     w.spec_on = sc0.spec_enabled != 0;
     w.capacity = sc0.cache_capacity;
     w.cur_bytes = h->st.cur_bytes;
     w.entries = h->st.entries;
-    w.lq_head = h->lq_head; w.lq_tail = h->lq_tail; w.lq_stamp = h->lq_stamp;
+    w.lq_stamp = h->lq_stamp;
     w.lq_mask = (uint32_t)h->lq_cap - 1u;
     w.c_hits = w.c_miss = w.c_evict = w.c_reject = w.c_wasted = w.c_ready = w.c_spec = 0;
     for (int q = 0; q < 6; q++) w.c_skip[q] = 0;
+    w.pops = 0;
+}
+
+__device__ void server_end(Win &w) {
+    WinHeader *h = w.h;
+    h->stats[OTF_ST_TIMER_POPS] += w.pops;
+    h->st.cur_bytes = w.cur_bytes;
+    h->st.entries = w.entries;
+    h->lq_stamp = w.lq_stamp;
+    h->stats[OTF_ST_HITS] += w.c_hits;
+    h->stats[OTF_ST_MISSES] += w.c_miss;
+    h->stats[OTF_ST_EVICTIONS] += w.c_evict;
+    h->stats[OTF_ST_REJECTED] += w.c_reject;
+    h->stats[OTF_ST_WASTED] += w.c_wasted;
+    h->stats[OTF_ST_READY_CALLBACKS] += w.c_ready;
+    h->stats[OTF_ST_SPEC_ENQUEUED] += w.c_spec;
+    for (int q = 0; q < 6; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += w.c_skip[q];
+    h->st.req_counter = w.req_counter;
+    h->st.n_req = w.n_req;
+}
+
+// One request of the window's sorted list (the list entry was loaded one event ahead).
+#define PHASE_A_REQUEST()                                                              \
+    do {                                                                               \
+        w.now = cw;                                                                    \
+        const int32_t cid = ncid, d = nd, pk = npk;                                    \
+        const uint16_t f = w.dflags[d], fn = w.dflags[d + 1];                          \
+        const int32_t segc = segcount[pk >> 16];                                       \
+        i++;                                                                           \
+        if (i < n) { cw = w.lw[i]; ncid = w.li[i]; nd = w.ld[i]; npk = w.lp[i]; }      \
+        server_request_fast(w, cid, d, pk, f, fn, segc);                               \
+    } while (0)
+
+// Phase A: replay the window's server events in (time, creation, tick) order.
+__device__ void phase_a(Win &w) {
+    WinHeader *h = w.h;
+    const int32_t K = w.S.sc->n_workers;
+    const int32_t n = h->n_list;
+    w.lq_head = h->lq_head; w.lq_tail = h->lq_tail;    // the compaction step may have moved them
     w.n_blist = h->n_blist;
     w.fq_n = h->fq_n;
     uint32_t due = 0;
     for (int32_t q = 0; q < K; q++) due |= (h->wk[q].win == w.k ? 1u : 0u) << q;
     w.due = due;
-    w.wdirty = true;
+    w.wdirty = due != 0;
     int32_t bw = -1;
     double bw_when = 0.0, bw_ctime = 0.0;
-    int64_t pops = 0;
     int32_t i = 0;
     double cw = 0.0;                                   // next request, loaded one event ahead
     int32_t ncid = 0, nd = 0, npk = 0;
     if (n > 0) { cw = w.lw[0]; ncid = w.li[0]; nd = w.ld[0]; npk = w.lp[0]; }
     const int32_t *segcount = w.S.segcounts;
+    w.pops += n;                                       // every request is one timer pop
     for (;;) {
         if (w.wdirty) {                                // earliest worker timer in this window
             bw = -1;
@@ -601,10 +641,17 @@ __device__ void phase_a(Win &w) {
             }
             w.wdirty = false;
         }
+        if (bw < 0) {                                  // no worker timer due: requests only (common)
+            while (i < n) {
+                PHASE_A_REQUEST();
+                if (w.fq_n > 0) drain_handoffs(w);
+                if (w.wdirty) break;                   // a started job ends inside this window (rare)
+            }
+            if (!w.wdirty) break;
+            continue;
+        }
         bool take_worker;
-        if (bw < 0 && i >= n) break;
-        if (bw < 0) take_worker = false;
-        else if (i >= n) take_worker = true;
+        if (i >= n) take_worker = true;
         else if (bw_when < cw) take_worker = true;
         else if (cw < bw_when) take_worker = false;
         else {
@@ -613,50 +660,16 @@ __device__ void phase_a(Win &w) {
             else if (cc < bw_ctime) take_worker = false;
             else { w.S.flag(OTF_S_TIE); take_worker = true; }
         }
-        pops++;
-#ifdef WIN_DIAG
-        long long dg0 = clock64();
-#endif
         if (take_worker) {
+            w.pops++;
             w.now = bw_when;
             server_worker_done(w, bw);
-#ifdef WIN_DIAG
-            h->stats[30] += clock64() - dg0;
-#endif
         } else {
-            w.now = cw;
-            const int32_t cid = ncid, d = nd, pk = npk;
-            const uint16_t f = w.dflags[d], fn = w.dflags[d + 1];
-            const int32_t segc = segcount[pk >> 16];
-            i++;
-            if (i < n) { cw = w.lw[i]; ncid = w.li[i]; nd = w.ld[i]; npk = w.lp[i]; }
-            server_request_fast(w, cid, d, pk, f, fn, segc);
-#ifdef WIN_DIAG
-            h->stats[29] += clock64() - dg0;
-#endif
+            PHASE_A_REQUEST();
         }
-#ifdef WIN_DIAG
-        long long dg1 = clock64();
-#endif
         if (w.fq_n > 0) drain_handoffs(w);
-#ifdef WIN_DIAG
-        h->stats[31] += clock64() - dg1;
-#endif
     }
-    h->stats[OTF_ST_TIMER_POPS] += pops;
-    h->st.cur_bytes = w.cur_bytes;
-    h->st.entries = w.entries;
-    h->lq_head = w.lq_head; h->lq_tail = w.lq_tail; h->lq_stamp = w.lq_stamp;
-    h->stats[OTF_ST_HITS] += w.c_hits;
-    h->stats[OTF_ST_MISSES] += w.c_miss;
-    h->stats[OTF_ST_EVICTIONS] += w.c_evict;
-    h->stats[OTF_ST_REJECTED] += w.c_reject;
-    h->stats[OTF_ST_WASTED] += w.c_wasted;
-    h->stats[OTF_ST_READY_CALLBACKS] += w.c_ready;
-    h->stats[OTF_ST_SPEC_ENQUEUED] += w.c_spec;
-    for (int q = 0; q < 6; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += w.c_skip[q];
-    h->st.req_counter = w.req_counter;
-    h->st.n_req = w.n_req;
+    h->lq_head = w.lq_head; h->lq_tail = w.lq_tail;
     h->n_blist = w.n_blist;
 }
 
@@ -1070,6 +1083,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
 
     // ---- window loop --------------------------------------------------------------
     t_start = clock64();
+    if (tid == 0) server_begin(w);
     for (;;) {
         if (warp == 0) {
             t0 = clock64();
@@ -1249,7 +1263,10 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
         }
         if (tid == 0) h->stats[OTF_ST_CYC_CLIENTS] += clock64() - t0;
     }
-    if (tid == 0) h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
+    if (tid == 0) {
+        server_end(w);
+        h->stats[OTF_ST_CYC_TOTAL] += clock64() - t_start;
+    }
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
     if (!(h->st.status & OTF_S_TIE)) {
