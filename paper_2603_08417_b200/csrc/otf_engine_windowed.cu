@@ -841,34 +841,32 @@ __device__ void sort_list(Win &w, int lane) {
     if (lane == 0) h->n_ties = 0;
     if (n <= 1) { __syncwarp(); return; }
     if (n <= RANK_SORT_MAX) {
-        double my_w[RANK_SORT_MAX / 32];
-        int32_t my_s[RANK_SORT_MAX / 32], my_r[RANK_SORT_MAX / 32];
-        int16_t my_id[RANK_SORT_MAX / 32], my_d[RANK_SORT_MAX / 32];
-#pragma unroll
-        for (int t = 0; t < RANK_SORT_MAX / 32; t++) {
-            int32_t i = lane + 32 * t;
-            if (i >= n) break;
-            double wi = w.lw[i];
-            int32_t idi = w.li[i];
-            int32_t r = 0;
+        // each lane ranks elements lane and lane + 32 in ONE pass over the list (one
+        // pair of broadcast loads per j for both), and spots equal times on the way
+        const int32_t i0 = lane, i1 = lane + 32;
+        const bool v0 = i0 < n, v1 = i1 < n;
+        const double w0 = v0 ? w.lw[i0] : INFINITY, w1 = v1 ? w.lw[i1] : INFINITY;
+        const int32_t id0 = v0 ? w.li[i0] : 0x7fff, id1 = v1 ? w.li[i1] : 0x7fff;
+        int32_t r0 = 0, r1 = 0, e0 = 0, e1 = 0;
 #pragma unroll 4
-            for (int32_t j = 0; j < n; j++) {          // branch-free (time, client) compare
-                double wj = w.lw[j];
-                int32_t idj = w.li[j];
-                r += (int32_t)((wj < wi) | ((wj == wi) & (idj < idi)));
-            }
-            my_w[t] = wi; my_id[t] = (int16_t)idi; my_r[t] = r;
-            my_d[t] = w.ld[i]; my_s[t] = w.lp[i];
+        for (int32_t j = 0; j < n; j++) {              // branch-free (time, client) compare
+            const double wj = w.lw[j];
+            const int32_t idj = w.li[j];
+            r0 += (int32_t)((wj < w0) | ((wj == w0) & (idj < id0)));
+            r1 += (int32_t)((wj < w1) | ((wj == w1) & (idj < id1)));
+            e0 += (int32_t)(wj == w0);
+            e1 += (int32_t)(wj == w1);
         }
+        const int16_t d0 = v0 ? w.ld[i0] : 0, d1 = v1 ? w.ld[i1] : 0;
+        const int32_t s0 = v0 ? w.lp[i0] : 0, s1 = v1 ? w.lp[i1] : 0;
+        const bool tie = (v0 && e0 > 1) || (v1 && e1 > 1);   // equal request times (rare)
+        const bool any = __any_sync(0xffffffffu, tie);
+        __syncwarp();                                  // every lane has read the list
+        if (v0) { w.lw[r0] = w0; w.li[r0] = (int16_t)id0; w.ld[r0] = d0; w.lp[r0] = s0; }
+        if (v1) { w.lw[r1] = w1; w.li[r1] = (int16_t)id1; w.ld[r1] = d1; w.lp[r1] = s1; }
+        if (lane == 0) h->n_ties = any ? 1 : 0;
         __syncwarp();
-#pragma unroll
-        for (int t = 0; t < RANK_SORT_MAX / 32; t++) {
-            int32_t i = lane + 32 * t;
-            if (i >= n) break;
-            int32_t r = my_r[t];
-            w.lw[r] = my_w[t]; w.li[r] = my_id[t];
-            w.ld[r] = my_d[t]; w.lp[r] = my_s[t];
-        }
+        return;
     } else {
         int32_t p = 1;
         while (p < n) p <<= 1;
