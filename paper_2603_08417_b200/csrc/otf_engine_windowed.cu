@@ -698,6 +698,32 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
 
 __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid);
 
+// Client state moves through L2 with the evict-first policy: a client's next
+// event is ~15 windows away, far beyond the L2's reach at full occupancy, so
+// keeping its lines only evicts what does get reused (trace samples of the
+// clients now transferring, segment sizes, bucket arrays).
+static_assert(sizeof(Client) % 16 == 0, "Client moves as 16-byte vectors");
+__device__ __forceinline__ void load_client_stream(Client &dst, const Client *src) {
+#ifdef WIN_NO_CS
+    dst = *src;
+#else
+    int4 *d = reinterpret_cast<int4 *>(&dst);
+    const int4 *p = reinterpret_cast<const int4 *>(src);
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(Client) / 16); q++) d[q] = __ldcs(p + q);
+#endif
+}
+__device__ __forceinline__ void store_client_stream(Client *dst, const Client &src) {
+#ifdef WIN_NO_CS
+    *dst = src;
+#else
+    int4 *p = reinterpret_cast<int4 *>(dst);
+    const int4 *s = reinterpret_cast<const int4 *>(&src);
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(Client) / 16); q++) __stcs(p + q, s[q]);
+#endif
+}
+
 __device__ void client_local(Win &w, int32_t cid) {
     Client c = w.cl[cid];                              // one vectorised load; state lives in registers
     client_local_body(w, c, cid);
@@ -1230,14 +1256,14 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
             int32_t i = lane;
             int32_t ncid = 0;
             Client nc;
-            if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; nc = w.cl[ncid]; }
+            if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; load_client_stream(nc, &w.cl[ncid]); }
             while (i < total) {
                 const int32_t cid = ncid;
                 Client c = nc;
                 i += 32;
-                if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; nc = w.cl[ncid]; }
+                if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; load_client_stream(nc, &w.cl[ncid]); }
                 client_local_body(w, c, cid);
-                w.cl[cid] = c;
+                store_client_stream(&w.cl[cid], c);
             }
             __syncwarp();
             if (h->st.status & OTF_S_TIE) break;
