@@ -50,6 +50,7 @@ struct Scn {
     double lat_sum, stall_sum, startup_sum;   // this lane's float sums
     Pcg64 *picks;                             // [n_clients] sequence-pick streams (scratch)
     uint64_t mag_g, mag_rg;                   // d / max_nseg, d / (n_ranks * max_nseg) by multiply-high
+    double inv_grid_step;                     // 1 / sc->grid_step (0 when the trace grid is irregular)
     uint32_t div_g, div_rg;
     const int64_t *sizes, *bitrates, *manifest_b;
     const int32_t *segcounts;
@@ -81,6 +82,7 @@ struct Scn {
         div_rg = (uint32_t)(sc->n_ranks * sc->max_nseg);
         mag_g = 0xffffffffffffffffull / div_g + 1ull;
         mag_rg = 0xffffffffffffffffull / div_rg + 1ull;
+        inv_grid_step = sc->grid_step > 0 ? 1.0 / sc->grid_step : 0.0;
     }
     // floor(d / div) = umul64hi(d, floor((2^64-1)/div) + 1), exact for d, div < 2^31
     __device__ __forceinline__ uint32_t qdiv(uint32_t d, uint64_t mag, uint32_t) const {
@@ -130,12 +132,14 @@ struct Scn {
             t.period = tf[0];
             t.pbits = tf[1];
             t.grid = tf[2];
+            t.inv_grid = t.grid > 0 ? 1.0 / t.grid : 0.0;
             return t;
         }
         t.starts = starts;
         t.values = values + (int64_t)cid * sc->n_samples;
         t.period = sc->period;
         t.grid = sc->grid_step;
+        t.inv_grid = inv_grid_step;
         t.pbits = pbits[cid];
         t.n = sc->n_samples;
         return t;

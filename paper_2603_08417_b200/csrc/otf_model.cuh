@@ -35,13 +35,14 @@ struct Trace {
     const double *values;   // [n]
     double period, pbits;
     double grid;            // > 0: starts[i] == i * grid exactly
+    double inv_grid;        // 1 / grid (an estimate's multiplier; exactness comes from the fix-up)
     int32_t n;
 };
 
 // bisect_right(starts, phase) - 1, clamped at 0 (netem.py:80)
 OTF_HD int32_t trace_piece(const Trace &tr, double phase) {
     if (tr.grid > 0) {
-        double q = phase / tr.grid;
+        double q = phase * tr.inv_grid;                // estimate; the two loops below make it exact
         int32_t i = q < (double)tr.n ? (int32_t)q : tr.n - 1;
         if (i < 0) i = 0;
         while (i + 1 < tr.n && (double)(i + 1) * tr.grid <= phase) i++;
@@ -64,11 +65,14 @@ OTF_HD double piece_start(const Trace &tr, int32_t i) {
 OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
     int32_t i = trace_piece(tr, phase);
     double spent = 0.0, pos = phase;
+    double v_next = i < tr.n ? tr.values[i] : 0.0;
     for (; i < tr.n; i++) {
+        const double v_here = v_next;
+        if (i + 1 < tr.n) v_next = tr.values[i + 1];   // loaded one piece ahead (transfers span 1-2)
         double seg_end = (i + 1 < tr.n) ? piece_start(tr, i + 1) : tr.period;
         double width = seg_end - pos;
         if (width > 0) {
-            double v = tr.values[i];
+            double v = v_here;
             if (v > 0) {
                 if (v * width >= bits) { spent_out = spent + bits / v; left_out = 0.0; return; }
                 bits -= v * width;
