@@ -399,6 +399,10 @@ class ExperimentConfig:
             raise ConfigError("the GPU engine runs the virtual clock only")
         if not 0 <= self.client.retries < 255:
             raise ConfigError("client.retries must be in [0, 255) for the GPU engine")
+        if not 0 <= int(self.seed) < 2 ** 64:
+            # numpy's SeedSequence rejects negative entropy; seeds are carried as uint64 words
+            # through the C ABI (otf_scenario.seed, otf_np_draws entropy)
+            raise ConfigError("seed must be in [0, 2**64) for the GPU engine")
 
 
 def nominal_ladder_bytes(config: ExperimentConfig) -> float:

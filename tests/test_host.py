@@ -217,3 +217,12 @@ def test_trace_tables_many_clients_threaded():
                                   spread, 2e6, 400e6, v2.ctypes.data_as(dp), p2.ctypes.data_as(dp), 1), "b")
     assert np.array_equal(v1.view(np.int64), v2.view(np.int64))
     assert np.array_equal(p1.view(np.int64), p2.view(np.int64))
+
+
+def test_seed_range_is_validated():
+    """Seeds travel as uint64 entropy words (SeedSequence([seed, ...])): out-of-range seeds
+    are refused up front instead of being silently truncated."""
+    for bad in (-1, 2 ** 64):
+        with pytest.raises((ConfigError, ValueError)):
+            ExperimentConfig(seed=bad).validate()
+    ExperimentConfig(seed=2 ** 64 - 1).validate()
