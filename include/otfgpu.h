@@ -68,6 +68,7 @@ enum {
     /* windowed engine profile: SM cycles spent per phase (lane 0's clock) */
     OTF_ST_CYC_SCAN, OTF_ST_CYC_SORT, OTF_ST_CYC_SERVER, OTF_ST_CYC_CLIENTS, OTF_ST_CYC_TOTAL,
     OTF_ST_CYC_LOCAL,   /* client-local phase run concurrently with the server lane */
+    OTF_ST_PAR_WINDOWS, /* windows whose server events took the parallel (request-only) pass */
     OTF_ST_NSLOTS = 32
 };
 

@@ -55,6 +55,7 @@ constexpr int16_t NIL = -1;
 #define WIN_WARPS 1
 #endif
 constexpr int WIN_THREADS = 32 * WIN_WARPS;   // threads per scenario (see windowed_kernel)
+constexpr int PAR_MAX = 128;       // windows up to this many requests may take the parallel server pass
 
 struct WWorker {
     double when, ctime;
@@ -97,6 +98,11 @@ struct WinHeader {
     int32_t n_loc;                       // this window's client-local events (bucket array)
     int32_t list_cap;                    // capacity of the window's server-event list (dynamic region)
     int32_t ctl, cur_m;                  // window-loop control word + the window being run
+    uint8_t ev_flags[PAR_MAX];           // parallel server pass: per request outcome (EV_*)
+    uint8_t ev_touch[PAR_MAX];           //   LRU touches before it (exclusive prefix)
+    uint8_t par_list[PAR_MAX];           //   the list partitioned by owner lane (time order kept)
+    uint32_t par_cnt[32];                //   per owner lane: count, then next slot
+    int32_t hand_safe;                   // no transcode can end within the window it starts in
     double wsum[WIN_WARPS][3];           // per-warp float sums (fixed-order final reduction)
 };
 
@@ -183,6 +189,7 @@ struct Win {
     uint32_t c_hits, c_miss, c_evict, c_reject, c_wasted, c_ready, c_spec, c_pops;
     uint32_t c_skip[6];
     int64_t pops;
+    double svc_floor;                                  // min over ranks rho * min segment duration
 };
 
 // window index of a timer: the k with k*W <= when < (k+1)*W (both bounds as doubles);
@@ -576,6 +583,13 @@ __device__ void server_begin(Win &w) {
     w.c_hits = w.c_miss = w.c_evict = w.c_reject = w.c_wasted = w.c_ready = w.c_spec = 0;
     for (int q = 0; q < 6; q++) w.c_skip[q] = 0;
     w.pops = 0;
+    double rho_min = INFINITY, dur_min = INFINITY;     // service-time floor (parallel pass guard)
+    for (int32_t r = 0; r < sc0.n_ranks; r++) rho_min = fmin(rho_min, w.S.rho[r]);
+    for (int32_t q = 0; q < sc0.n_seq; q++) {
+        const int32_t last = w.S.segcounts[q] - 1;
+        dur_min = fmin(dur_min, fmin(w.S.segdur[q], seg_duration(w.S.seqdur[q], w.S.segdur[q], last)));
+    }
+    w.svc_floor = rho_min * dur_min;
 }
 
 __device__ void server_end(Win &w) {
@@ -607,6 +621,282 @@ __device__ void server_end(Win &w) {
         if (i < n) { cw = w.lw[i]; ncid = w.li[i]; nd = w.ld[i]; npk = w.lp[i]; }      \
         server_request_fast(w, cid, d, pk, f, fn, segc);                               \
     } while (0)
+
+// ---- parallel server pass for request-only windows -------------------------------
+// When no worker timer falls in the window, no worker is idle (every enqueue
+// joins the FIFO: Queue.put_nowait with no getter, sim.py:229-240), and the
+// backend has neither a queue bound nor demand priority, the window's server
+// events are requests only and the cache contents cannot change (puts and
+// evictions happen only when a transcode completes, backend.py:205-207).  A
+// request then touches (a) its (sequence, rank)'s descriptors -- cached /
+// in-flight state, waiter lists, the speculative next segment -- and (b)
+// global sequence numbers: request ids, response slots, LRU touch stamps, job
+// ids and FIFO positions.  (a) is replayed per (sequence, rank) group, in
+// time order, by the lane that owns the group; (b) are exclusive prefix sums
+// over the window's time order.  The result is the serial order's, exactly.
+enum { EV_PATH = 7, EV_IMM = 8, EV_TOUCH = 16, EV_ENQ_D = 32, EV_ENQ_S = 64 };
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane, uint32_t &total) {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
+    WinHeader *h = w.h;
+    const otf_scenario &sc = *w.S.sc;
+    const int32_t n = h->n_list;
+    const uint32_t stored_mask = sc.stored_mask;
+    const bool cache_on = sc.cache_enabled != 0, spec_on = sc.spec_enabled != 0;
+    const int32_t n_ranks = sc.n_ranks;
+#ifdef WIN_DIAG
+    long long dga = clock64();
+#endif
+    // (a) per-group replay: lane (seq * n_ranks + rank) % 32 owns the group.  First a
+    // stable partition of the list by owner lane (time order kept inside each lane's
+    // run), so that every lane then walks ITS requests while the others walk theirs.
+    h->par_cnt[lane] = 0;
+    __syncwarp();
+    for (int32_t base = 0; base < n; base += 32) {      // counts per owner
+        const int32_t i = base + lane;
+        const int32_t pk = i < n ? w.lp[i] : 0;
+        const int32_t own = i < n ? ((((pk >> 16) * n_ranks) + (pk & 0xff)) & 31) : 32 + lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, own);
+        if (i < n && (peers & ((1u << lane) - 1u)) == 0) h->par_cnt[own] += __popc(peers);
+        __syncwarp();
+    }
+    const uint32_t my_cnt = h->par_cnt[lane];
+    uint32_t n_all;
+    const uint32_t my_off = warp_excl_scan(my_cnt, lane, n_all);
+    __syncwarp();
+    h->par_cnt[lane] = my_off;                          // now: the next free slot of each owner's run
+    __syncwarp();
+    for (int32_t base = 0; base < n; base += 32) {      // scatter, stable
+        const int32_t i = base + lane;
+        const int32_t pk = i < n ? w.lp[i] : 0;
+        const int32_t own = i < n ? ((((pk >> 16) * n_ranks) + (pk & 0xff)) & 31) : 32 + lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, own);
+        if (i < n) h->par_list[h->par_cnt[own] + __popc(peers & ((1u << lane) - 1u))] = (uint8_t)i;
+        __syncwarp();
+        if (i < n && (peers & ((1u << lane) - 1u)) == 0) h->par_cnt[own] += __popc(peers);
+        __syncwarp();
+    }
+    uint32_t hits = 0, miss = 0, sk0 = 0, sk1 = 0, sk3 = 0, sk4 = 0, spec = 0;
+    for (uint32_t k = my_off; k < my_off + my_cnt; k++) {
+        const int32_t i = h->par_list[k];
+        const int32_t pk = w.lp[i];
+        const int32_t rank = pk & 0xff, seq = pk >> 16;
+        const int32_t d = w.ld[i], cid = w.li[i], index = (pk >> 8) & 0xff;
+        uint32_t fl;
+        if ((stored_mask >> rank) & 1u) {
+            fl = EV_IMM | OTF_PATH_STORAGE;
+        } else {
+            const uint16_t f = w.dflags[d];
+            if (cache_on && (f & DF_CACHED)) {
+                hits++;
+                fl = EV_IMM | EV_TOUCH | OTF_PATH_CACHE;
+            } else {
+                if (cache_on) miss++;
+                if (df_inflight(f)) {
+                    fl = OTF_PATH_WAITED;
+                } else {                               // demand job: in flight, no waiter yet
+                    w.dflags[d] = (uint16_t)((f & DF_CACHED) | DF_NOWAIT);
+                    fl = EV_ENQ_D | OTF_PATH_TRANSCODED;
+                }
+            }
+            {                                          // maybe_speculate (backend.py:135-154)
+                if (!spec_on) sk0++;
+                else if (index + 1 >= w.S.segcounts[seq]) sk1++;
+                else {
+                    const uint16_t fn = w.dflags[d + 1];
+                    if (cache_on && (fn & DF_CACHED)) sk3++;
+                    else if (df_inflight(fn)) sk4++;
+                    else {
+                        w.dflags[d + 1] = (uint16_t)((fn & DF_CACHED) | DF_NOWAIT);
+                        fl |= EV_ENQ_S;
+                        spec++;
+                    }
+                }
+            }
+            if (!(fl & EV_IMM)) add_waiter(w, d, cid);
+        }
+        h->ev_flags[i] = (uint8_t)fl;
+    }
+    __syncwarp();
+#ifdef WIN_DIAG
+    if (lane == 0) h->stats[28] += clock64() - dga;
+    dga = clock64();
+#endif
+    // (b) sequence numbers in time order: exclusive prefix sums over the list
+    // (lane l holds requests 4l .. 4l+3)
+    constexpr int E = PAR_MAX / 32;
+    uint32_t fl[E], c_imm = 0, c_tch = 0, c_enq = 0, c_enq_d = 0;
+#pragma unroll
+    for (int t = 0; t < E; t++) {
+        const int32_t i = E * lane + t;
+        fl[t] = i < n ? h->ev_flags[i] : 0u;
+        c_imm += (fl[t] >> 3) & 1u;
+        c_tch += (fl[t] >> 4) & 1u;
+        c_enq += ((fl[t] >> 5) & 1u) + ((fl[t] >> 6) & 1u);
+        c_enq_d += (fl[t] >> 5) & 1u;
+    }
+    uint32_t n_imm, n_tch, n_enq;
+    uint32_t p_imm = warp_excl_scan(c_imm, lane, n_imm);
+    uint32_t p_tch = warp_excl_scan(c_tch, lane, n_tch);
+    uint32_t p_enq = warp_excl_scan(c_enq, lane, n_enq);
+    const uint32_t n_enq_d = warp_sum(c_enq_d);
+    // the server lane's scalars (lane 0's registers) as the bases
+    const int64_t req_base = __shfl_sync(0xffffffffu, (long long)w.req_counter, 0);
+    const int64_t slot_base = __shfl_sync(0xffffffffu, (long long)w.n_req, 0);
+    const int32_t blist_base = __shfl_sync(0xffffffffu, w.n_blist, 0);
+    const uint32_t lq_tail = __shfl_sync(0xffffffffu, w.lq_tail, 0);
+    const uint32_t stamp_base = __shfl_sync(0xffffffffu, w.lq_stamp, 0);
+    const uint32_t lq_mask = (uint32_t)h->lq_cap - 1u;
+    const int32_t jq_base = h->jq_head + h->jq_n;
+    const int64_t job_base = h->st.n_job;
+    // the first n_hand enqueues (time order) go to the idle workers (getters, FIFO);
+    // the rest join the job FIFO
+    const uint32_t n_hand = min(n_enq, (uint32_t)h->gq_n);
+#pragma unroll
+    for (int t = 0; t < E; t++) {
+        const int32_t i = E * lane + t;
+        if (i >= n) continue;
+        const uint32_t f = fl[t];
+        h->ev_touch[i] = (uint8_t)p_tch;
+        const int32_t cid = w.li[i], d = w.ld[i];
+        const double now = w.lw[i];
+        Client &c = w.cl[cid];
+        c.req_id = (int32_t)(req_base + i);
+        c.arrival = now;
+        c.path = (int32_t)(f & EV_PATH);
+        if (f & EV_IMM) {                              // respond (server.py:76-77)
+            c.req_slot = (int32_t)(slot_base + p_imm);
+            c.pc = C_SEG_RESP;
+            c.next_when = now;
+            w.blist[blist_base + (int32_t)p_imm] = cid;
+        } else {
+            c.pc = C_SEG_WAIT;
+        }
+        if (f & EV_TOUCH) {                            // lru_touch, in time order
+            LqEnt e; e.desc = d; e.stamp = stamp_base + p_tch + 1u;
+            w.lq[(lq_tail + p_tch) & lq_mask] = e;
+        }
+        uint32_t q = p_enq;
+        for (int k = 0; k < 2; k++) {                  // Backend._enqueue: demand job first, then the speculative one
+            const uint32_t bit = k ? EV_ENQ_S : EV_ENQ_D;
+            if (!(f & bit)) continue;
+            const int32_t jd = k ? d + 1 : d;
+            const int64_t j = job_base + q;
+            if (q >= n_hand) {                         // Queue.put_nowait with no getter: the FIFO
+                int32_t pos = jq_base + (int32_t)(q - n_hand);
+                if (pos >= h->jq_cap) pos -= h->jq_cap;
+                JobEnt je; je.desc = jd; je.job = (int32_t)j;
+                w.jq[pos] = je;
+            }
+            if (w.S.records) {
+                if (j < sc.job_cap) {
+                    const int64_t o = sc.job_off + j;
+                    w.S.b->job_seq[o] = w.S.desc_seq(jd);
+                    w.S.b->job_rep[o] = w.S.desc_rank(jd);
+                    w.S.b->job_index[o] = w.S.desc_index(jd);
+                    w.S.b->job_origin[o] = k ? OTF_ORIGIN_SPECULATIVE : OTF_ORIGIN_DEMAND;
+                    w.S.b->job_outcome[o] = OTF_OUTCOME_PENDING;
+                    w.S.b->job_enq[o] = now;
+                    w.S.b->job_start[o] = NAN;
+                    w.S.b->job_fin[o] = NAN;
+                } else {
+                    w.S.flag(OTF_S_RECORD_OVERFLOW);
+                }
+            }
+            q++;
+        }
+        p_imm += (f >> 3) & 1u;
+        p_tch += (f >> 4) & 1u;
+        p_enq += ((f >> 5) & 1u) + ((f >> 6) & 1u);
+    }
+    __syncwarp();
+    // the latest touch stamp per descriptor: each lane over its own requests, in time order
+    for (uint32_t k = my_off; k < my_off + my_cnt; k++) {
+        const int32_t i = h->par_list[k];
+        if (h->ev_flags[i] & EV_TOUCH) w.lstamp[w.ld[i]] = stamp_base + h->ev_touch[i] + 1u;
+    }
+    // counters back into lane 0's registers / the header
+    hits = warp_sum(hits); miss = warp_sum(miss); spec = warp_sum(spec);
+    sk0 = warp_sum(sk0); sk1 = warp_sum(sk1); sk3 = warp_sum(sk3); sk4 = warp_sum(sk4);
+    if (lane == 0) {
+        w.req_counter += n;
+        w.n_req += n_imm;
+        w.n_blist += (int32_t)n_imm;
+        w.lq_tail += n_tch;
+        w.lq_stamp += n_tch;
+        w.c_hits += hits; w.c_miss += miss; w.c_spec += spec;
+        w.c_skip[0] += sk0; w.c_skip[1] += sk1; w.c_skip[3] += sk3; w.c_skip[4] += sk4;
+        w.pops += n;
+        h->st.n_job += n_enq;
+        h->jq_n += (int32_t)(n_enq - n_hand);
+        // hand-offs, in time order: put_nowait -> the first getter's ready hop ->
+        // worker_run (backend.py:186-204); parallel_ok made sure none ends in this window
+        uint32_t q = 0;
+        for (int32_t i = 0; i < n && q < n_hand; i++) {
+            const uint32_t f = h->ev_flags[i];
+            for (int k = 0; k < 2 && q < n_hand; k++) {
+                if (!(f & (k ? EV_ENQ_S : EV_ENQ_D))) continue;
+                const int32_t wid = h->gq[h->gq_head];
+                h->gq_head = (h->gq_head + 1 == sc.n_workers) ? 0 : h->gq_head + 1;
+                h->gq_n--;
+                w.c_ready++;
+                w.now = w.lw[i];
+                worker_run(w, wid, w.ld[i] + k, (int32_t)(job_base + q));
+                q++;
+            }
+        }
+        h->stats[OTF_ST_JOBS_TOTAL] += n_enq;
+        h->stats[OTF_ST_JOBS_DEMAND] += n_enq_d;
+        h->stats[OTF_ST_JOBS_SPEC] += n_enq - n_enq_d;
+        h->lq_head = w.lq_head; h->lq_tail = w.lq_tail;
+        h->n_blist = w.n_blist;
+#ifdef WIN_DIAG
+        h->stats[31] += clock64() - dga;
+#endif
+    }
+    __syncwarp();
+}
+
+// Can this window take the parallel server pass?  (lane 0; see phase_a_parallel)
+__device__ __forceinline__ bool parallel_ok(Win &w) {
+    const WinHeader *h = w.h;
+    const otf_scenario &sc = *w.S.sc;
+    const int32_t n = h->n_list;
+#ifdef WIN_DIAG
+    {
+        WinHeader *hm = w.h;
+        if (h->gq_n > 0) hm->stats[30]++;
+        if (n > PAR_MAX) hm->stats[31]++;
+        for (int32_t q = 0; q < sc.n_workers; q++)
+            if (h->wk[q].win == w.k) { hm->stats[24]++; break; }   // (diag build: overrides the sort cycles)
+    }
+#endif
+    if (n < 2 || n > PAR_MAX || h->n_ties || h->fq_n > 0 || sc.demand_priority || sc.queue_bound > 0)
+        return false;
+    for (int32_t q = 0; q < sc.n_workers; q++)
+        if (h->wk[q].win == w.k) return false;         // a transcode completes in this window
+    // an idle worker handed a job here must not finish inside the window: its service
+    // time (rho * duration) * (1 + eps) is at least svc_floor * (1 + its next eps)
+    if (h->gq_n > 0 && !h->hand_safe) return false;
+    w.lq_head = h->lq_head; w.lq_tail = h->lq_tail; w.n_blist = h->n_blist;
+    return w.lq_tail - w.lq_head + (uint32_t)n <= w.lq_mask;   // room for every touch
+}
 
 // Phase A: replay the window's server events in (time, creation, tick) order.
 __device__ void phase_a(Win &w) {
@@ -1108,6 +1398,16 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
     // ---- window loop --------------------------------------------------------------
     t_start = clock64();
     if (tid == 0) server_begin(w);
+    {
+        // hand-offs are safe in the parallel server pass if no transcode can end inside
+        // the window it starts in: svc >= svc_floor * (1 + min eps) >= 2 W
+        double emin = sc.noise > 0 ? INFINITY : 0.0;
+        if (sc.noise > 0)
+            for (int64_t q = tid; q < (int64_t)K * sc.eps_stride; q += WIN_THREADS) emin = fmin(emin, w.S.eps[q]);
+        for (int o = 16; o > 0; o >>= 1) emin = fmin(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+        if (tid == 0) h->hand_safe = (w.svc_floor * (1.0 + emin) >= 2.0 * w.W) ? 1 : 0;
+        __syncthreads();
+    }
     for (;;) {
         if (warp == 0) {
             t0 = clock64();
@@ -1235,12 +1535,28 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
         w.E = (double)(m + 1) * w.W;
         t0 = clock64();
         // thread 0 = the server lane; with two warps, warp 1 runs the local timers meanwhile
-        if (tid == 0) {
-            // ---- phase A: server lane ----
-            if (h->n_ties) order_ties(w);
-            phase_a(w);
-            h->k_done = m;
-            h->stats[OTF_ST_CYC_SERVER] += clock64() - t0;
+        {
+            // ---- phase A: the server events (the whole warp in request-only windows) ----
+            int par = 0;
+#ifdef WIN_DIAG
+            long long dgp = clock64();
+#endif
+            if (tid == 0) par = parallel_ok(w) ? 1 : 0;
+#ifdef WIN_DIAG
+            if (tid == 0) h->stats[30] += clock64() - dgp;
+#endif
+            if (warp == 0) par = __shfl_sync(0xffffffffu, par, 0);
+            if (par && warp == 0) {
+                phase_a_parallel(w, lane);
+            } else if (tid == 0) {
+                if (h->n_ties) order_ties(w);
+                phase_a(w);
+            }
+            if (tid == 0) {
+                h->k_done = m;
+                h->stats[OTF_ST_CYC_SERVER] += clock64() - t0;
+                if (par) h->stats[OTF_ST_PAR_WINDOWS]++;
+            }
         }
         if constexpr (WIN_WARPS == 1) {
             // ---- phase B: the window's local timers, then the clients phase A responded

@@ -23,7 +23,7 @@ def timeit(name, cfgs, eng, reps=2):
         print("  windows/scn", st[22] / len(cfgs), "cycles/window", tot / max(1, st[22]),
               "scan %.2f sort %.2f server %.2f clients %.2f" % (st[23]/tot, st[24]/tot, st[25]/tot, st[26]/tot),
               "pops/scn", st[20]/len(cfgs), "ready", st[21]/len(cfgs),
-              "| local(concurrent) %.2f" % (st[28]/tot))
+              "| local(concurrent) %.2f | parallel server windows %.3f" % (st[28]/tot, st[29] / max(1, st[22])))
         if os.environ.get("OTF_DIAG"):
             for name, rows in (("all", slice(None)), ("TCP", [i for i in range(len(cfgs)) if i % 16 in (4, 5, 6, 7)])):
                 S = br.stats[rows].sum(0).astype(float)
@@ -31,6 +31,9 @@ def timeit(name, cfgs, eng, reps=2):
                       "scan %.0f sort %.0f cycles; requests/window %.1f" % (name,
                       S[25] / S[22], S[29] / S[22], S[30] / S[22], S[31] / S[22], S[26] / S[22], S[28] / S[22],
                       S[23] / S[22], S[24] / S[22], br.counts[rows, 0].sum() / S[22]))
+        if os.environ.get("OTF_PAR_DIAG"):
+            print("  par-diag: per window: parallel_ok %.0f, group replay %.0f, prefix+effects+handoffs %.0f, server total %.0f" % (
+                st[30] / st[22], st[28] / st[22], st[31] / st[22], st[25] / st[22]))
         per = br.stats[:, 27].astype(float)
         print("  scenario cycles: mean %.3g max %.3g (max/mean %.3f), max at %d" % (per.mean(), per.max(), per.max() / per.mean(), per.argmax()))
         if len(cfgs) % 16 == 0:
