@@ -55,7 +55,7 @@ constexpr int16_t NIL = -1;
 #define WIN_WARPS 1
 #endif
 constexpr int WIN_THREADS = 32 * WIN_WARPS;   // threads per scenario (see windowed_kernel)
-constexpr int PAR_MAX = 128;       // windows up to this many requests may take the parallel server pass
+constexpr int PAR_MAX = 256;       // windows up to this many requests may take the parallel server pass (uint8 indices)
 
 struct WWorker {
     double when, ctime;
@@ -739,17 +739,17 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
     dga = clock64();
 #endif
     // (b) sequence numbers in time order: exclusive prefix sums over the list
-    // (lane l holds requests 4l .. 4l+3)
-    constexpr int E = PAR_MAX / 32;
-    uint32_t fl[E], c_imm = 0, c_tch = 0, c_enq = 0, c_enq_d = 0;
-#pragma unroll
-    for (int t = 0; t < E; t++) {
+    // (lane l holds requests E*l .. E*l+E-1)
+    const int32_t E = (n + 31) >> 5;                    // requests per lane (runtime: one copy of the code)
+    uint32_t c_imm = 0, c_tch = 0, c_enq = 0, c_enq_d = 0;
+#pragma unroll 1
+    for (int32_t t = 0; t < E; t++) {
         const int32_t i = E * lane + t;
-        fl[t] = i < n ? h->ev_flags[i] : 0u;
-        c_imm += (fl[t] >> 3) & 1u;
-        c_tch += (fl[t] >> 4) & 1u;
-        c_enq += ((fl[t] >> 5) & 1u) + ((fl[t] >> 6) & 1u);
-        c_enq_d += (fl[t] >> 5) & 1u;
+        const uint32_t f = i < n ? h->ev_flags[i] : 0u;
+        c_imm += (f >> 3) & 1u;
+        c_tch += (f >> 4) & 1u;
+        c_enq += ((f >> 5) & 1u) + ((f >> 6) & 1u);
+        c_enq_d += (f >> 5) & 1u;
     }
     uint32_t n_imm, n_tch, n_enq;
     uint32_t p_imm = warp_excl_scan(c_imm, lane, n_imm);
@@ -768,11 +768,11 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
     // the first n_hand enqueues (time order) go to the idle workers (getters, FIFO);
     // the rest join the job FIFO
     const uint32_t n_hand = min(n_enq, (uint32_t)h->gq_n);
-#pragma unroll
-    for (int t = 0; t < E; t++) {
+#pragma unroll 1
+    for (int32_t t = 0; t < E; t++) {
         const int32_t i = E * lane + t;
-        if (i >= n) continue;
-        const uint32_t f = fl[t];
+        if (i >= n) break;
+        const uint32_t f = h->ev_flags[i];
         h->ev_touch[i] = (uint8_t)p_tch;
         const int32_t cid = w.li[i], d = w.ld[i];
         const double now = w.lw[i];
