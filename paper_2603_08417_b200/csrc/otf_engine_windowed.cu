@@ -1572,12 +1572,12 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
             int32_t i = lane;
             int32_t ncid = 0;
             Client nc;
-            if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; load_client_stream(nc, &w.cl[ncid]); }
+            if (i < total) { ncid = i < nb ? w.blist[i] : al[i - nb]; load_client_stream(nc, &w.cl[ncid]); }
             while (i < total) {
                 const int32_t cid = ncid;
                 Client c = nc;
                 i += 32;
-                if (i < total) { ncid = i < nl ? al[i] : w.blist[i - nl]; load_client_stream(nc, &w.cl[ncid]); }
+                if (i < total) { ncid = i < nb ? w.blist[i] : al[i - nb]; load_client_stream(nc, &w.cl[ncid]); }
                 client_local_body(w, c, cid);
                 store_client_stream(&w.cl[cid], c);
             }
