@@ -227,6 +227,9 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
         }
         atomicOr(&h->bits[slot >> 5], 1u << (slot & 31));
     } else {                                           // beyond the wheel (rare): far list
+#ifdef WIN_FAR_DIAG
+        atomicAdd((unsigned long long *)&h->stats[28], wk >= WIN_NONE ? (1ull << 32) : 1ull);
+#endif
         int32_t old = atomicExch(&h->far_head, c);
         w.bnext[c] = (int16_t)old;
         atomicAdd(&h->far_n, 1);
@@ -1430,7 +1433,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
                         int32_t c = h->arr_next;
                         while (c < N) {
                             int32_t wk = timer_win(w, w.S.arrival(c));
-                            if (wk == WIN_NONE || wk - m >= RING) break;
+                            if (wk == WIN_NONE || wk - w.k >= RING) break;   // wheel base is m - 1 here
                             bucket_push(w, c, wk, false);
                             c++;
                         }

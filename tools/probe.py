@@ -2,6 +2,7 @@
 import sys, time, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+import numpy as np
 from paper_2603_08417_b200 import engine, inputs, workloads, _lib
 
 def timeit(name, cfgs, eng, reps=2):
@@ -31,6 +32,10 @@ def timeit(name, cfgs, eng, reps=2):
                       "scan %.0f sort %.0f cycles; requests/window %.1f" % (name,
                       S[25] / S[22], S[29] / S[22], S[30] / S[22], S[31] / S[22], S[26] / S[22], S[28] / S[22],
                       S[23] / S[22], S[24] / S[22], br.counts[rows, 0].sum() / S[22]))
+        if os.environ.get("OTF_FAR_DIAG"):
+            v = br.stats[:, 28].astype(np.int64)
+            print("  far-diag: far pushes per scenario %.1f (of which beyond the horizon %.1f), windows %.0f" % (
+                (v & 0xffffffff).sum() / len(cfgs), (v >> 32).sum() / len(cfgs), st[22] / len(cfgs)))
         if os.environ.get("OTF_PAR_DIAG"):
             print("  par-diag: per window: parallel_ok %.0f, group replay %.0f, prefix+effects+handoffs %.0f, server total %.0f" % (
                 st[30] / st[22], st[28] / st[22], st[31] / st[22], st[25] / st[22]))
