@@ -124,6 +124,14 @@ __host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {   // power of t
     return c;
 }
 
+// A server-bucket entry carries the request's sort key and descriptor words, so
+// the window's gather is one coalesced read instead of bucket -> client state.
+struct SrvEnt {
+    double when;                                       // fire time (the request's arrival)
+    int32_t pk;                                        // rank | index << 8 | seq << 16
+    int16_t cid, desc;
+};
+
 struct WinGlobalLayout {
     int64_t clients, picks, blist, jobq, specq, lstamp, lq, bsrv, bloc, total;
 };
@@ -144,7 +152,7 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     L.specq = o;   o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.lstamp = o;  o += align256((int64_t)sizeof(uint32_t) * n_desc);
     L.lq = o;      o += align256((int64_t)sizeof(LqEnt) * 2 * lq_capacity(n_desc));
-    L.bsrv = o;    o += align256((int64_t)sizeof(int32_t) * RING * bucket_cap_srv(n_clients));
+    L.bsrv = o;    o += align256((int64_t)sizeof(SrvEnt) * RING * bucket_cap_srv(n_clients));
     L.bloc = o;    o += align256((int64_t)sizeof(int32_t) * RING * bucket_cap_loc(n_clients));
     L.total = o;
     return L;
@@ -171,7 +179,8 @@ struct Win {
     uint16_t *dflags;                                  // descriptor words (DF_*), shared
     Client *cl;
     int32_t *blist;
-    int32_t *bsrv, *bloc;                              // bucket arrays [RING][cap]
+    SrvEnt *bsrv;                                      // bucket arrays [RING][cap]
+    int32_t *bloc;
     int32_t scap, lcap;
     JobEnt *jq, *sq;
     double W, invW, H, E, now;
@@ -210,7 +219,7 @@ __device__ __forceinline__ int32_t timer_win(const Win &w, double when) {
 }
 
 // Put client c on the bucket of window `wk` (any lane; lock-free push).
-__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool srv) {
+__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool srv, const Client &cl) {
     WinHeader *h = w.h;
     if (wk - w.k < RING) {
         int32_t slot = wk & (RING - 1);
@@ -218,7 +227,16 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
         const uint32_t sh = (slot & 1) << 4;
         int32_t pos = (int32_t)((atomicAdd(srv ? &h->cnt_srv[slot >> 1] : &h->cnt_loc[slot >> 1], 1u << sh) >> sh) & 0xffffu);
         if (pos < cap) {
-            (srv ? w.bsrv : w.bloc)[(int64_t)slot * cap + pos] = c;
+            if (srv) {
+                SrvEnt e;
+                e.when = cl.next_when;
+                e.pk = cl.rank | (cl.index << 8) | (cl.seq << 16);
+                e.cid = (int16_t)c;
+                e.desc = (int16_t)cl.desc;
+                w.bsrv[(int64_t)slot * cap + pos] = e;
+            } else {
+                w.bloc[(int64_t)slot * cap + pos] = c;
+            }
         } else {                                       // bucket full (rare): overflow list
             int32_t old = atomicExch(&h->ovf_head, c);
             w.bnext[c] = (int16_t)old;
@@ -985,7 +1003,7 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
     const int32_t k = timer_win(w, when);
     if (k == WIN_NONE) return false;
     if (srv && k <= w.k) w.S.flag(OTF_S_TIE);          // lookahead violated (cannot happen)
-    bucket_push(w, cid, k, srv);                       // the single push site (code size)
+    bucket_push(w, cid, k, srv, c);                    // the single push site (code size)
     return false;
 }
 
@@ -1311,7 +1329,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
     w.cl = (Client *)(g + L.clients);
     w.S.picks = (Pcg64 *)(g + L.picks);
     w.blist = (int32_t *)(g + L.blist);
-    w.bsrv = (int32_t *)(g + L.bsrv);
+    w.bsrv = (SrvEnt *)(g + L.bsrv);
     w.bloc = (int32_t *)(g + L.bloc);
     w.scap = bucket_cap_srv(N);
     w.lcap = bucket_cap_loc(N);
@@ -1434,7 +1452,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
                         while (c < N) {
                             int32_t wk = timer_win(w, w.S.arrival(c));
                             if (wk == WIN_NONE || wk - w.k >= RING) break;   // wheel base is m - 1 here
-                            bucket_push(w, c, wk, false);
+                            bucket_push(w, c, wk, false, w.cl[c]);
                             c++;
                         }
                         h->arr_next = c;
@@ -1451,7 +1469,7 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
                         while (c >= 0) {
                             int32_t nx = w.bnext[c];
                             const Client &cl = w.cl[c];
-                            bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT);
+                            bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT, cl);
                             c = nx;
                         }
                     }
@@ -1498,11 +1516,17 @@ __global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
                     if (lane == 0) atomicOr(&h->st.status, OTF_S_TIE);
                     ctl = CTL_STOP;
                 } else {
-                    const int32_t *as = w.bsrv + (int64_t)slot * w.scap;
-                    for (int32_t i = lane; i < nlist; i += 32) {   // gather sort keys + request descriptors
-                        int32_t c = i < ns ? as[i] : w.li[i];
+                    const SrvEnt *as = w.bsrv + (int64_t)slot * w.scap;
+                    for (int32_t i = lane; i < ns; i += 32) {      // gather sort keys + request descriptors
+                        const SrvEnt e = as[i];
+                        w.li[i] = e.cid;
+                        w.lw[i] = e.when;
+                        w.ld[i] = e.desc;
+                        w.lp[i] = e.pk;
+                    }
+                    for (int32_t i = ns + lane; i < nlist; i += 32) {   // overflowed pushes: from the client state
+                        const int32_t c = w.li[i];
                         const Client &cl = w.cl[c];
-                        w.li[i] = (int16_t)c;
                         w.lw[i] = cl.next_when;
                         w.ld[i] = (int16_t)cl.desc;
                         w.lp[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
