@@ -114,6 +114,14 @@ def test_config4_points_vs_oracle():
     _oracle_cmp(cfgs)
 
 
+def test_config4_largest_points_vs_oracle():
+    """BASELINE config 4 at its largest client counts, full 600 s horizon: 10,000 clients
+    (windows of ~180 requests: the shared-memory bitonic sort, the parallel server pass
+    at up to 256 requests, the largest shared-memory class) and 3,000 clients."""
+    _oracle_cmp([workloads.c4(seed=7, clients=10000, variant="TCP"),
+                 workloads.c4(seed=8, clients=3000, variant="TCPF")])
+
+
 def test_config5_point_vs_oracle():
     """BASELINE config 5 (10-rank ladder) at reduced client count and horizon."""
     _oracle_cmp([workloads.c5(seed=s, clients=400, horizon_s=120.0, variant=v)
