@@ -51,10 +51,7 @@ constexpr uint16_t DF_IDLE = 0x7FFF;
 constexpr uint16_t DF_NOWAIT = 0x7FFE;
 __device__ __forceinline__ bool df_inflight(uint16_t f) { return (f & 0x7FFF) != DF_IDLE; }
 constexpr int16_t NIL = -1;
-#ifndef WIN_WARPS
-#define WIN_WARPS 1
-#endif
-constexpr int WIN_THREADS = 32 * WIN_WARPS;   // threads per scenario (see windowed_kernel)
+constexpr int WIN_MAX_WARPS = 2;   // warps per scenario: 1, or 2 for the big shared-memory classes
 constexpr int PAR_MAX = 256;       // windows up to this many requests may take the parallel server pass (uint8 indices)
 
 struct WWorker {
@@ -103,7 +100,7 @@ struct WinHeader {
     uint8_t par_list[PAR_MAX];           //   the list partitioned by owner lane (time order kept)
     uint32_t par_cnt[32];                //   per owner lane: count, then next slot
     int32_t hand_safe;                   // no transcode can end within the window it starts in
-    double wsum[WIN_WARPS][3];           // per-warp float sums (fixed-order final reduction)
+    double wsum[WIN_MAX_WARPS][3];       // per-warp float sums (fixed-order final reduction)
 };
 
 // Server events one window can hold: the list lives in the dynamic shared region.
@@ -1288,16 +1285,14 @@ enum { CTL_RUN = 0, CTL_REFILE = 1, CTL_STOP = 2 };
 // (clients with a local timer due are never touched by phase A: they are not
 // waiting on the backend and have no pending request).  Finally both warps run
 // the clients phase A responded to.
-template <bool RECORDS>
-// 7 CTAs per SM run 1,024 scenarios on 148 SMs in one wave.  The register file
-// is split over the 4 SM sub-partitions (16k each), so 2 warps per CTA cap the
-// kernel at 128 registers; one warp per CTA leaves it ~210.
-#if WIN_WARPS == 1
-#define WIN_BOUNDS __launch_bounds__(32, 8)
-#else
-#define WIN_BOUNDS __launch_bounds__(WIN_THREADS, 7)
-#endif
-__global__ void WIN_BOUNDS windowed_kernel(const otf_batch b) {
+// NW warps per scenario.  NW = 1: 7 CTAs per SM run 1,024 config-5 scenarios on
+// 148 SMs in one wave; the register file is split over the 4 SM sub-partitions
+// (16 k each), so two-warp CTAs at that occupancy would cap the kernel at 128
+// registers.  NW = 2 serves the shared-memory classes that fit at most 4 CTAs
+// per SM anyway (10,000-client scenarios): 8 warps per SM keep ~240 registers.
+template <bool RECORDS, int NW>
+__global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(const otf_batch b) {
+    constexpr int WIN_WARPS = NW, WIN_THREADS = 32 * NW;
     extern __shared__ __align__(16) uint8_t smem[];
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -1687,11 +1682,14 @@ int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
 
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
     int smem = (int)b.shared_bytes;
-    auto kern = b.mode == OTF_MODE_RECORDS ? otf::windowed_kernel<true> : otf::windowed_kernel<false>;
+    // two warps per scenario once shared memory allows at most 4 CTAs per SM
+    const int nw = (smem + 1024) * 5 > 228 * 1024 ? 2 : 1;
+    auto kern = b.mode == OTF_MODE_RECORDS ? (nw == 2 ? otf::windowed_kernel<true, 2> : otf::windowed_kernel<true, 1>)
+                                           : (nw == 2 ? otf::windowed_kernel<false, 2> : otf::windowed_kernel<false, 1>);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return 1;
     }
-    kern<<<b.n_scenarios, otf::WIN_THREADS, smem, stream>>>(b);
+    kern<<<b.n_scenarios, 32 * nw, smem, stream>>>(b);
     return 0;
 }
