@@ -993,7 +993,17 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
     c.ctime = now;
     c.next_when = when;
     const bool srv = next_pc == C_SEG_LAT;             // a server event: always a later window
+#ifndef WIN_NO_FOLD
+    // A client-local timer (anything but the request-latency timer, which reaches the
+    // server) is run right away, even if it fires in a later window: nothing but the
+    // client itself can act on a client in a local sleep (it neither waits on the
+    // backend nor has a request pending), and nothing it does before its next request
+    // is seen by anyone else ("Local chains").  The only cut is the
+    // horizon: a timer after it never fires (sim.py:352).
+    if (!srv && when <= w.H) {
+#else
     if (!srv && when <= w.H && when < w.E) {           // fires inside this window: keep going
+#endif
         now = when;
         return true;
     }
