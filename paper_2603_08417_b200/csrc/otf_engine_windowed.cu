@@ -1192,29 +1192,33 @@ __device__ void sort_list(Win &w, int lane) {
     if (lane == 0) h->n_ties = 0;
     if (n <= 1) { __syncwarp(); return; }
     if (n <= RANK_SORT_MAX) {
-        // each lane ranks elements lane and lane + 32 in ONE pass over the list (one
-        // pair of broadcast loads per j for both), and spots equal times on the way
+        // each lane ranks elements lane and lane + 32 in one pass over the list (one
+        // pair of broadcast loads per j for both).  Non-negative doubles order like
+        // their bit patterns, so the compares run on the integer pipe.
         const int32_t i0 = lane, i1 = lane + 32;
         const bool v0 = i0 < n, v1 = i1 < n;
         const double w0 = v0 ? w.lw[i0] : INFINITY, w1 = v1 ? w.lw[i1] : INFINITY;
         const int32_t id0 = v0 ? w.li[i0] : 0x7fff, id1 = v1 ? w.li[i1] : 0x7fff;
-        int32_t r0 = 0, r1 = 0, e0 = 0, e1 = 0;
+        const unsigned long long t0 = (unsigned long long)__double_as_longlong(w0);
+        const unsigned long long t1 = (unsigned long long)__double_as_longlong(w1);
+        const unsigned long long *lwb = reinterpret_cast<const unsigned long long *>(w.lw);
+        int32_t r0 = 0, r1 = 0;
 #pragma unroll 4
         for (int32_t j = 0; j < n; j++) {              // branch-free (time, client) compare
-            const double wj = w.lw[j];
+            const unsigned long long tj = lwb[j];
             const int32_t idj = w.li[j];
-            r0 += (int32_t)((wj < w0) | ((wj == w0) & (idj < id0)));
-            r1 += (int32_t)((wj < w1) | ((wj == w1) & (idj < id1)));
-            e0 += (int32_t)(wj == w0);
-            e1 += (int32_t)(wj == w1);
+            r0 += (int32_t)((tj < t0) | ((tj == t0) & (idj < id0)));
+            r1 += (int32_t)((tj < t1) | ((tj == t1) & (idj < id1)));
         }
         const int16_t d0 = v0 ? w.ld[i0] : 0, d1 = v1 ? w.ld[i1] : 0;
         const int32_t s0 = v0 ? w.lp[i0] : 0, s1 = v1 ? w.lp[i1] : 0;
-        const bool tie = (v0 && e0 > 1) || (v1 && e1 > 1);   // equal request times (rare)
-        const bool any = __any_sync(0xffffffffu, tie);
         __syncwarp();                                  // every lane has read the list
         if (v0) { w.lw[r0] = w0; w.li[r0] = (int16_t)id0; w.ld[r0] = d0; w.lp[r0] = s0; }
         if (v1) { w.lw[r1] = w1; w.li[r1] = (int16_t)id1; w.ld[r1] = d1; w.lp[r1] = s1; }
+        __syncwarp();
+        // equal request times (rare): neighbours in the sorted list
+        const bool tie = (i0 > 0 && v0 && w.lw[i0] == w.lw[i0 - 1]) || (v1 && w.lw[i1] == w.lw[i1 - 1]);
+        const bool any = __any_sync(0xffffffffu, tie);
         if (lane == 0) h->n_ties = any ? 1 : 0;
         __syncwarp();
         return;
