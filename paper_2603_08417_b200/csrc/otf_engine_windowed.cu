@@ -905,15 +905,20 @@ __device__ __forceinline__ bool parallel_ok(Win &w) {
             if (h->wk[q].win == w.k) { hm->stats[24]++; break; }   // (diag build: overrides the sort cycles)
     }
 #endif
-    if (n < 2 || n > PAR_MAX || h->n_ties || h->fq_n > 0 || sc.demand_priority || sc.queue_bound > 0)
-        return false;
-    for (int32_t q = 0; q < sc.n_workers; q++)
-        if (h->wk[q].win == w.k) return false;         // a transcode completes in this window
-    // an idle worker handed a job here must not finish inside the window: its service
-    // time (rho * duration) * (1 + eps) is at least svc_floor * (1 + its next eps)
-    if (h->gq_n > 0 && !h->hand_safe) return false;
-    w.lq_head = h->lq_head; w.lq_tail = h->lq_tail; w.n_blist = h->n_blist;
-    return w.lq_tail - w.lq_head + (uint32_t)n <= w.lq_mask;   // room for every touch
+    // every word loaded up front and combined without early exits: one shared-memory
+    // round trip on the lane instead of a chain of them
+    const int32_t n_ties = h->n_ties, fq_n = h->fq_n, gq_n = h->gq_n, hand_safe = h->hand_safe;
+    const uint32_t lq_head = h->lq_head, lq_tail = h->lq_tail;
+    const int32_t n_blist = h->n_blist;
+    bool due = false;                                  // a transcode completes in this window
+#pragma unroll 4
+    for (int32_t q = 0; q < sc.n_workers; q++) due |= h->wk[q].win == w.k;
+    w.lq_head = lq_head; w.lq_tail = lq_tail; w.n_blist = n_blist;
+    // an idle worker handed a job here must not finish inside the window (hand_safe:
+    // svc >= svc_floor * (1 + min eps) >= 2 W for every job, checked at kernel start)
+    return (n >= 2) & (n <= PAR_MAX) & (n_ties == 0) & (fq_n == 0) & (sc.demand_priority == 0) &
+           (sc.queue_bound <= 0) & !due & ((gq_n == 0) | (hand_safe != 0)) &
+           (lq_tail - lq_head + (uint32_t)n <= w.lq_mask);   // room for every touch
 }
 
 // Phase A: replay the window's server events in (time, creation, tick) order.
