@@ -1465,6 +1465,29 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
             if (m == WIN_NONE) {
                 ctl = CTL_STOP;
             } else {
+#ifndef WIN_SERIAL_ARRIVALS
+                if (arr_win != WIN_NONE && arr_win - m < RING / 2) {   // arrivals entering the wheel:
+                    // a batch of ~RING/2 windows' worth, 32 clients at a time (offsets are a
+                    // cumulative sum, so the clients that fit form a prefix of each chunk)
+                    w.k = m - 1;                           // windows before m are empty: wheel base = m
+                    int32_t base = h->arr_next;
+                    for (;;) {
+                        const int32_t c = base + lane;
+                        const int32_t wk = c < N ? timer_win(w, w.S.arrival(c)) : WIN_NONE;
+                        const bool ok = wk != WIN_NONE && wk - w.k < RING;
+                        if (ok) bucket_push(w, c, wk, false, w.cl[c]);
+                        const int32_t got = __popc(__ballot_sync(0xffffffffu, ok));
+                        base += got;
+                        if (got < 32) break;
+                    }
+                    if (lane == 0) {
+                        h->k_done = m - 1;
+                        h->arr_next = base;
+                        h->arr_win = base < N ? timer_win(w, w.S.arrival(base)) : WIN_NONE;
+                    }
+                    __syncwarp();
+                }
+#else
                 if (arr_win != WIN_NONE && arr_win - m < RING) {   // arrivals entering the wheel
                     if (lane == 0) {
                         h->k_done = m - 1;                 // windows before m are empty: wheel base = m
@@ -1481,6 +1504,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                     }
                     __syncwarp();
                 }
+#endif
                 if (h->far_n > 0 && h->far_min < m + RING / 2) {   // far timers close to the wheel: re-file
                     if (lane == 0) {
                         int32_t c = h->far_head;
@@ -1545,6 +1569,14 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         w.ld[i] = e.desc;
                         w.lp[i] = e.pk;
                     }
+#ifndef WIN_NO_NEXT_PF
+                    {                                      // warm L2 with the next window's request entries
+                        const int32_t sn = (m + 1) & (RING - 1);
+                        const int32_t nn = min((int32_t)((h->cnt_srv[sn >> 1] >> ((sn & 1) << 4)) & 0xffffu), w.scap);
+                        if (8 * lane < nn)
+                            asm volatile("prefetch.global.L2 [%0];" :: "l"(w.bsrv + (int64_t)sn * w.scap + 8 * lane));
+                    }
+#endif
                     for (int32_t i = ns + lane; i < nlist; i += 32) {   // overflowed pushes: from the client state
                         const int32_t c = w.li[i];
                         const Client &cl = w.cl[c];
