@@ -9,12 +9,15 @@
 // are responses delivered at the server event's instant.  Cutting virtual time
 // into windows [k*W, (k+1)*W) with W slightly below `latency` therefore gives:
 //   * every server event of window k was armed before the window started, so
-//     the server lane (lane 0) can replay all of them -- plus the worker
-//     service timers (backend.py:186-216) and the ready-queue hops they cause
-//     (sim.py:126-130, 229-247) -- in exact (time, tick) order first;
-//   * afterwards each client's local events in the window depend only on its
-//     own state and the responses just produced, so all 32 lanes run them in
-//     parallel (client.py:229-305, orchestrator.py:336-348).
+//     the server pass can replay all of them -- plus the worker service timers
+//     (backend.py:186-216) and the ready-queue hops they cause (sim.py:126-130,
+//     229-247) -- in exact (time, tick) order first.  In request-only windows
+//     the whole warp does it (phase_a_parallel: per-(sequence, rank) groups on
+//     their owner lanes, sequence numbers by prefix sums); otherwise lane 0;
+//   * afterwards the clients just responded to, and the window's local timers,
+//     run on the 32 lanes (client.py:229-305, orchestrator.py:336-348).  A
+//     client in a local sleep cannot be reached by anyone else, so each runs
+//     its local chain in place up to its next request (arm()).
 // The only order information this loses is the global tick counter
 // (sim.py:304-309), which breaks ties between timers at the identical
 // instant.  Server events are ordered by (time, creation time) and ties the
@@ -22,9 +25,10 @@
 // scenario on the exact engine; session registration ties are checked on the
 // host.  Parity tests pin both engines to the reference's outputs.
 //
-// Layout: scenario hot state in shared memory (per-client window index, cache
-// flags + LRU links, the window's server-event list, worker timers,
-// counters); client coroutine state, waiter lists and the job FIFO in the
+// Layout: scenario hot state in shared memory (timer-wheel counts and bitmap,
+// descriptor words with the waiter-list tails, client links, the window's
+// server-event list, worker timers, counters); client coroutine state, the
+// wheel's bucket arrays, the job FIFOs and the LRU touch queue in the
 // scenario's global scratch arena.
 #include <cuda_runtime.h>
 #include <math.h>
