@@ -238,6 +238,26 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
     m = _lib.MODE_RECORDS if mode == "records" else _lib.MODE_HISTOGRAM
     eng = _lib.ENGINE_WINDOWED if engine == "windowed" else _lib.ENGINE_EXACT
     configs = list(configs)
+    if m == _lib.MODE_RECORDS and _caps is None and len(configs) > 1:
+        # record buffers grow with the requests (~212 B per expected request): a big
+        # sweep in records mode runs in chunks that fit half the free device memory
+        from .inputs import _default_caps, lower
+        from .config import ExperimentConfig
+        dev = require_cuda(device)
+        budget = torch.cuda.mem_get_info(dev)[0] // 2
+        need = []
+        for c in configs:
+            r, s_, g, j = _default_caps(lower(ExperimentConfig.from_reference(c)))
+            need.append(48 * r + 48 * s_ + 28 * g + 44 * j)
+        if sum(need) > budget:
+            out, chunk, used = [], [], 0
+            for c, b in zip(configs, need):
+                if chunk and used + b > budget:
+                    out += run_batch(chunk, mode, engine, device, max_retries)
+                    chunk, used = [], 0
+                chunk.append(c)
+                used += b
+            return out + run_batch(chunk, mode, engine, device, max_retries)
     results: list = [None] * len(configs)
     todo = list(range(len(configs)))
     caps = {i: tuple(c) for i, c in enumerate(_caps)} if _caps is not None else {}   # test hook

@@ -186,6 +186,20 @@ def test_histogram_mode_matches_records():
         assert np.array_equal(r.stats_raw[:18], h.stats_raw[:18])
 
 
+def test_records_mode_chunks_to_fit_device_memory(monkeypatch):
+    """A records-mode sweep whose record buffers exceed half the free device memory
+    runs in chunks; the results equal the one-launch run."""
+    import torch
+    cfgs = [workloads.c3(seed=4, fraction=f) for f in (0.0, 0.2, 0.6)] + [workloads.c1(seed=6)]
+    whole = engine.run_batch(cfgs, mode="records")
+    free, total = torch.cuda.mem_get_info()
+    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda *a, **k: (60_000_000, total))   # ~1 config per chunk
+    chunked = engine.run_batch(cfgs, mode="records")
+    for a, b in zip(whole, chunked):
+        errs = parity.compare(b.arrays, a.arrays)
+        assert not errs, errs[:5]
+
+
 def test_no_cpu_fallback_without_library(monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libotfgpu.so")
