@@ -223,6 +223,19 @@ int otf_gen_traces(uint64_t seed, int64_t n_traces, int32_t n_samples, const dou
                    double mu, double sigma, double decay, double spread, double floor_bps, double cap_bps,
                    double *values, double *pbits, int32_t n_threads);
 
+/* Many trace tables in one parallel region (one per (seed, netem) of a sweep):
+ * job q = otf_gen_traces(seed, n_traces, ...) for clients 0..n_traces-1. */
+typedef struct otf_trace_job {
+    uint64_t seed;
+    int64_t n_traces;
+    int32_t n_samples, pad;
+    const double *starts;
+    double period, mu, sigma, decay, spread, floor_bps, cap_bps;
+    double *values;                   /* [n_traces][n_samples] */
+    double *pbits;                    /* [n_traces] */
+} otf_trace_job;
+int otf_gen_traces_multi(int32_t n_jobs, const otf_trace_job *jobs, int32_t n_threads);
+
 /* DEVICE: fill segment-size tables (one thread per entry). */
 int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
                   int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream);

@@ -88,6 +88,12 @@ class Batch(ctypes.Structure):
                    ("shared_bytes", _i64), ("engine_flags", _i32), ("pad_flags", _i32)])
 
 
+class TraceJob(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("n_traces", _i64), ("n_samples", _i32), ("pad", _i32),
+                ("starts", _vp), ("period", _f64), ("mu", _f64), ("sigma", _f64), ("decay", _f64),
+                ("spread", _f64), ("floor_bps", _f64), ("cap_bps", _f64), ("values", _vp), ("pbits", _vp)]
+
+
 class SizeTable(ctypes.Structure):
     _fields_ = [
         ("n_seq", _i32), ("n_ranks", _i32), ("max_nseg", _i32), ("pad", _i32),
@@ -99,7 +105,7 @@ class SizeTable(ctypes.Structure):
 
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
            "otf_scratch_bytes", "otf_shared_bytes", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
-           "otf_gen_noise", "otf_gen_traces", "otf_gen_sizes", "otf_run_batch")
+           "otf_gen_noise", "otf_gen_traces", "otf_gen_traces_multi", "otf_gen_sizes", "otf_run_batch")
 DRAW_STANDARD_NORMAL, DRAW_NORMAL, DRAW_EXPONENTIAL, DRAW_STANDARD_EXPONENTIAL = 0, 1, 2, 3
 
 
@@ -148,6 +154,8 @@ def lib():
     L.otf_gen_traces.restype = ctypes.c_int
     L.otf_gen_traces.argtypes = [ctypes.c_uint64, _i64, _i32, _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
                                  _P(_f64), _P(_f64), _i32]
+    L.otf_gen_traces_multi.restype = ctypes.c_int
+    L.otf_gen_traces_multi.argtypes = [_i32, _vp, _i32]
     L.otf_gen_sizes.restype = ctypes.c_int
     L.otf_gen_sizes.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp, _vp]
     L.otf_run_batch.restype = ctypes.c_int

@@ -200,6 +200,36 @@ int otf_gen_traces(uint64_t seed, int64_t n_traces, int32_t n_samples, const dou
     return OTF_OK;
 }
 
+int otf_gen_traces_multi(int32_t n_jobs, const otf_trace_job *jobs, int32_t n_threads) {
+    if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return otf_fail(OTF_EINVAL, "otf_gen_traces_multi: bad arguments");
+    std::vector<int64_t> first((size_t)n_jobs + 1, 0);   // flattened (job, client) index space
+    for (int32_t q = 0; q < n_jobs; q++) {
+        const otf_trace_job &J = jobs[q];
+        if (J.n_traces < 0 || J.n_samples <= 0 || !J.starts || (J.n_traces > 0 && (!J.values || !J.pbits)))
+            return otf_fail(OTF_EINVAL, "otf_gen_traces_multi: bad job");
+        first[(size_t)q + 1] = first[(size_t)q] + J.n_traces;
+    }
+    otf::parallel_for(first[(size_t)n_jobs], n_threads, 16, [&](int64_t lo, int64_t hi) {
+        std::vector<double> z, terms;
+        int32_t q = (int32_t)(std::upper_bound(first.begin(), first.end(), lo) - first.begin()) - 1;
+        for (int64_t t = lo; t < hi; t++) {
+            while (t >= first[(size_t)q + 1]) q++;
+            const otf_trace_job &J = jobs[q];
+            const int64_t c = t - first[(size_t)q];
+            z.resize((size_t)J.n_samples + 1);
+            terms.resize((size_t)J.n_samples);
+            uint64_t ent[3] = {J.seed, 2, (uint64_t)c};
+            otf::Pcg64 g;
+            otf::seed_stream(g, ent, 3);
+            for (int32_t i = 0; i <= J.n_samples; i++) z[(size_t)i] = otf::np_standard_normal(g);
+            otf::trace_from_normals(z.data(), J.n_samples, J.starts, J.period, J.mu, J.sigma, J.decay, J.spread,
+                                    J.floor_bps, J.cap_bps, J.values + c * (int64_t)J.n_samples, J.pbits + c,
+                                    terms.data());
+        }
+    });
+    return OTF_OK;
+}
+
 int otf_build_traces(int64_t n_traces, int32_t n_samples, const double *normals, const double *starts,
                      double period, double mu, double sigma, double decay, double spread,
                      double floor_bps, double cap_bps, double *values, double *pbits, int32_t n_threads) {

@@ -128,7 +128,8 @@ def lower(cfg: ExperimentConfig) -> Lowered:
 
 
 class _Pools:
-    def __init__(self):
+    def __init__(self, threads: int = 1):
+        self.threads = threads
         self.parts = {"f64": [], "i64": [], "i32": []}
         self.size = {"f64": 0, "i64": 0, "i32": 0}
         self.memo = {}
@@ -149,7 +150,9 @@ class _Pools:
         return self.add(kind, np.zeros(n), key)
 
     def defer(self, kind: str, n: int, fill) -> int:
-        """Reserve n elements that fill(view) writes in place when the pool is laid out."""
+        """Reserve n elements that fill(view) writes in place when the pool is laid out.
+        A fill may instead return an _lib.TraceJob (run with every other table's in one
+        parallel host call) or a callable to run after those jobs."""
         off = self.size[kind]
         self.parts[kind].append((int(n), fill))
         self.size[kind] += int(n)
@@ -166,15 +169,26 @@ class _Pools:
         else:
             out = np.empty(total, dtype=dt)
         pos = 0
+        jobs, after = [], []
         for part in self.parts[kind]:
             if isinstance(part, tuple):
                 n, fill = part
-                fill(out[pos:pos + n])
+                r = fill(out[pos:pos + n])
+                if isinstance(r, _lib.TraceJob):
+                    jobs.append(r)
+                elif callable(r):
+                    after.append(r)
             else:
                 n = part.size
                 out[pos:pos + n] = part
             pos += n
         out[pos:] = 0
+        if jobs:                                       # every trace table of the batch in one call
+            arr = (_lib.TraceJob * len(jobs))(*jobs)
+            _lib.check(_lib.lib().otf_gen_traces_multi(len(jobs), ctypes.addressof(arr), self.threads),
+                       "otf_gen_traces_multi")
+        for f in after:
+            f()
         return out
 
 
@@ -222,7 +236,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     L = _lib.lib()
     threads = threads or os.cpu_count() or 1
     lows = [lower(ExperimentConfig.from_reference(c)) for c in configs]
-    P = _Pools()
+    P = _Pools(threads)
     scen = (_lib.Scenario * max(1, len(lows)))()
     tables = []
     scratch_off = 0
@@ -258,17 +272,16 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
 
         def fill_values(view, seed=seed, nmax=nmax, n=n, starts_a=starts_a, period=period, ne=ne, decay=decay,
                         spread=spread, pbits=pbits):
-            # generated straight into the (pinned) pool: no intermediate copy
-            dp = ctypes.POINTER(ctypes.c_double)
-            rc = L.otf_gen_traces(seed, nmax, n, starts_a.ctypes.data_as(dp), period, math.log(ne.median_bps),
-                                  ne.sigma, decay, spread, ne.floor_bps, ne.cap_bps, view.ctypes.data_as(dp),
-                                  pbits.ctypes.data_as(dp), threads)
-            _lib.check(rc, "otf_gen_traces")
+            # generated straight into the (pinned) pool, all tables in one parallel call
+            return _lib.TraceJob(seed=seed, n_traces=nmax, n_samples=n, pad=0, starts=starts_a.ctypes.data,
+                                 period=period, mu=math.log(ne.median_bps), sigma=ne.sigma, decay=decay,
+                                 spread=spread, floor_bps=ne.floor_bps, cap_bps=ne.cap_bps,
+                                 values=view.ctypes.data, pbits=pbits.ctypes.data)
 
         grid = float(ne.step_s) if all(x == float(i) * ne.step_s for i, x in enumerate(starts)) else 0.0
         trace_tab[key] = dict(n=n, period=period, grid=grid,
                               starts=P.add("f64", starts_a), values=P.defer("f64", nmax * n, fill_values),
-                              pbits=P.defer("f64", nmax, lambda view, pbits=pbits: np.copyto(view, pbits)))
+                              pbits=P.defer("f64", nmax, lambda view, pbits=pbits: (lambda: np.copyto(view, pbits))))
         input_bytes += 8 * (nmax * n + nmax) + starts_a.nbytes
 
     # -- worker noise: one table per (seed, noise), longest draw count --
