@@ -220,7 +220,7 @@ class BatchResult:
         low = self.inp.lowered[i]
         return ExperimentResult(low.cfg, self.arrays(i) if self.rec else {}, self.stats[i], low.seq_ids,
                                 sizes=self.sizes(i), seq_dur=low.seq_dur, seq_segdur=low.seq_segdur,
-                                qoe=parse_qoe(self.qoe[i]), status=int(self.status[i]))
+                                qoe=self.qoe[i], status=int(self.status[i]))
 
     @property
     def total_requests(self) -> int:

@@ -217,17 +217,36 @@ class ExperimentResult:
     def __init__(self, config, arrays: dict, stats: np.ndarray, seq_ids: list[str], sizes=None,
                  seq_dur=None, seq_segdur=None, qoe: dict | None = None, status: int = 0):
         self.config = config
-        self.fingerprint = fingerprint(config.to_dict())
         self.arrays = arrays
         self.stats_raw = stats
         self.seq_ids = seq_ids
-        self.qoe = qoe
+        self._qoe = qoe                                # dict, or a raw otf_qoe row parsed on first use
         self.status = status
         self._sizes = sizes
         self._seq_dur = seq_dur
         self._seq_segdur = seq_segdur
         self._requests = self._sessions = self._jobs = None
-        self.backend_stats = self._backend_stats()
+        self._fingerprint = self._bstats = None
+
+    # derived fields are computed on first use: a 1,024-scenario sweep returns 1,024 results
+    @property
+    def fingerprint(self) -> str:
+        if self._fingerprint is None:
+            self._fingerprint = fingerprint(self.config.to_dict())
+        return self._fingerprint
+
+    @property
+    def backend_stats(self) -> dict:
+        if self._bstats is None:
+            self._bstats = self._backend_stats()
+        return self._bstats
+
+    @property
+    def qoe(self):
+        if self._qoe is not None and not isinstance(self._qoe, dict):
+            from .engine import parse_qoe
+            self._qoe = parse_qoe(self._qoe)
+        return self._qoe
 
     def _backend_stats(self) -> dict:
         st = self.stats_raw
