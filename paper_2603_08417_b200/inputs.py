@@ -308,9 +308,11 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         ladder = sorted(cfg.ladder)
         cat_key = (cfg.seed, cfg.size_jitter, tuple(low.seq_ids), tuple(low.seq_dur), tuple(low.seq_segdur),
                    tuple(ladder))
-        keys = [int.from_bytes(hashlib.sha256(s.encode("utf-8")).digest()[:8], "big") for s in low.seq_ids]
         o_bitrates = P.add("i64", [b for _, b in ladder], key=("bitrates", tuple(ladder)))
-        o_keys = P.add("i64", np.array(keys, dtype=np.uint64).view(np.int64), key=("keys", tuple(low.seq_ids)))
+        if ("i64", ("keys", tuple(low.seq_ids))) not in P.memo:
+            keys = [int.from_bytes(hashlib.sha256(s.encode("utf-8")).digest()[:8], "big") for s in low.seq_ids]
+            P.add("i64", np.array(keys, dtype=np.uint64).view(np.int64), key=("keys", tuple(low.seq_ids)))
+        o_keys = P.memo[("i64", ("keys", tuple(low.seq_ids)))]
         o_seqdur = P.add("f64", low.seq_dur, key=("seqdur", cat_key))
         o_segdur = P.add("f64", low.seq_segdur, key=("segdur", cat_key))
         o_counts = P.add("i32", low.counts, key=("counts", cat_key))
