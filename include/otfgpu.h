@@ -236,6 +236,24 @@ typedef struct otf_trace_job {
 } otf_trace_job;
 int otf_gen_traces_multi(int32_t n_jobs, const otf_trace_job *jobs, int32_t n_threads);
 
+/* ---- the per-client model functions (csrc/otf_model.cuh) on their own, for
+ * validation against the reference's known answers (tests/test_model_kat.py) ---- */
+
+/* BandwidthTrace.completion_time (netem.py:77-118) over a looping trace of n
+ * pieces; grid > 0 when starts[i] == i * grid exactly.  HOST pointers. */
+double otf_model_completion_time(const double *starts, const double *values, int32_t n, double period, double pbits,
+                                 double grid, double start, int64_t nbytes);
+
+/* select_quality (client.py:134-146); bitrates[r-1] is rank r, top = n ranks. */
+int32_t otf_model_select_quality(double level, int32_t cur, int32_t has_est, double est, const int64_t *bitrates,
+                                 int32_t top, double panic, double safe, double headroom);
+
+/* DEVICE: completion_time for n (start, nbytes) queries over one trace (device
+ * pointers), as the engines compute it (--fmad=false). */
+int otf_model_completion_times(const double *starts, const double *values, int32_t n_samples, double period,
+                               double pbits, double grid, const double *start, const int64_t *nbytes, int32_t n,
+                               double *out, void *stream);
+
 /* DEVICE: fill segment-size tables (one thread per entry). */
 int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
                   int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream);

@@ -34,9 +34,50 @@ static int check_cuda(const char *what) {
     return OTF_OK;
 }
 
+namespace {
+// A Trace over caller pointers (host or device), as Scn::trace() builds it.
+__host__ __device__ inline otf::Trace model_trace(const double *starts, const double *values, int32_t n,
+                                                   double period, double pbits, double grid) {
+    otf::Trace t;
+    t.starts = starts; t.values = values; t.n = n;
+    t.period = period; t.pbits = pbits; t.grid = grid;
+    t.inv_grid = grid > 0 ? 1.0 / grid : 0.0;
+    return t;
+}
+
+__global__ void model_completion_kernel(const double *starts, const double *values, int32_t n_samples,
+                                        double period, double pbits, double grid, const double *start,
+                                        const int64_t *nbytes, int32_t n, double *out) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n)
+        out[i] = otf::completion_time(model_trace(starts, values, n_samples, period, pbits, grid), start[i], nbytes[i]);
+}
+}  // namespace
+
 extern "C" {
 
 int otf_version(void) { return OTF_ABI_VERSION; }
+
+double otf_model_completion_time(const double *starts, const double *values, int32_t n, double period, double pbits,
+                                 double grid, double start, int64_t nbytes) {
+    return otf::completion_time(model_trace(starts, values, n, period, pbits, grid), start, nbytes);
+}
+
+int32_t otf_model_select_quality(double level, int32_t cur, int32_t has_est, double est, const int64_t *bitrates,
+                                 int32_t top, double panic, double safe, double headroom) {
+    return otf::select_quality(level, cur, has_est != 0, est, bitrates, top, panic, safe, headroom);
+}
+
+int otf_model_completion_times(const double *starts, const double *values, int32_t n_samples, double period,
+                               double pbits, double grid, const double *start, const int64_t *nbytes, int32_t n,
+                               double *out, void *stream) {
+    if (n < 0 || n_samples <= 0 || (n > 0 && (!starts || !values || !start || !nbytes || !out)))
+        return fail(OTF_EINVAL, "otf_model_completion_times: bad arguments");
+    if (n == 0) return OTF_OK;
+    model_completion_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(starts, values, n_samples, period,
+                                                                               pbits, grid, start, nbytes, n, out);
+    return check_cuda("otf_model_completion_times");
+}
 
 const char *otf_last_error(void) { return g_last_error.c_str(); }
 

@@ -21,7 +21,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_library_exports_every_header_symbol():
     L = _lib.lib()
     header = open(os.path.join(ROOT, "include", "otfgpu.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|int64_t|size_t|const char \*)\s*\*?\s*(otf_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|int32_t|double|size_t|const char \*)\s*\*?\s*(otf_\w+)\s*\(",
+                              header, re.M))
     assert declared == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(L, name), name
