@@ -248,6 +248,12 @@ double otf_model_completion_time(const double *starts, const double *values, int
 int32_t otf_model_select_quality(double level, int32_t cur, int32_t has_est, double est, const int64_t *bitrates,
                                  int32_t top, double panic, double safe, double headroom);
 
+/* PlayerBuffer (client.py:74-121) from buf_reset(t0): op[i] = 1 -> on_segment(t[i],
+ * dur[i]), 0 -> advance(t[i]); out[i][6] = level, phase (0 startup, 1 playing,
+ * 2 stalled), stall events, stall time, started_at (NaN until playback), last sync. */
+int otf_model_buffer_run(double t0, int32_t n, const int32_t *op, const double *t, const double *dur, double startup,
+                         double resume, double *out);
+
 /* DEVICE: completion_time for n (start, nbytes) queries over one trace (device
  * pointers), as the engines compute it (--fmad=false). */
 int otf_model_completion_times(const double *starts, const double *values, int32_t n_samples, double period,

@@ -106,7 +106,7 @@ class SizeTable(ctypes.Structure):
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
            "otf_scratch_bytes", "otf_shared_bytes", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
            "otf_gen_noise", "otf_gen_traces", "otf_gen_traces_multi", "otf_model_completion_time",
-           "otf_model_select_quality", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch")
+           "otf_model_select_quality", "otf_model_buffer_run", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch")
 DRAW_STANDARD_NORMAL, DRAW_NORMAL, DRAW_EXPONENTIAL, DRAW_STANDARD_EXPONENTIAL = 0, 1, 2, 3
 
 
@@ -161,6 +161,8 @@ def lib():
     L.otf_model_completion_time.argtypes = [_P(_f64), _P(_f64), _i32, _f64, _f64, _f64, _f64, _i64]
     L.otf_model_select_quality.restype = _i32
     L.otf_model_select_quality.argtypes = [_f64, _i32, _i32, _f64, _P(_i64), _i32, _f64, _f64, _f64]
+    L.otf_model_buffer_run.restype = ctypes.c_int
+    L.otf_model_buffer_run.argtypes = [_f64, _i32, _P(_i32), _P(_f64), _P(_f64), _f64, _f64, _P(_f64)]
     L.otf_model_completion_times.restype = ctypes.c_int
     L.otf_model_completion_times.argtypes = [_vp, _vp, _i32, _f64, _f64, _f64, _vp, _vp, _i32, _vp, _vp]
     L.otf_gen_sizes.restype = ctypes.c_int

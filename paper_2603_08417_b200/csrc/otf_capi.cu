@@ -68,6 +68,21 @@ int32_t otf_model_select_quality(double level, int32_t cur, int32_t has_est, dou
     return otf::select_quality(level, cur, has_est != 0, est, bitrates, top, panic, safe, headroom);
 }
 
+int otf_model_buffer_run(double t0, int32_t n, const int32_t *op, const double *t, const double *dur, double startup,
+                         double resume, double *out) {
+    if (n < 0 || (n > 0 && (!op || !t || !dur || !out))) return fail(OTF_EINVAL, "otf_model_buffer_run: bad arguments");
+    otf::Buffer b;
+    otf::buf_reset(b, t0);
+    for (int32_t i = 0; i < n; i++) {
+        if (op[i]) otf::buf_on_segment(b, t[i], dur[i], startup, resume);
+        else otf::buf_advance(b, t[i]);
+        double *o = out + 6 * (int64_t)i;
+        o[0] = b.level; o[1] = b.phase; o[2] = b.stall_events; o[3] = b.stall_time; o[4] = b.started_at;
+        o[5] = b.last_sync;
+    }
+    return OTF_OK;
+}
+
 int otf_model_completion_times(const double *starts, const double *values, int32_t n_samples, double period,
                                double pbits, double grid, const double *start, const int64_t *nbytes, int32_t n,
                                double *out, void *stream) {

@@ -8,7 +8,9 @@ Writes tests/golden/model_kat.json:
   plus 400 random looping traces of 1-12 pieces, starts and sizes;
 * select_quality: select_quality(level, cur, est, ladder, ClientConfig())
   (client.py:134-146) on the reference test ladder's band edges plus 400
-  random points.
+  random points;
+* PlayerBuffer.advance / on_segment (client.py:91-121): 200 random sequences
+  with the state after every step.
 The engine's restatement (csrc/otf_model.cuh) must reproduce every value
 bit-for-bit (tests/test_model_kat.py on the host build, -m gpu on the device).
 """
@@ -23,7 +25,7 @@ import sys
 
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from otfstream.client import ClientConfig, select_quality  # noqa: E402
+from otfstream.client import BufferConfig, ClientConfig, PlayerBuffer, select_quality  # noqa: E402
 from otfstream.netem import BandwidthTrace  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -76,8 +78,30 @@ def main():
     for level, cur, est in points:
         sq.append([level, cur, est, select_quality(level, cur, est, dict(LADDER), cfg)])
 
+    # PlayerBuffer (client.py:74-121): random advance / on_segment sequences
+    phases = {"startup": 0, "playing": 1, "stalled": 2, "finished": 3}
+    bufs = []
+    bc = BufferConfig()
+    for _ in range(200):
+        t = rnd.uniform(0, 100)
+        b = PlayerBuffer(bc, t)
+        seq = {"t0": t, "ops": []}
+        for _ in range(rnd.randint(1, 40)):
+            t += rnd.choice([0.0, rnd.uniform(0, 0.5), rnd.uniform(0, 3), rnd.uniform(0, 12)])
+            if rnd.random() < 0.5:
+                dur = rnd.choice([1.0, 2.0, rnd.uniform(0.1, 4.0)])
+                b.on_segment(t, dur)
+                op = [1, t, dur]
+            else:
+                b.advance(t)
+                op = [0, t, 0.0]
+            seq["ops"].append(op + [b.level, phases[b.phase], b.stall_events, b.stall_time,
+                                    b.started_at if b.started_at is not None else float("nan"), b.last_sync])
+        bufs.append(seq)
+
     out = {"ladder": [b for _, b in LADDER],
            "client": {"panic": cfg.buffer.panic_s, "safe": cfg.buffer.safe_s, "headroom": cfg.headroom},
+           "buffer": {"startup": bc.startup_s, "resume": bc.resume_s, "sequences": bufs},
            "completion_time": ct, "select_quality": sq}
     with open(os.path.join(HERE, "model_kat.json"), "w") as fh:
         json.dump(out, fh, allow_nan=True)

@@ -3,8 +3,9 @@
 tests/golden/model_kat.json holds answers of the UNMODIFIED reference
 (tests/golden/make_model_kat.py): BandwidthTrace.completion_time
 (netem.py:77-118), including the reference's own netem test cases
-(tests/test_netem.py:28-86), and select_quality (client.py:134-146), including
-its band-edge tests (tests/test_client.py:138-171).  The host build of the
+(tests/test_netem.py:28-86), select_quality (client.py:134-146), including
+its band-edge tests (tests/test_client.py:138-171), and PlayerBuffer
+(client.py:74-121) step sequences.  The host build of the
 same source must match them bit-for-bit (CPU tests).  The device build must
 match the host build bit-for-bit (-m gpu).
 """
@@ -72,6 +73,26 @@ def test_select_quality_matches_reference():
                                          ladder.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(ladder),
                                          c["panic"], c["safe"], c["headroom"])
         assert got == want, (level, cur, est, got, want)
+
+
+def test_player_buffer_matches_reference():
+    """PlayerBuffer.advance / on_segment (client.py:91-121): 200 random sequences, the
+    state after every step, bit-exact (stall counts are a discrete outcome)."""
+    L = _lib.lib()
+    B = KAT["buffer"]
+    for seq in B["sequences"]:
+        ops = np.asarray([int(o[0]) for o in seq["ops"]], dtype=np.int32)
+        t = np.asarray([o[1] for o in seq["ops"]], dtype=np.float64)
+        dur = np.asarray([o[2] for o in seq["ops"]], dtype=np.float64)
+        out = np.empty((len(ops), 6))
+        _lib.check(L.otf_model_buffer_run(seq["t0"], len(ops), ops.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                          t.ctypes.data_as(dp), dur.ctypes.data_as(dp), B["startup"], B["resume"],
+                                          out.ctypes.data_as(dp)), "otf_model_buffer_run")
+        for o, got in zip(seq["ops"], out):
+            want = o[3:]
+            assert got[0] == want[0] and int(got[1]) == want[1] and int(got[2]) == want[2], (seq["t0"], o, got)
+            assert got[3] == want[3] and got[5] == want[5], (o, got)
+            assert (math.isnan(got[4]) and math.isnan(want[4])) or got[4] == want[4], (o, got)
 
 
 @pytest.mark.gpu
