@@ -51,6 +51,9 @@ struct Scn {
     Pcg64 *picks;                             // [n_clients] sequence-pick streams (scratch)
     uint64_t mag_g, mag_rg;                   // d / max_nseg, d / (n_ranks * max_nseg) by multiply-high
     double inv_grid_step;                     // 1 / sc->grid_step (0 when the trace grid is irregular)
+    // the client model's constants in registers (read on every event; a shared-memory
+    // reload after each atomic would sit on the client's dependency chain)
+    double panic, safe, headroom, alpha, startup, resume;
     uint32_t div_g, div_rg;
     const int64_t *sizes, *bitrates, *manifest_b;
     const int32_t *segcounts;
@@ -83,6 +86,8 @@ struct Scn {
         mag_g = 0xffffffffffffffffull / div_g + 1ull;
         mag_rg = 0xffffffffffffffffull / div_rg + 1ull;
         inv_grid_step = sc->grid_step > 0 ? 1.0 / sc->grid_step : 0.0;
+        panic = sc->panic; safe = sc->safe; headroom = sc->headroom;
+        alpha = sc->alpha; startup = sc->startup; resume = sc->resume;
     }
     // floor(d / div) = umul64hi(d, floor((2^64-1)/div) + 1), exact for d, div < 2^31
     __device__ __forceinline__ uint32_t qdiv(uint32_t d, uint64_t mag, uint32_t) const {
@@ -341,7 +346,7 @@ __device__ __forceinline__ void client_start_playback(Client &c, double now) {
 __device__ __forceinline__ void client_select(Scn &S, Client &c) {
     if (c.index > 0)
         c.rank = select_quality(c.buf.level, c.rank, c.has_est != 0, c.est, S.bitrates, S.sc->n_ranks,
-                                S.sc->panic, S.sc->safe, S.sc->headroom);
+                                S.panic, S.safe, S.headroom);
 }
 
 // client.py:261-268; returns true when the session has more segments, else
@@ -350,9 +355,9 @@ __device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
     double dt = now - c.xfer_start;                       // SegmentFetch.rate_bps
     double rate = dt > 0 ? ((double)c.size * 8.0) / dt : INFINITY;
     if (!c.has_est) { c.est = rate; c.has_est = 1; }
-    else c.est = S.sc->alpha * rate + (1.0 - S.sc->alpha) * c.est;
+    else c.est = S.alpha * rate + (1.0 - S.alpha) * c.est;
     double duration = seg_duration(S.seqdur[c.seq], S.segdur[c.seq], c.index);
-    buf_on_segment(c.buf, now, duration, S.sc->startup, S.sc->resume);
+    buf_on_segment(c.buf, now, duration, S.startup, S.resume);
     int64_t g = atomicAdd((unsigned long long *)&S.st->n_seg, 1ull);
     if (S.records) {
         if (g < S.sc->seg_cap) {

@@ -185,6 +185,7 @@ struct Win {
     int32_t scap, lcap;
     JobEnt *jq, *sq;
     double W, invW, H, E, now;
+    double L, target;                                  // request latency, buffer target (registers)
     int32_t k;
     // lane 0's register copies of the hot server counters during phase A
     int64_t req_counter, n_req;
@@ -1111,9 +1112,9 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             c.pc = C_SESSION;
             continue;
         case C_SESSION:
-            if (!(now < sc.horizon)) { c.pc = C_DONE; return; }
+            if (!(now < w.H)) { c.pc = C_DONE; return; }
             client_new_session(S, c, cid, now);
-            delay = sc.latency;                        // manifest request latency (netem.py:138-139)
+            delay = w.L;                               // manifest request latency (netem.py:138-139)
             next = C_MAN_LAT;
             break;
         case C_MAN_LAT:
@@ -1128,8 +1129,8 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
         case C_INDEX_HEAD:
         case C_TARGET_WAIT:
             buf_advance(c.buf, now);
-            if (c.buf.phase == PH_PLAYING && c.buf.level >= sc.target) {
-                delay = c.buf.level - sc.target + 1e-9;
+            if (c.buf.phase == PH_PLAYING && c.buf.level >= w.target) {
+                delay = c.buf.level - w.target + 1e-9;
                 next = C_TARGET_WAIT;
                 break;
             }
@@ -1137,7 +1138,7 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             c.attempt = 0;                             // _fetch_with_retry (client.py:291-305)
             c.requested = now;
             c.desc = S.desc_id(c.seq, c.rank, c.index);
-            delay = sc.latency;                        // request latency, then MediaServer.segment
+            delay = w.L;                               // request latency, then MediaServer.segment
             next = C_SEG_LAT;
             break;
         case C_SEG_RESP:
@@ -1170,7 +1171,7 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
         case C_RETRY:                                  // after sleep(backoff): backoff *= 2
             c.attempt++;
             c.requested = now;
-            delay = sc.latency;
+            delay = w.L;
             next = C_SEG_LAT;
             break;
         default:
@@ -1368,6 +1369,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     w.W = sc.latency * (1.0 - 0x1p-20);
     w.invW = 1.0 / w.W;
     w.H = sc.horizon;
+    w.L = sc.latency;
+    w.target = sc.target;
     w.k = -1;
 
     // ---- init -------------------------------------------------------------------
