@@ -1104,7 +1104,6 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
     double now = c.next_when;
     for (;;) {
         double delay = 0.0;
-        int64_t nbytes = 0;
         int32_t next = C_DONE;
         bool xfer = false;
         switch (c.pc) {
@@ -1118,7 +1117,6 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             next = C_MAN_LAT;
             break;
         case C_MAN_LAT:
-            nbytes = S.manifest(c.seq);
             next = C_MAN_XFER;
             xfer = true;
             break;
@@ -1143,9 +1141,7 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             break;
         case C_SEG_RESP:
             record_response(w, c, now);
-            c.size = (int32_t)S.size(c.desc);
             c.xfer_start = now;
-            nbytes = c.size;
             next = C_SEG_XFER;
             xfer = true;
             break;
@@ -1177,7 +1173,14 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
         default:
             return;
         }
-        if (xfer) delay = completion_time(S.trace(cid), now, nbytes) - now;
+        if (xfer) {
+            // the trace samples, the period bits and the byte count load together
+            const Trace tr = S.trace(cid);
+            const TraceAhead a = trace_ahead(tr, trace_phase(tr, now));
+            const int64_t nbytes = next == C_SEG_XFER ? (int64_t)(int32_t)S.size(c.desc) : S.manifest(c.seq);
+            if (next == C_SEG_XFER) c.size = (int32_t)nbytes;
+            delay = completion_time_at(tr, a, now, nbytes) - now;
+        }
         if (!arm(w, c, cid, now, delay, next)) return;
         if (next == C_SEG_LAT) { S.flag(OTF_S_INTERNAL); return; }   // zero latency never reaches this engine
     }

@@ -61,14 +61,29 @@ OTF_HD double piece_start(const Trace &tr, int32_t i) {
     return tr.grid > 0 ? (double)i * tr.grid : tr.starts[i];
 }
 
-// BandwidthTrace._drain_from (netem.py:77-95)
-OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
-    int32_t i = trace_piece(tr, phase);
-    double spent = 0.0, pos = phase;
-    double v_next = i < tr.n ? tr.values[i] : 0.0;
+// The first two samples a drain from `phase` reads: a caller may issue these
+// loads before it knows the byte count (completion_time_at).
+struct TraceAhead {
+    double phase, v0, v1;
+    int32_t i;
+};
+
+OTF_HD TraceAhead trace_ahead(const Trace &tr, double phase) {
+    TraceAhead a;
+    a.phase = phase;
+    a.i = trace_piece(tr, phase);
+    a.v0 = a.i < tr.n ? tr.values[a.i] : 0.0;
+    a.v1 = a.i + 1 < tr.n ? tr.values[a.i + 1] : 0.0;
+    return a;
+}
+
+// BandwidthTrace._drain_from (netem.py:77-95) from piece a.i, whose sample and
+// the next one are already loaded; later samples load two pieces ahead.
+OTF_HD void drain_from_at(const Trace &tr, const TraceAhead &a, double bits, double &spent_out, double &left_out) {
+    int32_t i = a.i;
+    double spent = 0.0, pos = a.phase;
+    double v_here = a.v0, v_next = a.v1;
     for (; i < tr.n; i++) {
-        const double v_here = v_next;
-        if (i + 1 < tr.n) v_next = tr.values[i + 1];   // loaded one piece ahead (transfers span 1-2)
         double seg_end = (i + 1 < tr.n) ? piece_start(tr, i + 1) : tr.period;
         double width = seg_end - pos;
         if (width > 0) {
@@ -80,32 +95,42 @@ OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent
             spent += width;
             pos = seg_end;
         }
+        v_here = v_next;
+        if (i + 2 < tr.n) v_next = tr.values[i + 2];
     }
     spent_out = spent;
     left_out = bits;
 }
 
-// BandwidthTrace.completion_time for a looping trace (netem.py:97-118).  The
-// two _drain_from calls share one loop so the walk is emitted once.
-OTF_HD double completion_time(const Trace &tr, double start, int64_t nbytes) {
+OTF_HD void drain_from(const Trace &tr, double phase, double bits, double &spent_out, double &left_out) {
+    drain_from_at(tr, trace_ahead(tr, phase), bits, spent_out, left_out);
+}
+
+// fmod(start, period) == start for 0 <= start < period (exact)
+OTF_HD double trace_phase(const Trace &tr, double start) {
+    return (start >= 0.0 && start < tr.period) ? start : fmod(start, tr.period);
+}
+
+// BandwidthTrace.completion_time for a looping trace (netem.py:97-118), the
+// first drain starting from a = trace_ahead(tr, trace_phase(tr, start)).
+OTF_HD double completion_time_at(const Trace &tr, const TraceAhead &a, double start, int64_t nbytes) {
     double bits = (double)nbytes * 8.0;
     if (bits <= 0) return start;
     if (tr.pbits <= 0) return INFINITY;
     double t = start, spent, left;
-    // fmod(start, period) == start for 0 <= start < period (exact)
-    double phase = (start >= 0.0 && start < tr.period) ? start : fmod(start, tr.period);
-    for (int pass = 0; pass < 2; pass++) {
-        drain_from(tr, phase, bits, spent, left);
-        t += spent;
-        if (left <= 0 || pass == 1) return t;
-        double whole = floor(left / tr.pbits);
-        t += whole * tr.period;
-        left -= whole * tr.pbits;
-        if (left <= 0) return t;
-        bits = left;
-        phase = 0.0;
-    }
-    return t;
+    drain_from_at(tr, a, bits, spent, left);
+    t += spent;
+    if (left <= 0) return t;
+    double whole = floor(left / tr.pbits);
+    t += whole * tr.period;
+    left -= whole * tr.pbits;
+    if (left <= 0) return t;
+    drain_from(tr, 0.0, left, spent, left);
+    return t + spent;
+}
+
+OTF_HD double completion_time(const Trace &tr, double start, int64_t nbytes) {
+    return completion_time_at(tr, trace_ahead(tr, trace_phase(tr, start)), start, nbytes);
 }
 
 struct Buffer {
