@@ -1197,8 +1197,9 @@ __device__ __forceinline__ bool key_gt(double wa, int32_t ia, double wb, int32_t
     return wa > wb || (wa == wb && ia > ib);
 }
 
-// Order the window's server events by (time, client): rank sort for small
-// windows, in-place bitonic sort for large ones (ties are flagged afterwards).
+// Order the window's server events by time: rank sort for small windows, in-place
+// bitonic sort for large ones.  Equal times are flagged afterwards; order_ties
+// then orders each group by arm time, a result independent of the group's order.
 __device__ void sort_list(Win &w, int lane) {
     WinHeader *h = w.h;
     const int32_t n = h->n_list;
@@ -1206,7 +1207,7 @@ __device__ void sort_list(Win &w, int lane) {
     if (n <= 1) { __syncwarp(); return; }
     if (n <= RANK_SORT_MAX) {
         // each lane ranks elements lane and lane + 32 in one pass over the list (one
-        // pair of broadcast loads per j for both).  Non-negative doubles order like
+        // broadcast load per j for both).  Non-negative doubles order like
         // their bit patterns, so the compares run on the integer pipe.
         const int32_t i0 = lane, i1 = lane + 32;
         const bool v0 = i0 < n, v1 = i1 < n;
@@ -1217,11 +1218,10 @@ __device__ void sort_list(Win &w, int lane) {
         const unsigned long long *lwb = reinterpret_cast<const unsigned long long *>(w.lw);
         int32_t r0 = 0, r1 = 0;
 #pragma unroll 4
-        for (int32_t j = 0; j < n; j++) {              // branch-free (time, client) compare
-            const unsigned long long tj = lwb[j];
-            const int32_t idj = w.li[j];
-            r0 += (int32_t)((tj < t0) | ((tj == t0) & (idj < id0)));
-            r1 += (int32_t)((tj < t1) | ((tj == t1) & (idj < id1)));
+        for (int32_t j = 0; j < n; j++) {              // branch-free (time, list position) compare:
+            const unsigned long long tj = lwb[j];      //   equal times are flagged below and
+            r0 += (int32_t)((tj < t0) | ((tj == t0) & (j < i0)));   //   reordered by order_ties,
+            r1 += (int32_t)((tj < t1) | ((tj == t1) & (j < i1)));   //   whose result is order-free
         }
         const int16_t d0 = v0 ? w.ld[i0] : 0, d1 = v1 ? w.ld[i1] : 0;
         const int32_t s0 = v0 ? w.lp[i0] : 0, s1 = v1 ? w.lp[i1] : 0;
@@ -1572,12 +1572,16 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                     ctl = CTL_STOP;
                 } else {
                     const SrvEnt *as = w.bsrv + (int64_t)slot * w.scap;
-                    for (int32_t i = lane; i < ns; i += 32) {      // gather sort keys + request descriptors
-                        const SrvEnt e = as[i];
+                    for (int32_t i = lane; i < ns; i += 64) {      // gather sort keys + request descriptors
+                        const SrvEnt e = as[i];                    //   (both loads issue before the stores)
+                        const bool two = i + 32 < ns;
+                        SrvEnt f;
+                        if (two) f = as[i + 32];
                         w.li[i] = e.cid;
                         w.lw[i] = e.when;
                         w.ld[i] = e.desc;
                         w.lp[i] = e.pk;
+                        if (two) { w.li[i + 32] = f.cid; w.lw[i + 32] = f.when; w.ld[i + 32] = f.desc; w.lp[i + 32] = f.pk; }
                     }
 #ifndef WIN_NO_NEXT_PF
                     {                                      // warm L2 with the next window's request entries
