@@ -57,6 +57,10 @@ __device__ __forceinline__ bool df_inflight(uint16_t f) { return (f & 0x7FFF) !=
 constexpr int16_t NIL = -1;
 constexpr int WIN_MAX_WARPS = 2;   // warps per scenario: 1, or 2 for the big shared-memory classes
 constexpr int PAR_MAX = 256;       // windows up to this many requests may take the parallel server pass (uint8 indices)
+#ifndef WIN_SORT_UNROLL
+#define WIN_SORT_UNROLL 2
+#endif
+constexpr int SORT_UNROLL = WIN_SORT_UNROLL;   // rank-sort inner loop unroll (A/B switch)
 
 struct WWorker {
     double when, ctime;
@@ -1151,6 +1155,13 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             next = C_PLAYOUT;
             break;
         case C_PLAYOUT:
+#ifndef WIN_NO_PICK_PF
+            {                                          // the next session's pick stream (48 B):
+                const char *pk = reinterpret_cast<const char *>(S.picks + cid);   // in flight
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(pk));              // while the
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(pk + 47));         // session closes
+            }
+#endif
             client_finish_session(S, c, now);
             c.pc = C_SESSION;
             continue;
@@ -1217,7 +1228,7 @@ __device__ void sort_list(Win &w, int lane) {
         const unsigned long long t1 = (unsigned long long)__double_as_longlong(w1);
         const unsigned long long *lwb = reinterpret_cast<const unsigned long long *>(w.lw);
         int32_t r0 = 0, r1 = 0;
-#pragma unroll 4
+#pragma unroll SORT_UNROLL
         for (int32_t j = 0; j < n; j++) {              // branch-free (time, list position) compare:
             const unsigned long long tj = lwb[j];      //   equal times are flagged below and
             r0 += (int32_t)((tj < t0) | ((tj == t0) & (j < i0)));   //   reordered by order_ties,
