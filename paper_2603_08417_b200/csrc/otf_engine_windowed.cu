@@ -720,6 +720,7 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
         __syncwarp();
     }
     uint32_t hits = 0, miss = 0, sk0 = 0, sk1 = 0, sk3 = 0, sk4 = 0, spec = 0;
+    OTF_NOUNROLL
     for (uint32_t k = my_off; k < my_off + my_cnt; k++) {
         const int32_t i = h->par_list[k];
         const int32_t pk = w.lp[i];
@@ -854,6 +855,7 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
     }
     __syncwarp();
     // the latest touch stamp per descriptor: each lane over its own requests, in time order
+    OTF_NOUNROLL
     for (uint32_t k = my_off; k < my_off + my_cnt; k++) {
         const int32_t i = h->par_list[k];
         if (h->ev_flags[i] & EV_TOUCH) w.lstamp[w.ld[i]] = stamp_base + h->ev_touch[i] + 1u;

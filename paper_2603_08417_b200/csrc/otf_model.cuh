@@ -14,6 +14,14 @@
 
 #include "otfgpu.h"
 
+// Loops that run 1-2 times are kept rolled: the engine is sensitive to its hot
+// code size (instruction fetch is a third of its stall samples).
+#if defined(__CUDA_ARCH__) && !defined(OTF_UNROLL_OK)
+#define OTF_NOUNROLL _Pragma("unroll 1")
+#else
+#define OTF_NOUNROLL
+#endif
+
 #ifndef OTF_HD
 #define OTF_HD __host__ __device__ __forceinline__
 #endif
@@ -45,7 +53,9 @@ OTF_HD int32_t trace_piece(const Trace &tr, double phase) {
         double q = phase * tr.inv_grid;                // estimate; the two loops below make it exact
         int32_t i = q < (double)tr.n ? (int32_t)q : tr.n - 1;
         if (i < 0) i = 0;
+        OTF_NOUNROLL
         while (i + 1 < tr.n && (double)(i + 1) * tr.grid <= phase) i++;
+        OTF_NOUNROLL
         while (i > 0 && (double)i * tr.grid > phase) i--;
         return i;
     }
@@ -83,6 +93,7 @@ OTF_HD void drain_from_at(const Trace &tr, const TraceAhead &a, double bits, dou
     int32_t i = a.i;
     double spent = 0.0, pos = a.phase;
     double v_here = a.v0, v_next = a.v1;
+    OTF_NOUNROLL
     for (; i < tr.n; i++) {
         double seg_end = (i + 1 < tr.n) ? piece_start(tr, i + 1) : tr.period;
         double width = seg_end - pos;
@@ -111,6 +122,25 @@ OTF_HD double trace_phase(const Trace &tr, double start) {
     return (start >= 0.0 && start < tr.period) ? start : fmod(start, tr.period);
 }
 
+// The rest of a transfer that outlasts the trace's end (netem.py:109-118): whole
+// periods, then a drain from phase 0.  Rare, so kept out of line (scalar arguments).
+#ifdef __CUDA_ARCH__
+static __device__ __noinline__
+#else
+static inline
+#endif
+double completion_wrap(const double *starts, const double *values, int32_t n, double period, double pbits,
+                       double grid, double inv_grid, double t, double left) {
+    const Trace tr{starts, values, period, pbits, grid, inv_grid, n};
+    double whole = floor(left / tr.pbits);
+    t += whole * tr.period;
+    left -= whole * tr.pbits;
+    if (left <= 0) return t;
+    double spent;
+    drain_from(tr, 0.0, left, spent, left);
+    return t + spent;
+}
+
 // BandwidthTrace.completion_time for a looping trace (netem.py:97-118), the
 // first drain starting from a = trace_ahead(tr, trace_phase(tr, start)).
 OTF_HD double completion_time_at(const Trace &tr, const TraceAhead &a, double start, int64_t nbytes) {
@@ -121,12 +151,7 @@ OTF_HD double completion_time_at(const Trace &tr, const TraceAhead &a, double st
     drain_from_at(tr, a, bits, spent, left);
     t += spent;
     if (left <= 0) return t;
-    double whole = floor(left / tr.pbits);
-    t += whole * tr.period;
-    left -= whole * tr.pbits;
-    if (left <= 0) return t;
-    drain_from(tr, 0.0, left, spent, left);
-    return t + spent;
+    return completion_wrap(tr.starts, tr.values, tr.n, tr.period, tr.pbits, tr.grid, tr.inv_grid, t, left);
 }
 
 OTF_HD double completion_time(const Trace &tr, double start, int64_t nbytes) {
@@ -206,7 +231,9 @@ OTF_HD int lat_bin(double lat) {
     int k = e * 4 + (int)((bitsx >> 50) & 3);
     if (k < 0) k = 0;
     if (k > OTF_LAT_BINS - 2) k = OTF_LAT_BINS - 2;
+    OTF_NOUNROLL
     while (k + 1 <= OTF_LAT_BINS - 2 && lat >= lat_edge(k + 1)) k++;
+    OTF_NOUNROLL
     while (k > 0 && lat < lat_edge(k)) k--;
     return 1 + k;
 }
