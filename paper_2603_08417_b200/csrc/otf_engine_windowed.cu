@@ -60,7 +60,12 @@ constexpr int PAR_MAX = 256;       // windows up to this many requests may take 
 #ifndef WIN_SORT_UNROLL
 #define WIN_SORT_UNROLL 2
 #endif
-constexpr int SORT_UNROLL = WIN_SORT_UNROLL;   // rank-sort inner loop unroll (A/B switch)
+constexpr int SORT_UNROLL = WIN_SORT_UNROLL;
+#ifdef WIN_NO_PHASE_CYCLES                           // per-phase cycle counters (tools/probe.py)
+#define WCLOCK() 0LL
+#else
+#define WCLOCK() clock64()
+#endif   // rank-sort inner loop unroll (A/B switch)
 
 struct WWorker {
     double when, ctime;
@@ -1108,6 +1113,8 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
     Scn &S = w.S;
     const otf_scenario &sc = *S.sc;
     double now = c.next_when;
+    // a response (segment or OverloadError) is recorded first: one inlined copy
+    if (c.pc == C_SEG_RESP || c.pc == C_SEG_ERR) record_response(w, c, now);
     for (;;) {
         double delay = 0.0;
         int32_t next = C_DONE;
@@ -1146,7 +1153,6 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             next = C_SEG_LAT;
             break;
         case C_SEG_RESP:
-            record_response(w, c, now);
             c.xfer_start = now;
             next = C_SEG_XFER;
             xfer = true;
@@ -1168,7 +1174,6 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             c.pc = C_SESSION;
             continue;
         case C_SEG_ERR:                                // OverloadError response
-            record_response(w, c, now);
             if (c.attempt == sc.retries) {             // give up: the session is aborted
                 client_abort_session(S, c, now);
                 c.pc = C_SESSION;
@@ -1475,7 +1480,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     }
     for (;;) {
         if (warp == 0) {
-            t0 = clock64();
+            t0 = WCLOCK();
             // next window: wheel, far list, worker timers, next arrival
             int32_t m = wheel_next(h, h->k_done, lane);
             int32_t mw = lane < K ? h->wk[lane].win : WIN_NONE;
@@ -1623,11 +1628,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         h->cur_m = m;
                     }
                     __syncwarp();
-                    t1 = clock64();
+                    t1 = WCLOCK();
                     if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
                     t0 = t1;
                     sort_list(w, lane);
-                    t1 = clock64();
+                    t1 = WCLOCK();
                     if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
                 }
             }
@@ -1640,7 +1645,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         const int32_t m = h->cur_m;
         w.k = m;
         w.E = (double)(m + 1) * w.W;
-        t0 = clock64();
+        t0 = WCLOCK();
         // thread 0 = the server lane; with two warps, warp 1 runs the local timers meanwhile
         {
             // ---- phase A: the server events (the whole warp in request-only windows) ----
@@ -1661,7 +1666,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
             }
             if (tid == 0) {
                 h->k_done = m;
-                h->stats[OTF_ST_CYC_SERVER] += clock64() - t0;
+                h->stats[OTF_ST_CYC_SERVER] += WCLOCK() - t0;
                 if (par) h->stats[OTF_ST_PAR_WINDOWS]++;
             }
         }
@@ -1669,7 +1674,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
             // ---- phase B: the window's local timers, then the clients phase A responded
             // to, in ONE loop: a single inlined copy of the client state machine ----
             __syncwarp();
-            t0 = clock64();
+            t0 = WCLOCK();
             const int32_t nl = h->n_loc, nb = h->n_blist;
             const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
             // software-pipelined: the next event's client state is loaded (into registers)
@@ -1703,12 +1708,12 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
             __syncthreads();
             if (h->st.status & OTF_S_TIE) break;
             // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
-            t0 = clock64();
+            t0 = WCLOCK();
             const int32_t nb = h->n_blist;
             for (int32_t i = tid; i < nb; i += WIN_THREADS) client_local(w, w.blist[i]);
             __syncthreads();
         }
-        if (tid == 0) h->stats[OTF_ST_CYC_CLIENTS] += clock64() - t0;
+        if (tid == 0) h->stats[OTF_ST_CYC_CLIENTS] += WCLOCK() - t0;
     }
     if (tid == 0) {
         server_end(w);
