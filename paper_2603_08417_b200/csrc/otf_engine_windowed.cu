@@ -1256,10 +1256,12 @@ __device__ void sort_list(Win &w, int lane) {
     } else {
         int32_t p = 1;
         while (p < n) p <<= 1;
+        OTF_NOUNROLL
         for (int32_t i = n + lane; i < p; i += 32) { w.lw[i] = INFINITY; w.li[i] = 32767; }
         __syncwarp();
         for (int32_t size = 2; size <= p; size <<= 1) {
             for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                OTF_NOUNROLL
                 for (int32_t t = lane; t < (p >> 1); t += 32) {
                     int32_t lo = 2 * t - (t & (stride - 1));
                     int32_t hi = lo + stride;
@@ -1279,6 +1281,7 @@ __device__ void sort_list(Win &w, int lane) {
     }
     __syncwarp();
     bool tie = false;                                  // any equal request times? (rare)
+    OTF_NOUNROLL
     for (int32_t i = lane + 1; i < n; i += 32) tie |= w.lw[i] == w.lw[i - 1];
     bool any = __any_sync(0xffffffffu, tie);
     if (lane == 0) h->n_ties = any ? 1 : 0;
@@ -1590,6 +1593,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                     ctl = CTL_STOP;
                 } else {
                     const SrvEnt *as = w.bsrv + (int64_t)slot * w.scap;
+                    OTF_NOUNROLL
                     for (int32_t i = lane; i < ns; i += 64) {      // gather sort keys + request descriptors
                         const SrvEnt e = as[i];                    //   (both loads issue before the stores)
                         const bool two = i + 32 < ns;
@@ -1609,6 +1613,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                             asm volatile("prefetch.global.L2 [%0];" :: "l"(w.bsrv + (int64_t)sn * w.scap + 8 * lane));
                     }
 #endif
+                    OTF_NOUNROLL
                     for (int32_t i = ns + lane; i < nlist; i += 32) {   // overflowed pushes: from the client state
                         const int32_t c = w.li[i];
                         const Client &cl = w.cl[c];
