@@ -193,7 +193,7 @@ def main():
     # first pass: find scenarios the windowed engine hands to the exact engine (ties)
     db.launch(stream)
     br = db.fetch()
-    flagged = [i for i in range(len(my_cfgs)) if br.status[i] & (_lib.S_TIE | _lib.S_EPS_OVERFLOW)]
+    flagged = [i for i in range(len(my_cfgs)) if br.status[i] & (_lib.S_TIE | _lib.S_UNFIT | _lib.S_EPS_OVERFLOW)]
     exact_db = None
     if flagged:
         exact_inp = inputs.build_inputs([my_cfgs[i] for i in flagged], engine=_lib.ENGINE_EXACT,

@@ -47,6 +47,9 @@ typedef enum {
 #define OTF_S_TIE 0x8              /* windowed engine met an ordering tie it cannot resolve:
                                       the host re-runs the scenario on the exact engine */
 #define OTF_S_HUNG 0x10            /* a client slept forever (starved trace), informative */
+#define OTF_S_UNFIT 0x20           /* outside the windowed engine's limits (client / descriptor /
+                                      worker counts, segments per sequence, simultaneous requests):
+                                      the host re-runs the scenario on the exact engine */
 
 /* ---- enums shared with the host (values are part of the ABI) ---- */
 enum { OTF_PATH_STORAGE = 0, OTF_PATH_CACHE = 1, OTF_PATH_WAITED = 2, OTF_PATH_TRANSCODED = 3, OTF_PATH_ERROR = 4 };
@@ -179,6 +182,12 @@ size_t otf_sizeof_qoe(void);
 /* Engine scratch bytes for one scenario (host-side layout helper). */
 int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
                           int32_t n_ranks, int32_t max_nseg);
+
+/* 1 if the scenario (HOST pointer) is inside `engine`'s limits, else 0.  The
+ * windowed engine has fixed-width ids (see OTF_S_UNFIT); the exact engine
+ * takes every scenario.  Shared memory is checked separately against the
+ * device's opt-in limit (otf_shared_bytes). */
+int32_t otf_engine_fits(int32_t engine, const otf_scenario *sc);
 
 /* Per-scenario dynamic shared memory of the windowed engine (host-side helper). */
 int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,

@@ -28,7 +28,7 @@ OUTCOME_PENDING, OUTCOME_COMPLETED, OUTCOME_DROPPED = 0, 1, 2
 POP_UNIFORM, POP_ZIPF = 0, 1
 ENGINE_EXACT, ENGINE_WINDOWED = 0, 1
 MODE_HISTOGRAM, MODE_RECORDS = 0, 1
-S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG = 0x1, 0x2, 0x4, 0x8, 0x10
+S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG, S_UNFIT = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 SM_COUNT_B200, SMEM_PER_SM = 148, 227 * 1024
 
 ST_NSLOTS = 32
@@ -104,7 +104,7 @@ class SizeTable(ctypes.Structure):
 
 
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
-           "otf_scratch_bytes", "otf_shared_bytes", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
+           "otf_scratch_bytes", "otf_shared_bytes", "otf_engine_fits", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
            "otf_gen_noise", "otf_gen_traces", "otf_gen_traces_multi", "otf_model_completion_time",
            "otf_model_select_quality", "otf_model_buffer_run", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch")
 DRAW_STANDARD_NORMAL, DRAW_NORMAL, DRAW_EXPONENTIAL, DRAW_STANDARD_EXPONENTIAL = 0, 1, 2, 3
@@ -141,6 +141,8 @@ def lib():
         getattr(L, f).restype = ctypes.c_size_t
     L.otf_scratch_bytes.restype = _i64
     L.otf_scratch_bytes.argtypes = [_i32] * 6
+    L.otf_engine_fits.restype = _i32
+    L.otf_engine_fits.argtypes = [_i32, _P(Scenario)]
     L.otf_shared_bytes.restype = _i64
     L.otf_shared_bytes.argtypes = [_i32] * 6
     L.otf_build_traces.restype = ctypes.c_int

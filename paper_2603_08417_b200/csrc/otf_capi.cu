@@ -16,6 +16,7 @@ int otf_launch_exact(const otf_batch &b, cudaStream_t stream);
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream);
 int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc);
 int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc);
+bool otf_windowed_fits(const otf_scenario &sc);
 int otf_launch_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t *i64_pool,
                      const double *f64_pool, const int32_t *i32_pool, cudaStream_t stream);
 
@@ -105,6 +106,12 @@ int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, 
     int64_t n_desc = (int64_t)n_seq * n_ranks * max_nseg;
     if (engine == OTF_ENGINE_WINDOWED) return otf_windowed_scratch_bytes(n_clients, n_workers, n_desc);
     return otf::exact_layout(n_clients, n_workers, n_desc).total;
+}
+
+int32_t otf_engine_fits(int32_t engine, const otf_scenario *sc) {
+    if (!sc) return 0;
+    if (engine == OTF_ENGINE_WINDOWED) return otf_windowed_fits(*sc) ? 1 : 0;
+    return engine == OTF_ENGINE_EXACT ? 1 : 0;
 }
 
 int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,

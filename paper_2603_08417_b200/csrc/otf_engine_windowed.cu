@@ -177,6 +177,18 @@ __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_d
     return (o + 15) & ~(int64_t)15;
 }
 
+// The windowed engine's limits (anything outside them runs on the exact engine;
+// the host checks the same predicate up front, otf_windowed_fits):
+//   16-bit client ids and descriptor words, the server-event key packing
+//   rank | index << 8 | seq << 16 (index < 256), the shared catalog tables, the
+//   worker masks, and a positive request latency (the lookahead).
+__host__ __device__ inline bool win_fits(const otf_scenario &sc) {
+    const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
+    return sc.n_workers <= MAXK && sc.n_clients <= MAXN && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB &&
+           sc.max_nseg <= 256 && D < 32767 && sc.latency > 0 &&
+           sc.horizon / (sc.latency * (1.0 - 0x1p-20)) < 5.0e8;
+}
+
 struct Win {
     Scn S;
     WinHeader *h;
@@ -1398,8 +1410,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     w.k = -1;
 
     // ---- init -------------------------------------------------------------------
-    const bool fits = K <= MAXK && N <= MAXN && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB && D < 32767 &&
-                      sc.latency > 0 && sc.horizon / (sc.latency * (1.0 - 0x1p-20)) < 5.0e8;
+    const bool fits = win_fits(sc);
     if (tid == 0) {
         EngineState z = {};
         z.lru_head = z.lru_tail = -1;
@@ -1417,7 +1428,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
         h->list_cap = lcap;
         h->ctl = CTL_RUN; h->cur_m = 0;
-        if (!fits) h->st.status |= OTF_S_TIE;          // not for this engine: host re-runs it exactly
+        if (!fits) h->st.status |= OTF_S_UNFIT;        // not for this engine: host re-runs it exactly
     }
     __syncthreads();
     if (!fits) goto done;
@@ -1466,7 +1477,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         seed_picks(&w.S.picks[c], sc.seed, c);
     }
     __syncthreads();
-    if (h->st.status & OTF_S_TIE) goto done;
+    if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) goto done;
 
     // ---- window loop --------------------------------------------------------------
     t_start = clock64();
@@ -1478,7 +1489,12 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         if (sc.noise > 0)
             for (int64_t q = tid; q < (int64_t)K * sc.eps_stride; q += WIN_THREADS) emin = fmin(emin, w.S.eps[q]);
         for (int o = 16; o > 0; o >>= 1) emin = fmin(emin, __shfl_xor_sync(0xffffffffu, emin, o));
-        if (tid == 0) h->hand_safe = (w.svc_floor * (1.0 + emin) >= 2.0 * w.W) ? 1 : 0;
+        if (lane == 0) h->wsum[0][warp] = emin;          // every warp's partial minimum
+        __syncthreads();
+        if (tid == 0) {
+            for (int q = 1; q < WIN_WARPS; q++) emin = fmin(emin, h->wsum[0][q]);
+            h->hand_safe = (w.svc_floor * (1.0 + emin) >= 2.0 * w.W) ? 1 : 0;
+        }
         __syncthreads();
     }
     for (;;) {
@@ -1589,7 +1605,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                 }
                 const int32_t nlist = ns + n_ovf;
                 if (nlist > h->list_cap) {                 // too many simultaneous requests for this engine
-                    if (lane == 0) atomicOr(&h->st.status, OTF_S_TIE);
+                    if (lane == 0) atomicOr(&h->st.status, OTF_S_UNFIT);
                     ctl = CTL_STOP;
                 } else {
                     const SrvEnt *as = w.bsrv + (int64_t)slot * w.scap;
@@ -1699,7 +1715,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                 store_client_stream(&w.cl[cid], c);
             }
             __syncwarp();
-            if (h->st.status & OTF_S_TIE) break;
+            if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) break;
         } else {
             if (warp > 0) {
                 // ---- phase B1: the window's client-local timers, concurrent with phase A ----
@@ -1711,7 +1727,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                 if (b1 == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
             }
             __syncthreads();
-            if (h->st.status & OTF_S_TIE) break;
+            if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) break;
             // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
             t0 = WCLOCK();
             const int32_t nb = h->n_blist;
@@ -1726,7 +1742,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     }
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
-    if (!(h->st.status & OTF_S_TIE)) {
+    if (!(h->st.status & (OTF_S_TIE | OTF_S_UNFIT))) {
         for (int32_t c = tid; c < N; c += WIN_THREADS) client_harvest(w.S, w.cl[c], sc.horizon);
     }
     __syncthreads();
@@ -1770,6 +1786,8 @@ int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t
     (void)n_workers;
     return otf::win_global_layout(n_clients, n_desc).total;
 }
+
+bool otf_windowed_fits(const otf_scenario &sc) { return otf::win_fits(sc); }
 
 int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
     return otf::win_smem_bytes(n_clients, n_desc);

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
+import logging
 
 import numpy as np
 import torch
@@ -20,6 +21,7 @@ from .results import ExperimentResult
 
 __all__ = ["DeviceBatch", "BatchResult", "run_batch", "run_experiment", "require_cuda"]
 
+_log = logging.getLogger(__name__)
 _NP = {"i8": np.int64, "i4": np.int32, "f8": np.float64}
 _TORCH = {"i8": torch.int64, "i4": torch.int32, "f8": torch.float64}
 _REC_GROUP = {"req": 0, "sess": 1, "seg": 2, "job": 3}
@@ -220,7 +222,7 @@ class BatchResult:
         low = self.inp.lowered[i]
         return ExperimentResult(low.cfg, self.arrays(i) if self.rec else {}, self.stats[i], low.seq_ids,
                                 sizes=self.sizes(i), seq_dur=low.seq_dur, seq_segdur=low.seq_segdur,
-                                qoe=self.qoe[i], status=int(self.status[i]))
+                                qoe=self.qoe[i], status=int(self.status[i]), counts=self.counts[i])
 
     @property
     def total_requests(self) -> int:
@@ -235,6 +237,7 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
     with exact sizes; scenarios the windowed engine flags with an ordering tie
     are re-run on the exact engine.
     """
+    require_cuda(device)                               # no CPU path: fail before any host work
     m = _lib.MODE_RECORDS if mode == "records" else _lib.MODE_HISTOGRAM
     eng = _lib.ENGINE_WINDOWED if engine == "windowed" else _lib.ENGINE_EXACT
     configs = list(configs)
@@ -263,6 +266,15 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
     caps = {i: tuple(c) for i, c in enumerate(_caps)} if _caps is not None else {}   # test hook
     eps_scale = {i: _eps_scale for i in todo} if _eps_scale != 1.0 else {}         # test hook
     engines = {i: eng for i in todo}
+    if eng == _lib.ENGINE_WINDOWED:                    # outside the windowed engine's limits: exact, up front
+        from .inputs import windowed_fits
+        limit = torch.cuda.get_device_properties(require_cuda(device)).shared_memory_per_block_optin
+        for i in todo:
+            ok, why = windowed_fits(configs[i], limit)
+            if not ok:
+                engines[i] = _lib.ENGINE_EXACT
+                _log.warning("scenario %d runs on the exact engine (outside the windowed engine's limits: %s)",
+                             i, why)
     for _attempt in range(max_retries + 1):
         if not todo:
             break
@@ -285,7 +297,10 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                 if st & _lib.S_INTERNAL:
                     raise _lib.OtfError(f"scenario {i}: engine invariant violated (status {st:#x})")
                 retry = False
-                if st & _lib.S_TIE or (m == _lib.MODE_RECORDS and br.session_tie(k)):
+                if st & _lib.S_UNFIT:
+                    _log.warning("scenario %d: outside the windowed engine's limits at run time "
+                                 "(status %#x); re-running it on the exact engine", i, st)
+                if st & (_lib.S_TIE | _lib.S_UNFIT) or (m == _lib.MODE_RECORDS and br.session_tie(k)):
                     engines[i] = _lib.ENGINE_EXACT
                     retry = True
                 if st & _lib.S_EPS_OVERFLOW:

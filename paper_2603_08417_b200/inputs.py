@@ -213,6 +213,28 @@ class BatchInputs:
     pinned: bool = False        # pools allocated page-locked (torch pinned memory)
 
 
+def windowed_fits(cfg, smem_limit: int | None = None) -> tuple[bool, str]:
+    """Is this config inside the windowed engine's limits (otf_engine_fits) and, when
+    smem_limit is given, does its per-CTA shared memory fit the device?  Returns
+    (fits, reason); scenarios that do not fit run on the exact engine."""
+    L = _lib.lib()
+    low = lower(ExperimentConfig.from_reference(cfg))
+    c = low.cfg
+    sc = _lib.Scenario()
+    sc.n_clients, sc.n_workers, sc.n_seq, sc.n_ranks = c.clients, c.workers, len(low.seq_ids), low.n_ranks
+    sc.max_nseg = max(low.counts)
+    sc.latency, sc.horizon = float(c.client.latency_s), float(c.horizon_s)
+    if not L.otf_engine_fits(_lib.ENGINE_WINDOWED, ctypes.byref(sc)):
+        return False, (f"clients={sc.n_clients} workers={sc.n_workers} sequences={sc.n_seq} ranks={sc.n_ranks} "
+                       f"segments/sequence={sc.max_nseg} latency={sc.latency}")
+    if smem_limit is not None:
+        smem = int(L.otf_shared_bytes(_lib.ENGINE_WINDOWED, sc.n_clients, sc.n_workers, sc.n_seq, sc.n_ranks,
+                                      sc.max_nseg))
+        if smem > smem_limit:
+            return False, f"{smem} B of shared memory per scenario > {smem_limit} B"
+    return True, ""
+
+
 def _default_caps(low: Lowered) -> tuple[int, int, int, int]:
     cfg = low.cfg
     per_client = cfg.horizon_s / max(min(low.seq_segdur), 1e-3)

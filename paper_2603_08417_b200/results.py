@@ -215,12 +215,14 @@ class ExperimentResult:
     """orchestrator.py:271-324, backed by the engine's SoA arrays."""
 
     def __init__(self, config, arrays: dict, stats: np.ndarray, seq_ids: list[str], sizes=None,
-                 seq_dur=None, seq_segdur=None, qoe: dict | None = None, status: int = 0):
+                 seq_dur=None, seq_segdur=None, qoe: dict | None = None, status: int = 0, counts=None):
         self.config = config
         self.arrays = arrays
         self.stats_raw = stats
         self.seq_ids = seq_ids
         self._qoe = qoe                                # dict, or a raw otf_qoe row parsed on first use
+        self.qoe_row = None if isinstance(qoe, dict) or qoe is None else np.asarray(qoe)
+        self.counts = None if counts is None else np.asarray(counts)   # requests, sessions, segments, jobs
         self.status = status
         self._sizes = sizes
         self._seq_dur = seq_dur

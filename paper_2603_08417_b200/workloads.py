@@ -23,7 +23,7 @@ import math
 
 from .config import FIXTURE_LADDER, LADDER_10, ExperimentConfig, nominal_ladder_bytes
 
-__all__ = ["c1", "c2", "c3", "c4", "c5", "with_cache_fraction", "C4_CLIENTS", "C4_VARIANTS"]
+__all__ = ["c1", "c2", "c3", "c4", "c5", "c3_sweep", "c4_sweep", "c5_sweep", "with_cache_fraction", "C4_CLIENTS", "C4_VARIANTS"]
 
 C4_CLIENTS = (10, 30, 100, 300, 1000, 3000, 10000)
 C4_VARIANTS = ("B", "T", "TC", "TCP", "TCF", "TCPF")
@@ -73,6 +73,14 @@ def c5(seed: int = 1, variant: str = "TCPF", fraction: float = 0.20, clients: in
                 arrival_rate_per_s=clients / 60.0, popularity="zipf", zipf_exponent=0.8)
     base.update(kw)
     return with_cache_fraction(ExperimentConfig(**base), fraction)
+
+
+C3_FRACTIONS = tuple(k / 10 for k in range(11))
+
+
+def c3_sweep(seeds=range(1, 2)):
+    """Config 3: TCP with the cache swept 0..100% of the ladder in 10% steps, per seed."""
+    return [c3(seed=s, fraction=f) for s in seeds for f in C3_FRACTIONS]
 
 
 def c4_sweep(seeds=range(1, 65)):
