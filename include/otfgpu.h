@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define OTF_ABI_VERSION 1
+#define OTF_ABI_VERSION 2
 
 /* ---- status codes (ValueError / RuntimeError on the Python side) ---- */
 typedef enum {
@@ -50,6 +50,8 @@ typedef enum {
 #define OTF_S_UNFIT 0x20           /* outside the windowed engine's limits (client / descriptor /
                                       worker counts, segments per sequence, simultaneous requests):
                                       the host re-runs the scenario on the exact engine */
+#define OTF_S_TAIL_OVERFLOW 0x40   /* a summary tail buffer (nonzero latencies / stalled sessions) was
+                                      too small: otf_qoe.n_lat_tail / n_stall_tail are exact, re-run */
 
 /* ---- enums shared with the host (values are part of the ABI) ---- */
 enum { OTF_PATH_STORAGE = 0, OTF_PATH_CACHE = 1, OTF_PATH_WAITED = 2, OTF_PATH_TRANSCODED = 3, OTF_PATH_ERROR = 4 };
@@ -116,21 +118,54 @@ typedef struct otf_scenario {
     int64_t sess_off, sess_cap;
     int64_t seg_off, seg_cap;
     int64_t job_off, job_cap;
+    /* summary tails (both modes; cap 0 = none): the nonzero request latencies
+     * (otf_batch.tail_lat) and the sessions with a nonzero stall time
+     * (otf_batch.tail_stall, 2 * stl_cap entries: the second half is the sort
+     * buffer of the summary pass) */
+    int64_t lat_off, lat_cap;
+    int64_t stl_off, stl_cap;
 } otf_scenario;
 
-/* Fused QoE / fulfillment epilogue (metrics.py:67-116, orchestrator.py:280-309). */
+/* Fused QoE / fulfillment epilogue (metrics.py:67-116, orchestrator.py:280-309).
+ * Every field ExperimentResult.summary() reports is exact here, so a sweep
+ * needs no per-request records:
+ *   requests / sessions / jobs        n_requests, n_sessions, otf_batch.counts[3]
+ *   instant_fraction                  lat_hist[0] / n_requests  (lat_hist[0] counts latency < 0.010 exactly)
+ *   latency_p50_s / latency_p99_s     latency_p50 / latency_p99: sorted(latencies)[n // 2] and
+ *                                     [min(n - 1, int(0.99 * n))], selected on the device
+ *   stalls_mean                       n_stalls / n_sessions
+ *   stall_time_total_s                stall_time_sum: the reference's left-to-right sum in
+ *                                     session registration order (metrics.py:88-92)
+ *   quality_fractions / mean_rank     rank_count[r] / n_segments
+ * latency_sum and startup_delay_sum are correctly rounded exact sums (== math.fsum). */
 #define OTF_LAT_BINS 64      /* bin 0: latency < 10 ms (instant); then 4 bins per octave from 10 ms */
 #define OTF_STALL_BINS 32    /* sessions by stall count, last bin = ">= 31" */
-#define OTF_RANK_BINS 16     /* segments by representation rank */
+#define OTF_RANK_BINS 32     /* segments by representation rank (rank < 32) */
+/* otf_qoe.summary_flags */
+#define OTF_Q_ORDER_STATS 0x1  /* latency_p50 / latency_p99 / stall_time_sum were computed */
+#define OTF_Q_INEXACT_SUM 0x2  /* a value outside [2^-76, 2^64) reached an exact sum (sum approximate) */
+#define OTF_Q_RANKS_CAPPED 0x4 /* a rank >= OTF_RANK_BINS was counted in the last bin */
 typedef struct otf_qoe {
     int64_t lat_hist[OTF_LAT_BINS];
     int64_t path_count[8];            /* by OTF_PATH_* */
     int64_t stall_hist[OTF_STALL_BINS];
     int64_t rank_count[OTF_RANK_BINS];
     int64_t n_requests, n_sessions, n_segments, n_finished, n_started;
-    int64_t pad;
-    double latency_sum, stall_time_sum, startup_delay_sum, pad2;
+    int64_t n_stalls;                 /* stall events summed over sessions */
+    double latency_sum, stall_time_sum, startup_delay_sum;
+    double latency_p50, latency_p99;
+    int64_t n_lat_tail;               /* requests with a nonzero latency */
+    int64_t n_stall_tail;             /* sessions with a nonzero stall time */
+    int64_t summary_flags;            /* OTF_Q_* */
 } otf_qoe;
+
+/* One session with a nonzero stall time (summary tail): registration time and
+ * session id give the registration order the reference sums in. */
+typedef struct otf_stall_ent {
+    double reg_time;
+    double stall_time;
+    int64_t sid;
+} otf_stall_ent;
 
 typedef struct otf_batch {
     int32_t n_scenarios;
@@ -158,6 +193,8 @@ typedef struct otf_batch {
                                          (max of otf_shared_bytes over the batch) */
     int32_t engine_flags;             /* reserved, 0 */
     int32_t pad_flags;
+    double *tail_lat;                 /* summary tails at otf_scenario.lat_off / stl_off (may be NULL */
+    otf_stall_ent *tail_stall;        /*   when every cap is 0) */
 } otf_batch;
 
 /* A segment-size table: Catalog.descriptor sizes (content.py:204-218) for one
@@ -263,6 +300,11 @@ int32_t otf_model_select_quality(double level, int32_t cur, int32_t has_est, dou
 int otf_model_buffer_run(double t0, int32_t n, const int32_t *op, const double *t, const double *dur, double startup,
                          double resume, double *out);
 
+/* HOST: the engines' exact sum (csrc/otf_xacc.cuh) of n non-negative doubles:
+ * the correctly rounded sum (== math.fsum) or, with a value outside
+ * [2^-76, 2^64), returns 1 (*out is then the sum of the covered values). */
+int otf_model_exact_sum(const double *v, int64_t n, double *out);
+
 /* DEVICE: completion_time for n (start, nbytes) queries over one trace (device
  * pointers), as the engines compute it (--fmad=false). */
 int otf_model_completion_times(const double *starts, const double *values, int32_t n_samples, double period,
@@ -273,7 +315,9 @@ int otf_model_completion_times(const double *starts, const double *values, int32
 int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
                   int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream);
 
-/* DEVICE: run every scenario of the batch to its horizon (sim.py:347-360). */
+/* DEVICE: run every scenario of the batch to its horizon (sim.py:347-360), then
+ * the summary pass: order statistics of the latency tail and the
+ * registration-order stall sum into each scenario's otf_qoe. */
 int otf_run_batch(const otf_batch *batch, int32_t engine, void *stream);
 
 #ifdef __cplusplus

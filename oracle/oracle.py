@@ -360,3 +360,56 @@ def backend_stats(res: dict, cache_enabled: bool) -> dict:
         out["cache"] = {k: int(st[ST[k]]) for k in
                         ("capacity_bytes", "current_bytes", "entries", "hits", "misses", "evictions", "rejected")}
     return out
+
+
+# ---- the fused QoE block (include/otfgpu.h otf_qoe) restated from records -------------
+LAT_BINS, STALL_BINS, RANK_BINS = 64, 32, 32
+_LAT_EDGES = np.array([(0.01 * (1.0 + 0.25 * (k & 3))) * 2.0 ** (k >> 2) for k in range(LAT_BINS - 1)])
+
+
+def lat_bins(lat: np.ndarray) -> np.ndarray:
+    """Latency histogram bin: 0 = instant (< 10 ms, metrics.py:38,77), then 4 bins per
+    octave with lower edges 0.01 * (1 + q/4) * 2^o (csrc/otf_model.cuh lat_bin)."""
+    k = np.searchsorted(_LAT_EDGES, lat, side="right") - 1
+    return np.where(lat < 0.010, 0, 1 + np.clip(k, 0, LAT_BINS - 2))
+
+
+def qoe_block(res: dict) -> dict:
+    """Every otf_qoe field from one run's records (registration / response order):
+    the counters and histograms, the reference's summary statistics
+    (orchestrator.py:280-309, metrics.py:67-116: sorted latencies at n // 2 and
+    min(n - 1, int(0.99 n)), the left-to-right stall-time sum in registration
+    order) and the exact sums (math.fsum) of latencies and startup delays."""
+    lat = res["req_response"] - res["req_arrival"]
+    n = len(lat)
+    stalls = np.asarray(res["sess_stalls"], dtype=np.int64)
+    st = np.asarray(res["sess_stall_time"], dtype=np.float64)
+    su = np.asarray(res["sess_startup"], dtype=np.float64)
+    total = 0.0
+    for x in st[st != 0.0]:                            # registration order, plain double adds
+        total += float(x)
+    srt = np.sort(lat)
+    return {
+        "lat_hist": [int(x) for x in np.bincount(lat_bins(lat), minlength=LAT_BINS)],
+        "path_count": [int((res["req_path"] == p).sum()) for p in range(5)],
+        "stall_hist": [int(x) for x in np.bincount(np.minimum(stalls, STALL_BINS - 1), minlength=STALL_BINS)],
+        "rank_count": [int(x) for x in np.bincount(np.minimum(res["seg_rep"], RANK_BINS - 1), minlength=RANK_BINS)],
+        "n_requests": n, "n_sessions": len(stalls), "n_segments": len(res["seg_rep"]),
+        "n_finished": int((np.asarray(res["sess_flags"]) & 1).sum()), "n_started": int((~np.isnan(su)).sum()),
+        "n_stalls": int(stalls.sum()),
+        "latency_sum": math.fsum(lat.tolist()),
+        "stall_time_sum": total,
+        "startup_delay_sum": math.fsum(su[~np.isnan(su)].tolist()),
+        "latency_p50": float(srt[n // 2]) if n else 0.0,
+        "latency_p99": float(srt[min(n - 1, int(0.99 * n))]) if n else 0.0,
+        "n_lat_tail": int((lat != 0.0).sum()), "n_stall_tail": int((st != 0.0).sum()),
+    }
+
+
+def run_qoe(cfg) -> dict:
+    """oracle run -> its QoE block plus the backend stats row (pool-friendly: small result)."""
+    r = run(cfg)
+    q = qoe_block(r)
+    q["stats"] = [int(x) for x in r["stats"][:18]]
+    q["n_job"] = int(r["n_job"])
+    return q

@@ -15,7 +15,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_PATH = os.environ.get("OTFGPU_LIB_OVERRIDE") or os.path.join(HERE, "libotfgpu.so")   # override: tools/ experiments
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _P = ctypes.POINTER
 _vp = ctypes.c_void_p
@@ -28,7 +28,9 @@ OUTCOME_PENDING, OUTCOME_COMPLETED, OUTCOME_DROPPED = 0, 1, 2
 POP_UNIFORM, POP_ZIPF = 0, 1
 ENGINE_EXACT, ENGINE_WINDOWED = 0, 1
 MODE_HISTOGRAM, MODE_RECORDS = 0, 1
-S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG, S_UNFIT = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG, S_UNFIT, S_TAIL_OVERFLOW = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
+Q_ORDER_STATS, Q_INEXACT_SUM, Q_RANKS_CAPPED = 0x1, 0x2, 0x4
 SM_COUNT_B200, SMEM_PER_SM = 148, 227 * 1024
 
 ST_NSLOTS = 32
@@ -37,7 +39,7 @@ ST = dict(jobs_total=0, jobs_demand=1, jobs_speculative=2, wasted_avoided=3, spe
           evictions=16, rejected=17, status=18, hung=19, timer_pops=20, ready_callbacks=21, windows=22,
           cyc_scan=23, cyc_sort=24, cyc_server=25, cyc_clients=26, cyc_total=27)
 SKIP_REASONS = ("disabled", "end-of-sequence", "stored", "cached", "in-flight", "overload")
-LAT_BINS, STALL_BINS, RANK_BINS = 64, 32, 16
+LAT_BINS, STALL_BINS, RANK_BINS = 64, 32, 32
 
 
 class Scenario(ctypes.Structure):
@@ -56,6 +58,7 @@ class Scenario(ctypes.Structure):
         ("off_eps", _i64), ("eps_stride", _i64), ("scratch_off", _i64),
         ("req_off", _i64), ("req_cap", _i64), ("sess_off", _i64), ("sess_cap", _i64),
         ("seg_off", _i64), ("seg_cap", _i64), ("job_off", _i64), ("job_cap", _i64),
+        ("lat_off", _i64), ("lat_cap", _i64), ("stl_off", _i64), ("stl_cap", _i64),
     ]
 
 
@@ -64,9 +67,14 @@ class Qoe(ctypes.Structure):
         ("lat_hist", _i64 * LAT_BINS), ("path_count", _i64 * 8), ("stall_hist", _i64 * STALL_BINS),
         ("rank_count", _i64 * RANK_BINS),
         ("n_requests", _i64), ("n_sessions", _i64), ("n_segments", _i64), ("n_finished", _i64),
-        ("n_started", _i64), ("pad", _i64),
-        ("latency_sum", _f64), ("stall_time_sum", _f64), ("startup_delay_sum", _f64), ("pad2", _f64),
+        ("n_started", _i64), ("n_stalls", _i64),
+        ("latency_sum", _f64), ("stall_time_sum", _f64), ("startup_delay_sum", _f64),
+        ("latency_p50", _f64), ("latency_p99", _f64),
+        ("n_lat_tail", _i64), ("n_stall_tail", _i64), ("summary_flags", _i64),
     ]
+
+
+STALL_ENT_BYTES = 24   # otf_stall_ent: reg_time f64, stall_time f64, sid i64
 
 
 RECORD_FIELDS = [  # (name, numpy dtype) in otf_batch order
@@ -85,7 +93,8 @@ class Batch(ctypes.Structure):
                  ("i64_pool", _vp), ("i32_pool", _vp), ("scratch", _vp)]
                 + [(n, _vp) for n, _ in RECORD_FIELDS]
                 + [("counts", _vp), ("stats", _vp), ("qoe", _vp), ("status", _vp), ("order", _vp),
-                   ("shared_bytes", _i64), ("engine_flags", _i32), ("pad_flags", _i32)])
+                   ("shared_bytes", _i64), ("engine_flags", _i32), ("pad_flags", _i32),
+                   ("tail_lat", _vp), ("tail_stall", _vp)])
 
 
 class TraceJob(ctypes.Structure):
@@ -106,7 +115,7 @@ class SizeTable(ctypes.Structure):
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
            "otf_scratch_bytes", "otf_shared_bytes", "otf_engine_fits", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
            "otf_gen_noise", "otf_gen_traces", "otf_gen_traces_multi", "otf_model_completion_time",
-           "otf_model_select_quality", "otf_model_buffer_run", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch")
+           "otf_model_select_quality", "otf_model_buffer_run", "otf_model_exact_sum", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch")
 DRAW_STANDARD_NORMAL, DRAW_NORMAL, DRAW_EXPONENTIAL, DRAW_STANDARD_EXPONENTIAL = 0, 1, 2, 3
 
 
@@ -165,6 +174,8 @@ def lib():
     L.otf_model_select_quality.argtypes = [_f64, _i32, _i32, _f64, _P(_i64), _i32, _f64, _f64, _f64]
     L.otf_model_buffer_run.restype = ctypes.c_int
     L.otf_model_buffer_run.argtypes = [_f64, _i32, _P(_i32), _P(_f64), _P(_f64), _f64, _f64, _P(_f64)]
+    L.otf_model_exact_sum.restype = ctypes.c_int
+    L.otf_model_exact_sum.argtypes = [_P(_f64), _i64, _P(_f64)]
     L.otf_model_completion_times.restype = ctypes.c_int
     L.otf_model_completion_times.argtypes = [_vp, _vp, _i32, _f64, _f64, _f64, _vp, _vp, _i32, _vp, _vp]
     L.otf_gen_sizes.restype = ctypes.c_int

@@ -14,6 +14,7 @@
 
 int otf_launch_exact(const otf_batch &b, cudaStream_t stream);
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream);
+int otf_launch_summary(const otf_batch &b, int32_t engine, cudaStream_t stream);
 int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc);
 int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc);
 bool otf_windowed_fits(const otf_scenario &sc);
@@ -84,6 +85,20 @@ int otf_model_buffer_run(double t0, int32_t n, const int32_t *op, const double *
     return OTF_OK;
 }
 
+int otf_model_exact_sum(const double *v, int64_t n, double *out) {
+    if (!out || (n > 0 && !v)) return fail(OTF_EINVAL, "otf_model_exact_sum: bad arguments");
+    unsigned long long limb[otf::XACC_LIMBS] = {};
+    int inexact = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int q;
+        uint32_t c0, c1, c2;
+        if (!otf::xacc_split(v[i], q, c0, c1, c2)) { inexact = 1; continue; }
+        limb[q] += c0; limb[q + 1] += c1; limb[q + 2] += c2;
+    }
+    *out = otf::xacc_round(limb);
+    return inexact;
+}
+
 int otf_model_completion_times(const double *starts, const double *values, int32_t n_samples, double period,
                                double pbits, double grid, const double *start, const int64_t *nbytes, int32_t n,
                                double *out, void *stream) {
@@ -147,7 +162,10 @@ int otf_run_batch(const otf_batch *batch, int32_t engine, void *stream) {
         if (otf_launch_windowed(b, s) != 0) return fail(OTF_ECUDA, "otf_run_batch: shared memory request too large");
     }
     else return fail(OTF_EINVAL, "otf_run_batch: unknown engine");
-    return check_cuda("otf_run_batch");
+    int rc = check_cuda("otf_run_batch");
+    if (rc != OTF_OK) return rc;
+    if (otf_launch_summary(b, engine, s) != 0) return fail(OTF_ECUDA, "otf_run_batch: summary pass");
+    return check_cuda("otf_run_batch (summary pass)");
 }
 
 }  // extern "C"

@@ -24,16 +24,6 @@ struct EngineState {                 // first 256 B of every scenario arena
     int32_t pad;
 };
 
-// QoE accumulators: 32-bit counters (native shared/global atomics); the float
-// sums are accumulated per lane (Scn members) and reduced at the end.
-struct QoeAcc {
-    uint32_t lat_hist[OTF_LAT_BINS];
-    uint32_t path_count[8];
-    uint32_t stall_hist[OTF_STALL_BINS];
-    uint32_t rank_count[OTF_RANK_BINS];
-    uint32_t n_requests, n_sessions, n_segments, n_finished, n_started, pad[3];
-};
-
 __device__ __forceinline__ void qoe_zero(QoeAcc *a, int lane, int nlanes) {
     uint32_t *p = (uint32_t *)a;
     for (int i = lane; i < (int)(sizeof(QoeAcc) / 4); i += nlanes) p[i] = 0;
@@ -47,8 +37,9 @@ struct Scn {
     int64_t *stats;
     otf_qoe *q;                      // final destination (global)
     QoeAcc *qa;                      // counters while running (shared or scratch)
-    double lat_sum, stall_sum, startup_sum;   // this lane's float sums
-    Pcg64 *picks;                             // [n_clients] sequence-pick streams (scratch)
+    ClientCold *cold;                         // [n_clients] pick streams + registration times (scratch)
+    double *tail_lat;                         // summary tails (NULL when the caps are 0)
+    otf_stall_ent *tail_stall;
     uint64_t mag_g, mag_rg;                   // d / max_nseg, d / (n_ranks * max_nseg) by multiply-high
     double inv_grid_step;                     // 1 / sc->grid_step (0 when the trace grid is irregular)
     // the client model's constants in registers (read on every event; a shared-memory
@@ -80,6 +71,8 @@ struct Scn {
         pbits = b->f64_pool + sc->off_pbits;
         arrivals = b->f64_pool + sc->off_arrivals;
         eps = b->f64_pool + sc->off_eps;
+        tail_lat = (b->tail_lat && sc->lat_cap > 0) ? b->tail_lat + sc->lat_off : nullptr;
+        tail_stall = (b->tail_stall && sc->stl_cap > 0) ? b->tail_stall + sc->stl_off : nullptr;
         records = b->mode == OTF_MODE_RECORDS;
         div_g = (uint32_t)sc->max_nseg;
         div_rg = (uint32_t)(sc->n_ranks * sc->max_nseg);
@@ -101,19 +94,29 @@ struct Scn {
         *st = z;
         for (int i = 0; i < OTF_ST_NSLOTS; i++) stats[i] = 0;
         qoe_zero(qa, 0, 1);
-        lat_sum = stall_sum = startup_sum = 0.0;
     }
 
-    // write the final otf_qoe (sums already reduced into this lane's members)
+    // write the final otf_qoe; the summary pass (otf_summary.cu) adds the
+    // latency sum, the order statistics and the registration-order stall sum
     __device__ void flush_qoe() const {
         for (int i = 0; i < OTF_LAT_BINS; i++) q->lat_hist[i] = qa->lat_hist[i];
         for (int i = 0; i < 8; i++) q->path_count[i] = qa->path_count[i];
         for (int i = 0; i < OTF_STALL_BINS; i++) q->stall_hist[i] = qa->stall_hist[i];
         for (int i = 0; i < OTF_RANK_BINS; i++) q->rank_count[i] = qa->rank_count[i];
         q->n_requests = qa->n_requests; q->n_sessions = qa->n_sessions; q->n_segments = qa->n_segments;
-        q->n_finished = qa->n_finished; q->n_started = qa->n_started; q->pad = 0;
-        q->latency_sum = lat_sum; q->stall_time_sum = stall_sum; q->startup_delay_sum = startup_sum;
-        q->pad2 = 0.0;
+        q->n_finished = qa->n_finished; q->n_started = qa->n_started; q->n_stalls = qa->n_stalls;
+        q->latency_sum = 0.0; q->stall_time_sum = 0.0;
+        q->startup_delay_sum = xacc_round(qa->sup);
+        q->latency_p50 = 0.0; q->latency_p99 = 0.0;
+        q->n_lat_tail = qa->n_lat_tail; q->n_stall_tail = qa->n_stl_tail;
+        q->summary_flags = qa->flags;
+    }
+
+    // a nonzero request latency: kept for the order statistics and the exact sum
+    __device__ __forceinline__ void tail_latency(double lat) {
+        const uint32_t pos = atomicAdd(&qa->n_lat_tail, 1u);
+        if (pos < (uint64_t)sc->lat_cap) tail_lat[pos] = lat;
+        else flag(OTF_S_TAIL_OVERFLOW);
     }
 
     __device__ __forceinline__ int64_t &stat(int i) { return stats[i]; }
@@ -228,7 +231,7 @@ struct Scn {
         qa->lat_hist[lat_bin(lat)]++;
         qa->path_count[c.path]++;
         qa->n_requests++;
-        lat_sum += lat;
+        if (lat != 0.0) tail_latency(lat);
     }
 
     __device__ void sync_session(const Client &c, double now) {      // _sync_report (client.py:284-288)
@@ -240,16 +243,29 @@ struct Scn {
         b->sess_startup[o] = isnan(c.buf.started_at) ? NAN : c.buf.started_at - c.buf.session_start;
     }
 
-    // session QoE, once per session when its numbers are final
-    __device__ void qoe_session(const Client &c, bool finished) {
+    // session QoE, once per session when its numbers are final (the report as
+    // _sync_report left it, client.py:284-288)
+    __device__ void qoe_session(const Client &c, int32_t cid, bool finished) {
         int32_t stalls = c.buf_live ? c.buf.stall_events : 0;
         atomicAdd(&qa->n_sessions, 1u);
         atomicAdd(&qa->stall_hist[stalls < OTF_STALL_BINS - 1 ? stalls : OTF_STALL_BINS - 1], 1u);
         if (c.buf_live) {
-            stall_sum += c.buf.stall_time;
+            if (stalls) atomicAdd(&qa->n_stalls, (uint32_t)stalls);
+            if (c.buf.stall_time != 0.0) {             // summed in registration order by the summary pass
+                const uint32_t pos = atomicAdd(&qa->n_stl_tail, 1u);
+                if (pos < (uint64_t)sc->stl_cap) {
+                    otf_stall_ent e;
+                    e.reg_time = cold[cid].reg_time;
+                    e.stall_time = c.buf.stall_time;
+                    e.sid = c.session;
+                    tail_stall[pos] = e;
+                } else {
+                    flag(OTF_S_TAIL_OVERFLOW);
+                }
+            }
             if (!isnan(c.buf.started_at)) {
                 atomicAdd(&qa->n_started, 1u);
-                startup_sum += c.buf.started_at - c.buf.session_start;
+                xacc_add(qa->sup, c.buf.started_at - c.buf.session_start, &qa->flags);
             }
         }
         if (finished) atomicAdd(&qa->n_finished, 1u);
@@ -304,12 +320,13 @@ static __device__ __noinline__ int32_t draw_sequence(Pcg64 *g, int32_t n_seq, in
 }
 
 __device__ __forceinline__ void client_arrive(Scn &S, Client &c, int32_t cid) {
-    seed_picks(&S.picks[cid], S.sc->seed, cid);
+    seed_picks(&S.cold[cid].picks, S.sc->seed, cid);
 }
 
 // orchestrator.py:341-345 + client.py:237-239: pick a sequence, register a report
 __device__ inline void client_new_session(Scn &S, Client &c, int32_t cid, double now) {
-    int32_t seq = draw_sequence(&S.picks[cid], S.sc->n_seq, S.sc->popularity, S.zipf);
+    int32_t seq = draw_sequence(&S.cold[cid].picks, S.sc->n_seq, S.sc->popularity, S.zipf);
+    S.cold[cid].reg_time = now;                        // registration order (client.py:237-239)
     c.seq = seq;
     int64_t sid = atomicAdd((unsigned long long *)&S.st->n_sess, 1ull);
     c.session = (int32_t)sid;
@@ -371,6 +388,7 @@ __device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
             S.flag(OTF_S_RECORD_OVERFLOW);
         }
     }
+    if (c.rank >= OTF_RANK_BINS) atomicOr(&S.qa->flags, (uint32_t)OTF_Q_RANKS_CAPPED);
     atomicAdd(&S.qa->rank_count[c.rank < OTF_RANK_BINS ? c.rank : OTF_RANK_BINS - 1], 1u);
     atomicAdd(&S.qa->n_segments, 1u);
     S.sync_session(c, now);
@@ -381,35 +399,35 @@ __device__ inline bool client_segment_done(Scn &S, Client &c, double now) {
 }
 
 // client.py:272-280 (+ the finally clause)
-__device__ inline void client_finish_session(Scn &S, Client &c, double now) {
+__device__ inline void client_finish_session(Scn &S, Client &c, int32_t cid, double now) {
     buf_advance(c.buf, now);
     c.buf.phase = PH_FINISHED;
     if (S.records && c.session < S.sc->sess_cap) S.b->sess_flags[S.sc->sess_off + c.session] |= 1;
     S.sync_session(c, now);
-    S.qoe_session(c, true);
+    S.qoe_session(c, cid, true);
     c.buf_live = 0;
     c.sess_open = 0;
 }
 
 // Session given up after the last retry (client.py:257-260 + the finally
 // clause): flagged aborted, synced without advancing the buffer.
-__device__ inline void client_abort_session(Scn &S, Client &c, double now) {
+__device__ inline void client_abort_session(Scn &S, Client &c, int32_t cid, double now) {
     if (S.records && c.session < S.sc->sess_cap) S.b->sess_flags[S.sc->sess_off + c.session] |= 2;
     S.sync_session(c, now);
-    S.qoe_session(c, false);
+    S.qoe_session(c, cid, false);
     c.buf_live = 0;
     c.sess_open = 0;
 }
 
 // SessionReport.harvest at the horizon (orchestrator.py:357-359, client.py:177-187)
-__device__ inline void client_harvest(Scn &S, Client &c, double horizon) {
+__device__ inline void client_harvest(Scn &S, Client &c, int32_t cid, double horizon) {
     if (c.pc == C_HUNG) S.flag(OTF_S_HUNG);
     if (!c.sess_open) return;
     if (c.buf_live) {
         buf_advance(c.buf, horizon);
         S.sync_session(c, horizon);
     }
-    S.qoe_session(c, false);
+    S.qoe_session(c, cid, false);
 }
 
 }  // namespace otf

@@ -281,7 +281,7 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
                 w.S.record_request(c, w.now);
                 c.size = sz;
                 if (c.attempt == sc.retries) {
-                    client_abort_session(w.S, c, w.now);
+                    client_abort_session(w.S, c, cid, w.now);
                     c.pc = C_SESSION;
                     break;
                 }
@@ -320,7 +320,7 @@ __device__ void client_step(ExactWorld &w, int32_t cid) {
             if (sc.latency > 0 && do_sleep(w, c, task, sc.latency)) return;
             break;
         case C_PLAYOUT:                     // client.py:272-280
-            client_finish_session(w.S, c, w.now);
+            client_finish_session(w.S, c, cid, w.now);
             c.pc = C_SESSION;
             break;
         default:
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
     ExactLayout L = exact_layout(sc.n_clients, sc.n_workers, n_desc);
     uint8_t *base = b.scratch + sc.scratch_off;
     w.cl = (Client *)(base + L.clients);
-    w.S.picks = (Pcg64 *)(base + L.picks);
+    w.S.cold = (ClientCold *)(base + L.picks);
     w.wk = (Worker *)(base + L.workers);
     w.heap = (Timer *)(base + L.heap);
     w.ready = (ReadyEnt *)(base + L.ready);
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(64) exact_kernel(const otf_batch b) {
     if (sc.horizon > w.now) w.now = sc.horizon;
 
     // harvest at the horizon (orchestrator.py:357-359, client.py:177-187)
-    for (int32_t c = 0; c < sc.n_clients; c++) client_harvest(w.S, w.cl[c], w.now);
+    for (int32_t c = 0; c < sc.n_clients; c++) client_harvest(w.S, w.cl[c], c, w.now);
     w.S.finish();
     w.S.flush_qoe();
 }

@@ -113,7 +113,7 @@ struct WinHeader {
     uint8_t par_list[PAR_MAX];           //   the list partitioned by owner lane (time order kept)
     uint32_t par_cnt[32];                //   per owner lane: count, then next slot
     int32_t hand_safe;                   // no transcode can end within the window it starts in
-    double wsum[WIN_MAX_WARPS][3];       // per-warp float sums (fixed-order final reduction)
+    double wmin[WIN_MAX_WARPS];          // per-warp partial minima (hand_safe)
 };
 
 // Server events one window can hold: the list lives in the dynamic shared region.
@@ -156,7 +156,7 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     WinGlobalLayout L;
     int64_t o = 0;
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
-    L.picks = o;   o += align256((int64_t)sizeof(Pcg64) * n_clients);
+    L.picks = o;   o += align256((int64_t)sizeof(ClientCold) * n_clients);
     L.blist = o;   o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.specq = o;   o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
@@ -1115,7 +1115,7 @@ __device__ __forceinline__ void record_response(Win &w, const Client &c, double 
     atomicAdd(&q.lat_hist[lat_bin(lat)], 1u);
     atomicAdd(&q.path_count[c.path], 1u);
     atomicAdd(&q.n_requests, 1u);
-    S.lat_sum += lat;
+    if (lat != 0.0) S.tail_latency(lat);
 }
 
 // The client coroutine between two yields.  Every state computes either
@@ -1177,17 +1177,17 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
         case C_PLAYOUT:
 #ifndef WIN_NO_PICK_PF
             {                                          // the next session's pick stream (48 B):
-                const char *pk = reinterpret_cast<const char *>(S.picks + cid);   // in flight
+                const char *pk = reinterpret_cast<const char *>(S.cold + cid);    // in flight
                 asm volatile("prefetch.global.L1 [%0];" :: "l"(pk));              // while the
                 asm volatile("prefetch.global.L1 [%0];" :: "l"(pk + 47));         // session closes
             }
 #endif
-            client_finish_session(S, c, now);
+            client_finish_session(S, c, cid, now);
             c.pc = C_SESSION;
             continue;
         case C_SEG_ERR:                                // OverloadError response
             if (c.attempt == sc.retries) {             // give up: the session is aborted
-                client_abort_session(S, c, now);
+                client_abort_session(S, c, cid, now);
                 c.pc = C_SESSION;
                 continue;
             }
@@ -1389,7 +1389,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     w.lstamp = (uint32_t *)(g + L.lstamp);
     w.lq = (LqEnt *)(g + L.lq);
     w.cl = (Client *)(g + L.clients);
-    w.S.picks = (Pcg64 *)(g + L.picks);
+    w.S.cold = (ClientCold *)(g + L.picks);
     w.blist = (int32_t *)(g + L.blist);
     w.bsrv = (SrvEnt *)(g + L.bsrv);
     w.bloc = (int32_t *)(g + L.bloc);
@@ -1401,7 +1401,6 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     w.S.st = &h->st;
     w.S.stats = h->stats;
     w.S.qa = &h->qa;
-    w.S.lat_sum = w.S.stall_sum = w.S.startup_sum = 0.0;
     w.W = sc.latency * (1.0 - 0x1p-20);
     w.invW = 1.0 / w.W;
     w.H = sc.horizon;
@@ -1474,7 +1473,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         if (!(off > 0)) w.S.flag(OTF_S_TIE);           // instant start: tick order among clients matters
         // the client's pick stream (orchestrator.py:338-340), seeded here in parallel rather
         // than by one lane at the arrival: it is first drawn from after the arrival
-        seed_picks(&w.S.picks[c], sc.seed, c);
+        seed_picks(&w.S.cold[c].picks, sc.seed, c);
     }
     __syncthreads();
     if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) goto done;
@@ -1489,10 +1488,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         if (sc.noise > 0)
             for (int64_t q = tid; q < (int64_t)K * sc.eps_stride; q += WIN_THREADS) emin = fmin(emin, w.S.eps[q]);
         for (int o = 16; o > 0; o >>= 1) emin = fmin(emin, __shfl_xor_sync(0xffffffffu, emin, o));
-        if (lane == 0) h->wsum[0][warp] = emin;          // every warp's partial minimum
+        if (lane == 0) h->wmin[warp] = emin;             // every warp's partial minimum
         __syncthreads();
         if (tid == 0) {
-            for (int q = 1; q < WIN_WARPS; q++) emin = fmin(emin, h->wsum[0][q]);
+            for (int q = 1; q < WIN_WARPS; q++) emin = fmin(emin, h->wmin[q]);
             h->hand_safe = (w.svc_floor * (1.0 + emin) >= 2.0 * w.W) ? 1 : 0;
         }
         __syncthreads();
@@ -1743,7 +1742,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
     if (!(h->st.status & (OTF_S_TIE | OTF_S_UNFIT))) {
-        for (int32_t c = tid; c < N; c += WIN_THREADS) client_harvest(w.S, w.cl[c], sc.horizon);
+        for (int32_t c = tid; c < N; c += WIN_THREADS) client_harvest(w.S, w.cl[c], c, sc.horizon);
     }
     __syncthreads();
 done:
@@ -1758,26 +1757,8 @@ done:
         cnt[0] = h->st.n_req; cnt[1] = h->st.n_sess; cnt[2] = h->st.n_seg; cnt[3] = h->st.n_job;
         b.status[s] = h->st.status;
     }
-    // float sums: fixed-order reduction (lanes, then warps), then thread 0 writes the QoE block
-    for (int o = 16; o > 0; o >>= 1) {
-        w.S.lat_sum += __shfl_down_sync(0xffffffffu, w.S.lat_sum, o);
-        w.S.stall_sum += __shfl_down_sync(0xffffffffu, w.S.stall_sum, o);
-        w.S.startup_sum += __shfl_down_sync(0xffffffffu, w.S.startup_sum, o);
-    }
-    if (lane == 0 && warp > 0) {
-        h->wsum[warp - 1][0] = w.S.lat_sum;
-        h->wsum[warp - 1][1] = w.S.stall_sum;
-        h->wsum[warp - 1][2] = w.S.startup_sum;
-    }
     __syncthreads();
-    if (tid == 0) {
-        for (int q = 1; q < WIN_WARPS; q++) {
-            w.S.lat_sum += h->wsum[q - 1][0];
-            w.S.stall_sum += h->wsum[q - 1][1];
-            w.S.startup_sum += h->wsum[q - 1][2];
-        }
-        w.S.flush_qoe();
-    }
+    if (tid == 0) w.S.flush_qoe();                     // the summary pass completes the block
 }
 
 }  // namespace otf

@@ -4,6 +4,7 @@
 
 #include "otf_model.cuh"
 #include "otf_rng.cuh"
+#include "otf_xacc.cuh"
 #include "otfgpu.h"
 
 namespace otf {
@@ -40,6 +41,28 @@ struct Client {                 // 144 B: moved as a whole per event
     uint8_t attempt;            // _fetch_with_retry attempt (client.py:291-305); the backoff is
                                 // retry_backoff_s * 2^attempt (repeated doubling is exact)
 };                              // the pick stream lives in a separate (cold) array
+
+// The per-client state touched only at session boundaries: the sequence-pick
+// stream (orchestrator.py:338-342) and the session's registration time (the
+// order the reference sums stall times in, metrics.py:88-92).
+struct ClientCold {              // 64 B
+    Pcg64 picks;
+    double reg_time;
+    double pad;
+};
+
+// QoE accumulators: 32-bit counters (native shared/global atomics) and the
+// exact startup-delay sum (otf_xacc.cuh); see otf_qoe.
+struct QoeAcc {
+    uint32_t lat_hist[OTF_LAT_BINS];
+    uint32_t path_count[8];
+    uint32_t stall_hist[OTF_STALL_BINS];
+    uint32_t rank_count[OTF_RANK_BINS];
+    uint32_t n_requests, n_sessions, n_segments, n_finished, n_started, n_stalls;
+    uint32_t n_lat_tail, n_stl_tail, flags, pad[3];
+    unsigned long long sup[XACC_LIMBS];   // startup delays
+};
+static_assert(sizeof(QoeAcc) % 8 == 0, "QoeAcc limbs are 8-byte aligned");
 
 enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE, W_WOKEN };
 
@@ -80,9 +103,9 @@ OTF_HD ExactLayout exact_layout(int32_t n_clients, int32_t n_workers, int64_t n_
     int64_t n_tasks = (int64_t)n_clients + n_workers;
     int64_t o = 0;
     L.state = o; o += 256;                     // EngineState
-    o += 512;                                  // QoeAcc (at state + 256)
+    o += align256(sizeof(QoeAcc));             // QoeAcc (at state + 256)
     L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
-    L.picks = o;   o += align256((int64_t)sizeof(Pcg64) * n_clients);
+    L.picks = o;   o += align256((int64_t)sizeof(ClientCold) * n_clients);
     L.workers = o; o += align256((int64_t)sizeof(Worker) * n_workers);
     L.heap = o;    o += align256((int64_t)sizeof(Timer) * (n_tasks + 1));
     L.ready = o;   o += align256((int64_t)sizeof(ReadyEnt) * (n_tasks + 1));

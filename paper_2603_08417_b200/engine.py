@@ -71,6 +71,9 @@ class DeviceBatch:
             for name, dt in _lib.RECORD_FIELDS:
                 total = inp.rec_totals[_REC_GROUP[name.split("_")[0]]]
                 self.rec[name] = torch.empty(max(1, total), dtype=_TORCH[dt], device=dev)
+        self.tail_lat = torch.empty(max(1, inp.tail_totals[0]), dtype=torch.float64, device=dev)
+        self.tail_stall = torch.empty(max(1, inp.tail_totals[1]) * _lib.STALL_ENT_BYTES, dtype=torch.uint8,
+                                      device=dev)
         self.counts = torch.zeros((n, 4), dtype=torch.int64, device=dev)
         self.stats = torch.zeros((n, _lib.ST_NSLOTS), dtype=torch.int64, device=dev)
         self.qoe = torch.zeros((n, ctypes.sizeof(_lib.Qoe) // 8), dtype=torch.int64, device=dev)
@@ -84,6 +87,7 @@ class DeviceBatch:
             setattr(b, name, self.rec[name].data_ptr() if name in self.rec else None)
         b.counts, b.stats = self.counts.data_ptr(), self.stats.data_ptr()
         b.qoe, b.status = self.qoe.data_ptr(), self.status.data_ptr()
+        b.tail_lat, b.tail_stall = self.tail_lat.data_ptr(), self.tail_stall.data_ptr()
         # launch groups: scenarios of similar shared-memory size together (a big
         # scenario must not shrink everyone's occupancy), longest first within a group
         cost = np.array([l.cfg.clients * l.cfg.horizon_s / min(l.seq_segdur) for l in inp.lowered])
@@ -171,15 +175,19 @@ def order_sessions(a: dict) -> None:
             a[k] = a[k][seg_order]
 
 
+QOE_FIELDS = ("n_requests", "n_sessions", "n_segments", "n_finished", "n_started", "n_stalls", "latency_sum",
+              "stall_time_sum", "startup_delay_sum", "latency_p50", "latency_p99", "n_lat_tail", "n_stall_tail",
+              "summary_flags")
+
+
 def parse_qoe(row: np.ndarray) -> dict:
-    q = _lib.Qoe.from_buffer_copy(row.tobytes())
-    return {
-        "lat_hist": list(q.lat_hist), "path_count": list(q.path_count)[:5], "stall_hist": list(q.stall_hist),
-        "rank_count": list(q.rank_count), "n_requests": q.n_requests, "n_sessions": q.n_sessions,
-        "n_segments": q.n_segments, "n_finished": q.n_finished, "n_started": q.n_started,
-        "latency_sum": q.latency_sum, "stall_time_sum": q.stall_time_sum,
-        "startup_delay_sum": q.startup_delay_sum,
-    }
+    """One otf_qoe row (int64 words) as a dict of Python numbers / lists."""
+    q = _lib.Qoe.from_buffer_copy(np.ascontiguousarray(row).tobytes())
+    out = {"lat_hist": list(q.lat_hist), "path_count": list(q.path_count)[:5], "stall_hist": list(q.stall_hist),
+           "rank_count": list(q.rank_count)}
+    for f in QOE_FIELDS:
+        out[f] = getattr(q, f)
+    return out
 
 
 @dataclasses.dataclass
@@ -230,7 +238,7 @@ class BatchResult:
 
 
 def run_batch(configs, mode: str = "records", engine: str = "windowed", device=None,
-              max_retries: int = 4, _caps=None, _eps_scale: float = 1.0) -> list[ExperimentResult]:
+              max_retries: int = 4, _caps=None, _eps_scale: float = 1.0, _tail_caps=None) -> list[ExperimentResult]:
     """Run every config on the GPU; returns one ExperimentResult per config.
 
     Scenarios whose record buffers or noise tables were too small are re-run
@@ -264,6 +272,7 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
     results: list = [None] * len(configs)
     todo = list(range(len(configs)))
     caps = {i: tuple(c) for i, c in enumerate(_caps)} if _caps is not None else {}   # test hook
+    tcaps = {i: tuple(c) for i, c in enumerate(_tail_caps)} if _tail_caps is not None else {}   # test hook
     eps_scale = {i: _eps_scale for i in todo} if _eps_scale != 1.0 else {}         # test hook
     engines = {i: eng for i in todo}
     if eng == _lib.ENGINE_WINDOWED:                    # outside the windowed engine's limits: exact, up front
@@ -288,7 +297,9 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
             if any(c is not None for c in cap_list):
                 inp0 = build_inputs([configs[i] for i in idx], engine=e, mode=m, eps_scale=es)
                 use_caps = [c if c is not None else tuple(inp0.caps[k]) for k, c in enumerate(cap_list)]
-            inp = build_inputs([configs[i] for i in idx], engine=e, mode=m, caps=use_caps, eps_scale=es, pin=True)
+            tail = [tcaps.get(i) for i in idx]
+            inp = build_inputs([configs[i] for i in idx], engine=e, mode=m, caps=use_caps, eps_scale=es, pin=True,
+                               tail_caps=tail if any(t is not None for t in tail) else None)
             db = DeviceBatch(inp, device, pin=True)
             db.launch()
             br = db.fetch()
@@ -308,6 +319,10 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                     retry = True
                 if st & _lib.S_RECORD_OVERFLOW:
                     caps[i] = tuple(int(x) + 1 for x in br.counts[k])
+                    retry = True
+                if st & _lib.S_TAIL_OVERFLOW:
+                    q = _lib.Qoe.from_buffer_copy(br.qoe[k].tobytes())
+                    tcaps[i] = (int(q.n_lat_tail) + 1, int(q.n_stall_tail) + 1)
                     retry = True
                 if retry:
                     nxt.append(i)

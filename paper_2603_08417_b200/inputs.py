@@ -211,6 +211,9 @@ class BatchInputs:
     smem_per: list = dataclasses.field(default_factory=list)   # per scenario
     engine_flags: int = 0       # OTF_BF_*
     pinned: bool = False        # pools allocated page-locked (torch pinned memory)
+    tail_caps: np.ndarray = None      # [n][2] summary tails (nonzero latencies, stalled sessions)
+    tail_offsets: np.ndarray = None   # [n][2]
+    tail_totals: tuple = (0, 0)       # (latency doubles, stall entries incl. the sort half)
 
 
 def windowed_fits(cfg, smem_limit: int | None = None) -> tuple[bool, str]:
@@ -242,6 +245,28 @@ def _default_caps(low: Lowered) -> tuple[int, int, int, int]:
     return req, req + cfg.clients, req, 2 * req + 64
 
 
+def default_tail_caps(low: Lowered) -> tuple[int, int]:
+    """Summary-tail capacities: nonzero request latencies and stalled sessions.
+
+    Only requests that wait on a transcode have a nonzero latency (storage and
+    cache hits answer at the arrival instant, server.py:61-78), so variants with
+    every rank stored keep none and cache-less ones keep all; the rest are
+    sized at a quarter of the expected requests.  A session lasts at least its
+    sequence's duration unless the horizon cuts it, which bounds the sessions.
+    A tail that overflows is counted exactly and the scenario re-run with it."""
+    cfg = low.cfg
+    req = _default_caps(low)[0]
+    if len(low.stored) >= low.n_ranks:
+        frac = 0.0
+    elif not low.cache_enabled:
+        frac = 1.0
+    else:
+        frac = 0.25
+    sessions = cfg.clients * (int(cfg.horizon_s / max(min(low.seq_dur), 1e-3)) + 2)
+    stalled = sessions if not low.cache_enabled else sessions // 4
+    return int(req * frac) + 64, int(stalled) + 64
+
+
 def _eps_len(low: Lowered) -> int:
     cfg = low.cfg
     rho = cfg.per_rank_rho or {r: cfg.rho for r, _ in cfg.ladder}
@@ -253,7 +278,8 @@ def _eps_len(low: Lowered) -> int:
 
 
 def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.MODE_RECORDS,
-                 caps=None, eps_scale: float = 1, threads: int | None = None, pin: bool = False) -> BatchInputs:
+                 caps=None, eps_scale: float = 1, threads: int | None = None, pin: bool = False,
+                 tail_caps=None) -> BatchInputs:
     """Lower a list of ExperimentConfigs into one device batch (host arrays; page-locked if pin)."""
     L = _lib.lib()
     threads = threads or os.cpu_count() or 1
@@ -268,6 +294,9 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     input_bytes = 0
     shared_bytes = 0
     smem_per: list[int] = []
+    tcap_arr = np.zeros((len(lows), 2), dtype=np.int64)
+    toff_arr = np.zeros((len(lows), 2), dtype=np.int64)
+    ttot = [0, 0]
 
     # -- traces: one table per (seed, netem), long enough for the largest N --
     trace_groups: dict = {}
@@ -429,6 +458,13 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         smem_per.append(int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg)))
         shared_bytes = max(shared_bytes, smem_per[-1])
         scratch_off = (scratch_off + 255) & ~255
+        tc = tail_caps[si] if tail_caps is not None and tail_caps[si] is not None else default_tail_caps(low)
+        tcap_arr[si] = tc
+        toff_arr[si] = ttot
+        sc.lat_off, sc.lat_cap = int(ttot[0]), int(tc[0])
+        sc.stl_off, sc.stl_cap = int(ttot[1]), int(tc[1])
+        ttot[0] += int(tc[0])
+        ttot[1] += 2 * int(tc[1])                      # entries + the summary pass's sort half
         if mode == _lib.MODE_RECORDS:
             c = caps[si] if caps is not None else _default_caps(low)
             cap_arr[si] = c
@@ -444,7 +480,8 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         lowered=lows, scenarios=scen, size_tables=(_lib.SizeTable * max(1, len(tables)))(*tables),
         f64=P.concat("f64", pin), i64=P.concat("i64", pin), i32=P.concat("i32", pin), pinned=pin,
         scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
-        engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes, smem_per=smem_per)
+        engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes, smem_per=smem_per,
+        tail_caps=tcap_arr, tail_offsets=toff_arr, tail_totals=tuple(ttot))
 
 
 def n_size_tables(inp: BatchInputs) -> int:

@@ -263,8 +263,14 @@ class ExperimentResult:
                              "rejected")}
         return out
 
+    def _need_records(self, what: str) -> None:
+        if not self.arrays:
+            raise _lib.OtfError(f"ExperimentResult.{what} needs per-request records: this result comes from a "
+                                f"histogram-mode run; use run_batch(..., mode='records') (summary() works in both)")
+
     @property
     def requests(self) -> list[RequestRecord]:
+        self._need_records("requests")
         if self._requests is None:
             a = self.arrays
             ids = self.seq_ids
@@ -277,6 +283,7 @@ class ExperimentResult:
 
     @property
     def sessions(self) -> list[SessionReport]:
+        self._need_records("sessions")
         if self._sessions is None:
             a = self.arrays
             ids = self.seq_ids
@@ -293,6 +300,7 @@ class ExperimentResult:
 
     @property
     def jobs(self) -> list[TranscodeJob]:
+        self._need_records("jobs")
         if self._jobs is None:
             a = self.arrays
             ids = self.seq_ids
@@ -307,7 +315,11 @@ class ExperimentResult:
         return self._jobs
 
     def summary(self) -> dict:
-        """orchestrator.py:280-309"""
+        """orchestrator.py:280-309.  Records mode: from the records, as the reference.
+        Histogram mode: from the device's QoE block, field for field the same values
+        (otf_qoe in include/otfgpu.h lists how each one is formed)."""
+        if not self.arrays:
+            return self._summary_from_qoe()
         ladder_size = max(rank for rank, _ in self.config.ladder)
         n_req = len(self.arrays["req_id"])
         out = {
@@ -337,6 +349,42 @@ class ExperimentResult:
                 out["mean_rank"] = quality.mean_rank
             except ValueError:
                 pass
+        return out
+
+    def _summary_from_qoe(self) -> dict:
+        q = self.qoe
+        if q is None:
+            raise _lib.OtfError("no QoE block in this result")
+        ladder_size = max(rank for rank, _ in self.config.ladder)
+        n_req, n_sess = int(q["n_requests"]), int(q["n_sessions"])
+        jobs = int(self.counts[3]) if self.counts is not None else int(self.stats_raw[_lib.ST["jobs_total"]])
+        out = {
+            "fingerprint": self.fingerprint,
+            "variant": self.config.variant,
+            "clients": self.config.clients,
+            "workers": self.config.workers,
+            "segment_duration_s": self.config.segment_duration_s,
+            "requests": n_req,
+            "sessions": n_sess,
+            "jobs": jobs,
+            "backend": self.backend_stats,
+        }
+        if n_req:
+            if not q["summary_flags"] & _lib.Q_ORDER_STATS:
+                raise _lib.OtfError("the summary pass did not run for this scenario (status %#x)" % self.status)
+            out["instant_fraction"] = q["lat_hist"][0] / n_req          # metrics.py:77
+            out["latency_p50_s"] = q["latency_p50"]
+            out["latency_p99_s"] = q["latency_p99"]
+        if n_sess:
+            out["stalls_mean"] = int(q["n_stalls"]) / n_sess              # metrics.py:91
+            out["stall_time_total_s"] = q["stall_time_sum"]
+            total = int(q["n_segments"])
+            if total:
+                if ladder_size >= _lib.RANK_BINS or q["summary_flags"] & _lib.Q_RANKS_CAPPED:
+                    raise _lib.OtfError(f"quality fractions need ranks < {_lib.RANK_BINS} in histogram mode")
+                fractions = {rank: int(q["rank_count"][rank]) / total for rank in range(1, ladder_size + 1)}
+                out["quality_fractions"] = {str(k): v for k, v in fractions.items()}
+                out["mean_rank"] = sum(rank * frac for rank, frac in fractions.items())   # metrics.py:115
         return out
 
     def write(self, outdir) -> None:
