@@ -199,7 +199,7 @@ def main():
         exact_inp = inputs.build_inputs([my_cfgs[i] for i in flagged], engine=_lib.ENGINE_EXACT,
                                         mode=_lib.MODE_HISTOGRAM, eps_scale=4)
         exact_db = engine.DeviceBatch(exact_inp, dev, pin=True)
-    launches_per_step = 1 + len(db.groups) + (2 if exact_db is not None else 0)
+    launches_per_step = 1 + len(db.groups) + 1 + (3 if exact_db is not None else 0)   # sizes, engine groups, summary
     inp_h2d = db.h2d_bytes + (exact_db.h2d_bytes if exact_db is not None else 0)
     q_rows = db.qoe.shape[1]
 
@@ -226,6 +226,8 @@ def main():
     # per-kernel timing of the engine (events bracket the engine launch on its stream)
     eng_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
+    sum_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -237,8 +239,11 @@ def main():
                                       db.f64.data_ptr(), db.i32.data_ptr(), stream.cuda_stream)
             _lib.check(rc, "otf_gen_sizes")
         eng_evs[k][0].record(stream)
-        db.launch(stream, sizes=False)
+        db.launch(stream, sizes=False, summary=False)
         eng_evs[k][1].record(stream)
+        sum_evs[k][0].record(stream)
+        db.launch_summary(stream)
+        sum_evs[k][1].record(stream)
         if exact_db is not None:
             exact_db.launch(stream)
         gather_qoe()
@@ -250,6 +255,7 @@ def main():
     clk = clocks.stop() if clocks is not None else None
     elapsed_ms = t0.elapsed_time(t1)
     eng_ms = [a.elapsed_time(b) for a, b in eng_evs]
+    sum_ms = statistics.mean(a.elapsed_time(b) for a, b in sum_evs)
     br = db.fetch()
     my_req = int(br.counts[:, 0].sum())
     if exact_db is not None:
@@ -303,7 +309,8 @@ def main():
             traffic = tj.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "kernel": "otf::windowed_kernel",
-                "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": eng_ms_max}
+                "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": eng_ms_max,
+                "summary_pass_ms": sum_ms}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -118,12 +118,13 @@ typedef struct otf_scenario {
     int64_t sess_off, sess_cap;
     int64_t seg_off, seg_cap;
     int64_t job_off, job_cap;
-    /* summary tails (both modes; cap 0 = none): the nonzero request latencies
-     * (otf_batch.tail_lat) and the sessions with a nonzero stall time
-     * (otf_batch.tail_stall, 2 * stl_cap entries: the second half is the sort
-     * buffer of the summary pass) */
+    /* summary tails (both modes; see otf_batch.tail_*): the nonzero request
+     * latencies, every closed session (ses_cap records, then 2 * stl_cap
+     * entries where the summary pass gathers and orders the stalled ones), and
+     * the startup delays */
     int64_t lat_off, lat_cap;
-    int64_t stl_off, stl_cap;
+    int64_t ses_off, ses_cap, stl_cap;
+    int64_t sup_off, sup_cap;
 } otf_scenario;
 
 /* Fused QoE / fulfillment epilogue (metrics.py:67-116, orchestrator.py:280-309).
@@ -157,15 +158,23 @@ typedef struct otf_qoe {
     int64_t n_lat_tail;               /* requests with a nonzero latency */
     int64_t n_stall_tail;             /* sessions with a nonzero stall time */
     int64_t summary_flags;            /* OTF_Q_* */
+    /* n_sessions / n_started count the session records and startup delays the
+     * engines kept (summary tails); the summary pass derives the rest */
 } otf_qoe;
 
-/* One session with a nonzero stall time (summary tail): registration time and
- * session id give the registration order the reference sums in. */
-typedef struct otf_stall_ent {
+/* One closed session (summary tail): the report as _sync_report left it
+ * (client.py:284-288).  Registration time and session id give the
+ * registration order the reference sums stall times in. */
+typedef struct otf_sess_ent {
     double reg_time;
     double stall_time;
-    int64_t sid;
-} otf_stall_ent;
+    int32_t sid;
+    uint32_t stalls;                  /* stall events | OTF_SE_FINISHED */
+} otf_sess_ent;
+#define OTF_SE_FINISHED 0x80000000u
+
+/* otf_batch.engine_flags */
+#define OTF_BF_ENGINE_ONLY 0x1        /* otf_run_batch skips the summary pass (run it with otf_run_summary) */
 
 typedef struct otf_batch {
     int32_t n_scenarios;
@@ -191,10 +200,11 @@ typedef struct otf_batch {
     const int32_t *order;             /* optional launch order (longest first), NULL = identity */
     int64_t shared_bytes;             /* windowed engine: dynamic shared memory per scenario
                                          (max of otf_shared_bytes over the batch) */
-    int32_t engine_flags;             /* reserved, 0 */
+    int32_t engine_flags;             /* OTF_BF_* */
     int32_t pad_flags;
-    double *tail_lat;                 /* summary tails at otf_scenario.lat_off / stl_off (may be NULL */
-    otf_stall_ent *tail_stall;        /*   when every cap is 0) */
+    double *tail_lat;                 /* summary tails at otf_scenario.lat_off / ses_off / sup_off */
+    otf_sess_ent *tail_sess;
+    double *tail_sup;
 } otf_batch;
 
 /* A segment-size table: Catalog.descriptor sizes (content.py:204-218) for one
@@ -319,6 +329,10 @@ int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t to
  * the summary pass: order statistics of the latency tail and the
  * registration-order stall sum into each scenario's otf_qoe. */
 int otf_run_batch(const otf_batch *batch, int32_t engine, void *stream);
+
+/* DEVICE: the summary pass alone (after an OTF_BF_ENGINE_ONLY otf_run_batch on
+ * the same stream); `engine` is the engine that produced the tails. */
+int otf_run_summary(const otf_batch *batch, int32_t engine, void *stream);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@ MODE_HISTOGRAM, MODE_RECORDS = 0, 1
 S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG, S_UNFIT, S_TAIL_OVERFLOW = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
 Q_ORDER_STATS, Q_INEXACT_SUM, Q_RANKS_CAPPED = 0x1, 0x2, 0x4
+BF_ENGINE_ONLY = 0x1
 SM_COUNT_B200, SMEM_PER_SM = 148, 227 * 1024
 
 ST_NSLOTS = 32
@@ -58,7 +59,8 @@ class Scenario(ctypes.Structure):
         ("off_eps", _i64), ("eps_stride", _i64), ("scratch_off", _i64),
         ("req_off", _i64), ("req_cap", _i64), ("sess_off", _i64), ("sess_cap", _i64),
         ("seg_off", _i64), ("seg_cap", _i64), ("job_off", _i64), ("job_cap", _i64),
-        ("lat_off", _i64), ("lat_cap", _i64), ("stl_off", _i64), ("stl_cap", _i64),
+        ("lat_off", _i64), ("lat_cap", _i64), ("ses_off", _i64), ("ses_cap", _i64), ("stl_cap", _i64),
+        ("sup_off", _i64), ("sup_cap", _i64),
     ]
 
 
@@ -74,7 +76,7 @@ class Qoe(ctypes.Structure):
     ]
 
 
-STALL_ENT_BYTES = 24   # otf_stall_ent: reg_time f64, stall_time f64, sid i64
+SESS_ENT_BYTES = 24    # otf_sess_ent: reg_time f64, stall_time f64, sid i32, stalls u32
 
 
 RECORD_FIELDS = [  # (name, numpy dtype) in otf_batch order
@@ -94,7 +96,7 @@ class Batch(ctypes.Structure):
                 + [(n, _vp) for n, _ in RECORD_FIELDS]
                 + [("counts", _vp), ("stats", _vp), ("qoe", _vp), ("status", _vp), ("order", _vp),
                    ("shared_bytes", _i64), ("engine_flags", _i32), ("pad_flags", _i32),
-                   ("tail_lat", _vp), ("tail_stall", _vp)])
+                   ("tail_lat", _vp), ("tail_sess", _vp), ("tail_sup", _vp)])
 
 
 class TraceJob(ctypes.Structure):
@@ -115,7 +117,7 @@ class SizeTable(ctypes.Structure):
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
            "otf_scratch_bytes", "otf_shared_bytes", "otf_engine_fits", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
            "otf_gen_noise", "otf_gen_traces", "otf_gen_traces_multi", "otf_model_completion_time",
-           "otf_model_select_quality", "otf_model_buffer_run", "otf_model_exact_sum", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch")
+           "otf_model_select_quality", "otf_model_buffer_run", "otf_model_exact_sum", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch", "otf_run_summary")
 DRAW_STANDARD_NORMAL, DRAW_NORMAL, DRAW_EXPONENTIAL, DRAW_STANDARD_EXPONENTIAL = 0, 1, 2, 3
 
 
@@ -182,6 +184,8 @@ def lib():
     L.otf_gen_sizes.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp, _vp]
     L.otf_run_batch.restype = ctypes.c_int
     L.otf_run_batch.argtypes = [_P(Batch), _i32, _vp]
+    L.otf_run_summary.restype = ctypes.c_int
+    L.otf_run_summary.argtypes = [_P(Batch), _i32, _vp]
     if L.otf_version() != ABI_VERSION:
         raise OtfError(f"libotfgpu ABI {L.otf_version()} != {ABI_VERSION}")
     for name, st in (("otf_sizeof_scenario", Scenario), ("otf_sizeof_batch", Batch), ("otf_sizeof_qoe", Qoe)):

@@ -163,9 +163,16 @@ int otf_run_batch(const otf_batch *batch, int32_t engine, void *stream) {
     }
     else return fail(OTF_EINVAL, "otf_run_batch: unknown engine");
     int rc = check_cuda("otf_run_batch");
-    if (rc != OTF_OK) return rc;
-    if (otf_launch_summary(b, engine, s) != 0) return fail(OTF_ECUDA, "otf_run_batch: summary pass");
-    return check_cuda("otf_run_batch (summary pass)");
+    if (rc != OTF_OK || (b.engine_flags & OTF_BF_ENGINE_ONLY)) return rc;
+    return otf_run_summary(batch, engine, stream);
+}
+
+int otf_run_summary(const otf_batch *batch, int32_t engine, void *stream) {
+    if (!batch || batch->n_scenarios < 0) return fail(OTF_EINVAL, "otf_run_summary: bad batch");
+    if (batch->n_scenarios == 0) return OTF_OK;
+    if (otf_launch_summary(*batch, engine, (cudaStream_t)stream) != 0)
+        return fail(OTF_ECUDA, "otf_run_summary: shared memory request too large");
+    return check_cuda("otf_run_summary");
 }
 
 }  // extern "C"

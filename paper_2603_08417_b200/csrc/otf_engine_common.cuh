@@ -38,8 +38,9 @@ struct Scn {
     otf_qoe *q;                      // final destination (global)
     QoeAcc *qa;                      // counters while running (shared or scratch)
     ClientCold *cold;                         // [n_clients] pick streams + registration times (scratch)
-    double *tail_lat;                         // summary tails (NULL when the caps are 0)
-    otf_stall_ent *tail_stall;
+    double *tail_lat;                         // summary tails (otf_batch.tail_*)
+    otf_sess_ent *tail_sess;
+    double *tail_sup;
     uint64_t mag_g, mag_rg;                   // d / max_nseg, d / (n_ranks * max_nseg) by multiply-high
     double inv_grid_step;                     // 1 / sc->grid_step (0 when the trace grid is irregular)
     // the client model's constants in registers (read on every event; a shared-memory
@@ -71,8 +72,9 @@ struct Scn {
         pbits = b->f64_pool + sc->off_pbits;
         arrivals = b->f64_pool + sc->off_arrivals;
         eps = b->f64_pool + sc->off_eps;
-        tail_lat = (b->tail_lat && sc->lat_cap > 0) ? b->tail_lat + sc->lat_off : nullptr;
-        tail_stall = (b->tail_stall && sc->stl_cap > 0) ? b->tail_stall + sc->stl_off : nullptr;
+        tail_lat = b->tail_lat ? b->tail_lat + sc->lat_off : nullptr;
+        tail_sess = b->tail_sess ? b->tail_sess + sc->ses_off : nullptr;
+        tail_sup = b->tail_sup ? b->tail_sup + sc->sup_off : nullptr;
         records = b->mode == OTF_MODE_RECORDS;
         div_g = (uint32_t)sc->max_nseg;
         div_rg = (uint32_t)(sc->n_ranks * sc->max_nseg);
@@ -99,16 +101,16 @@ struct Scn {
     // write the final otf_qoe; the summary pass (otf_summary.cu) adds the
     // latency sum, the order statistics and the registration-order stall sum
     __device__ void flush_qoe() const {
+        int64_t n_req = 0;
         for (int i = 0; i < OTF_LAT_BINS; i++) q->lat_hist[i] = qa->lat_hist[i];
-        for (int i = 0; i < 8; i++) q->path_count[i] = qa->path_count[i];
-        for (int i = 0; i < OTF_STALL_BINS; i++) q->stall_hist[i] = qa->stall_hist[i];
+        for (int i = 0; i < 8; i++) { q->path_count[i] = qa->path_count[i]; n_req += qa->path_count[i]; }
+        for (int i = 0; i < OTF_STALL_BINS; i++) q->stall_hist[i] = 0;
         for (int i = 0; i < OTF_RANK_BINS; i++) q->rank_count[i] = qa->rank_count[i];
-        q->n_requests = qa->n_requests; q->n_sessions = qa->n_sessions; q->n_segments = qa->n_segments;
-        q->n_finished = qa->n_finished; q->n_started = qa->n_started; q->n_stalls = qa->n_stalls;
-        q->latency_sum = 0.0; q->stall_time_sum = 0.0;
-        q->startup_delay_sum = xacc_round(qa->sup);
+        q->n_requests = n_req; q->n_sessions = qa->n_ses_tail; q->n_segments = qa->n_segments;
+        q->n_finished = 0; q->n_started = qa->n_sup_tail; q->n_stalls = 0;
+        q->latency_sum = 0.0; q->stall_time_sum = 0.0; q->startup_delay_sum = 0.0;
         q->latency_p50 = 0.0; q->latency_p99 = 0.0;
-        q->n_lat_tail = qa->n_lat_tail; q->n_stall_tail = qa->n_stl_tail;
+        q->n_lat_tail = qa->n_lat_tail; q->n_stall_tail = 0;
         q->summary_flags = qa->flags;
     }
 
@@ -117,6 +119,27 @@ struct Scn {
         const uint32_t pos = atomicAdd(&qa->n_lat_tail, 1u);
         if (pos < (uint64_t)sc->lat_cap) tail_lat[pos] = lat;
         else flag(OTF_S_TAIL_OVERFLOW);
+    }
+    // playback started: the startup delay (client.py:128-131) is final
+    __device__ __forceinline__ void tail_startup(double startup) {
+        const uint32_t pos = atomicAdd(&qa->n_sup_tail, 1u);
+        if (pos < (uint64_t)sc->sup_cap) tail_sup[pos] = startup;
+        else flag(OTF_S_TAIL_OVERFLOW);
+    }
+    // a session's numbers are final (finished, aborted or harvested): its record
+    __device__ __forceinline__ void tail_session(double reg_time, double stall_time, int32_t sid, uint32_t stalls,
+                                                 bool finished) {
+        const uint32_t pos = atomicAdd(&qa->n_ses_tail, 1u);
+        if (pos < (uint64_t)sc->ses_cap) {
+            otf_sess_ent e;
+            e.reg_time = reg_time;
+            e.stall_time = stall_time;
+            e.sid = sid;
+            e.stalls = stalls | (finished ? OTF_SE_FINISHED : 0u);
+            tail_sess[pos] = e;
+        } else {
+            flag(OTF_S_TAIL_OVERFLOW);
+        }
     }
 
     __device__ __forceinline__ int64_t &stat(int i) { return stats[i]; }
@@ -230,7 +253,6 @@ struct Scn {
         double lat = response - c.arrival;
         qa->lat_hist[lat_bin(lat)]++;
         qa->path_count[c.path]++;
-        qa->n_requests++;
         if (lat != 0.0) tail_latency(lat);
     }
 
@@ -244,31 +266,12 @@ struct Scn {
     }
 
     // session QoE, once per session when its numbers are final (the report as
-    // _sync_report left it, client.py:284-288)
-    __device__ void qoe_session(const Client &c, int32_t cid, bool finished) {
-        int32_t stalls = c.buf_live ? c.buf.stall_events : 0;
-        atomicAdd(&qa->n_sessions, 1u);
-        atomicAdd(&qa->stall_hist[stalls < OTF_STALL_BINS - 1 ? stalls : OTF_STALL_BINS - 1], 1u);
-        if (c.buf_live) {
-            if (stalls) atomicAdd(&qa->n_stalls, (uint32_t)stalls);
-            if (c.buf.stall_time != 0.0) {             // summed in registration order by the summary pass
-                const uint32_t pos = atomicAdd(&qa->n_stl_tail, 1u);
-                if (pos < (uint64_t)sc->stl_cap) {
-                    otf_stall_ent e;
-                    e.reg_time = cold[cid].reg_time;
-                    e.stall_time = c.buf.stall_time;
-                    e.sid = c.session;
-                    tail_stall[pos] = e;
-                } else {
-                    flag(OTF_S_TAIL_OVERFLOW);
-                }
-            }
-            if (!isnan(c.buf.started_at)) {
-                atomicAdd(&qa->n_started, 1u);
-                xacc_add(qa->sup, c.buf.started_at - c.buf.session_start, &qa->flags);
-            }
-        }
-        if (finished) atomicAdd(&qa->n_finished, 1u);
+    // _sync_report left it, client.py:284-288); the work is out of line with
+    // scalar arguments (session closes are rare next to client events)
+    __device__ __forceinline__ void qoe_session(const Client &c, int32_t cid, bool finished) {
+        if (c.buf_live && !isnan(c.buf.started_at)) tail_startup(c.buf.started_at - c.buf.session_start);
+        tail_session(cold[cid].reg_time, c.buf_live ? c.buf.stall_time : 0.0, c.session,
+                     c.buf_live ? (uint32_t)c.buf.stall_events : 0u, finished);
     }
 
     __device__ void finish() {

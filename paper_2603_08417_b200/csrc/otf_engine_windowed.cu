@@ -108,6 +108,7 @@ struct WinHeader {
     int32_t n_loc;                       // this window's client-local events (bucket array)
     int32_t list_cap;                    // capacity of the window's server-event list (dynamic region)
     int32_t ctl, cur_m;                  // window-loop control word + the window being run
+    int32_t n_bsrv;                      // entries gathered from the window's server bucket
     uint8_t ev_flags[PAR_MAX];           // parallel server pass: per request outcome (EV_*)
     uint8_t ev_touch[PAR_MAX];           //   LRU touches before it (exclusive prefix)
     uint8_t par_list[PAR_MAX];           //   the list partitioned by owner lane (time order kept)
@@ -138,8 +139,55 @@ __host__ __device__ inline int64_t lq_capacity(int64_t n_desc) {   // power of t
 // the window's gather is one coalesced read instead of bucket -> client state.
 struct SrvEnt {
     double when;                                       // fire time (the request's arrival)
+    double ctime;                                      // arm time (orders equal fire times, sim.py:304-309)
     int32_t pk;                                        // rank | index << 8 | seq << 16
     int16_t cid, desc;
+};
+
+// The windowed engine's per-client coroutine state: what every client event
+// reads and writes, 64 B (four 16-byte vectors, half an L2 line).  The rest --
+// the pick stream and registration time (session boundaries) and, in records
+// mode, the request's id / response slot / request time -- is in WCold.  The
+// server pass never writes here: responses reach the client as RespMsg.
+// In registers (WClient) every field is a full word; in memory (WPacked) the
+// small ones are packed, and the struct is unpacked / packed once per event.
+struct WClient {
+    double level, last_sync, stall_time;               // PlayerBuffer (client.py:74-121)
+    double est;                                        // throughput EWMA; < 0: none yet (client.py:261-263)
+    double next_when;                                  // the pending timer's fire time (for a request:
+                                                       //   its arrival at the server)
+    double session_start;                              // buffer reset time (startup delay)
+    int32_t session;                                   // session id (registration counter)
+    int32_t seq, index;                                // the session's sequence (< 2^16), next segment (< 2^16)
+    int32_t pc, rank, attempt, flags;                  // < 2^8 each; flags: buffer phase (2 bits) | WF_*
+    uint32_t stall_events;
+};
+struct WPacked {
+    double level, last_sync, stall_time, est, next_when, session_start;
+    int32_t session;
+    uint32_t seq_index;                                // seq | index << 16
+    uint32_t small;                                    // pc | rank << 8 | attempt << 16 | flags << 24
+    uint32_t stall_events;
+};
+static_assert(sizeof(WPacked) == 64, "a client's hot state is half an L2 line");
+enum { WF_PHASE = 3, WF_LIVE = 4, WF_OPEN = 8 };       // buffer playing-state, buffer live, session open
+
+struct WCold {                                         // 128 B: session-boundary / records-mode state
+    Pcg64 picks;                                       // orchestrator.py:338-342
+    double reg_time;                                   // session registration time (metrics.py:88-92 order)
+    double ctime;                                      // arm time of a request pushed past a full bucket
+    int64_t req_id, req_slot;                          // records: MediaServer request id, response slot
+    double requested;                                  // records: the segment's request time (seg_start)
+    double pad[5];
+};
+static_assert(sizeof(WCold) == 128, "WCold is one L2 line");
+
+// A client event handed to the client lanes: a server response (segment,
+// waited transcode or OverloadError) at `when`, or a client-local timer
+// (path < 0) whose time is in the client's state.
+struct RespMsg {
+    double when;
+    int32_t cid, path;
 };
 
 struct WinGlobalLayout {
@@ -155,9 +203,9 @@ __host__ __device__ inline int32_t bucket_cap_loc(int32_t n_clients) { return 2 
 __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, int64_t n_desc) {
     WinGlobalLayout L;
     int64_t o = 0;
-    L.clients = o; o += align256((int64_t)sizeof(Client) * n_clients);
-    L.picks = o;   o += align256((int64_t)sizeof(ClientCold) * n_clients);
-    L.blist = o;   o += align256((int64_t)sizeof(int32_t) * (n_clients + 64));
+    L.clients = o; o += align256((int64_t)sizeof(WPacked) * n_clients);
+    L.picks = o;   o += align256((int64_t)sizeof(WCold) * n_clients);
+    L.blist = o;   o += align256((int64_t)sizeof(RespMsg) * (n_clients + 64));
     L.jobq = o;    o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.specq = o;   o += align256((int64_t)sizeof(JobEnt) * (n_desc + 1));
     L.lstamp = o;  o += align256((int64_t)sizeof(uint32_t) * n_desc);
@@ -199,8 +247,9 @@ struct Win {
     uint32_t *lstamp;                                  // latest touch stamp per descriptor (global)
     LqEnt *lq;                                         // touch queue (global, 2 * lq_cap)
     uint16_t *dflags;                                  // descriptor words (DF_*), shared
-    Client *cl;
-    int32_t *blist;
+    WPacked *cl;                                       // hot client state (global)
+    WCold *wc;                                         // cold client state (global)
+    RespMsg *blist;                                    // this window's responses (+ overflowed local timers)
     SrvEnt *bsrv;                                      // bucket arrays [RING][cap]
     int32_t *bloc;
     int32_t scap, lcap;
@@ -241,8 +290,10 @@ __device__ __forceinline__ int32_t timer_win(const Win &w, double when) {
     return k < WIN_NONE ? k : WIN_NONE;
 }
 
-// Put client c on the bucket of window `wk` (any lane; lock-free push).
-__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool srv, const Client &cl) {
+// Put client c on the bucket of window `wk` (any lane; lock-free push).  A server
+// event (request) carries its sort key, arm time and descriptor.
+__device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool srv, const WClient &cl, double ctime,
+                                            int32_t desc) {
     WinHeader *h = w.h;
     if (wk - w.k < RING) {
         int32_t slot = wk & (RING - 1);
@@ -253,14 +304,16 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
             if (srv) {
                 SrvEnt e;
                 e.when = cl.next_when;
-                e.pk = cl.rank | (cl.index << 8) | (cl.seq << 16);
+                e.ctime = ctime;
+                e.pk = (int32_t)cl.rank | ((int32_t)cl.index << 8) | ((int32_t)cl.seq << 16);
                 e.cid = (int16_t)c;
-                e.desc = (int16_t)cl.desc;
+                e.desc = (int16_t)desc;
                 w.bsrv[(int64_t)slot * cap + pos] = e;
             } else {
                 w.bloc[(int64_t)slot * cap + pos] = c;
             }
         } else {                                       // bucket full (rare): overflow list
+            if (srv) w.wc[c].ctime = ctime;            //   (the entry is rebuilt from the client state)
             int32_t old = atomicExch(&h->ovf_head, c);
             w.bnext[c] = (int16_t)old;
             atomicAdd(&h->ovf_n, 1);
@@ -424,15 +477,23 @@ __device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
 }
 
 // Response of MediaServer.segment (server.py:76-77): fix the record's slot
-// in response order and hand the client back to the client lanes at `now`.
-// The record itself and the request QoE are written by the client lane.
-__device__ __forceinline__ void respond(Win &w, int32_t cid) {
-    Client &c = w.cl[cid];
-    c.req_slot = (int32_t)w.n_req++;
-    c.pc = C_SEG_RESP;
-    c.next_when = w.now;
-    w.blist[w.n_blist++] = cid;
+// in response order and hand the client back to the client lanes at `now`
+// (a RespMsg: the client's own state is written by its lane only).  The
+// record itself and the request QoE are written by the client lane.
+__device__ __forceinline__ void respond(Win &w, int32_t cid, int32_t path) {
+    const int64_t slot = w.n_req++;
+    if (w.S.records) w.wc[cid].req_slot = slot;
+    RespMsg m;
+    m.when = w.now;
+    m.cid = cid;
+    m.path = path;
+    w.blist[w.n_blist++] = m;
 }
+
+// Waiter links reuse bnext (a waiting client has no pending timer): bits 0-14 are
+// the next waiter, bit 15 marks a client whose request created the demand job
+// (path "transcoded"; the others joined an in-flight job: "waited_inflight").
+constexpr uint16_t WL_TRANSCODED = 0x8000;
 
 __device__ void resolve(Win &w, int32_t d) {                             // backend.py:209-216
     const uint16_t f = w.dflags[d];
@@ -440,24 +501,26 @@ __device__ void resolve(Win &w, int32_t d) {                             // back
     w.dflags[d] = (uint16_t)((f & DF_CACHED) | DF_IDLE);
     const int32_t t = f & 0x7FFF;
     if (t == DF_NOWAIT) return;
-    int32_t c = w.bnext[t];                            // head: waiter Future callbacks, await order
+    int32_t c = (uint16_t)w.bnext[t] & 0x7FFF;         // head: waiter Future callbacks, await order
     for (;;) {
-        const int32_t nxt = w.bnext[c];
-        respond(w, c);
+        const uint16_t lk = (uint16_t)w.bnext[c];
+        respond(w, c, (lk & WL_TRANSCODED) ? OTF_PATH_TRANSCODED : OTF_PATH_WAITED);
         if (c == t) break;
-        c = nxt;
+        c = lk & 0x7FFF;
     }
 }
 
-// Append a waiter (waiter links reuse bnext: a waiting client has no pending timer).
-__device__ __forceinline__ void add_waiter(Win &w, int32_t d, int32_t cid) {
+// Append a waiter.
+__device__ __forceinline__ void add_waiter(Win &w, int32_t d, int32_t cid, bool transcoded) {
     const uint16_t f = w.dflags[d];
     const int32_t t = f & 0x7FFF;
+    const uint16_t tag = transcoded ? WL_TRANSCODED : 0;
     if (t == DF_NOWAIT) {
-        w.bnext[cid] = (int16_t)cid;
+        w.bnext[cid] = (int16_t)(cid | tag);
     } else {
-        w.bnext[cid] = w.bnext[t];
-        w.bnext[t] = (int16_t)cid;
+        const uint16_t lt = (uint16_t)w.bnext[t];
+        w.bnext[cid] = (int16_t)((lt & 0x7FFF) | tag);
+        w.bnext[t] = (int16_t)((lt & WL_TRANSCODED) | cid);
     }
     w.dflags[d] = (uint16_t)((f & DF_CACHED) | cid);
 }
@@ -559,12 +622,10 @@ __device__ __forceinline__ void speculate_next(Win &w, int32_t d, int32_t index,
 __device__ __forceinline__ void server_request_fast(Win &w, int32_t cid, int32_t d, int32_t pk, uint16_t f,
                                                     uint16_t fn, int32_t segc) {
     const int32_t rank = pk & 0xff, index = (pk >> 8) & 0xff;
-    Client &c = w.cl[cid];
-    c.req_id = (int32_t)w.req_counter++;
-    c.arrival = w.now;
+    const int64_t rid = w.req_counter++;
+    if (w.S.records) w.wc[cid].req_id = rid;
     if ((w.stored_mask >> rank) & 1u) {
-        c.path = OTF_PATH_STORAGE;
-        respond(w, cid);
+        respond(w, cid, OTF_PATH_STORAGE);
         return;
     }
     if (w.cache_on) {                                  // SegmentCache.get (cache.py:45-52)
@@ -572,25 +633,19 @@ __device__ __forceinline__ void server_request_fast(Win &w, int32_t cid, int32_t
             lru_touch(w, d);
             w.c_hits++;
             speculate_next(w, d, index, segc, fn);
-            c.path = OTF_PATH_CACHE;
-            respond(w, cid);
+            respond(w, cid, OTF_PATH_CACHE);
             return;
         }
         w.c_miss++;
     }
-    c.pc = C_SEG_WAIT;
     if (df_inflight(f)) {
         speculate_next(w, d, index, segc, fn);
-        c.path = OTF_PATH_WAITED;
-        add_waiter(w, d, cid);
+        add_waiter(w, d, cid, false);
     } else if (enqueue_job(w, d, OTF_ORIGIN_DEMAND)) {
-        c.path = OTF_PATH_ERROR;                       // OverloadError: error record (server.py:70-73)
-        respond(w, cid);
-        c.pc = C_SEG_ERR;
+        respond(w, cid, OTF_PATH_ERROR);               // OverloadError: error record (server.py:70-73)
     } else {
         speculate_next(w, d, index, segc, fn);
-        c.path = OTF_PATH_TRANSCODED;
-        add_waiter(w, d, cid);
+        add_waiter(w, d, cid, true);
     }
 }
 
@@ -774,7 +829,7 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
                     }
                 }
             }
-            if (!(fl & EV_IMM)) add_waiter(w, d, cid);
+            if (!(fl & EV_IMM)) add_waiter(w, d, cid, (fl & EV_PATH) == OTF_PATH_TRANSCODED);
         }
         h->ev_flags[i] = (uint8_t)fl;
     }
@@ -821,17 +876,16 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
         h->ev_touch[i] = (uint8_t)p_tch;
         const int32_t cid = w.li[i], d = w.ld[i];
         const double now = w.lw[i];
-        Client &c = w.cl[cid];
-        c.req_id = (int32_t)(req_base + i);
-        c.arrival = now;
-        c.path = (int32_t)(f & EV_PATH);
+        if (w.S.records) {
+            w.wc[cid].req_id = req_base + i;
+            if (f & EV_IMM) w.wc[cid].req_slot = slot_base + p_imm;
+        }
         if (f & EV_IMM) {                              // respond (server.py:76-77)
-            c.req_slot = (int32_t)(slot_base + p_imm);
-            c.pc = C_SEG_RESP;
-            c.next_when = now;
-            w.blist[blist_base + (int32_t)p_imm] = cid;
-        } else {
-            c.pc = C_SEG_WAIT;
+            RespMsg m;
+            m.when = now;
+            m.cid = cid;
+            m.path = (int32_t)(f & EV_PATH);
+            w.blist[blist_base + (int32_t)p_imm] = m;
         }
         if (f & EV_TOUCH) {                            // lru_touch, in time order
             LqEnt e; e.desc = d; e.stamp = stamp_base + p_tch + 1u;
@@ -949,6 +1003,17 @@ __device__ __forceinline__ bool parallel_ok(Win &w) {
            (lq_tail - lq_head + (uint32_t)n <= w.lq_mask);   // room for every touch
 }
 
+// Arm time of window request `cid` (rare tie-breaks only): the window's bucket
+// entries carry it; a request pushed past a full bucket kept it in its WCold.
+__device__ __noinline__ double req_ctime_at(const SrvEnt *as, int32_t ns, const WCold *wc, int32_t cid) {
+    for (int32_t i = 0; i < ns; i++)
+        if (as[i].cid == cid) return as[i].ctime;
+    return wc[cid].ctime;
+}
+__device__ __forceinline__ double req_ctime(const Win &w, int32_t cid) {
+    return req_ctime_at(w.bsrv + (int64_t)(w.k & (RING - 1)) * w.scap, w.h->n_bsrv, w.wc, cid);
+}
+
 // Phase A: replay the window's server events in (time, creation, tick) order.
 __device__ void phase_a(Win &w) {
     WinHeader *h = w.h;
@@ -996,7 +1061,7 @@ __device__ void phase_a(Win &w) {
         else if (bw_when < cw) take_worker = true;
         else if (cw < bw_when) take_worker = false;
         else {
-            double cc = w.cl[w.li[i]].ctime;
+            double cc = req_ctime(w, w.li[i]);
             if (bw_ctime < cc) take_worker = true;
             else if (cc < bw_ctime) take_worker = false;
             else { w.S.flag(OTF_S_TIE); take_worker = true; }
@@ -1015,18 +1080,37 @@ __device__ void phase_a(Win &w) {
 }
 
 // ---- client lanes ------------------------------------------------------------------
+// The client coroutine (orchestrator.py:336-348, client.py:229-305) over the
+// 64-byte WClient.  The buffer model functions (otf_model.cuh, pinned by the
+// reference's known answers) run on a Buffer view of its fields.
+__device__ __forceinline__ Buffer wbuf_get(const WClient &c) {
+    Buffer b;
+    b.level = c.level; b.last_sync = c.last_sync; b.stall_time = c.stall_time;
+    b.started_at = NAN; b.session_start = c.session_start;
+    b.phase = c.flags & WF_PHASE; b.stall_events = (int32_t)c.stall_events;
+    return b;
+}
+__device__ __forceinline__ void wbuf_put(WClient &c, const Buffer &b) {
+    c.level = b.level; c.last_sync = b.last_sync; c.stall_time = b.stall_time;
+    c.flags = (c.flags & ~WF_PHASE) | (b.phase & WF_PHASE); c.stall_events = (uint32_t)b.stall_events;
+}
+__device__ __forceinline__ void wbuf_advance(WClient &c, double now) {
+    Buffer b = wbuf_get(c);
+    buf_advance(b, now);
+    wbuf_put(c, b);
+}
+__device__ __forceinline__ int32_t wdesc(const Scn &S, const WClient &c) { return S.desc_id(c.seq, c.rank, c.index); }
+
 // Arm a sleep for client c at `now` (loop.sleep, sim.py:317-324): returns true
 // if the client keeps running inside this window (the timer fires before the
 // window ends), else files the timer on the wheel and returns false.
-__device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now, double delay, int32_t next_pc) {
+__device__ __forceinline__ bool arm(Win &w, WClient &c, int32_t cid, double &now, double delay, int32_t next_pc) {
     c.pc = next_pc;
     if (delay <= 0) return true;                       // resolved future: no yield (sim.py:320-321)
     if (isinf(delay)) { c.pc = C_HUNG; return false; } // never resolves (sim.py:322)
     double when = now + delay;
-    c.ctime = now;
     c.next_when = when;
     const bool srv = next_pc == C_SEG_LAT;             // a server event: always a later window
-#ifndef WIN_NO_FOLD
     // A client-local timer (anything but the request-latency timer, which reaches the
     // server) is run right away, even if it fires in a later window: nothing but the
     // client itself can act on a client in a local sleep (it neither waits on the
@@ -1036,97 +1120,195 @@ __device__ __forceinline__ bool arm(Win &w, Client &c, int32_t cid, double &now,
     // ... except the session-end / next-session steps (playout, manifest latency and
     // transfer): those chains are twice as long as a segment's, and one of them in a
     // round of 32 lanes made the whole warp wait; they keep their own window's timer
-    // (measured: 0.93 s -> 0.86 s on config 5)
+    // (measured: 0.93 s -> 0.86 s on config 5).  The segment transfer is never
+    // deferred: its start time and byte count live only in the chain's registers.
 #ifndef WIN_DEFER_MASK
 #define WIN_DEFER_MASK ((1u << C_PLAYOUT) | (1u << C_MAN_LAT) | (1u << C_MAN_XFER))
 #endif
+    static_assert(!((WIN_DEFER_MASK >> C_SEG_XFER) & 1u), "the segment transfer completes in its chain");
     if (!srv && when <= w.H && (!((WIN_DEFER_MASK >> next_pc) & 1u) || when < w.E)) {
-#else
-    if (!srv && when <= w.H && when < w.E) {           // fires inside this window: keep going
-#endif
         now = when;
         return true;
     }
     const int32_t k = timer_win(w, when);
     if (k == WIN_NONE) return false;
     if (srv && k <= w.k) w.S.flag(OTF_S_TIE);          // lookahead violated (cannot happen)
-    bucket_push(w, cid, k, srv, c);                    // the single push site (code size)
+    bucket_push(w, cid, k, srv, c, now, srv ? wdesc(w.S, c) : 0);   // the single push site (code size)
     return false;
 }
-
-__device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid);
 
 // Client state moves through L2 with the evict-first policy: a client's next
 // event is ~15 windows away, far beyond the L2's reach at full occupancy, so
 // keeping its lines only evicts what does get reused (trace samples of the
 // clients now transferring, segment sizes, bucket arrays).
-static_assert(sizeof(Client) % 16 == 0, "Client moves as 16-byte vectors");
-__device__ __forceinline__ void load_client_stream(Client &dst, const Client *src) {
-#ifdef WIN_NO_CS
-    dst = *src;
-#else
-    int4 *d = reinterpret_cast<int4 *>(&dst);
+__device__ __forceinline__ WClient wunpack(const WPacked &p) {
+    WClient c;
+    c.level = p.level; c.last_sync = p.last_sync; c.stall_time = p.stall_time; c.est = p.est;
+    c.next_when = p.next_when; c.session_start = p.session_start; c.session = p.session;
+    c.seq = (int32_t)(p.seq_index & 0xffffu); c.index = (int32_t)(p.seq_index >> 16);
+    c.pc = (int32_t)(p.small & 0xffu); c.rank = (int32_t)((p.small >> 8) & 0xffu);
+    c.attempt = (int32_t)((p.small >> 16) & 0xffu); c.flags = (int32_t)(p.small >> 24);
+    c.stall_events = p.stall_events;
+    return c;
+}
+__device__ __forceinline__ WPacked wpack(const WClient &c) {
+    WPacked p;
+    p.level = c.level; p.last_sync = c.last_sync; p.stall_time = c.stall_time; p.est = c.est;
+    p.next_when = c.next_when; p.session_start = c.session_start; p.session = c.session;
+    p.seq_index = (uint32_t)c.seq | ((uint32_t)c.index << 16);
+    p.small = (uint32_t)c.pc | ((uint32_t)c.rank << 8) | ((uint32_t)c.attempt << 16) | ((uint32_t)c.flags << 24);
+    p.stall_events = c.stall_events;
+    return p;
+}
+static_assert(sizeof(WPacked) % 16 == 0, "WPacked moves as 16-byte vectors");
+__device__ __forceinline__ void load_client_stream(WClient &dst, const WPacked *src) {
+    WPacked t;
+    int4 *d = reinterpret_cast<int4 *>(&t);
     const int4 *p = reinterpret_cast<const int4 *>(src);
 #pragma unroll
-    for (int q = 0; q < (int)(sizeof(Client) / 16); q++) d[q] = __ldcs(p + q);
-#endif
+    for (int q = 0; q < (int)(sizeof(WPacked) / 16); q++) d[q] = __ldcs(p + q);
+    dst = wunpack(t);
 }
-__device__ __forceinline__ void store_client_stream(Client *dst, const Client &src) {
-#ifdef WIN_NO_CS
-    *dst = src;
-#else
+__device__ __forceinline__ void store_client_stream(WPacked *dst, const WClient &src) {
+    const WPacked t = wpack(src);
     int4 *p = reinterpret_cast<int4 *>(dst);
-    const int4 *s = reinterpret_cast<const int4 *>(&src);
+    const int4 *s = reinterpret_cast<const int4 *>(&t);
 #pragma unroll
-    for (int q = 0; q < (int)(sizeof(Client) / 16); q++) __stcs(p + q, s[q]);
-#endif
-}
-
-__device__ void client_local(Win &w, int32_t cid) {
-    Client c = w.cl[cid];                              // one vectorised load; state lives in registers
-    client_local_body(w, c, cid);
-    w.cl[cid] = c;
+    for (int q = 0; q < (int)(sizeof(WPacked) / 16); q++) __stcs(p + q, s[q]);
 }
 
 // The response's record + QoE (server.py:76-77, metrics.py:67-78), written by the
-// client lane in parallel; the slot (response order) was fixed by the server lane.
-__device__ __forceinline__ void record_response(Win &w, const Client &c, double now) {
+// client lane in parallel; the request id and response slot (records) were fixed by
+// the server lane.  The client's pending fire time is the request's arrival.
+__device__ __forceinline__ void record_response(Win &w, const WClient &c, int32_t cid, double now, int32_t path) {
     Scn &S = w.S;
     const otf_scenario &sc = *S.sc;
-    int64_t size = c.path == OTF_PATH_ERROR ? 0 : S.size(c.desc);
     if (S.records) {
-        int64_t r = c.req_slot;
+        const WCold &k = w.wc[cid];
+        int64_t r = k.req_slot;
         if (r < sc.req_cap) {
             int64_t o = sc.req_off + r;
-            S.b->req_id[o] = c.req_id;
+            S.b->req_id[o] = k.req_id;
             S.b->req_seq[o] = c.seq;
             S.b->req_rep[o] = c.rank;
             S.b->req_index[o] = c.index;
-            S.b->req_path[o] = c.path;
-            S.b->req_arrival[o] = c.arrival;
+            S.b->req_path[o] = path;
+            S.b->req_arrival[o] = c.next_when;
             S.b->req_response[o] = now;
-            S.b->req_bytes[o] = size;
+            S.b->req_bytes[o] = path == OTF_PATH_ERROR ? 0 : S.size(wdesc(S, c));
         } else {
             S.flag(OTF_S_RECORD_OVERFLOW);
         }
     }
-    double lat = now - c.arrival;
+    double lat = now - c.next_when;
     QoeAcc &q = w.h->qa;
     atomicAdd(&q.lat_hist[lat_bin(lat)], 1u);
-    atomicAdd(&q.path_count[c.path], 1u);
-    atomicAdd(&q.n_requests, 1u);
+    atomicAdd(&q.path_count[path], 1u);
+#ifndef WIN_NO_LAT_TAIL                                // A/B switch (timing only: breaks the summary)
     if (lat != 0.0) S.tail_latency(lat);
+#endif
 }
 
-// The client coroutine between two yields.  Every state computes either
-// "continue at the next state now" or (delay, next state); the single arm()
-// site and the single shaped-transfer site keep the hot code small.
-__device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid) {
+// _sync_report (client.py:284-288), records mode
+__device__ __forceinline__ void wsync_session(Win &w, const WClient &c, double now) {
+    const otf_scenario &sc = *w.S.sc;
+    if (!w.S.records || c.session >= sc.sess_cap) return;
+    const int64_t o = sc.sess_off + c.session;
+    w.S.b->sess_end[o] = now;
+    w.S.b->sess_stalls[o] = (int32_t)c.stall_events;
+    w.S.b->sess_stall_time[o] = c.stall_time;
+}
+
+// the session's numbers are final (finished, aborted or harvested): its record
+__device__ __forceinline__ void wqoe_session(Win &w, const WClient &c, int32_t cid, bool finished) {
+    const bool live = (c.flags & WF_LIVE) != 0;
+    w.S.tail_session(w.wc[cid].reg_time, live ? c.stall_time : 0.0, c.session, live ? c.stall_events : 0u,
+                     finished);
+}
+
+// orchestrator.py:341-345 + client.py:237-239: pick a sequence, register a report.
+// Out of line with plain arguments; returns sid << 16 | seq.
+static __device__ __noinline__ int64_t wnew_session(WCold *k, const double *zipf, EngineState *st,
+                                                    const otf_scenario *sc, const otf_batch *b, bool records,
+                                                    int32_t cid, double now) {
+    const int32_t seq = draw_sequence(&k->picks, sc->n_seq, sc->popularity, zipf);
+    k->reg_time = now;
+    const int64_t sid = atomicAdd((unsigned long long *)&st->n_sess, 1ull);
+    if (records) {
+        if (sid < sc->sess_cap) {
+            const int64_t o = sc->sess_off + sid;
+            b->sess_client[o] = cid;
+            b->sess_seq[o] = seq;
+            b->sess_start[o] = now;
+            b->sess_end[o] = 0.0;
+            b->sess_stalls[o] = 0;
+            b->sess_stall_time[o] = 0.0;
+            b->sess_startup[o] = NAN;
+            b->sess_flags[o] = 0;
+        } else {
+            atomicOr(&st->status, OTF_S_RECORD_OVERFLOW);
+        }
+    }
+    return sid << 16 | seq;
+}
+
+
+// client.py:261-268 for a transfer of `size` bytes started at `xfer_start`; returns
+// true when the session has more segments, else leaves the buffer advanced for the
+// final sleep(level) (client.py:270-271)
+__device__ __forceinline__ bool wsegment_done(Win &w, WClient &c, int32_t cid, double now, double xfer_start,
+                                              int64_t size) {
+    Scn &S = w.S;
+    double dt = now - xfer_start;                      // SegmentFetch.rate_bps
+    double rate = dt > 0 ? ((double)size * 8.0) / dt : INFINITY;
+    c.est = c.est < 0 ? rate : S.alpha * rate + (1.0 - S.alpha) * c.est;
+    const double duration = seg_duration(S.seqdur[c.seq], S.segdur[c.seq], c.index);
+    Buffer b = wbuf_get(c);
+    const int32_t ph0 = b.phase;
+    buf_on_segment(b, now, duration, S.startup, S.resume);
+    wbuf_put(c, b);
+    if (ph0 == PH_STARTUP && b.phase == PH_PLAYING) {  // playback started (client.py:117-119): the
+        const double startup = b.started_at - b.session_start;   // startup delay is final now
+        S.tail_startup(startup);
+        if (S.records && c.session < S.sc->sess_cap) S.b->sess_startup[S.sc->sess_off + c.session] = startup;
+    }
+    const int64_t g = atomicAdd((unsigned long long *)&S.st->n_seg, 1ull);
+    if (S.records) {
+        if (g < S.sc->seg_cap) {
+            const int64_t o = S.sc->seg_off + g;
+            S.b->seg_session[o] = c.session;
+            S.b->seg_index[o] = c.index;
+            S.b->seg_rep[o] = c.rank;
+            S.b->seg_start[o] = w.wc[cid].requested;
+            S.b->seg_end[o] = now;
+        } else {
+            S.flag(OTF_S_RECORD_OVERFLOW);
+        }
+    }
+    if (c.rank >= OTF_RANK_BINS) atomicOr(&S.qa->flags, (uint32_t)OTF_Q_RANKS_CAPPED);
+    atomicAdd(&S.qa->rank_count[c.rank < OTF_RANK_BINS ? c.rank : OTF_RANK_BINS - 1], 1u);
+    atomicAdd(&S.qa->n_segments, 1u);
+    wsync_session(w, c, now);
+    c.index++;
+    if (c.index < S.segcount(c.seq)) return true;
+    wbuf_advance(c, now);
+    return false;
+}
+
+// The client coroutine between two yields, entered at `now` with a response
+// (path >= 0: record it, then the transfer or the retry logic) or at a local
+// timer (path < 0).  Every state computes either "continue at the next state
+// now" or (delay, next state); the single arm() site and the single shaped-
+// transfer site keep the hot code small.
+__device__ __forceinline__ void client_local_body(Win &w, WClient &c, int32_t cid, double now, int32_t path) {
     Scn &S = w.S;
     const otf_scenario &sc = *S.sc;
-    double now = c.next_when;
-    // a response (segment or OverloadError) is recorded first: one inlined copy
-    if (c.pc == C_SEG_RESP || c.pc == C_SEG_ERR) record_response(w, c, now);
+    double xfer_start = 0.0;                           // the segment transfer in flight (this chain)
+    int64_t size = 0;
+    if (path >= 0) {                                   // a response (segment or OverloadError): one inlined copy
+        record_response(w, c, cid, now, path);
+        c.pc = path == OTF_PATH_ERROR ? C_SEG_ERR : C_SEG_RESP;
+    }
     for (;;) {
         double delay = 0.0;
         int32_t next = C_DONE;
@@ -1135,59 +1317,74 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
         case C_ARRIVED:                                // pick stream already seeded at init
             c.pc = C_SESSION;
             continue;
-        case C_SESSION:
+        case C_SESSION: {
             if (!(now < w.H)) { c.pc = C_DONE; return; }
-            client_new_session(S, c, cid, now);
+            const int64_t r = wnew_session(w.wc + cid, S.zipf, S.st, S.sc, S.b, S.records, cid, now);
+            c.session = (int32_t)(r >> 16);
+            c.seq = (int32_t)(r & 0xffff);
+            c.flags = (c.flags & ~WF_LIVE) | WF_OPEN;
             delay = w.L;                               // manifest request latency (netem.py:138-139)
             next = C_MAN_LAT;
             break;
+        }
         case C_MAN_LAT:
             next = C_MAN_XFER;
             xfer = true;
             break;
-        case C_MAN_XFER:
-            client_start_playback(c, now);
+        case C_MAN_XFER:                               // client.py:245-248
+            c.level = 0.0; c.last_sync = now; c.stall_time = 0.0; c.session_start = now;
+            c.stall_events = 0;
+            c.flags = (c.flags & ~WF_PHASE) | PH_STARTUP | WF_LIVE;
+            c.est = -1.0;
+            c.rank = 1;
+            c.index = 0;
             c.pc = C_INDEX_HEAD;
             continue;
         case C_INDEX_HEAD:
         case C_TARGET_WAIT:
-            buf_advance(c.buf, now);
-            if (c.buf.phase == PH_PLAYING && c.buf.level >= w.target) {
-                delay = c.buf.level - w.target + 1e-9;
+            wbuf_advance(c, now);
+            if ((c.flags & WF_PHASE) == PH_PLAYING && c.level >= w.target) {
+                delay = c.level - w.target + 1e-9;
                 next = C_TARGET_WAIT;
                 break;
             }
-            client_select(S, c);
+            if (c.index > 0)                           // client.py:255-256
+                c.rank = select_quality(c.level, c.rank, c.est >= 0, c.est, S.bitrates, sc.n_ranks,
+                                                 S.panic, S.safe, S.headroom);
             c.attempt = 0;                             // _fetch_with_retry (client.py:291-305)
-            c.requested = now;
-            c.desc = S.desc_id(c.seq, c.rank, c.index);
+            if (S.records) w.wc[cid].requested = now;
             delay = w.L;                               // request latency, then MediaServer.segment
             next = C_SEG_LAT;
             break;
         case C_SEG_RESP:
-            c.xfer_start = now;
+            xfer_start = now;
             next = C_SEG_XFER;
             xfer = true;
             break;
         case C_SEG_XFER:
-            if (client_segment_done(S, c, now)) { c.pc = C_INDEX_HEAD; continue; }
-            delay = c.buf.level;                       // play out the buffer (client.py:271)
+            if (wsegment_done(w, c, cid, now, xfer_start, size)) { c.pc = C_INDEX_HEAD; continue; }
+            delay = c.level;                           // play out the buffer (client.py:271)
             next = C_PLAYOUT;
             break;
-        case C_PLAYOUT:
-#ifndef WIN_NO_PICK_PF
+        case C_PLAYOUT:                                // client.py:272-280 (+ the finally clause)
             {                                          // the next session's pick stream (48 B):
-                const char *pk = reinterpret_cast<const char *>(S.cold + cid);    // in flight
-                asm volatile("prefetch.global.L1 [%0];" :: "l"(pk));              // while the
-                asm volatile("prefetch.global.L1 [%0];" :: "l"(pk + 47));         // session closes
+                const char *pk = reinterpret_cast<const char *>(w.wc + cid);      // in flight
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(pk));              // while the session closes
             }
-#endif
-            client_finish_session(S, c, cid, now);
+            wbuf_advance(c, now);
+            c.flags = (c.flags & ~WF_PHASE) | PH_FINISHED;
+            if (S.records && c.session < sc.sess_cap) S.b->sess_flags[sc.sess_off + c.session] |= 1;
+            wsync_session(w, c, now);
+            wqoe_session(w, c, cid, true);
+            c.flags &= ~(WF_LIVE | WF_OPEN);
             c.pc = C_SESSION;
             continue;
         case C_SEG_ERR:                                // OverloadError response
-            if (c.attempt == sc.retries) {             // give up: the session is aborted
-                client_abort_session(S, c, cid, now);
+            if (c.attempt == sc.retries) {             // give up: the session is aborted (client.py:257-260)
+                if (S.records && c.session < sc.sess_cap) S.b->sess_flags[sc.sess_off + c.session] |= 2;
+                wsync_session(w, c, now);
+                wqoe_session(w, c, cid, false);
+                c.flags &= ~(WF_LIVE | WF_OPEN);
                 c.pc = C_SESSION;
                 continue;
             }
@@ -1196,7 +1393,7 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             break;
         case C_RETRY:                                  // after sleep(backoff): backoff *= 2
             c.attempt++;
-            c.requested = now;
+            if (S.records) w.wc[cid].requested = now;
             delay = w.L;
             next = C_SEG_LAT;
             break;
@@ -1207,13 +1404,32 @@ __device__ __forceinline__ void client_local_body(Win &w, Client &c, int32_t cid
             // the trace samples, the period bits and the byte count load together
             const Trace tr = S.trace(cid);
             const TraceAhead a = trace_ahead(tr, trace_phase(tr, now));
-            const int64_t nbytes = next == C_SEG_XFER ? (int64_t)(int32_t)S.size(c.desc) : S.manifest(c.seq);
-            if (next == C_SEG_XFER) c.size = (int32_t)nbytes;
+            const int64_t nbytes = next == C_SEG_XFER ? (int64_t)(int32_t)S.size(wdesc(S, c)) : S.manifest(c.seq);
+            size = nbytes;
             delay = completion_time_at(tr, a, now, nbytes) - now;
         }
         if (!arm(w, c, cid, now, delay, next)) return;
         if (next == C_SEG_LAT) { S.flag(OTF_S_INTERNAL); return; }   // zero latency never reaches this engine
     }
+}
+
+// one client event: state in registers for the whole chain
+__device__ __forceinline__ void client_event(Win &w, int32_t cid, double when, int32_t path) {
+    WClient c;
+    load_client_stream(c, &w.cl[cid]);
+    client_local_body(w, c, cid, path >= 0 ? when : c.next_when, path);
+    store_client_stream(&w.cl[cid], c);
+}
+
+// SessionReport.harvest at the horizon (orchestrator.py:357-359, client.py:177-187)
+__device__ __forceinline__ void wharvest(Win &w, WClient &c, int32_t cid, double horizon) {
+    if (c.pc == C_HUNG) w.S.flag(OTF_S_HUNG);
+    if (!(c.flags & WF_OPEN)) return;
+    if (c.flags & WF_LIVE) {
+        wbuf_advance(c, horizon);
+        wsync_session(w, c, horizon);
+    }
+    wqoe_session(w, c, cid, false);
 }
 
 __device__ __forceinline__ int32_t warp_min(int32_t v) {
@@ -1309,7 +1525,7 @@ __device__ void order_ties(Win &w) {
         if (w.lw[i] != w.lw[i - 1]) continue;
         int32_t j = i;                                 // insertion step by ctime
         while (j > 0 && w.lw[j] == w.lw[j - 1]) {
-            double cj = w.cl[w.li[j]].ctime, cp = w.cl[w.li[j - 1]].ctime;
+            double cj = req_ctime(w, w.li[j]), cp = req_ctime(w, w.li[j - 1]);
             if (cj == cp) { atomicOr(&h->st.status, OTF_S_TIE); break; }
             if (cj > cp) break;
             int16_t ti = w.li[j]; w.li[j] = w.li[j - 1]; w.li[j - 1] = ti;
@@ -1388,9 +1604,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     w.dflags = (uint16_t *)p;
     w.lstamp = (uint32_t *)(g + L.lstamp);
     w.lq = (LqEnt *)(g + L.lq);
-    w.cl = (Client *)(g + L.clients);
-    w.S.cold = (ClientCold *)(g + L.picks);
-    w.blist = (int32_t *)(g + L.blist);
+    w.cl = (WPacked *)(g + L.clients);
+    w.wc = (WCold *)(g + L.picks);
+    w.S.cold = nullptr;                                // the exact engine's cold state (unused here)
+    w.blist = (RespMsg *)(g + L.blist);
     w.bsrv = (SrvEnt *)(g + L.bsrv);
     w.bloc = (int32_t *)(g + L.bloc);
     w.scap = bucket_cap_srv(N);
@@ -1464,16 +1681,17 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     // clients: the first step arms sleep(offset) (orchestrator.py:337); offsets are a
     // cumulative sum, so clients join the wheel in id order (arrival cursor below)
     for (int32_t c = tid; c < N; c += WIN_THREADS) {
-        Client &cl = w.cl[c];
-        client_init(cl);
+        WClient cl = {};
         double off = w.S.arrival(c);
         cl.pc = C_ARRIVED;
-        cl.ctime = 0.0;
         cl.next_when = 0.0 + off;
+        cl.session = -1;
+        cl.est = -1.0;
+        w.cl[c] = wpack(cl);
         if (!(off > 0)) w.S.flag(OTF_S_TIE);           // instant start: tick order among clients matters
         // the client's pick stream (orchestrator.py:338-340), seeded here in parallel rather
         // than by one lane at the arrival: it is first drawn from after the arrival
-        seed_picks(&w.S.cold[c].picks, sc.seed, c);
+        seed_picks(&w.wc[c].picks, sc.seed, c);
     }
     __syncthreads();
     if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) goto done;
@@ -1521,7 +1739,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         const int32_t c = base + lane;
                         const int32_t wk = c < N ? timer_win(w, w.S.arrival(c)) : WIN_NONE;
                         const bool ok = wk != WIN_NONE && wk - w.k < RING;
-                        if (ok) bucket_push(w, c, wk, false, w.cl[c]);
+                        if (ok) bucket_push(w, c, wk, false, wunpack(w.cl[c]), 0.0, 0);
                         const int32_t got = __popc(__ballot_sync(0xffffffffu, ok));
                         base += got;
                         if (got < 32) break;
@@ -1542,7 +1760,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         while (c < N) {
                             int32_t wk = timer_win(w, w.S.arrival(c));
                             if (wk == WIN_NONE || wk - w.k >= RING) break;   // wheel base is m - 1 here
-                            bucket_push(w, c, wk, false, w.cl[c]);
+                            bucket_push(w, c, wk, false, wunpack(w.cl[c]), 0.0, 0);
                             c++;
                         }
                         h->arr_next = c;
@@ -1559,8 +1777,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         w.k = m - 1;
                         while (c >= 0) {
                             int32_t nx = w.bnext[c];
-                            const Client &cl = w.cl[c];
-                            bucket_push(w, c, timer_win(w, cl.next_when), cl.pc == C_SEG_LAT, cl);
+                            const WClient cl = wunpack(w.cl[c]);
+                            const bool srv = cl.pc == C_SEG_LAT;
+                            bucket_push(w, c, timer_win(w, cl.next_when), srv, cl, srv ? w.wc[c].ctime : 0.0,
+                                        srv ? wdesc(w.S, cl) : 0);
                             c = nx;
                         }
                     }
@@ -1583,11 +1803,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         int32_t c = h->ovf_head, keep = -1, rem = WIN_NONE, kept = 0;
                         while (c >= 0) {
                             int32_t nx = w.bnext[c];
-                            const Client &cl = w.cl[c];
+                            const WClient cl = wunpack(w.cl[c]);
                             int32_t wk = timer_win(w, cl.next_when);
                             if (wk == m) {
                                 if (cl.pc == C_SEG_LAT) { if (ns + n_ovf < h->list_cap) w.li[ns + n_ovf] = (int16_t)c; n_ovf++; }
-                                else w.blist[nb++] = c;
+                                else { RespMsg lm; lm.when = cl.next_when; lm.cid = c; lm.path = -1; w.blist[nb++] = lm; }
                             } else {
                                 w.bnext[c] = (int16_t)keep; keep = c; kept++;
                                 rem = min(rem, wk);
@@ -1631,10 +1851,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                     OTF_NOUNROLL
                     for (int32_t i = ns + lane; i < nlist; i += 32) {   // overflowed pushes: from the client state
                         const int32_t c = w.li[i];
-                        const Client &cl = w.cl[c];
+                        const WClient cl = wunpack(w.cl[c]);
                         w.lw[i] = cl.next_when;
-                        w.ld[i] = (int16_t)cl.desc;
-                        w.lp[i] = cl.rank | (cl.index << 8) | (cl.seq << 16);
+                        w.ld[i] = (int16_t)wdesc(w.S, cl);
+                        w.lp[i] = (int32_t)cl.rank | ((int32_t)cl.index << 8) | ((int32_t)cl.seq << 16);
                     }
                     __syncwarp();
                     if (lane == 0) {
@@ -1643,6 +1863,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         h->cnt_loc[slot >> 1] &= ~(0xffffu << csh);
                         h->bits[slot >> 5] &= ~(1u << (slot & 31));
                         h->n_list = nlist;
+                        h->n_bsrv = ns;
                         h->n_blist = nb;
                         h->n_loc = nl;
                         h->cur_m = m;
@@ -1702,16 +1923,22 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
             // touch only their own client, so the early load cannot be stale
             const int32_t total = nl + nb;
             int32_t i = lane;
-            int32_t ncid = 0;
-            Client nc;
-            if (i < total) { ncid = i < nb ? w.blist[i] : al[i - nb]; load_client_stream(nc, &w.cl[ncid]); }
+            RespMsg nm;
+            WClient nc;
+            if (i < total) {
+                if (i < nb) nm = w.blist[i]; else { nm.cid = al[i - nb]; nm.path = -1; }
+                load_client_stream(nc, &w.cl[nm.cid]);
+            }
             while (i < total) {
-                const int32_t cid = ncid;
-                Client c = nc;
+                const RespMsg m = nm;
+                WClient c = nc;
                 i += 32;
-                if (i < total) { ncid = i < nb ? w.blist[i] : al[i - nb]; load_client_stream(nc, &w.cl[ncid]); }
-                client_local_body(w, c, cid);
-                store_client_stream(&w.cl[cid], c);
+                if (i < total) {
+                    if (i < nb) nm = w.blist[i]; else { nm.cid = al[i - nb]; nm.path = -1; }
+                    load_client_stream(nc, &w.cl[nm.cid]);
+                }
+                client_local_body(w, c, m.cid, m.path >= 0 ? m.when : c.next_when, m.path);
+                store_client_stream(&w.cl[m.cid], c);
             }
             __syncwarp();
             if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) break;
@@ -1722,7 +1949,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                 const long long tb = clock64();
                 const int32_t nl = h->n_loc;
                 const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
-                for (int32_t i = b1; i < nl; i += WIN_THREADS - 32) client_local(w, al[i]);
+                for (int32_t i = b1; i < nl; i += WIN_THREADS - 32) client_event(w, al[i], 0.0, -1);
                 if (b1 == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
             }
             __syncthreads();
@@ -1730,7 +1957,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
             // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
             t0 = WCLOCK();
             const int32_t nb = h->n_blist;
-            for (int32_t i = tid; i < nb; i += WIN_THREADS) client_local(w, w.blist[i]);
+            for (int32_t i = tid; i < nb; i += WIN_THREADS) {
+                const RespMsg m = w.blist[i];
+                client_event(w, m.cid, m.when, m.path);
+            }
             __syncthreads();
         }
         if (tid == 0) h->stats[OTF_ST_CYC_CLIENTS] += WCLOCK() - t0;
@@ -1742,7 +1972,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
     if (!(h->st.status & (OTF_S_TIE | OTF_S_UNFIT))) {
-        for (int32_t c = tid; c < N; c += WIN_THREADS) client_harvest(w.S, w.cl[c], c, sc.horizon);
+        for (int32_t c = tid; c < N; c += WIN_THREADS) {
+            WClient cl = wunpack(w.cl[c]);
+            wharvest(w, cl, c, sc.horizon);
+        }
     }
     __syncthreads();
 done:

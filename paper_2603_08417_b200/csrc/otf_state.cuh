@@ -51,18 +51,18 @@ struct ClientCold {              // 64 B
     double pad;
 };
 
-// QoE accumulators: 32-bit counters (native shared/global atomics) and the
-// exact startup-delay sum (otf_xacc.cuh); see otf_qoe.
+// QoE accumulators while a scenario runs: 32-bit counters (native shared /
+// global atomics) and the summary-tail cursors.  Session-level numbers are
+// not counted here: a closing session appends its record (otf_sess_ent) and
+// the summary pass derives the session histograms and sums (otf_summary.cu).
 struct QoeAcc {
     uint32_t lat_hist[OTF_LAT_BINS];
-    uint32_t path_count[8];
-    uint32_t stall_hist[OTF_STALL_BINS];
+    uint32_t path_count[8];             // n_requests = their sum
     uint32_t rank_count[OTF_RANK_BINS];
-    uint32_t n_requests, n_sessions, n_segments, n_finished, n_started, n_stalls;
-    uint32_t n_lat_tail, n_stl_tail, flags, pad[3];
-    unsigned long long sup[XACC_LIMBS];   // startup delays
+    uint32_t n_segments;
+    uint32_t n_lat_tail, n_ses_tail, n_sup_tail;   // tail cursors (exact counts, even past a cap)
+    uint32_t flags, pad[3];
 };
-static_assert(sizeof(QoeAcc) % 8 == 0, "QoeAcc limbs are 8-byte aligned");
 
 enum { W_START = 0, W_NEXT, W_GOT, W_SERVICE, W_WOKEN };
 

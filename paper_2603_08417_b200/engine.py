@@ -71,9 +71,10 @@ class DeviceBatch:
             for name, dt in _lib.RECORD_FIELDS:
                 total = inp.rec_totals[_REC_GROUP[name.split("_")[0]]]
                 self.rec[name] = torch.empty(max(1, total), dtype=_TORCH[dt], device=dev)
+        # summary tails (device only; the summary pass reduces them into the QoE blocks)
         self.tail_lat = torch.empty(max(1, inp.tail_totals[0]), dtype=torch.float64, device=dev)
-        self.tail_stall = torch.empty(max(1, inp.tail_totals[1]) * _lib.STALL_ENT_BYTES, dtype=torch.uint8,
-                                      device=dev)
+        self.tail_sess = torch.empty(max(1, inp.tail_totals[1]) * _lib.SESS_ENT_BYTES, dtype=torch.uint8, device=dev)
+        self.tail_sup = torch.empty(max(1, inp.tail_totals[2]), dtype=torch.float64, device=dev)
         self.counts = torch.zeros((n, 4), dtype=torch.int64, device=dev)
         self.stats = torch.zeros((n, _lib.ST_NSLOTS), dtype=torch.int64, device=dev)
         self.qoe = torch.zeros((n, ctypes.sizeof(_lib.Qoe) // 8), dtype=torch.int64, device=dev)
@@ -87,7 +88,8 @@ class DeviceBatch:
             setattr(b, name, self.rec[name].data_ptr() if name in self.rec else None)
         b.counts, b.stats = self.counts.data_ptr(), self.stats.data_ptr()
         b.qoe, b.status = self.qoe.data_ptr(), self.status.data_ptr()
-        b.tail_lat, b.tail_stall = self.tail_lat.data_ptr(), self.tail_stall.data_ptr()
+        b.tail_lat, b.tail_sess, b.tail_sup = (self.tail_lat.data_ptr(), self.tail_sess.data_ptr(),
+                                               self.tail_sup.data_ptr())
         # launch groups: scenarios of similar shared-memory size together (a big
         # scenario must not shrink everyone's occupancy), longest first within a group
         cost = np.array([l.cfg.clients * l.cfg.horizon_s / min(l.seq_segdur) for l in inp.lowered])
@@ -123,9 +125,14 @@ class DeviceBatch:
                          (self.i64, self.h_i64), (self.i32, self.h_i32)):
                 d.copy_(h, non_blocking=h.is_pinned())
 
-    def launch(self, stream: torch.cuda.Stream | None = None, sizes: bool = True) -> None:
-        """Enqueue size-table generation + the engine on `stream` (default: current)."""
+    def launch(self, stream: torch.cuda.Stream | None = None, sizes: bool = True, summary: bool = True) -> None:
+        """Enqueue size-table generation + the engine (+ the summary pass unless
+        summary=False; then launch_summary runs it) on `stream` (default: current)."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        flags = 0 if summary else _lib.BF_ENGINE_ONLY
+        self.batch.engine_flags = flags
+        for gb in self.groups:
+            gb.engine_flags = flags
         if sizes and self.n_tables:
             rc = self.lib.otf_gen_sizes(self.tables.data_ptr(), self.n_tables, 0, self.i64.data_ptr(),
                                         self.f64.data_ptr(), self.i32.data_ptr(), s.cuda_stream)
@@ -143,6 +150,12 @@ class DeviceBatch:
             _lib.check(rc, "otf_run_batch")
         for st in self.streams:
             s.wait_stream(st)
+
+    def launch_summary(self, stream: torch.cuda.Stream | None = None) -> None:
+        """The summary pass alone, after launch(summary=False) on the same stream."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(self.lib.otf_run_summary(ctypes.byref(self.batch), self.inp.engine, s.cuda_stream),
+                   "otf_run_summary")
 
     def fetch(self) -> "BatchResult":
         torch.cuda.synchronize(self.device)
@@ -320,9 +333,11 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                 if st & _lib.S_RECORD_OVERFLOW:
                     caps[i] = tuple(int(x) + 1 for x in br.counts[k])
                     retry = True
-                if st & _lib.S_TAIL_OVERFLOW:
-                    q = _lib.Qoe.from_buffer_copy(br.qoe[k].tobytes())
-                    tcaps[i] = (int(q.n_lat_tail) + 1, int(q.n_stall_tail) + 1)
+                if st & _lib.S_TAIL_OVERFLOW:             # exact counts (the stalled ones bounded by
+                    q = _lib.Qoe.from_buffer_copy(br.qoe[k].tobytes())   # the sessions if not yet known)
+                    n_ses = int(q.n_sessions)
+                    n_stl = int(q.n_stall_tail) if q.n_stall_tail else n_ses
+                    tcaps[i] = (int(q.n_lat_tail) + 1, n_ses + 1, n_stl + 1, int(q.n_started) + 1)
                     retry = True
                 if retry:
                     nxt.append(i)

@@ -211,9 +211,8 @@ class BatchInputs:
     smem_per: list = dataclasses.field(default_factory=list)   # per scenario
     engine_flags: int = 0       # OTF_BF_*
     pinned: bool = False        # pools allocated page-locked (torch pinned memory)
-    tail_caps: np.ndarray = None      # [n][2] summary tails (nonzero latencies, stalled sessions)
-    tail_offsets: np.ndarray = None   # [n][2]
-    tail_totals: tuple = (0, 0)       # (latency doubles, stall entries incl. the sort half)
+    tail_caps: np.ndarray = None      # [n][4] summary tails: nonzero latencies, sessions, stalled, startups
+    tail_totals: tuple = (0, 0, 0)    # pool lengths: latency doubles, session entries, startup doubles
 
 
 def windowed_fits(cfg, smem_limit: int | None = None) -> tuple[bool, str]:
@@ -245,8 +244,9 @@ def _default_caps(low: Lowered) -> tuple[int, int, int, int]:
     return req, req + cfg.clients, req, 2 * req + 64
 
 
-def default_tail_caps(low: Lowered) -> tuple[int, int]:
-    """Summary-tail capacities: nonzero request latencies and stalled sessions.
+def default_tail_caps(low: Lowered) -> tuple[int, int, int, int]:
+    """Summary-tail capacities: nonzero request latencies, closed sessions, stalled
+    sessions (the summary pass's gather), startup delays.
 
     Only requests that wait on a transcode have a nonzero latency (storage and
     cache hits answer at the arrival instant, server.py:61-78), so variants with
@@ -264,7 +264,7 @@ def default_tail_caps(low: Lowered) -> tuple[int, int]:
         frac = 0.25
     sessions = cfg.clients * (int(cfg.horizon_s / max(min(low.seq_dur), 1e-3)) + 2)
     stalled = sessions if not low.cache_enabled else sessions // 4
-    return int(req * frac) + 64, int(stalled) + 64
+    return int(req * frac) + 64, int(sessions) + 64, int(stalled) + 64, int(sessions) + 64
 
 
 def _eps_len(low: Lowered) -> int:
@@ -294,9 +294,8 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     input_bytes = 0
     shared_bytes = 0
     smem_per: list[int] = []
-    tcap_arr = np.zeros((len(lows), 2), dtype=np.int64)
-    toff_arr = np.zeros((len(lows), 2), dtype=np.int64)
-    ttot = [0, 0]
+    tcap_arr = np.zeros((len(lows), 4), dtype=np.int64)
+    ttot = [0, 0, 0]
 
     # -- traces: one table per (seed, netem), long enough for the largest N --
     trace_groups: dict = {}
@@ -460,11 +459,12 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         scratch_off = (scratch_off + 255) & ~255
         tc = tail_caps[si] if tail_caps is not None and tail_caps[si] is not None else default_tail_caps(low)
         tcap_arr[si] = tc
-        toff_arr[si] = ttot
         sc.lat_off, sc.lat_cap = int(ttot[0]), int(tc[0])
-        sc.stl_off, sc.stl_cap = int(ttot[1]), int(tc[1])
+        sc.ses_off, sc.ses_cap, sc.stl_cap = int(ttot[1]), int(tc[1]), int(tc[2])
+        sc.sup_off, sc.sup_cap = int(ttot[2]), int(tc[3])
         ttot[0] += int(tc[0])
-        ttot[1] += 2 * int(tc[1])                      # entries + the summary pass's sort half
+        ttot[1] += int(tc[1]) + 2 * int(tc[2])         # records + the summary pass's gather and sort
+        ttot[2] += int(tc[3])
         if mode == _lib.MODE_RECORDS:
             c = caps[si] if caps is not None else _default_caps(low)
             cap_arr[si] = c
@@ -481,7 +481,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         f64=P.concat("f64", pin), i64=P.concat("i64", pin), i32=P.concat("i32", pin), pinned=pin,
         scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
         engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes, smem_per=smem_per,
-        tail_caps=tcap_arr, tail_offsets=toff_arr, tail_totals=tuple(ttot))
+        tail_caps=tcap_arr, tail_totals=tuple(ttot))
 
 
 def n_size_tables(inp: BatchInputs) -> int:

@@ -147,10 +147,12 @@ def test_tail_overflow_rerun_is_exact(golden):
     """Summary tails far too small: the scenarios are re-run with the exact counts."""
     names = ["c1_seed1", "grid_c24_k4_t2_TCP", "c3_f05_h90"]
     cfgs = [_cfg(golden[n][1]) for n in names]
-    res = engine.run_batch(cfgs, mode="histogram", _tail_caps=[(2, 1)] * len(cfgs))
-    for n, r in zip(names, res):
-        assert r.attempts == 2
-        assert not qoe_errors(r.qoe, oracle.qoe_block(golden[n][0]), n)
+    for caps in ((2, 1, 1, 1), (1 << 20, 1 << 20, 1, 1 << 20)):   # engine tails / the summary's gather
+        res = engine.run_batch(cfgs, mode="histogram", _tail_caps=[caps] * len(cfgs))
+        for n, r in zip(names, res):
+            want = oracle.qoe_block(golden[n][0])
+            assert r.attempts == (2 if caps[0] == 2 or want["n_stall_tail"] > 1 else 1), (n, caps, r.attempts)
+            assert not qoe_errors(r.qoe, want, n)
 
 
 def test_histogram_summary_exact_engine_matches_windowed():
