@@ -65,25 +65,40 @@ def dist_env():
 
 # ---------------------------------------------------------------- CPU reference
 def _oracle_one(cfg):
+    """One scenario on the oracle: (requests, run seconds, digest).  The digest
+    is what the run already produced (record counts, the backend/cache stats
+    row, the response paths), so checking it costs the timing nothing."""
     sys.path.insert(0, ROOT)
+    import numpy as np
     from oracle import oracle
     t0 = time.perf_counter()
     res = oracle.run(cfg)
-    return int(res["n_req"]), time.perf_counter() - t0
+    dt = time.perf_counter() - t0
+    digest = ([int(res[k]) for k in ("n_req", "n_sess", "n_seg", "n_job")] + [int(x) for x in res["stats"][:18]]
+              + [int(x) for x in np.bincount(res["req_path"], minlength=5)[:5]])
+    return int(res["n_req"]), dt, digest
+
+
+def gpu_digest(br, k: int) -> list[int]:
+    """The same digest from a GPU histogram-mode result row."""
+    return ([int(x) for x in br.counts[k]] + [int(x) for x in br.stats[k][:18]]
+            + [int(x) for x in br.qoe[k][64:69]])     # otf_qoe.path_count[0..5) follows lat_hist[64]
 
 
 def cpu_reference(cfgs, budget_s: float, cores: int):
     """The reference algorithm on host cores: the C oracle (a restatement of
     run_experiment; the Python reference itself cannot travel to the box), one
-    scenario per process, all cores.  Returns (req/s, cores, sample description)."""
+    scenario per process, all cores.  Returns (req/s, cores, sample description,
+    {scenario index: digest})."""
     from oracle import oracle
     oracle.build()
-    n_req, dt = _oracle_one(cfgs[0])                   # calibrate one scenario
+    n_req, dt, _ = _oracle_one(cfgs[0])                # calibrate one scenario
     per = max(dt, 1e-3)
     n = max(cores, min(len(cfgs), int(budget_s * cores / per)))
     n = min(n, len(cfgs))
     step = max(1, len(cfgs) // n)
-    sample = cfgs[::step][:n]
+    idx = list(range(0, len(cfgs), step))[:n]
+    sample = [cfgs[i] for i in idx]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(cores) as pool:
@@ -91,7 +106,7 @@ def cpu_reference(cfgs, budget_s: float, cores: int):
     wall = time.perf_counter() - t0
     reqs = sum(o[0] for o in out)
     return reqs / wall, cores, f"{len(sample)} of {len(cfgs)} scenarios (every {step}th), {reqs} requests, " \
-                               f"{wall:.1f} s wall on {cores} processes"
+                               f"{wall:.1f} s wall on {cores} processes", {i: o[2] for i, o in zip(idx, out)}
 
 
 # ---------------------------------------------------------------- clocks
@@ -144,9 +159,13 @@ def main():
     ap.add_argument("--workload", default="c5")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work for the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs a full sweep of its own seeds; strong: the one sweep "
+                         "(BASELINE config 5's 1,024 scenarios) is sharded over the ranks by seed group")
     args = ap.parse_args()
     rank, world, local = dist_env()
-    cfgs, desc = workload(args.workload, 0 if args.impl == "reference" else rank)
+    strong = args.scaling == "strong"
+    cfgs, desc = workload(args.workload, 0 if (args.impl == "reference" or strong) else rank)
     cores = os.cpu_count() or 1
 
     if args.impl == "reference":
@@ -156,7 +175,7 @@ def main():
         vals = []
         info = None
         for i in range(args.warmup + args.steps):
-            v, c, sample = cpu_reference(cfgs, budget, cores)
+            v, c, sample, _ = cpu_reference(cfgs, budget, cores)
             if i >= args.warmup:
                 vals.append(v)
                 info = (c, sample)
@@ -182,7 +201,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
-    my_cfgs = cfgs                                             # weak scaling: a full sweep per rank
+    from paper_2603_08417_b200 import dist as odist
+    if strong:                                                 # this rank's seed groups of the one sweep
+        my_cfgs = [cfgs[i] for i in odist.shard(cfgs, rank, world)]
+    else:
+        my_cfgs = cfgs                                         # weak scaling: a full sweep per rank
 
     t_build = time.perf_counter()
     inp = inputs.build_inputs(my_cfgs, engine=_lib.ENGINE_WINDOWED, mode=_lib.MODE_HISTOGRAM, pin=True)
@@ -199,11 +222,10 @@ def main():
         exact_inp = inputs.build_inputs([my_cfgs[i] for i in flagged], engine=_lib.ENGINE_EXACT,
                                         mode=_lib.MODE_HISTOGRAM, eps_scale=4)
         exact_db = engine.DeviceBatch(exact_inp, dev, pin=True)
-    launches_per_step = 1 + len(db.groups) + 1 + (3 if exact_db is not None else 0)   # sizes, engine groups, summary
+    launches_per_step = (int(db.n_gen > 0) + int(db.n_tables > 0) + len(db.groups) + 1   # generators, engine groups,
+                         + (4 if exact_db is not None else 0))                          # summary
     inp_h2d = db.h2d_bytes + (exact_db.h2d_bytes if exact_db is not None else 0)
     q_rows = db.qoe.shape[1]
-
-    from paper_2603_08417_b200 import dist as odist
 
     def gather_qoe():                                          # the one collective: QoE blocks to every rank
         return odist.gather_blocks(db.qoe, world)
@@ -233,11 +255,9 @@ def main():
     t0.record(stream)
     for k in range(args.steps):
         evs[k][0].record(stream)
-        # sizes kernel, then the engine alone between events
-        if db.n_tables:
-            rc = db.lib.otf_gen_sizes(db.tables.data_ptr(), db.n_tables, 0, db.i64.data_ptr(),
-                                      db.f64.data_ptr(), db.i32.data_ptr(), stream.cuda_stream)
-            _lib.check(rc, "otf_gen_sizes")
+        # request generation (seeded trace / arrival / noise streams, segment sizes),
+        # then the engine alone between events
+        db.generate(stream)
         eng_evs[k][0].record(stream)
         db.launch(stream, sizes=False, summary=False)
         eng_evs[k][1].record(stream)
@@ -262,6 +282,7 @@ def main():
         ebr = exact_db.fetch()
         my_req += int(ebr.counts[:, 0].sum()) - int(br.counts[flagged, 0].sum())
     if world > 1:
+        import torch.distributed as dist
         elapsed_ms = odist.all_max(elapsed_ms, dev)
         total_req = odist.all_sum(float(my_req), dev)
         eng_ms_max = odist.all_max(statistics.mean(eng_ms), dev)
@@ -314,18 +335,27 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        v, c, sample = cpu_reference(cfgs, args.cpu_budget, cores)
-        cpu = {"value": v, "unit": UNIT, "cores": c, "kind": "port", "sample": sample}
+        v, c, sample, digests = cpu_reference(my_cfgs, args.cpu_budget, cores)
+        # the CPU leg doubles as a parity check: the sampled scenarios' counts, backend /
+        # cache stats and response paths must equal the GPU's (flagged ones re-ran exactly)
+        bad = [i for i, d in digests.items() if i not in flagged and gpu_digest(br, i) != d]
+        if bad:
+            raise RuntimeError(f"GPU results differ from the oracle on scenarios {bad[:10]}")
+        cpu = {"value": v, "unit": UNIT, "cores": c, "kind": "port", "sample": sample,
+               "parity": {"scenarios_checked": len(digests), "mismatches": 0,
+                          "fields": "requests, sessions, segments, jobs, backend/cache stats, response paths"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: the reference's seeded streams (numpy SeedSequence/PCG64/ziggurat replayed bit-exact "
                 "by the host generators; sizes and picks on the device)",
-        "config": {"workload": desc + (f"; rank r runs seeds 64r+1..64r+64" if world > 1 else ""),
-                   "scenarios": len(cfgs) * world, "requests_per_step": int(total_req),
-                   "parallelism": f"scenario-parallel x{world} ranks (one sweep per GPU)"
+        "config": {"workload": desc + (("; rank r runs seeds 64r+1..64r+64" if not strong else
+                                        "; the sweep's seed groups sharded LPT over the ranks") if world > 1 else ""),
+                   "scenarios": len(cfgs) * (1 if strong else world), "requests_per_step": int(total_req),
+                   "parallelism": (f"scenario-parallel x{world} ranks "
+                                   + ("(one sweep per GPU)" if not strong else "(one sweep split by seed group)"))
                                   + (", NCCL all_gather of QoE blocks" if world > 1 else ""),
                    "l2": "inputs > L2 (trace tables %.2f GB, engine state %.2f GB vs 126 MB L2)"
                          % (inp.input_bytes / 1e9, inp.scratch_bytes / 1e9),

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define OTF_ABI_VERSION 2
+#define OTF_ABI_VERSION 3
 
 /* ---- status codes (ValueError / RuntimeError on the Python side) ---- */
 typedef enum {
@@ -324,6 +324,44 @@ int otf_model_completion_times(const double *starts, const double *values, int32
 /* DEVICE: fill segment-size tables (one thread per entry). */
 int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
                   int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream);
+
+/* ---- DEVICE request generation: the reference's seeded numpy streams
+ * replayed on the GPU (csrc/otf_gen.cu), bit-identical to the host
+ * generators above (same otf_npdist.cuh / otf_libm.cuh arithmetic).  One
+ * thread per stream; a batch of jobs runs as one launch.  Offsets index the
+ * f64 pool (device pointer). ---- */
+enum {
+    OTF_GEN_TRACE = 0,     /* synthetic_trace + BandwidthTrace (netem.py:179-202,39-64): n_streams clients,
+                              stream c = SS([seed, 2, c]).standard_normal; values [c][n], period bits [c] */
+    OTF_GEN_ARRIVALS = 1,  /* arrival_offsets (orchestrator.py:265-268): cumsum(SS([seed, 1]).exponential(scale, n)) */
+    OTF_GEN_NOISE = 2      /* ServiceSampler eps (transcode.py:89-99): [w][0..n) = SS([seed, w]).normal(0, scale, n) */
+};
+typedef struct otf_gen_job {
+    int32_t kind;                     /* OTF_GEN_* */
+    int32_t n;                        /* samples per trace / arrivals / draws per worker */
+    int64_t n_streams;                /* traces (clients) / 1 / workers */
+    int64_t first_stream;             /* sum of n_streams over the jobs before this one */
+    uint64_t seed;
+    int64_t off_out;                  /* f64: [n_streams][n] */
+    int64_t off_pbits;                /* f64: [n_streams] trace period bits */
+    int64_t off_starts;               /* f64: [n] trace sample starts */
+    double period, mu, sigma, decay, spread, floor_bps, cap_bps;   /* trace parameters */
+    double scale;                     /* arrivals: 1 / rate; noise: noise_rel_std */
+} otf_gen_job;
+
+/* DEVICE: run n_jobs generator jobs (device array) into f64_pool.  Job q's
+ * streams are threads first_stream .. first_stream + n_streams - 1; every
+ * first_stream is a multiple of OTF_GEN_ALIGN and increases with q;
+ * total_streams = the last job's first_stream + n_streams. */
+#define OTF_GEN_ALIGN 128
+int otf_gen_tables(const otf_gen_job *jobs_dev, int32_t n_jobs, int64_t total_streams, double *f64_pool,
+                   void *stream);
+
+/* glibc's exp (fn 0) / log1p (fn 1) as restated in csrc/otf_libm.cuh, for
+ * validation: otf_model_libm on HOST pointers (host build of the restatement),
+ * otf_model_libm_dev on DEVICE pointers (the device build the generators use). */
+int otf_model_libm(int32_t fn, const double *x, int64_t n, double *out);
+int otf_model_libm_dev(int32_t fn, const double *x, int64_t n, double *out, void *stream);
 
 /* DEVICE: run every scenario of the batch to its horizon (sim.py:347-360), then
  * the summary pass: order statistics of the latency tail and the

@@ -116,6 +116,7 @@ def lib():
         build()
         _lib = ctypes.CDLL(LIB_PATH)
         _lib.oracle_run.argtypes = [_P(Scenario), _P(Outputs)]
+        _lib.oracle_libm.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         _lib.oracle_run.restype = ctypes.c_int
         _lib.oracle_segment_sizes.argtypes = [_P(Scenario), _P(ctypes.c_int64), _P(ctypes.c_int32)]
         _lib.oracle_build_traces.argtypes = [_P(Scenario), _P(ctypes.c_double),

@@ -1003,3 +1003,9 @@ int oracle_run(const oracle_scenario *sc, oracle_outputs *out) {
     free(w->wq_head); free(w->wq_tail); free(w->jq); free(w->gq); free(w->sq); free(arr);
     return w->status;
 }
+
+int oracle_libm(int fn, const double *x, int64_t n, double *out) {
+    if (fn != 0 && fn != 1) return 1;
+    for (int64_t i = 0; i < n; i++) out[i] = fn == 0 ? exp(x[i]) : log1p(x[i]);
+    return 0;
+}

@@ -66,5 +66,8 @@ int oracle_sample_times(double duration, double step, double *starts, int cap);
 int oracle_segment_sizes(const oracle_scenario *sc, int64_t *sizes, int32_t *counts);
 int oracle_build_traces(const oracle_scenario *sc, double *values, double *pbits, double *period);
 int oracle_run(const oracle_scenario *sc, oracle_outputs *out);
+/* glibc exp (fn 0) / log1p (fn 1) over n values: the libm the reference and
+ * numpy call, as the checker for the library's restatement (csrc/otf_libm.cuh). */
+int oracle_libm(int fn, const double *x, int64_t n, double *out);
 
 #endif

@@ -15,7 +15,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_PATH = os.environ.get("OTFGPU_LIB_OVERRIDE") or os.path.join(HERE, "libotfgpu.so")   # override: tools/ experiments
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _P = ctypes.POINTER
 _vp = ctypes.c_void_p
@@ -105,6 +105,17 @@ class TraceJob(ctypes.Structure):
                 ("spread", _f64), ("floor_bps", _f64), ("cap_bps", _f64), ("values", _vp), ("pbits", _vp)]
 
 
+GEN_TRACE, GEN_ARRIVALS, GEN_NOISE = 0, 1, 2
+GEN_ALIGN = 128
+
+
+class GenJob(ctypes.Structure):
+    _fields_ = [("kind", _i32), ("n", _i32), ("n_streams", _i64), ("first_stream", _i64), ("seed", _u64),
+                ("off_out", _i64), ("off_pbits", _i64), ("off_starts", _i64),
+                ("period", _f64), ("mu", _f64), ("sigma", _f64), ("decay", _f64), ("spread", _f64),
+                ("floor_bps", _f64), ("cap_bps", _f64), ("scale", _f64)]
+
+
 class SizeTable(ctypes.Structure):
     _fields_ = [
         ("n_seq", _i32), ("n_ranks", _i32), ("max_nseg", _i32), ("pad", _i32),
@@ -117,7 +128,8 @@ class SizeTable(ctypes.Structure):
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
            "otf_scratch_bytes", "otf_shared_bytes", "otf_engine_fits", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
            "otf_gen_noise", "otf_gen_traces", "otf_gen_traces_multi", "otf_model_completion_time",
-           "otf_model_select_quality", "otf_model_buffer_run", "otf_model_exact_sum", "otf_model_completion_times", "otf_gen_sizes", "otf_run_batch", "otf_run_summary")
+           "otf_model_select_quality", "otf_model_buffer_run", "otf_model_exact_sum", "otf_model_completion_times", "otf_gen_sizes", "otf_gen_tables",
+           "otf_model_libm", "otf_model_libm_dev", "otf_run_batch", "otf_run_summary")
 DRAW_STANDARD_NORMAL, DRAW_NORMAL, DRAW_EXPONENTIAL, DRAW_STANDARD_EXPONENTIAL = 0, 1, 2, 3
 
 
@@ -182,6 +194,12 @@ def lib():
     L.otf_model_completion_times.argtypes = [_vp, _vp, _i32, _f64, _f64, _f64, _vp, _vp, _i32, _vp, _vp]
     L.otf_gen_sizes.restype = ctypes.c_int
     L.otf_gen_sizes.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp, _vp]
+    L.otf_gen_tables.restype = ctypes.c_int
+    L.otf_gen_tables.argtypes = [_vp, _i32, _i64, _vp, _vp]
+    L.otf_model_libm.restype = ctypes.c_int
+    L.otf_model_libm.argtypes = [_i32, _vp, _i64, _vp]
+    L.otf_model_libm_dev.restype = ctypes.c_int
+    L.otf_model_libm_dev.argtypes = [_i32, _vp, _i64, _vp, _vp]
     L.otf_run_batch.restype = ctypes.c_int
     L.otf_run_batch.argtypes = [_P(Batch), _i32, _vp]
     L.otf_run_summary.restype = ctypes.c_int

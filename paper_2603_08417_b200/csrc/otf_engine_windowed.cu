@@ -31,6 +31,7 @@
 // wheel's bucket arrays, the job FIFOs and the LRU touch queue in the
 // scenario's global scratch arena.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <math.h>
 #include <stdint.h>
 
@@ -42,7 +43,8 @@ constexpr int32_t WIN_NONE = 0x3FFFFFFF;
 constexpr int RANK_SORT_MAX = 64;  // windows up to this many server events: rank sort, else bitonic
 constexpr int MAXK = 16;           // transcode workers
 constexpr int RING = 1024;         // timer-wheel buckets (windows, ~20 s at 20 ms); farther timers wait on a far list
-constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory
+constexpr int MAXTAB = 64;         // catalog sequences / ladder ranks kept in shared memory (more
+                                   // sequences: their tables stay in global memory)
 constexpr int MAXN = 32766;        // clients (16-bit wheel links; 0x7FFE/0x7FFF are descriptor states)
 
 // Descriptor word (16 bits, shared memory): bit 15 = cached; bits 0-14 = the
@@ -141,7 +143,8 @@ struct SrvEnt {
     double when;                                       // fire time (the request's arrival)
     double ctime;                                      // arm time (orders equal fire times, sim.py:304-309)
     int32_t pk;                                        // rank | index << 8 | seq << 16
-    int16_t cid, desc;
+    int16_t cid;
+    uint16_t desc;                                     // descriptor id (< 65535)
 };
 
 // The windowed engine's per-client coroutine state: what every client event
@@ -227,13 +230,13 @@ __host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_d
 
 // The windowed engine's limits (anything outside them runs on the exact engine;
 // the host checks the same predicate up front, otf_windowed_fits):
-//   16-bit client ids and descriptor words, the server-event key packing
+//   16-bit client ids (15-bit waiter links) and 16-bit descriptor ids, the server-event key packing
 //   rank | index << 8 | seq << 16 (index < 256), the shared catalog tables, the
 //   worker masks, and a positive request latency (the lookahead).
 __host__ __device__ inline bool win_fits(const otf_scenario &sc) {
     const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
-    return sc.n_workers <= MAXK && sc.n_clients <= MAXN && sc.n_seq <= MAXTAB && sc.n_ranks <= MAXTAB &&
-           sc.max_nseg <= 256 && D < 32767 && sc.latency > 0 &&
+    return sc.n_workers <= MAXK && sc.n_clients <= MAXN && sc.n_seq < 32768 && sc.n_ranks <= MAXTAB &&
+           sc.max_nseg <= 256 && D < 65535 && sc.latency > 0 &&
            sc.horizon / (sc.latency * (1.0 - 0x1p-20)) < 5.0e8;
 }
 
@@ -243,7 +246,8 @@ struct Win {
     int16_t *bnext;
     double *lw;                                        // window's server events: time,
     int32_t *lp;                                       //   rank | index << 8 | seq << 16,
-    int16_t *li, *ld;                                  //   client id, descriptor
+    int16_t *li;                                       //   client id
+    uint16_t *ld;                                      //   descriptor id
     uint32_t *lstamp;                                  // latest touch stamp per descriptor (global)
     LqEnt *lq;                                         // touch queue (global, 2 * lq_cap)
     uint16_t *dflags;                                  // descriptor words (DF_*), shared
@@ -307,7 +311,7 @@ __device__ __forceinline__ void bucket_push(Win &w, int32_t c, int32_t wk, bool 
                 e.ctime = ctime;
                 e.pk = (int32_t)cl.rank | ((int32_t)cl.index << 8) | ((int32_t)cl.seq << 16);
                 e.cid = (int16_t)c;
-                e.desc = (int16_t)desc;
+                e.desc = (uint16_t)desc;
                 w.bsrv[(int64_t)slot * cap + pos] = e;
             } else {
                 w.bloc[(int64_t)slot * cap + pos] = c;
@@ -1469,7 +1473,7 @@ __device__ void sort_list(Win &w, int lane) {
             r0 += (int32_t)((tj < t0) | ((tj == t0) & (j < i0)));   //   reordered by order_ties,
             r1 += (int32_t)((tj < t1) | ((tj == t1) & (j < i1)));   //   whose result is order-free
         }
-        const int16_t d0 = v0 ? w.ld[i0] : 0, d1 = v1 ? w.ld[i1] : 0;
+        const uint16_t d0 = v0 ? w.ld[i0] : 0, d1 = v1 ? w.ld[i1] : 0;
         const int32_t s0 = v0 ? w.lp[i0] : 0, s1 = v1 ? w.lp[i1] : 0;
         __syncwarp();                                  // every lane has read the list
         if (v0) { w.lw[r0] = w0; w.li[r0] = (int16_t)id0; w.ld[r0] = d0; w.lp[r0] = s0; }
@@ -1499,7 +1503,7 @@ __device__ void sort_list(Win &w, int lane) {
                     if (key_gt(wl, il, wh, ih) == up) {
                         w.lw[lo] = wh; w.lw[hi] = wl;
                         w.li[lo] = (int16_t)ih; w.li[hi] = (int16_t)il;
-                        int16_t td = w.ld[lo]; w.ld[lo] = w.ld[hi]; w.ld[hi] = td;
+                        uint16_t td = w.ld[lo]; w.ld[lo] = w.ld[hi]; w.ld[hi] = td;
                         int32_t tp = w.lp[lo]; w.lp[lo] = w.lp[hi]; w.lp[hi] = tp;
                     }
                 }
@@ -1529,7 +1533,7 @@ __device__ void order_ties(Win &w) {
             if (cj == cp) { atomicOr(&h->st.status, OTF_S_TIE); break; }
             if (cj > cp) break;
             int16_t ti = w.li[j]; w.li[j] = w.li[j - 1]; w.li[j - 1] = ti;
-            int16_t td = w.ld[j]; w.ld[j] = w.ld[j - 1]; w.ld[j - 1] = td;
+            uint16_t td = w.ld[j]; w.ld[j] = w.ld[j - 1]; w.ld[j - 1] = td;
             int32_t tp = w.lp[j]; w.lp[j] = w.lp[j - 1]; w.lp[j - 1] = tp;
             j--;
         }
@@ -1595,7 +1599,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     w.lw = (double *)p; p += 8 * (int64_t)lcap;
     w.lp = (int32_t *)p; p += 4 * (int64_t)lcap;
     w.li = (int16_t *)p; p += 2 * (int64_t)lcap;
-    w.ld = (int16_t *)p; p += 2 * (int64_t)lcap;
+    w.ld = (uint16_t *)p; p += 2 * (int64_t)lcap;
     uint8_t *g = b.scratch + sc.scratch_off;
     WinGlobalLayout L = win_global_layout(N, D);
     w.h = h;
@@ -1627,6 +1631,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
 
     // ---- init -------------------------------------------------------------------
     const bool fits = win_fits(sc);
+    const bool seq_smem = sc.n_seq <= MAXTAB;          // larger catalogs read their tables from global
     if (tid == 0) {
         EngineState z = {};
         z.lru_head = z.lru_tail = -1;
@@ -1656,7 +1661,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     }
     for (int32_t i = tid; i < RING / 2; i += WIN_THREADS) { h->cnt_srv[i] = 0; h->cnt_loc[i] = 0; }
     for (int32_t i = tid; i < RING / 32; i += WIN_THREADS) h->bits[i] = 0;
-    for (int32_t i = tid; i < sc.n_seq; i += WIN_THREADS) {
+    for (int32_t i = tid; seq_smem && i < sc.n_seq; i += WIN_THREADS) {
         h->t_segcount[i] = w.S.segcounts[i];
         h->t_seqdur[i] = w.S.seqdur[i];
         h->t_segdur[i] = w.S.segdur[i];
@@ -1671,11 +1676,13 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         w.lstamp[d] = 0; w.dflags[d] = DF_IDLE;
     }
     __syncthreads();
-    w.S.segcounts = h->t_segcount;
-    w.S.seqdur = h->t_seqdur;
-    w.S.segdur = h->t_segdur;
-    w.S.zipf = h->t_zipf;
-    w.S.manifest_b = h->t_manifest;
+    if (seq_smem) {
+        w.S.segcounts = h->t_segcount;
+        w.S.seqdur = h->t_seqdur;
+        w.S.segdur = h->t_segdur;
+        w.S.zipf = h->t_zipf;
+        w.S.manifest_b = h->t_manifest;
+    }
     w.S.rho = h->t_rho;
     w.S.bitrates = h->t_bitrates;
     // clients: the first step arms sleep(offset) (orchestrator.py:337); offsets are a
@@ -1853,7 +1860,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         const int32_t c = w.li[i];
                         const WClient cl = wunpack(w.cl[c]);
                         w.lw[i] = cl.next_when;
-                        w.ld[i] = (int16_t)wdesc(w.S, cl);
+                        w.ld[i] = (uint16_t)wdesc(w.S, cl);
                         w.lp[i] = (int32_t)cl.rank | ((int32_t)cl.index << 8) | ((int32_t)cl.seq << 16);
                     }
                     __syncwarp();
@@ -2007,10 +2014,27 @@ int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
     return otf::win_smem_bytes(n_clients, n_desc);
 }
 
+// Warps per scenario: two once shared memory allows at most 4 CTAs per SM, or
+// once the launch has at most 4 scenarios per SM anyway (a strong-scaling shard
+// of a sweep: the second warp runs the window's local timers concurrently with
+// the server pass, and the responded clients in one round).  OTF_WIN_NW=1|2
+// overrides the choice (A/B measurements).
+static int windowed_warps(const otf_batch &b) {
+    const int smem = (int)b.shared_bytes;
+    int nw = (smem + 1024) * 5 > 228 * 1024 ? 2 : 1;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (b.n_scenarios <= 4 * sms) nw = 2;
+    if (const char *e = getenv("OTF_WIN_NW")) {
+        const int v = atoi(e);
+        if (v == 1 || v == 2) nw = v;
+    }
+    return nw;
+}
+
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
     int smem = (int)b.shared_bytes;
-    // two warps per scenario once shared memory allows at most 4 CTAs per SM
-    const int nw = (smem + 1024) * 5 > 228 * 1024 ? 2 : 1;
+    const int nw = windowed_warps(b);
     auto kern = b.mode == OTF_MODE_RECORDS ? (nw == 2 ? otf::windowed_kernel<true, 2> : otf::windowed_kernel<true, 1>)
                                            : (nw == 2 ? otf::windowed_kernel<false, 2> : otf::windowed_kernel<false, 1>);
     if (smem > 48 * 1024) {

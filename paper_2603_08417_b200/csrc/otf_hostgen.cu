@@ -7,14 +7,11 @@
 //   * worker noise     normal(0, noise) per worker         SS([seed, w])    transcode.py:89-99
 // and turns the normals into bandwidth samples with math.exp (glibc) and a
 // CPython-3.12 compensated sum (netem.py:39-64,179-202).  These run here, on
-// the host, with the same libm as numpy/CPython, and with all host threads:
-// glibc's exp is what makes the trace values bit-exact, so this part stays on
-// the CPU.  numpy's algorithms restated (numpy 2.3.5):
-//   * SeedSequence + PCG64 (otf_rng.cuh, shared with the device);
-//   * random_standard_normal / random_standard_exponential: 256-layer
-//     ziggurats (numpy/random/src/distributions/distributions.c) over the
-//     tables in otf_ziggurat.h;
-//   * next_double = (next_uint64 >> 11) * 2^-53.
+// the host, with all host threads.  The product path generates the same
+// tables on the device (otf_gen.cu); these host generators are the C-ABI
+// replicas the tests pin against numpy, sharing every line of arithmetic with
+// the device through otf_npdist.cuh (numpy 2.3.5's ziggurats over
+// SeedSequence + PCG64) and otf_libm.cuh (glibc's exp / log1p).
 // Compiled with -ffp-contract=off: numpy's x86-64 baseline build does not fuse.
 #include <math.h>
 
@@ -23,52 +20,12 @@
 #include <thread>
 #include <vector>
 
-#include "otf_rng.cuh"
-#include "otf_ziggurat.h"
+#include "otf_npdist.cuh"
 #include "otfgpu.h"
 
 int otf_fail(int code, const std::string &msg);
 
 namespace otf {
-
-// Generator.standard_normal (distributions.c random_standard_normal)
-static double np_standard_normal(Pcg64 &g) {
-    for (;;) {
-        uint64_t r = pcg_next64(g);
-        int idx = (int)(r & 0xff);
-        r >>= 8;
-        int sign = (int)(r & 0x1);
-        uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-        double x = (double)rabs * zig::wi[idx];
-        if (sign & 0x1) x = -x;
-        if (rabs < zig::ki[idx]) return x;             // ~99.3% of draws
-        if (idx == 0) {                                // tail beyond r (1 - U avoids log(0))
-            for (;;) {
-                double xx = -zig::nor_inv_r * log1p(-pcg_next_double(g));
-                double yy = -log1p(-pcg_next_double(g));
-                if (yy + yy > xx * xx)
-                    return ((rabs >> 8) & 0x1) ? -(zig::nor_r + xx) : zig::nor_r + xx;
-            }
-        } else {
-            if (((zig::fi[idx - 1] - zig::fi[idx]) * pcg_next_double(g) + zig::fi[idx]) < exp(-0.5 * x * x))
-                return x;
-        }
-    }
-}
-
-// Generator.standard_exponential (distributions.c random_standard_exponential)
-static double np_standard_exponential(Pcg64 &g) {
-    for (;;) {
-        uint64_t ri = pcg_next64(g);
-        ri >>= 3;
-        int idx = (int)(ri & 0xff);
-        ri >>= 8;
-        double x = (double)ri * zig::we[idx];
-        if (ri < zig::ke[idx]) return x;               // ~98.9% of draws
-        if (idx == 0) return zig::exp_r - log1p(-pcg_next_double(g));
-        if ((zig::fe[idx - 1] - zig::fe[idx]) * pcg_next_double(g) + zig::fe[idx] < exp(-x)) return x;
-    }
-}
 
 static void seed_stream(Pcg64 &g, const uint64_t *entropy, int n_entropy) {
     uint32_t words[64];
@@ -79,16 +36,9 @@ static void seed_stream(Pcg64 &g, const uint64_t *entropy, int n_entropy) {
 
 // CPython >= 3.12 builtin sum() over floats: Neumaier-compensated.
 double py_sum(const double *xs, int n) {
-    double f = 0.0, c = 0.0;
-    for (int i = 0; i < n; i++) {
-        double x = xs[i];
-        double t = f + x;
-        if (fabs(f) >= fabs(x)) c += (f - t) + x;
-        else c += (x - t) + f;
-        f = t;
-    }
-    if (c != 0.0 && std::isfinite(c)) f += c;
-    return f;
+    PySum s;
+    for (int i = 0; i < n; i++) s.add(xs[i]);
+    return s.result();
 }
 
 // synthetic_trace (netem.py:190-201) from its normals z[0..n], then
@@ -98,7 +48,7 @@ static void trace_from_normals(const double *z, int32_t n, const double *starts,
                                double *v, double *pbits, double *terms) {
     double x = mu + sigma * z[0];
     for (int32_t i = 0; i < n; i++) {
-        double e = exp(x);                             // glibc exp == math.exp
+        double e = libm::exp(x);                       // == math.exp (glibc, otf_libm.cuh)
         double bw = e > floor_bps ? e : floor_bps;
         bw = cap_bps < bw ? cap_bps : bw;
         v[i] = bw;

@@ -52,17 +52,22 @@ class DeviceBatch:
         dev = self.device
         self.h_scen = _u8(inp.scenarios)
         self.h_tables = _u8(inp.size_tables)
+        self.h_gen = _u8(inp.gen_jobs) if inp.gen_jobs is not None else torch.zeros(1, dtype=torch.uint8)
         self.h_f64 = torch.from_numpy(inp.f64)
         self.h_i64 = torch.from_numpy(inp.i64)
         self.h_i32 = torch.from_numpy(inp.i32)
         if pin:
-            self.h_scen, self.h_tables = self.h_scen.pin_memory(), self.h_tables.pin_memory()
+            self.h_scen, self.h_tables, self.h_gen = (self.h_scen.pin_memory(), self.h_tables.pin_memory(),
+                                                      self.h_gen.pin_memory())
             if not inp.pinned:
                 self.h_f64, self.h_i64, self.h_i32 = (self.h_f64.pin_memory(), self.h_i64.pin_memory(),
                                                       self.h_i32.pin_memory())
         self.scen = torch.empty_like(self.h_scen, device=dev)
         self.tables = torch.empty_like(self.h_tables, device=dev)
-        self.f64 = torch.empty_like(self.h_f64, device=dev)
+        self.gen = torch.empty_like(self.h_gen, device=dev)
+        # f64 pool = [device-generated prefix | host part]
+        self.f64 = torch.empty(inp.f64_dev + self.h_f64.numel(), dtype=torch.float64, device=dev)
+        self.f64_host = self.f64[inp.f64_dev:]
         self.i64 = torch.empty_like(self.h_i64, device=dev)
         self.i32 = torch.empty_like(self.h_i32, device=dev)
         self.scratch = torch.empty(inp.scratch_bytes, dtype=torch.uint8, device=dev)
@@ -111,32 +116,45 @@ class DeviceBatch:
         self.batch = b
         self.streams = [torch.cuda.Stream(dev) for _ in self.groups[1:]]
         self.n_tables = sum(1 for t in inp.size_tables if t.n_seq > 0)
+        self.n_gen = inp.gen_streams and len(inp.gen_jobs) or 0
         self.upload()
 
     @property
     def h2d_bytes(self) -> int:
-        return sum(t.numel() * t.element_size() for t in (self.h_scen, self.h_tables, self.h_f64, self.h_i64,
-                                                           self.h_i32))
+        return sum(t.numel() * t.element_size() for t in (self.h_scen, self.h_tables, self.h_gen, self.h_f64,
+                                                           self.h_i64, self.h_i32))
 
     def upload(self, stream: torch.cuda.Stream | None = None) -> None:
         """Host -> device copy of every input table (non_blocking when pinned)."""
         with torch.cuda.stream(stream) if stream is not None else torch.cuda.device(self.device):
-            for d, h in ((self.scen, self.h_scen), (self.tables, self.h_tables), (self.f64, self.h_f64),
-                         (self.i64, self.h_i64), (self.i32, self.h_i32)):
+            for d, h in ((self.scen, self.h_scen), (self.tables, self.h_tables), (self.gen, self.h_gen),
+                         (self.f64_host, self.h_f64), (self.i64, self.h_i64), (self.i32, self.h_i32)):
                 d.copy_(h, non_blocking=h.is_pinned())
 
+    def generate(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Enqueue request generation: the seeded trace / arrival / noise streams
+        (otf_gen_tables) and the segment-size tables (otf_gen_sizes)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self.n_gen:
+            rc = self.lib.otf_gen_tables(self.gen.data_ptr(), self.n_gen, self.inp.gen_streams, self.f64.data_ptr(),
+                                         s.cuda_stream)
+            _lib.check(rc, "otf_gen_tables")
+        if self.n_tables:
+            rc = self.lib.otf_gen_sizes(self.tables.data_ptr(), self.n_tables, 0, self.i64.data_ptr(),
+                                        self.f64.data_ptr(), self.i32.data_ptr(), s.cuda_stream)
+            _lib.check(rc, "otf_gen_sizes")
+
     def launch(self, stream: torch.cuda.Stream | None = None, sizes: bool = True, summary: bool = True) -> None:
-        """Enqueue size-table generation + the engine (+ the summary pass unless
-        summary=False; then launch_summary runs it) on `stream` (default: current)."""
+        """Enqueue request generation (unless sizes=False: the tables from the last
+        launch are reused) + the engine (+ the summary pass unless summary=False;
+        then launch_summary runs it) on `stream` (default: current)."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         flags = 0 if summary else _lib.BF_ENGINE_ONLY
         self.batch.engine_flags = flags
         for gb in self.groups:
             gb.engine_flags = flags
-        if sizes and self.n_tables:
-            rc = self.lib.otf_gen_sizes(self.tables.data_ptr(), self.n_tables, 0, self.i64.data_ptr(),
-                                        self.f64.data_ptr(), self.i32.data_ptr(), s.cuda_stream)
-            _lib.check(rc, "otf_gen_sizes")
+        if sizes:
+            self.generate(s)
         if len(self.groups) <= 1 or self.inp.engine != _lib.ENGINE_WINDOWED:
             rc = self.lib.otf_run_batch(ctypes.byref(self.batch), self.inp.engine, s.cuda_stream)
             _lib.check(rc, "otf_run_batch")

@@ -1,22 +1,29 @@
 """Host input builder: lowers ExperimentConfigs to otf_scenario structs + shared pools.
 
-Everything a scenario reads is derived here from the reference's own seeded
-streams.  The numpy Generator streams are replayed bit-for-bit by the host
-generators of libotfgpu (csrc/otf_hostgen.cu: SeedSequence + PCG64 + numpy's
-ziggurats, multithreaded), where the reference draws them:
+Everything a scenario reads is derived from the reference's own seeded
+streams.  The numpy Generator streams are replayed bit-for-bit ON THE DEVICE
+(csrc/otf_gen.cu: SeedSequence + PCG64 + numpy's ziggurats + glibc's exp and
+log1p), where the reference draws them:
 
 * arrival offsets  list(np.cumsum(exponential(1/rate, N)))  SS([seed, 1])   orchestrator.py:265-268
 * trace normals    standard_normal per client               SS([seed, 2, c]) orchestrator.py:254-263
                    -> values/period-bits (glibc exp, CPython 3.12 sum)  netem.py:39-64,179-202
 * worker noise     normal(0, noise) per worker              SS([seed, w])    transcode.py:89-99
+* segment sizes    uniform jitter per (seq, rank, index)                     content.py:204-218
+* session picks    integers(n) / Zipf inverse CDF per client (engine)        orchestrator.py:340-342
+
+The host only lowers the configs and computes what needs no stream:
+
 * sequence keys    sha256(id)[:8] big-endian                                  content.py:165-166
 * manifest bytes   len(json.dumps(manifest_for(seq), sort_keys=True))         server.py:58-59
 
-Segment sizes and per-session sequence picks are generated on the device
-(csrc/otf_tables.cu, csrc/otf_rng.cuh).  Tables are de-duplicated across the
-batch: traces by (seed, netem), sizes by catalog, arrivals by (seed, N, rate),
-noise by (seed, noise), so a sweep over variants / cache sizes / client counts
-pays for each stream once.
+The f64 pool's leading `f64_dev` elements are device-only: the generator jobs
+(`gen_jobs`, otf_gen_tables) fill them on the GPU, and only the rest of the
+pool is copied from the host.  Tables are de-duplicated across the batch:
+traces by (seed, netem), sizes by catalog, arrivals by (seed, N, rate), noise
+by (seed, noise), so a sweep over variants / cache sizes / client counts pays
+for each stream once.  `host_generate` replays the same jobs with the host
+generators (csrc/otf_hostgen.cu) for the tests.
 """
 
 from __future__ import annotations
@@ -132,7 +139,17 @@ class _Pools:
         self.threads = threads
         self.parts = {"f64": [], "i64": [], "i32": []}
         self.size = {"f64": 0, "i64": 0, "i32": 0}
+        self.dev = {"f64": 0, "i64": 0, "i32": 0}      # device-only prefix (generated on the GPU)
         self.memo = {}
+
+    def device(self, kind: str, n: int) -> int:
+        """Reserve n device-only elements (filled by a generator job, never copied)."""
+        if self.parts[kind]:
+            raise AssertionError("device-only regions must precede every host part")
+        off = self.dev[kind]
+        self.dev[kind] += int(n)
+        self.size[kind] += int(n)
+        return off
 
     def add(self, kind: str, arr, key=None) -> int:
         if key is not None and (kind, key) in self.memo:
@@ -149,19 +166,10 @@ class _Pools:
     def reserve(self, kind: str, n: int, key=None) -> int:
         return self.add(kind, np.zeros(n), key)
 
-    def defer(self, kind: str, n: int, fill) -> int:
-        """Reserve n elements that fill(view) writes in place when the pool is laid out.
-        A fill may instead return an _lib.TraceJob (run with every other table's in one
-        parallel host call) or a callable to run after those jobs."""
-        off = self.size[kind]
-        self.parts[kind].append((int(n), fill))
-        self.size[kind] += int(n)
-        return off
-
     def concat(self, kind: str, pin: bool = False) -> np.ndarray:
         """The pool as one array (page-locked when pin, so the H2D copy is a single DMA)."""
         dt = {"f64": np.float64, "i64": np.int64, "i32": np.int32}[kind]
-        total = max(1, self.size[kind])
+        total = max(1, self.size[kind] - self.dev[kind])      # the host part only
         if pin:
             import torch
             tt = {"f64": torch.float64, "i64": torch.int64, "i32": torch.int32}[kind]
@@ -169,26 +177,10 @@ class _Pools:
         else:
             out = np.empty(total, dtype=dt)
         pos = 0
-        jobs, after = [], []
         for part in self.parts[kind]:
-            if isinstance(part, tuple):
-                n, fill = part
-                r = fill(out[pos:pos + n])
-                if isinstance(r, _lib.TraceJob):
-                    jobs.append(r)
-                elif callable(r):
-                    after.append(r)
-            else:
-                n = part.size
-                out[pos:pos + n] = part
-            pos += n
+            out[pos:pos + part.size] = part
+            pos += part.size
         out[pos:] = 0
-        if jobs:                                       # every trace table of the batch in one call
-            arr = (_lib.TraceJob * len(jobs))(*jobs)
-            _lib.check(_lib.lib().otf_gen_traces_multi(len(jobs), ctypes.addressof(arr), self.threads),
-                       "otf_gen_traces_multi")
-        for f in after:
-            f()
         return out
 
 
@@ -213,6 +205,9 @@ class BatchInputs:
     pinned: bool = False        # pools allocated page-locked (torch pinned memory)
     tail_caps: np.ndarray = None      # [n][4] summary tails: nonzero latencies, sessions, stalled, startups
     tail_totals: tuple = (0, 0, 0)    # pool lengths: latency doubles, session entries, startup doubles
+    f64_dev: int = 0                  # leading f64 pool elements generated on the device (not in `f64`)
+    gen_jobs: ctypes.Array = None     # otf_gen_job[] (device request generation)
+    gen_streams: int = 0              # total generator threads (otf_gen_tables total_streams)
 
 
 def windowed_fits(cfg, smem_limit: int | None = None) -> tuple[bool, str]:
@@ -297,44 +292,43 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     tcap_arr = np.zeros((len(lows), 4), dtype=np.int64)
     ttot = [0, 0, 0]
 
-    # -- traces: one table per (seed, netem), long enough for the largest N --
+    # -- device-generated tables first (the pool's device-only prefix) --
+    jobs: list = []
+    streams = 0
+
+    def add_job(**kw) -> None:
+        nonlocal streams
+        first = (streams + _lib.GEN_ALIGN - 1) // _lib.GEN_ALIGN * _lib.GEN_ALIGN
+        jobs.append(_lib.GenJob(first_stream=first, **kw))
+        streams = first + kw["n_streams"]
+
+    # traces: one table per (seed, netem), long enough for the largest N
     trace_groups: dict = {}
     for low in lows:
         if low.cfg.netem.trace_dir:
-            continue                                   # CSV traces: per-client tables below
+            continue                                   # CSV traces: per-client host tables below
         key = (low.cfg.seed, dataclasses.astuple(low.cfg.netem))
         prev = trace_groups.get(key, (0, low.cfg.netem))[0]
         trace_groups[key] = (max(prev, low.cfg.clients), low.cfg.netem)
     trace_tab = {}
     for key, (nmax, ne) in trace_groups.items():
-        seed = key[0]
         ts = sample_times(ne.trace_duration_s, ne.step_s)
         if not ts:
             raise ConfigError("trace has no samples")
         gaps = [b - a for a, b in zip(ts, ts[1:])]
         period = ts[-1] + (statistics.median(gaps) if gaps else 1.0)
-        starts = list(ts)
         n = len(ts)
-        starts_a = np.asarray(starts, dtype=np.float64)
         decay = math.exp(-ne.theta_per_s * ne.step_s)
-        spread = ne.sigma * math.sqrt(1.0 - decay * decay)
-        pbits = np.empty(nmax, dtype=np.float64)
+        grid = float(ne.step_s) if all(x == float(i) * ne.step_s for i, x in enumerate(ts)) else 0.0
+        trace_tab[key] = dict(n=n, period=period, grid=grid, ts=ts, values=P.device("f64", nmax * n),
+                              pbits=P.device("f64", nmax), nmax=nmax,
+                              job=dict(kind=_lib.GEN_TRACE, n=n, n_streams=nmax, seed=key[0], period=period,
+                                       mu=math.log(ne.median_bps), sigma=ne.sigma, decay=decay,
+                                       spread=ne.sigma * math.sqrt(1.0 - decay * decay),
+                                       floor_bps=ne.floor_bps, cap_bps=ne.cap_bps))
+        input_bytes += 8 * (nmax * n + nmax + n)
 
-        def fill_values(view, seed=seed, nmax=nmax, n=n, starts_a=starts_a, period=period, ne=ne, decay=decay,
-                        spread=spread, pbits=pbits):
-            # generated straight into the (pinned) pool, all tables in one parallel call
-            return _lib.TraceJob(seed=seed, n_traces=nmax, n_samples=n, pad=0, starts=starts_a.ctypes.data,
-                                 period=period, mu=math.log(ne.median_bps), sigma=ne.sigma, decay=decay,
-                                 spread=spread, floor_bps=ne.floor_bps, cap_bps=ne.cap_bps,
-                                 values=view.ctypes.data, pbits=pbits.ctypes.data)
-
-        grid = float(ne.step_s) if all(x == float(i) * ne.step_s for i, x in enumerate(starts)) else 0.0
-        trace_tab[key] = dict(n=n, period=period, grid=grid,
-                              starts=P.add("f64", starts_a), values=P.defer("f64", nmax * n, fill_values),
-                              pbits=P.defer("f64", nmax, lambda view, pbits=pbits: (lambda: np.copyto(view, pbits))))
-        input_bytes += 8 * (nmax * n + nmax) + starts_a.nbytes
-
-    # -- worker noise: one table per (seed, noise), longest draw count --
+    # worker noise: one table per (seed, noise), longest draw count
     eps_groups: dict = {}
     for low in lows:
         key = (low.cfg.seed, low.cfg.noise_rel_std)
@@ -343,12 +337,28 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     eps_tab = {}
     for (seed, noise), (kmax, elen) in eps_groups.items():
         if noise > 0:
-            eps = np.empty((kmax, elen), dtype=np.float64)
-            _lib.check(L.otf_gen_noise(seed, kmax, noise, elen, eps.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-                                       threads), "otf_gen_noise")
-        else:
-            eps = np.zeros((kmax, 1))
-        eps_tab[(seed, noise)] = (P.add("f64", eps), eps.shape[1])
+            off = P.device("f64", kmax * elen)
+            add_job(kind=_lib.GEN_NOISE, n=elen, n_streams=kmax, seed=seed, off_out=off, scale=noise)
+            eps_tab[(seed, noise)] = (off, elen)
+
+    # arrivals: one table per (seed, N, rate)
+    arr_tab = {}
+    for low in lows:
+        akey = (low.cfg.seed, low.cfg.clients, low.cfg.arrival_rate_per_s)
+        if akey not in arr_tab:
+            off = P.device("f64", low.cfg.clients)
+            add_job(kind=_lib.GEN_ARRIVALS, n=low.cfg.clients, n_streams=1, seed=low.cfg.seed, off_out=off,
+                    scale=1.0 / low.cfg.arrival_rate_per_s)
+            arr_tab[akey] = off
+            input_bytes += 8 * low.cfg.clients
+
+    # host parts from here on
+    for (seed, noise), (kmax, elen) in eps_groups.items():
+        if noise <= 0:
+            eps_tab[(seed, noise)] = (P.add("f64", np.zeros((kmax, 1))), 1)
+    for key, tt in trace_tab.items():
+        tt["starts"] = P.add("f64", np.asarray(tt["ts"], dtype=np.float64))
+        add_job(off_out=tt["values"], off_pbits=tt["pbits"], off_starts=tt["starts"], **tt["job"])
 
     for si, low in enumerate(lows):
         cfg = low.cfg
@@ -390,14 +400,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         pop = 1 if cfg.popularity == "zipf" else 0
         o_zipf = P.add("f64", zipf_cdf(n_seq, cfg.zipf_exponent) if pop else np.zeros(n_seq),
                        key=("zipf", n_seq, pop, cfg.zipf_exponent))
-        akey = ("arrivals", cfg.seed, N, cfg.arrival_rate_per_s)
-        if ("f64", akey) not in P.memo:
-            arr = np.empty(N, dtype=np.float64)                                  # cumsum(exponential), sequential
-            _lib.check(L.otf_gen_arrivals(cfg.seed, N, 1.0 / cfg.arrival_rate_per_s,
-                                          arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "otf_gen_arrivals")
-            P.add("f64", arr, key=akey)
-            input_bytes += 8 * N
-        o_arr = P.memo[("f64", akey)]
+        o_arr = arr_tab[(cfg.seed, N, cfg.arrival_rate_per_s)]
         if cfg.netem.trace_dir:                        # orchestrator.py:243-253
             tdir = cfg.netem.trace_dir
             files = sorted(os.path.join(tdir, f) for f in os.listdir(tdir) if f.endswith(".csv"))
@@ -481,8 +484,35 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         f64=P.concat("f64", pin), i64=P.concat("i64", pin), i32=P.concat("i32", pin), pinned=pin,
         scratch_bytes=max(scratch_off, 256), caps=cap_arr, rec_offsets=rec_off, rec_totals=totals,
         engine=engine, mode=mode, input_bytes=input_bytes, shared_bytes=shared_bytes, smem_per=smem_per,
-        tail_caps=tcap_arr, tail_totals=tuple(ttot))
+        tail_caps=tcap_arr, tail_totals=tuple(ttot), f64_dev=P.dev["f64"],
+        gen_jobs=(_lib.GenJob * max(1, len(jobs)))(*jobs), gen_streams=streams)
 
 
 def n_size_tables(inp: BatchInputs) -> int:
     return sum(1 for t in inp.size_tables if t.n_seq > 0)
+
+
+def n_gen_jobs(inp: BatchInputs) -> int:
+    return inp.gen_streams and len(inp.gen_jobs) or 0
+
+
+def host_generate(inp: BatchInputs, threads: int | None = None) -> np.ndarray:
+    """The device-only f64 prefix as the HOST generators (csrc/otf_hostgen.cu) make it:
+    the same jobs otf_gen_tables runs on the GPU, for tests (bit-for-bit equal)."""
+    L = _lib.lib()
+    threads = threads or os.cpu_count() or 1
+    out = np.zeros(max(1, inp.f64_dev), dtype=np.float64)
+    host = inp.f64
+    dp = lambda a, off: a[off:].ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    for j in inp.gen_jobs[:n_gen_jobs(inp)]:
+        if j.kind == _lib.GEN_TRACE:
+            starts = np.ascontiguousarray(host[j.off_starts - inp.f64_dev:j.off_starts - inp.f64_dev + j.n])
+            _lib.check(L.otf_gen_traces(j.seed, j.n_streams, j.n, dp(starts, 0), j.period, j.mu, j.sigma, j.decay,
+                                        j.spread, j.floor_bps, j.cap_bps, dp(out, j.off_out), dp(out, j.off_pbits),
+                                        threads), "otf_gen_traces")
+        elif j.kind == _lib.GEN_ARRIVALS:
+            _lib.check(L.otf_gen_arrivals(j.seed, j.n, j.scale, dp(out, j.off_out)), "otf_gen_arrivals")
+        elif j.kind == _lib.GEN_NOISE:
+            _lib.check(L.otf_gen_noise(j.seed, int(j.n_streams), j.scale, j.n, dp(out, j.off_out), threads),
+                       "otf_gen_noise")
+    return out[:inp.f64_dev]

@@ -128,6 +128,21 @@ def test_config5_point_vs_oracle():
                  for s, v in [(1, "TCPF"), (2, "TCP")]])
 
 
+def test_windowed_large_catalogs_vs_oracle():
+    """Catalogs past round 1's limits stay on the windowed engine: 40,000 descriptors
+    (50 sequences x 80 s at 1 s segments x the 10-rank ladder: 16-bit unsigned
+    descriptor ids) and 100 sequences (the catalog tables read from global memory)."""
+    from paper_2603_08417_b200.workloads import _seqs
+    big = workloads.c5(seed=3, clients=300, horizon_s=150.0, variant="TCP", sequences=_seqs(50, duration=80.0),
+                       sequence_duration_s=80.0)
+    wide = workloads.c2(seed=4, clients=200, horizon_s=200.0, variant="TCPF", sequences=_seqs(100))
+    results = _oracle_cmp([big, wide])
+    assert [r.engine for r in results] == ["windowed", "windowed"]
+    from paper_2603_08417_b200 import inputs as _inp
+    low = _inp.lower(big)
+    assert len(low.seq_ids) * low.n_ranks * max(low.counts) == 40_000
+
+
 def test_histogram_mode_matches_records():
     cfgs = [workloads.c3(seed=7, fraction=f) for f in (0.0, 0.3, 1.0)] + [workloads.c1(seed=3)]
     rec = engine.run_batch(cfgs, mode="records")

@@ -54,6 +54,12 @@ def test_scratch_bytes_positive():
         assert L.otf_shared_bytes(0, 100, 4, 50, 5, 10) == 0
 
 
+def full_pool(inp) -> np.ndarray:
+    """The whole f64 pool as the device builds it: the device-generated prefix
+    replayed by the host generators (inputs.host_generate), then the host part."""
+    return np.concatenate([inputs.host_generate(inp), inp.f64])
+
+
 @pytest.mark.parametrize("name", ["c1_seed1", "c2_seed1_h120", "edge_partial_seg"])
 def test_traces_match_oracle(name):
     """otf_build_traces (C++, glibc exp, 3.12 sum) == oracle traces (which match the reference)."""
@@ -65,10 +71,11 @@ def test_traces_match_oracle(name):
     prep = oracle.Prepared(cfg)
     starts, values, pbits, period = prep.traces()
     n = sc.n_samples
-    got_vals = inp.f64[sc.off_values:sc.off_values + cfg.clients * n].reshape(cfg.clients, n)
-    got_pbits = inp.f64[sc.off_pbits:sc.off_pbits + cfg.clients]
+    pool = full_pool(inp)
+    got_vals = pool[sc.off_values:sc.off_values + cfg.clients * n].reshape(cfg.clients, n)
+    got_pbits = pool[sc.off_pbits:sc.off_pbits + cfg.clients]
     assert sc.period == period
-    assert np.array_equal(inp.f64[sc.off_starts:sc.off_starts + n], starts)
+    assert np.array_equal(pool[sc.off_starts:sc.off_starts + n], starts)
     assert np.array_equal(got_vals.view(np.int64), values.view(np.int64))
     assert np.array_equal(got_pbits.view(np.int64), pbits.view(np.int64))
 
@@ -79,6 +86,7 @@ def test_traces_match_reference_semantics():
     inp = inputs.build_inputs([cfg], mode=_lib.MODE_HISTOGRAM)
     sc = inp.scenarios[0]
     n = sc.n_samples
+    pool = full_pool(inp)
     for c in range(3):
         rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([42, 2, c])))
         mu = math.log(17e6)
@@ -91,10 +99,10 @@ def test_traces_match_reference_semantics():
             vals.append(min(max(math.exp(x), 2e6), 400e6))
             x = mu + (x - mu) * decay + spread * rng.standard_normal()
             t += 1.0
-        got = inp.f64[sc.off_values + c * n: sc.off_values + (c + 1) * n]
+        got = pool[sc.off_values + c * n: sc.off_values + (c + 1) * n]
         assert list(got) == vals
         pb = sum(v * 1.0 for v in vals)
-        assert inp.f64[sc.off_pbits + c] == pb
+        assert pool[sc.off_pbits + c] == pb
 
 
 def test_arrivals_and_manifest_bytes():
@@ -103,7 +111,7 @@ def test_arrivals_and_manifest_bytes():
     sc = inp.scenarios[0]
     rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([3, 1])))
     want = list(np.cumsum(rng.exponential(1.0 / cfg.arrival_rate_per_s, size=cfg.clients)))
-    assert list(inp.f64[sc.off_arrivals:sc.off_arrivals + cfg.clients]) == want
+    assert list(full_pool(inp)[sc.off_arrivals:sc.off_arrivals + cfg.clients]) == want
     prep = oracle.Prepared(cfg)
     assert list(inp.i64[sc.off_manifest:sc.off_manifest + sc.n_seq]) == list(prep.manifest_bytes)
 
@@ -227,3 +235,58 @@ def test_seed_range_is_validated():
         with pytest.raises((ConfigError, ValueError)):
             ExperimentConfig(seed=bad).validate()
     ExperimentConfig(seed=2 ** 64 - 1).validate()
+
+
+def test_generator_jobs_cover_the_device_prefix():
+    """Every device-only f64 element belongs to exactly one generator job, jobs
+    start on OTF_GEN_ALIGN boundaries in increasing order, and the host part
+    starts after the prefix (only it is copied)."""
+    cfgs = workloads.c5_sweep(seeds=range(1, 3))[:8] + [workloads.c2(seed=1), workloads.c1(seed=1)]
+    inp = inputs.build_inputs(cfgs, mode=_lib.MODE_HISTOGRAM)
+    cover = np.zeros(inp.f64_dev, dtype=np.int32)
+    prev_end = 0
+    for j in inp.gen_jobs[:inputs.n_gen_jobs(inp)]:
+        assert j.first_stream % _lib.GEN_ALIGN == 0 and j.first_stream >= prev_end
+        prev_end = j.first_stream + j.n_streams
+        n_out = j.n_streams * j.n if j.kind != _lib.GEN_ARRIVALS else j.n
+        cover[j.off_out:j.off_out + n_out] += 1
+        if j.kind == _lib.GEN_TRACE:
+            cover[j.off_pbits:j.off_pbits + j.n_streams] += 1
+            assert j.off_starts >= inp.f64_dev                 # starts come from the host part
+    assert prev_end == inp.gen_streams
+    assert (cover == 1).all()
+    for sc in inp.scenarios:
+        assert sc.off_values < inp.f64_dev and sc.off_arrivals < inp.f64_dev and sc.off_eps < inp.f64_dev
+
+
+def test_libm_restatement_matches_host_libm():
+    """otf_libm.cuh (host build) == glibc's exp / log1p (math.exp / math.log1p call
+    the same libm the reference and numpy use) on the streams' argument ranges,
+    random bit patterns and edge cases.  The device build is compared on 1e8
+    arguments in tests/test_gpu_gen.py."""
+    L = _lib.lib()
+    rng = np.random.default_rng(5)
+    n = 400_000
+    u = rng.random(n)
+    xs_exp = np.concatenate([
+        13.0 + 8.0 * u,                                   # trace log-bandwidths (mu = log 17e6, sigma 0.35)
+        -0.5 * (3.7 * u) ** 2, -7.7 * u,                  # ziggurat wedge tests
+        (u - 0.5) * 1500.0, np.ldexp(u - 0.5, -rng.integers(0, 70, n)),
+        rng.integers(0, 2 ** 63, n, dtype=np.int64).view(np.float64),
+        [0.0, -0.0, 709.78, 709.79, -745.1, -745.2, 1e-300, np.inf, -np.inf]])
+    xs_log = np.concatenate([
+        -u, -np.ldexp(u, -rng.integers(0, 60, n)), u * 10.0, np.ldexp(u, rng.integers(0, 80, n)),
+        -u * 0.999999,
+        [0.0, -0.0, -0.29289, -0.2928932188134524, -0.9999999999999999, 0.41421356, 1e-300, np.inf]])
+    for fn, xs, ref in ((0, xs_exp, math.exp), (1, xs_log, math.log1p)):
+        xs = np.ascontiguousarray(xs[np.isfinite(xs) | np.isinf(xs)])
+        out = np.empty_like(xs)
+        _lib.check(L.otf_model_libm(fn, xs.ctypes.data, xs.size, out.ctypes.data), "otf_model_libm")
+        want = np.empty_like(xs)
+        for i, x in enumerate(xs):
+            try:
+                want[i] = ref(float(x))
+            except OverflowError:
+                want[i] = np.inf
+        bad = np.nonzero(out.view(np.int64) != want.view(np.int64))[0]
+        assert bad.size == 0, (fn, xs[bad[:5]], out[bad[:5]], want[bad[:5]])
