@@ -50,6 +50,8 @@ typedef enum {
 #define OTF_S_UNFIT 0x20           /* outside the windowed engine's limits (client / descriptor /
                                       worker counts, segments per sequence, simultaneous requests):
                                       the host re-runs the scenario on the exact engine */
+#define OTF_S_LIST_OVERFLOW 0x80  /* windowed engine: more simultaneous requests in one window than
+                                      otf_scenario.list_cap: the host re-runs it with a larger list */
 #define OTF_S_TAIL_OVERFLOW 0x40   /* a summary tail buffer (nonzero latencies / stalled sessions) was
                                       too small: otf_qoe.n_lat_tail / n_stall_tail are exact, re-run */
 
@@ -96,7 +98,8 @@ typedef struct otf_scenario {
     double grid_step;                 /* > 0 when starts[i] == i * grid_step exactly (bisect-free lookup) */
     double retry_backoff;             /* ClientConfig.retry_backoff_s */
     int32_t demand_priority;          /* BackendPolicy.demand_priority (backend.py:103-105,174-184) */
-    int32_t pad2;
+    int32_t list_cap;                 /* windowed engine: server events one window can hold (0 = the
+                                         default for n_clients, otf_list_cap); more -> OTF_S_LIST_OVERFLOW */
     int64_t off_tr_i;                 /* CSV traces (netem.trace_dir): i64 [n_clients][3] = starts offset,
                                          values offset, samples (f64 pool); -1 = synthetic traces */
     int64_t off_tr_f;                 /* f64 [n_clients][3] = period, period bits, grid step */
@@ -201,7 +204,9 @@ typedef struct otf_batch {
     int64_t shared_bytes;             /* windowed engine: dynamic shared memory per scenario
                                          (max of otf_shared_bytes over the batch) */
     int32_t engine_flags;             /* OTF_BF_* */
-    int32_t pad_flags;
+    int32_t concurrent;               /* scenarios resident alongside this launch (its own plus those
+                                         of launches running concurrently on other streams); sizes
+                                         the warps per scenario.  0 = n_scenarios */
     double *tail_lat;                 /* summary tails at otf_scenario.lat_off / ses_off / sup_off */
     otf_sess_ent *tail_sess;
     double *tail_sup;
@@ -236,9 +241,14 @@ int64_t otf_scratch_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, 
  * device's opt-in limit (otf_shared_bytes). */
 int32_t otf_engine_fits(int32_t engine, const otf_scenario *sc);
 
-/* Per-scenario dynamic shared memory of the windowed engine (host-side helper). */
+/* Per-scenario dynamic shared memory of the windowed engine (host-side helper),
+ * with the default server-event list capacity (otf_list_cap). */
 int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, int32_t n_seq,
                          int32_t n_ranks, int32_t max_nseg);
+/* The same with an explicit list capacity (otf_scenario.list_cap > 0). */
+int64_t otf_shared_bytes_cap(int32_t n_clients, int32_t n_seq, int32_t n_ranks, int32_t max_nseg, int32_t list_cap);
+/* The windowed engine's default server-event list capacity for n_clients. */
+int32_t otf_list_cap(int32_t n_clients);
 
 /* HOST function: synthetic traces (netem.py:179-202) + BandwidthTrace period
  * bits (netem.py:39-64) from numpy's standard-normal draws.  normals is

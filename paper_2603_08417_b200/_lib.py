@@ -28,8 +28,8 @@ OUTCOME_PENDING, OUTCOME_COMPLETED, OUTCOME_DROPPED = 0, 1, 2
 POP_UNIFORM, POP_ZIPF = 0, 1
 ENGINE_EXACT, ENGINE_WINDOWED = 0, 1
 MODE_HISTOGRAM, MODE_RECORDS = 0, 1
-S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG, S_UNFIT, S_TAIL_OVERFLOW = (
-    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
+S_RECORD_OVERFLOW, S_EPS_OVERFLOW, S_INTERNAL, S_TIE, S_HUNG, S_UNFIT, S_TAIL_OVERFLOW, S_LIST_OVERFLOW = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
 Q_ORDER_STATS, Q_INEXACT_SUM, Q_RANKS_CAPPED = 0x1, 0x2, 0x4
 BF_ENGINE_ONLY = 0x1
 SM_COUNT_B200, SMEM_PER_SM = 148, 227 * 1024
@@ -52,7 +52,7 @@ class Scenario(ctypes.Structure):
         ("horizon", _f64), ("latency", _f64),
         ("target", _f64), ("safe", _f64), ("panic", _f64), ("resume", _f64), ("startup", _f64),
         ("alpha", _f64), ("headroom", _f64), ("noise", _f64), ("period", _f64), ("grid_step", _f64), ("retry_backoff", _f64),
-        ("demand_priority", _i32), ("pad2", _i32), ("off_tr_i", _i64), ("off_tr_f", _i64),
+        ("demand_priority", _i32), ("list_cap", _i32), ("off_tr_i", _i64), ("off_tr_f", _i64),
         ("off_sizes", _i64), ("off_bitrates", _i64), ("off_manifest", _i64), ("off_segcount", _i64),
         ("off_seqdur", _i64), ("off_segdur", _i64), ("off_rho", _i64), ("off_zipf", _i64),
         ("off_starts", _i64), ("off_values", _i64), ("off_pbits", _i64), ("off_arrivals", _i64),
@@ -95,7 +95,7 @@ class Batch(ctypes.Structure):
                  ("i64_pool", _vp), ("i32_pool", _vp), ("scratch", _vp)]
                 + [(n, _vp) for n, _ in RECORD_FIELDS]
                 + [("counts", _vp), ("stats", _vp), ("qoe", _vp), ("status", _vp), ("order", _vp),
-                   ("shared_bytes", _i64), ("engine_flags", _i32), ("pad_flags", _i32),
+                   ("shared_bytes", _i64), ("engine_flags", _i32), ("concurrent", _i32),
                    ("tail_lat", _vp), ("tail_sess", _vp), ("tail_sup", _vp)])
 
 
@@ -126,7 +126,7 @@ class SizeTable(ctypes.Structure):
 
 
 EXPORTS = ("otf_version", "otf_last_error", "otf_sizeof_scenario", "otf_sizeof_batch", "otf_sizeof_qoe",
-           "otf_scratch_bytes", "otf_shared_bytes", "otf_engine_fits", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
+           "otf_scratch_bytes", "otf_shared_bytes", "otf_shared_bytes_cap", "otf_list_cap", "otf_engine_fits", "otf_build_traces", "otf_np_draws", "otf_gen_arrivals",
            "otf_gen_noise", "otf_gen_traces", "otf_gen_traces_multi", "otf_model_completion_time",
            "otf_model_select_quality", "otf_model_buffer_run", "otf_model_exact_sum", "otf_model_completion_times", "otf_gen_sizes", "otf_gen_tables",
            "otf_model_libm", "otf_model_libm_dev", "otf_run_batch", "otf_run_summary")
@@ -168,6 +168,10 @@ def lib():
     L.otf_engine_fits.argtypes = [_i32, _P(Scenario)]
     L.otf_shared_bytes.restype = _i64
     L.otf_shared_bytes.argtypes = [_i32] * 6
+    L.otf_shared_bytes_cap.restype = _i64
+    L.otf_shared_bytes_cap.argtypes = [_i32] * 5
+    L.otf_list_cap.restype = _i32
+    L.otf_list_cap.argtypes = [_i32]
     L.otf_build_traces.restype = ctypes.c_int
     L.otf_build_traces.argtypes = [_i64, _i32, _P(_f64), _P(_f64), _f64, _f64, _f64, _f64, _f64, _f64, _f64,
                                    _P(_f64), _P(_f64), _i32]

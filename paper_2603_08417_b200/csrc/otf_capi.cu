@@ -16,7 +16,8 @@ int otf_launch_exact(const otf_batch &b, cudaStream_t stream);
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream);
 int otf_launch_summary(const otf_batch &b, int32_t engine, cudaStream_t stream);
 int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t n_desc);
-int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc);
+int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc, int32_t list_cap);
+int32_t otf_windowed_list_cap(int32_t n_clients);
 bool otf_windowed_fits(const otf_scenario &sc);
 int otf_launch_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t *i64_pool,
                      const double *f64_pool, const int32_t *i32_pool, cudaStream_t stream);
@@ -133,8 +134,14 @@ int64_t otf_shared_bytes(int32_t engine, int32_t n_clients, int32_t n_workers, i
                          int32_t n_ranks, int32_t max_nseg) {
     (void)n_workers;
     if (engine != OTF_ENGINE_WINDOWED) return 0;
-    return otf_windowed_shared_bytes(n_clients, (int64_t)n_seq * n_ranks * max_nseg);
+    return otf_windowed_shared_bytes(n_clients, (int64_t)n_seq * n_ranks * max_nseg, 0);
 }
+
+int64_t otf_shared_bytes_cap(int32_t n_clients, int32_t n_seq, int32_t n_ranks, int32_t max_nseg, int32_t list_cap) {
+    return otf_windowed_shared_bytes(n_clients, (int64_t)n_seq * n_ranks * max_nseg, list_cap);
+}
+
+int32_t otf_list_cap(int32_t n_clients) { return otf_windowed_list_cap(n_clients); }
 
 int otf_gen_sizes(const otf_size_table *tables_dev, int32_t n_tables, int64_t total_entries,
                   int64_t *i64_pool, const double *f64_pool, const int32_t *i32_pool, void *stream) {

@@ -219,9 +219,14 @@ __host__ __device__ inline WinGlobalLayout win_global_layout(int32_t n_clients, 
     return L;
 }
 
-__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc) {
+// the scenario's server-event list capacity (otf_scenario.list_cap, default by client count)
+__host__ __device__ inline int32_t win_list_cap_sc(const otf_scenario &sc) {
+    return sc.list_cap > 0 ? sc.list_cap : win_list_cap(sc.n_clients);
+}
+
+__host__ __device__ inline int64_t win_smem_bytes(int32_t n_clients, int64_t n_desc, int32_t list_cap) {
     int64_t o = (sizeof(WinHeader) + 15) & ~(int64_t)15;
-    o += 16 * (int64_t)win_list_cap(n_clients);   // when f64, pack i32, id i16, desc i16
+    o += 16 * (int64_t)list_cap;          // when f64, pack i32, id i16, desc u16
     o += 2 * (int64_t)n_clients;          // wheel / waiter next links (int16)
     o = (o + 15) & ~(int64_t)15;
     o += 2 * (n_desc + 1);                // descriptor words (DF_*), +1: the server lane reads d + 1 early
@@ -1455,6 +1460,61 @@ __device__ void sort_list(Win &w, int lane) {
     const int32_t n = h->n_list;
     if (lane == 0) h->n_ties = 0;
     if (n <= 1) { __syncwarp(); return; }
+#ifdef WIN_REG_SORT
+    if (n <= 64) {
+        // bitonic network over 64 positions in registers: lane holds positions lane and
+        // lane + 32; keys are (time bit pattern, list position) -- non-negative doubles order
+        // like their bit patterns, and the position breaks equal times (flagged below and
+        // reordered by order_ties).  Then every lane gathers its two positions' payloads.
+        const bool v0 = lane < n, v1 = lane + 32 < n;
+        unsigned long long k0 = v0 ? (unsigned long long)__double_as_longlong(w.lw[lane]) : ~0ull;
+        unsigned long long k1 = v1 ? (unsigned long long)__double_as_longlong(w.lw[lane + 32]) : ~0ull;
+        int32_t j0 = lane, j1 = lane + 32;
+        OTF_NOUNROLL
+        for (int32_t size = 2; size <= 64; size <<= 1) {
+            OTF_NOUNROLL
+            for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                if (stride == 32) {                    // partner: the lane's other position
+                    const bool sw = (k0 > k1) | ((k0 == k1) & (j0 > j1));   // size == 64: ascending
+                    const unsigned long long tk = sw ? k1 : k0;
+                    k1 = sw ? k0 : k1; k0 = tk;
+                    const int32_t tj = sw ? j1 : j0;
+                    j1 = sw ? j0 : j1; j0 = tj;
+                } else {
+                    const bool lower = (lane & stride) == 0;
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        unsigned long long &k = h ? k1 : k0;
+                        int32_t &j = h ? j1 : j0;
+                        const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, stride);
+                        const int32_t pj = __shfl_xor_sync(0xffffffffu, j, stride);
+                        const bool asc = ((lane + 32 * h) & size) == 0 || size == 64;
+                        const bool mine_gt = (k > pk) | ((k == pk) & (j > pj));
+                        // keep the smaller key when this position is the lower one of an ascending pair
+                        const bool take = (lower == asc) ? mine_gt : !mine_gt;
+                        k = take ? pk : k;
+                        j = take ? pj : j;
+                    }
+                }
+            }
+        }
+        const int16_t c0 = v0 ? w.li[j0] : 0, c1 = v1 ? w.li[j1] : 0;
+        const uint16_t d0 = v0 ? w.ld[j0] : 0, d1 = v1 ? w.ld[j1] : 0;
+        const int32_t s0 = v0 ? w.lp[j0] : 0, s1 = v1 ? w.lp[j1] : 0;
+        __syncwarp();                                  // every lane has read its payloads
+        if (v0) { w.lw[lane] = __longlong_as_double((long long)k0); w.li[lane] = c0; w.ld[lane] = d0; w.lp[lane] = s0; }
+        if (v1) { w.lw[lane + 32] = __longlong_as_double((long long)k1); w.li[lane + 32] = c1; w.ld[lane + 32] = d1; w.lp[lane + 32] = s1; }
+        // equal request times (rare): neighbours in the sorted order
+        const unsigned long long up0 = __shfl_up_sync(0xffffffffu, k0, 1);
+        const unsigned long long last0 = __shfl_sync(0xffffffffu, k0, 31);
+        const unsigned long long up1 = __shfl_up_sync(0xffffffffu, k1, 1);
+        const bool tie = (lane > 0 && v0 && k0 == up0) || (v1 && k1 == (lane > 0 ? up1 : last0));
+        const bool any = __any_sync(0xffffffffu, tie);
+        if (lane == 0) h->n_ties = any ? 1 : 0;
+        __syncwarp();
+        return;
+    }
+#endif
     if (n <= RANK_SORT_MAX) {
         // each lane ranks elements lane and lane + 32 in one pass over the list (one
         // broadcast load per j for both).  Non-negative doubles order like
@@ -1563,6 +1623,27 @@ __device__ int32_t wheel_next(WinHeader *h, int32_t k_done, int lane) {
     return warp_min(best);
 }
 
+#ifdef WIN_PF_RESP
+// Warm L2 with what the request's response chain reads in phase B (a cache hit
+// answers at the request's own arrival time): the client's hot state, the trace
+// sample the transfer starts in, the trace's period bits and the segment size.
+// Issued by all lanes at the window's gather, ~15 k cycles before phase B.
+__device__ __forceinline__ void prefetch_response(const Win &w, const SrvEnt &e) {
+    const Scn &S = w.S;
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(w.cl + e.cid));
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(S.sizes + e.desc));
+    if (S.sc->off_tr_i < 0) {
+        const double q = e.when * S.inv_grid_step;
+        const int32_t i = q < (double)S.sc->n_samples ? (int32_t)q : 0;
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(S.values + (int64_t)e.cid * S.sc->n_samples + i));
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(S.pbits + e.cid));
+    }
+}
+#endif
+
+// status bits that end a scenario's run early (the host re-runs it)
+#define WIN_ABORT_BITS (OTF_S_TIE | OTF_S_UNFIT | OTF_S_LIST_OVERFLOW)
+
 // Window-loop control word (shared): what both warps do after the selection step.
 enum { CTL_RUN = 0, CTL_REFILE = 1, CTL_STOP = 2 };
 
@@ -1595,7 +1676,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     const int32_t N = sc.n_clients, K = sc.n_workers;
     const int64_t D = (int64_t)sc.n_seq * sc.n_ranks * sc.max_nseg;
     uint8_t *p = smem + ((sizeof(WinHeader) + 15) & ~(size_t)15);
-    const int32_t lcap = win_list_cap(sc.n_clients);
+    const int32_t lcap = win_list_cap_sc(sc);
     w.lw = (double *)p; p += 8 * (int64_t)lcap;
     w.lp = (int32_t *)p; p += 4 * (int64_t)lcap;
     w.li = (int16_t *)p; p += 2 * (int64_t)lcap;
@@ -1701,7 +1782,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         seed_picks(&w.wc[c].picks, sc.seed, c);
     }
     __syncthreads();
-    if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) goto done;
+    if (h->st.status & WIN_ABORT_BITS) goto done;
 
     // ---- window loop --------------------------------------------------------------
     t_start = clock64();
@@ -1751,6 +1832,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         base += got;
                         if (got < 32) break;
                     }
+                    __syncwarp();                          // every lane has read arr_win / arr_next
                     if (lane == 0) {
                         h->k_done = m - 1;
                         h->arr_next = base;
@@ -1830,8 +1912,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                     nb = h->n_blist;
                 }
                 const int32_t nlist = ns + n_ovf;
-                if (nlist > h->list_cap) {                 // too many simultaneous requests for this engine
-                    if (lane == 0) atomicOr(&h->st.status, OTF_S_UNFIT);
+                if (nlist > h->list_cap) {                 // more simultaneous requests than the list holds:
+                    if (lane == 0) atomicOr(&h->st.status, OTF_S_LIST_OVERFLOW);   // re-run with a larger one
                     ctl = CTL_STOP;
                 } else {
                     const SrvEnt *as = w.bsrv + (int64_t)slot * w.scap;
@@ -1841,6 +1923,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         const bool two = i + 32 < ns;
                         SrvEnt f;
                         if (two) f = as[i + 32];
+#ifdef WIN_PF_RESP
+                        prefetch_response(w, e);
+                        if (two) prefetch_response(w, f);
+#endif
                         w.li[i] = e.cid;
                         w.lw[i] = e.when;
                         w.ld[i] = e.desc;
@@ -1948,7 +2034,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                 store_client_stream(&w.cl[m.cid], c);
             }
             __syncwarp();
-            if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) break;
+            if (h->st.status & WIN_ABORT_BITS) break;
         } else {
             if (warp > 0) {
                 // ---- phase B1: the window's client-local timers, concurrent with phase A ----
@@ -1960,7 +2046,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                 if (b1 == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
             }
             __syncthreads();
-            if (h->st.status & (OTF_S_TIE | OTF_S_UNFIT)) break;
+            if (h->st.status & WIN_ABORT_BITS) break;
             // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
             t0 = WCLOCK();
             const int32_t nb = h->n_blist;
@@ -1978,7 +2064,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
     }
 
     // ---- horizon: harvest (orchestrator.py:357-359) ----
-    if (!(h->st.status & (OTF_S_TIE | OTF_S_UNFIT))) {
+    if (!(h->st.status & WIN_ABORT_BITS)) {
         for (int32_t c = tid; c < N; c += WIN_THREADS) {
             WClient cl = wunpack(w.cl[c]);
             wharvest(w, cl, c, sc.horizon);
@@ -2010,9 +2096,11 @@ int64_t otf_windowed_scratch_bytes(int32_t n_clients, int32_t n_workers, int64_t
 
 bool otf_windowed_fits(const otf_scenario &sc) { return otf::win_fits(sc); }
 
-int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc) {
-    return otf::win_smem_bytes(n_clients, n_desc);
+int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc, int32_t list_cap) {
+    return otf::win_smem_bytes(n_clients, n_desc, list_cap > 0 ? list_cap : otf::win_list_cap(n_clients));
 }
+
+int32_t otf_windowed_list_cap(int32_t n_clients) { return otf::win_list_cap(n_clients); }
 
 // Warps per scenario: two once shared memory allows at most 4 CTAs per SM, or
 // once the launch has at most 4 scenarios per SM anyway (a strong-scaling shard
@@ -2024,7 +2112,8 @@ static int windowed_warps(const otf_batch &b) {
     int nw = (smem + 1024) * 5 > 228 * 1024 ? 2 : 1;
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (b.n_scenarios <= 4 * sms) nw = 2;
+    const int32_t resident = b.concurrent > b.n_scenarios ? b.concurrent : b.n_scenarios;
+    if (resident <= 4 * sms) nw = 2;
     if (const char *e = getenv("OTF_WIN_NW")) {
         const int v = atoi(e);
         if (v == 1 || v == 2) nw = v;

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(SUM_THREADS) summary_kernel(const otf_batch b,
                 const long long want = S.rem[r];
                 const unsigned hit = __ballot_sync(0xffffffffu, (long long)x > want);
                 const int L = __ffs(hit) - 1;          // first lane whose prefix passes the rank
+                __syncwarp();                          // every lane has read S.rem[r]
                 if (lane == L) {
                     long long below = (long long)(x - mine);
                     int bin = lane * per;

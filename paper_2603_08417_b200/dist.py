@@ -15,7 +15,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-RERUN_BITS = 0x2 | 0x8 | 0x20                          # OTF_S_EPS_OVERFLOW | OTF_S_TIE | OTF_S_UNFIT
+RERUN_BITS = 0x2 | 0x8 | 0x20 | 0x80                   # OTF_S_EPS_OVERFLOW | TIE | UNFIT | LIST_OVERFLOW
 
 __all__ = ["scenario_cost", "shard", "gather_blocks", "all_max", "all_sum", "run_sharded"]
 

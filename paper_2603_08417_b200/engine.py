@@ -110,9 +110,11 @@ class DeviceBatch:
             gb.order = self.order.data_ptr() + 4 * int(idx[0])
             gb.shared_bytes = int(smem[order[idx]].max())
             gb.engine_flags = 0
+            gb.concurrent = n                          # the groups run concurrently (side streams)
             self.groups.append(gb)
         b.order = self.order.data_ptr()
         b.shared_bytes = inp.shared_bytes
+        b.concurrent = n
         self.batch = b
         self.streams = [torch.cuda.Stream(dev) for _ in self.groups[1:]]
         self.n_tables = sum(1 for t in inp.size_tables if t.n_seq > 0)
@@ -305,6 +307,7 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
     caps = {i: tuple(c) for i, c in enumerate(_caps)} if _caps is not None else {}   # test hook
     tcaps = {i: tuple(c) for i, c in enumerate(_tail_caps)} if _tail_caps is not None else {}   # test hook
     eps_scale = {i: _eps_scale for i in todo} if _eps_scale != 1.0 else {}         # test hook
+    lcaps: dict = {}                                   # server-event list capacities after an overflow
     engines = {i: eng for i in todo}
     if eng == _lib.ENGINE_WINDOWED:                    # outside the windowed engine's limits: exact, up front
         from .inputs import windowed_fits
@@ -329,8 +332,10 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                 inp0 = build_inputs([configs[i] for i in idx], engine=e, mode=m, eps_scale=es)
                 use_caps = [c if c is not None else tuple(inp0.caps[k]) for k, c in enumerate(cap_list)]
             tail = [tcaps.get(i) for i in idx]
+            lc = [lcaps.get(i, 0) for i in idx]
             inp = build_inputs([configs[i] for i in idx], engine=e, mode=m, caps=use_caps, eps_scale=es, pin=True,
-                               tail_caps=tail if any(t is not None for t in tail) else None)
+                               tail_caps=tail if any(t is not None for t in tail) else None,
+                               list_caps=lc if any(lc) else None)
             db = DeviceBatch(inp, device, pin=True)
             db.launch()
             br = db.fetch()
@@ -342,6 +347,10 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                 if st & _lib.S_UNFIT:
                     _log.warning("scenario %d: outside the windowed engine's limits at run time "
                                  "(status %#x); re-running it on the exact engine", i, st)
+                if st & _lib.S_LIST_OVERFLOW:             # a burst of simultaneous requests: a 4x list
+                    if not _grow_list_cap(configs[i], lcaps, i, device):
+                        engines[i] = _lib.ENGINE_EXACT
+                    retry = True
                 if st & (_lib.S_TIE | _lib.S_UNFIT) or (m == _lib.MODE_RECORDS and br.session_tie(k)):
                     engines[i] = _lib.ENGINE_EXACT
                     retry = True
@@ -363,10 +372,30 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
                     results[i] = br.result(k)
                     results[i].engine = "exact" if e == _lib.ENGINE_EXACT else "windowed"
                     results[i].attempts = _attempt + 1
+                    results[i].list_cap = lcaps.get(i, 0)
+                    results[i].eps_scale = es
         todo = nxt
     if todo:
         raise _lib.OtfError(f"scenarios {todo} did not converge after {max_retries} retries")
     return results
+
+
+def _grow_list_cap(cfg, lcaps: dict, i: int, device) -> bool:
+    """Quadruple scenario i's server-event list (a power of two, at most 16,384
+    entries and the device's shared memory); False when it cannot grow."""
+    from .config import ExperimentConfig
+    from .inputs import lower
+    L = _lib.lib()
+    low = lower(ExperimentConfig.from_reference(cfg))
+    cur = lcaps.get(i) or int(L.otf_list_cap(low.cfg.clients))
+    new = cur * 4
+    limit = torch.cuda.get_device_properties(require_cuda(device)).shared_memory_per_block_optin
+    smem = int(L.otf_shared_bytes_cap(low.cfg.clients, len(low.seq_ids), low.n_ranks, max(low.counts), new))
+    if new > 16384 or smem > limit:
+        _log.warning("scenario %d: %d simultaneous requests exceed the windowed engine's list; exact engine", i, cur)
+        return False
+    lcaps[i] = new
+    return True
 
 
 def run_experiment(config) -> ExperimentResult:

@@ -114,14 +114,41 @@ class Lowered:
     stored: list[int]
     cache_enabled: bool
     spec_enabled: bool
+    cat_key: tuple = ()         # (seed, jitter, ids, durations, segment durations, ladder): one size table
+
+_LOWER_MEMO: dict = {}
+
+
+def _netem_key(ne) -> tuple:
+    return tuple(ne.__dict__.values())                 # NetemConfig: flat scalar fields
+
+
+def _lower_key(cfg: ExperimentConfig):
+    """Every field validate() and the catalog read: configs of a sweep that differ
+    only in client count, horizon, cache size within the policy's limits... share
+    one validated lowering."""
+    seqs = tuple((e["id"], e.get("duration_s"), e.get("segment_duration_s")) for e in cfg.sequences) \
+        if cfg.sequences else None
+    return (cfg.variant, cfg.cache_capacity_bytes > 0, cfg.workers, cfg.queue_bound, cfg.demand_priority,
+            tuple(tuple(x) for x in cfg.ladder), seqs, cfg.seed, cfg.size_jitter, cfg.rho,
+            tuple(sorted((cfg.per_rank_rho or {}).items())), cfg.noise_rel_std, cfg.clock, cfg.client.retries,
+            cfg.segment_duration_s, cfg.sequence_duration_s)
 
 
 def lower(cfg: ExperimentConfig) -> Lowered:
+    """Validate (the reference's constructor checks) and lower one config; the
+    catalog part is shared by every config with the same _lower_key."""
+    key = _lower_key(cfg)
+    hit = _LOWER_MEMO.get(key)
+    if hit is not None:
+        if not 0 <= int(cfg.seed) < 2 ** 64:           # (part of the key; kept for clarity)
+            raise ConfigError("seed must be in [0, 2**64) for the GPU engine")
+        return dataclasses.replace(hit, cfg=cfg)
     cfg.validate()
     cat = cfg.catalog_config()
     policy = cfg.policy()
     seqs = cat.sequences
-    return Lowered(
+    low = Lowered(
         cfg=cfg,
         seq_ids=[s.id for s in seqs],
         seq_dur=[s.duration_s for s in seqs],
@@ -132,6 +159,12 @@ def lower(cfg: ExperimentConfig) -> Lowered:
         cache_enabled=policy.cache_enabled,
         spec_enabled=policy.speculative_enabled,
     )
+    low.cat_key = (cfg.seed, cfg.size_jitter, tuple(low.seq_ids), tuple(low.seq_dur), tuple(low.seq_segdur),
+                   tuple(sorted(tuple(x) for x in cfg.ladder)))
+    if len(_LOWER_MEMO) > 65536:
+        _LOWER_MEMO.clear()
+    _LOWER_MEMO[key] = low
+    return low
 
 
 class _Pools:
@@ -272,9 +305,39 @@ def _eps_len(low: Lowered) -> int:
     return int(min(cfg.horizon_s / min_svc + 64, 1 << 26))
 
 
+_EPS_MEMO: dict = {}
+_MAN_MEMO: dict = {}
+
+
+def _manifest_bytes(low: Lowered, ladder, key) -> list[int]:
+    """len(json.dumps(manifest_for(seq), sort_keys=True)) per sequence (server.py:58-59)."""
+    man = _MAN_MEMO.get(key)
+    if man is None:
+        man = []
+        for sid, dur, segdur, cnt in zip(low.seq_ids, low.seq_dur, low.seq_segdur, low.counts):
+            m = {"sequence": sid, "duration_s": dur, "segment_duration_s": segdur, "segment_count": cnt,
+                 "representations": [{"rank": r, "bitrate_bps": b} for r, b in ladder],
+                 "url_template": URL_TEMPLATE}
+            man.append(len(json.dumps(m, sort_keys=True).encode("utf-8")))
+        if len(_MAN_MEMO) > 4096:
+            _MAN_MEMO.clear()
+        _MAN_MEMO[key] = man
+    return man
+
+
+def _eps_len_memo(low: Lowered) -> int:
+    cfg = low.cfg
+    key = (cfg.horizon_s, cfg.noise_rel_std, cfg.rho, tuple(sorted((cfg.per_rank_rho or {}).items())),
+           tuple(cfg.ladder[i][0] for i in range(len(cfg.ladder))), tuple(low.seq_segdur), tuple(low.seq_dur))
+    v = _EPS_MEMO.get(key)
+    if v is None:
+        v = _EPS_MEMO[key] = _eps_len(low)
+    return v
+
+
 def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.MODE_RECORDS,
                  caps=None, eps_scale: float = 1, threads: int | None = None, pin: bool = False,
-                 tail_caps=None) -> BatchInputs:
+                 tail_caps=None, list_caps=None) -> BatchInputs:
     """Lower a list of ExperimentConfigs into one device batch (host arrays; page-locked if pin)."""
     L = _lib.lib()
     threads = threads or os.cpu_count() or 1
@@ -307,7 +370,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     for low in lows:
         if low.cfg.netem.trace_dir:
             continue                                   # CSV traces: per-client host tables below
-        key = (low.cfg.seed, dataclasses.astuple(low.cfg.netem))
+        key = (low.cfg.seed, _netem_key(low.cfg.netem))
         prev = trace_groups.get(key, (0, low.cfg.netem))[0]
         trace_groups[key] = (max(prev, low.cfg.clients), low.cfg.netem)
     trace_tab = {}
@@ -333,7 +396,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     for low in lows:
         key = (low.cfg.seed, low.cfg.noise_rel_std)
         k, e = eps_groups.get(key, (0, 0))
-        eps_groups[key] = (max(k, low.cfg.workers), max(e, max(1, int(_eps_len(low) * eps_scale))))
+        eps_groups[key] = (max(k, low.cfg.workers), max(e, max(1, int(_eps_len_memo(low) * eps_scale))))
     eps_tab = {}
     for (seed, noise), (kmax, elen) in eps_groups.items():
         if noise > 0:
@@ -366,8 +429,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         n_seq, n_ranks = len(low.seq_ids), low.n_ranks
         max_nseg = max(low.counts)
         ladder = sorted(cfg.ladder)
-        cat_key = (cfg.seed, cfg.size_jitter, tuple(low.seq_ids), tuple(low.seq_dur), tuple(low.seq_segdur),
-                   tuple(ladder))
+        cat_key = low.cat_key
         o_bitrates = P.add("i64", [b for _, b in ladder], key=("bitrates", tuple(ladder)))
         if ("i64", ("keys", tuple(low.seq_ids))) not in P.memo:
             keys = [int.from_bytes(hashlib.sha256(s.encode("utf-8")).digest()[:8], "big") for s in low.seq_ids]
@@ -386,20 +448,17 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
             tables.append(t)
             input_bytes += 8 * n_seq * n_ranks * max_nseg
         o_sizes = P.memo[("i64", ("sizes", cat_key))]
-        if ("i64", ("manifest", cat_key)) not in P.memo:
-            man = []
-            for sid, dur, segdur, cnt in zip(low.seq_ids, low.seq_dur, low.seq_segdur, low.counts):
-                m = {"sequence": sid, "duration_s": dur, "segment_duration_s": segdur, "segment_count": cnt,
-                     "representations": [{"rank": r, "bitrate_bps": b} for r, b in ladder],
-                     "url_template": URL_TEMPLATE}
-                man.append(len(json.dumps(m, sort_keys=True).encode("utf-8")))   # server.py:58-59
-            P.add("i64", man, key=("manifest", cat_key))
-        o_man = P.memo[("i64", ("manifest", cat_key))]
+        mkey = ("manifest", cat_key[2:])                # manifests do not depend on the seed
+        if ("i64", mkey) not in P.memo:
+            P.add("i64", _manifest_bytes(low, ladder, cat_key[2:]), key=mkey)
+        o_man = P.memo[("i64", mkey)]
         rho_map = cfg.per_rank_rho or {r: cfg.rho for r, _ in ladder}
         o_rho = P.add("f64", [float(rho_map[r]) for r, _ in ladder], key=("rho", tuple(sorted(rho_map.items()))))
         pop = 1 if cfg.popularity == "zipf" else 0
-        o_zipf = P.add("f64", zipf_cdf(n_seq, cfg.zipf_exponent) if pop else np.zeros(n_seq),
-                       key=("zipf", n_seq, pop, cfg.zipf_exponent))
+        zkey = ("zipf", n_seq, pop, cfg.zipf_exponent)
+        o_zipf = P.memo.get(("f64", zkey))
+        if o_zipf is None:
+            o_zipf = P.add("f64", zipf_cdf(n_seq, cfg.zipf_exponent) if pop else np.zeros(n_seq), key=zkey)
         o_arr = arr_tab[(cfg.seed, N, cfg.arrival_rate_per_s)]
         if cfg.netem.trace_dir:                        # orchestrator.py:243-253
             tdir = cfg.netem.trace_dir
@@ -425,7 +484,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
             tt = dict(n=0, period=0.0, grid=0.0, starts=0, values=0, pbits=0,
                       tr_i=P.add("i64", ti), tr_f=P.add("f64", tf))
         else:
-            tt = trace_tab[(cfg.seed, dataclasses.astuple(cfg.netem))]
+            tt = trace_tab[(cfg.seed, _netem_key(cfg.netem))]
         o_eps, eps_stride = eps_tab[(cfg.seed, cfg.noise_rel_std)]
 
         sc = scen[si]
@@ -457,7 +516,10 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.off_eps, sc.eps_stride = o_eps, eps_stride
         sc.scratch_off = scratch_off
         scratch_off += int(L.otf_scratch_bytes(engine, N, K, n_seq, n_ranks, max_nseg))
-        smem_per.append(int(L.otf_shared_bytes(engine, N, K, n_seq, n_ranks, max_nseg)))
+        lc = int(list_caps[si]) if list_caps is not None and list_caps[si] else 0
+        sc.list_cap = lc
+        smem_per.append(int(L.otf_shared_bytes_cap(N, n_seq, n_ranks, max_nseg, lc))
+                        if engine == _lib.ENGINE_WINDOWED else 0)
         shared_bytes = max(shared_bytes, smem_per[-1])
         scratch_off = (scratch_off + 255) & ~255
         tc = tail_caps[si] if tail_caps is not None and tail_caps[si] is not None else default_tail_caps(low)

@@ -23,7 +23,8 @@ import math
 
 from .config import FIXTURE_LADDER, LADDER_10, ExperimentConfig, nominal_ladder_bytes
 
-__all__ = ["c1", "c2", "c3", "c4", "c5", "c3_sweep", "c4_sweep", "c5_sweep", "with_cache_fraction", "C4_CLIENTS", "C4_VARIANTS"]
+__all__ = ["c1", "c2", "c3", "c4", "c5", "c3_sweep", "c4_sweep", "c5_sweep", "c5t_sweep", "with_cache_fraction",
+           "C4_CLIENTS", "C4_VARIANTS"]
 
 C4_CLIENTS = (10, 30, 100, 300, 1000, 3000, 10000)
 C4_VARIANTS = ("B", "T", "TC", "TCP", "TCF", "TCPF")
@@ -95,3 +96,16 @@ def c5_sweep(seeds=range(1, 65), clients: int = 2800):
     """1,024 scenarios = 64 seeds x 4 variants x 4 cache fractions."""
     return [c5(seed=s, variant=v, fraction=f, clients=clients)
             for s in seeds for v in C5_VARIANTS for f in C5_FRACTIONS]
+
+
+C5T_VARIANTS = ("T", "TC", "TCP", "TCF")
+C5T_FRACTIONS = (0.0, 0.005, 0.01, 0.02)
+
+
+def c5t_sweep(seeds=range(1, 65), clients: int = 2800):
+    """The transcode-bound counterpart of config 5 (not a BASELINE config): the same
+    2,800-client / 600 s / 10-rank scenarios with no cache (T) or caches of
+    0-2% of the ladder, so most requests wait on the 4 transcoders.  T ignores the
+    cache size: its four points per seed are the same simulation."""
+    return [c5(seed=s, variant=v, fraction=f, clients=clients)
+            for s in seeds for v in C5T_VARIANTS for f in C5T_FRACTIONS]

@@ -169,3 +169,17 @@ def test_records_only_views_raise_in_histogram_mode():
     assert r.summary()["requests"] > 0
     with pytest.raises(_lib.OtfError):
         r.requests
+
+
+def test_list_overflow_reruns_windowed_with_larger_list():
+    """A transcode-bound config-5 point (TCP, cache 0.5% of the ladder, seed 60) sees a
+    burst of more simultaneous requests than the default 256-entry window list: the
+    engine flags OTF_S_LIST_OVERFLOW and run_batch re-runs it on the windowed engine
+    with a 4x list (not the one-thread exact engine), bit-exact vs the oracle."""
+    cfg = workloads.c5(seed=60, variant="TCP", fraction=0.005)
+    res = engine.run_batch([cfg], mode="histogram")[0]
+    assert res.engine == "windowed" and res.list_cap >= 1024, (res.engine, res.list_cap)
+    want = oracle.run_qoe(cfg)
+    errs = qoe_errors(res.qoe, want, "c5t seed 60")
+    assert not errs, errs
+    assert list(res.stats_raw[:18]) == want["stats"]

@@ -16,11 +16,13 @@ import sys
 
 path, cubin, kern = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+SRC = sys.argv[5] if len(sys.argv) > 5 else "paper_2603_08417_b200/csrc"     # the measured build's sources
 rows = list(csv.reader(open(path)))
 hdr = rows[1]
 data = [dict(zip(hdr, r)) for r in rows[2:] if r and r[0].startswith("0x")]
 txt = subprocess.run(["nvdisasm", "-gi", cubin], capture_output=True, text=True).stdout
 line_of, cur, opc = {}, None, {}
+fresh = True
 inside = False
 for ln in txt.split("\n"):
     if ln.startswith("//--------------------- .text."):
@@ -30,9 +32,13 @@ for ln in txt.split("\n"):
         continue
     m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
     if m:
-        cur = (m.group(1).split("/")[-1], int(m.group(2)))
+        if fresh:                                      # the first location line of a block is the
+            cur = (m.group(1).split("/")[-1], int(m.group(2)))   # innermost inlined frame
+            fresh = False
         continue
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/\s+(\S.*?);', ln)
+    if m:
+        fresh = True
     if m and cur:
         off = int(m.group(1), 16)
         line_of[off] = cur
@@ -62,7 +68,7 @@ print(f"total samples {tot}; {len(data)} SASS instructions, {hot} executed; opco
 for (f, ln), s in agg.most_common(top):
     if f not in files:
         try:
-            files[f] = open(subprocess.run(["bash", "-c", f"ls paper_2603_08417_b200/csrc/{f} 2>/dev/null || true"],
+            files[f] = open(subprocess.run(["bash", "-c", f"ls {SRC}/{f} 2>/dev/null || true"],
                                            capture_output=True, text=True).stdout.strip()).read().split("\n")
         except Exception:
             files[f] = []
