@@ -756,9 +756,7 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane, uint32_
 }
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+    return __reduce_add_sync(0xffffffffu, v);          // one REDUX (sm_80+), not five shuffles
 }
 
 __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
@@ -860,10 +858,13 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
         c_enq += ((f >> 5) & 1u) + ((f >> 6) & 1u);
         c_enq_d += (f >> 5) & 1u;
     }
-    uint32_t n_imm, n_tch, n_enq;
-    uint32_t p_imm = warp_excl_scan(c_imm, lane, n_imm);
-    uint32_t p_tch = warp_excl_scan(c_tch, lane, n_tch);
-    uint32_t p_enq = warp_excl_scan(c_enq, lane, n_enq);
+    // one scan for all three counts: 10-bit fields (n <= PAR_MAX = 256 requests, so
+    // every prefix and total is < 2 * 256 + 1 < 1024 and no field carries into the next)
+    static_assert(2 * PAR_MAX < 1024, "packed scan fields");
+    uint32_t n_pk;
+    const uint32_t p_pk = warp_excl_scan(c_imm | (c_tch << 10) | (c_enq << 20), lane, n_pk);
+    uint32_t p_imm = p_pk & 1023u, p_tch = (p_pk >> 10) & 1023u, p_enq = p_pk >> 20;
+    const uint32_t n_imm = n_pk & 1023u, n_tch = (n_pk >> 10) & 1023u, n_enq = n_pk >> 20;
     const uint32_t n_enq_d = warp_sum(c_enq_d);
     // the server lane's scalars (lane 0's registers) as the bases
     const int64_t req_base = __shfl_sync(0xffffffffu, (long long)w.req_counter, 0);
@@ -1442,7 +1443,7 @@ __device__ __forceinline__ void wharvest(Win &w, WClient &c, int32_t cid, double
 }
 
 __device__ __forceinline__ int32_t warp_min(int32_t v) {
-    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    v = __reduce_min_sync(0xffffffffu, v);
     return v;
 }
 
@@ -1623,11 +1624,12 @@ __device__ int32_t wheel_next(WinHeader *h, int32_t k_done, int lane) {
     return warp_min(best);
 }
 
-#ifdef WIN_PF_RESP
+#ifndef WIN_NO_PF_RESP
 // Warm L2 with what the request's response chain reads in phase B (a cache hit
 // answers at the request's own arrival time): the client's hot state, the trace
 // sample the transfer starts in, the trace's period bits and the segment size.
-// Issued by all lanes at the window's gather, ~15 k cycles before phase B.
+// Issued by all lanes at the window's gather, ~15 k cycles before phase B
+// (measured: -0.9% on the config-5 sweep, profiles/r02f_ab_redux_prefetch.txt).
 __device__ __forceinline__ void prefetch_response(const Win &w, const SrvEnt &e) {
     const Scn &S = w.S;
     asm volatile("prefetch.global.L2 [%0];" :: "l"(w.cl + e.cid));
@@ -1923,7 +1925,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                         const bool two = i + 32 < ns;
                         SrvEnt f;
                         if (two) f = as[i + 32];
-#ifdef WIN_PF_RESP
+#ifndef WIN_NO_PF_RESP
                         prefetch_response(w, e);
                         if (two) prefetch_response(w, f);
 #endif
