@@ -1516,6 +1516,51 @@ __device__ void sort_list(Win &w, int lane) {
         return;
     }
 #endif
+#ifdef WIN_QSORT
+    if (n <= RANK_SORT_MAX) {
+        // fast path: rank by a 32-bit fixed-point key q = (t - window start) * 2^32 / W,
+        // broadcast by shuffle.  q is monotone non-decreasing in t, so if the ranks come
+        // out a permutation the order is the time order; equal keys collide, which the
+        // check after the scatter sees (a position left unwritten) -- then the list is
+        // restored and ranked exactly below.
+        const int32_t i0 = lane, i1 = lane + 32;
+        const bool v0 = i0 < n, v1 = i1 < n;
+        const double w0 = v0 ? w.lw[i0] : INFINITY, w1 = v1 ? w.lw[i1] : INFINITY;
+        const int16_t c0 = v0 ? w.li[i0] : 0, c1 = v1 ? w.li[i1] : 0;
+        const uint16_t d0 = v0 ? w.ld[i0] : 0, d1 = v1 ? w.ld[i1] : 0;
+        const int32_t s0 = v0 ? w.lp[i0] : 0, s1 = v1 ? w.lp[i1] : 0;
+        const double base = (double)w.k * w.W, scale = w.invW * 4294967296.0;
+        const double x0 = (w0 - base) * scale, x1 = (w1 - base) * scale;
+        const uint32_t q0 = x0 <= 0.0 ? 0u : x0 >= 4294967295.0 ? 0xffffffffu : (uint32_t)x0;
+        const uint32_t q1 = x1 <= 0.0 ? 0u : x1 >= 4294967295.0 ? 0xffffffffu : (uint32_t)x1;
+        int32_t r0 = 0, r1 = 0;
+#pragma unroll 2
+        for (int32_t j = 0; j < n; j++) {
+            const uint32_t qj = __shfl_sync(0xffffffffu, j < 32 ? q0 : q1, j & 31);
+            r0 += (int32_t)(qj < q0);
+            r1 += (int32_t)(qj < q1);
+        }
+        __syncwarp();                                  // every lane has read the list
+        if (v0) w.lw[i0] = NAN;                        // unwritten positions stay NaN
+        if (v1) w.lw[i1] = NAN;
+        __syncwarp();
+        if (v0) { w.lw[r0] = w0; w.li[r0] = c0; w.ld[r0] = d0; w.lp[r0] = s0; }
+        if (v1) { w.lw[r1] = w1; w.li[r1] = c1; w.ld[r1] = d1; w.lp[r1] = s1; }
+        __syncwarp();
+        // strictly increasing and every position written: the exact order, no ties
+        const bool ok0 = !v0 || (w.lw[i0] == w.lw[i0] && (i0 == 0 || w.lw[i0] > w.lw[i0 - 1]));
+        const bool ok1 = !v1 || (w.lw[i1] == w.lw[i1] && w.lw[i1] > w.lw[i1 - 1]);
+        if (__all_sync(0xffffffffu, ok0 && ok1)) {
+            if (lane == 0) h->n_ties = 0;
+            __syncwarp();
+            return;
+        }
+        __syncwarp();                                  // collision or tie: restore, rank exactly
+        if (v0) { w.lw[i0] = w0; w.li[i0] = c0; w.ld[i0] = d0; w.lp[i0] = s0; }
+        if (v1) { w.lw[i1] = w1; w.li[i1] = c1; w.ld[i1] = d1; w.lp[i1] = s1; }
+        __syncwarp();
+    }
+#endif
     if (n <= RANK_SORT_MAX) {
         // each lane ranks elements lane and lane + 32 in one pass over the list (one
         // broadcast load per j for both).  Non-negative doubles order like
@@ -1579,6 +1624,46 @@ __device__ void sort_list(Win &w, int lane) {
     bool any = __any_sync(0xffffffffu, tie);
     if (lane == 0) h->n_ties = any ? 1 : 0;
     __syncwarp();
+}
+
+// Two-warp bitonic sort of a large window's list (NW = 2: the big client classes,
+// e.g. ~180 requests per window at 10,000 clients): both warps take the
+// compare-exchanges of every stage, a CTA barrier between stages.  Called by all
+// threads after the window selection; the result and the tie flag are the same
+// as sort_list's.
+__device__ void sort_list_cta(Win &w, int tid, int nthreads) {
+    WinHeader *h = w.h;
+    const int32_t n = h->n_list;
+    int32_t p = 1;
+    while (p < n) p <<= 1;
+    OTF_NOUNROLL
+    for (int32_t i = n + tid; i < p; i += nthreads) { w.lw[i] = INFINITY; w.li[i] = 32767; }
+    __syncthreads();
+    for (int32_t size = 2; size <= p; size <<= 1) {
+        for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            OTF_NOUNROLL
+            for (int32_t t = tid; t < (p >> 1); t += nthreads) {
+                const int32_t lo = 2 * t - (t & (stride - 1));
+                const int32_t hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const double wl = w.lw[lo], wh = w.lw[hi];
+                const int32_t il = w.li[lo], ih = w.li[hi];
+                if (key_gt(wl, il, wh, ih) == up) {
+                    w.lw[lo] = wh; w.lw[hi] = wl;
+                    w.li[lo] = (int16_t)ih; w.li[hi] = (int16_t)il;
+                    const uint16_t td = w.ld[lo]; w.ld[lo] = w.ld[hi]; w.ld[hi] = td;
+                    const int32_t tp = w.lp[lo]; w.lp[lo] = w.lp[hi]; w.lp[hi] = tp;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    bool tie = false;                                  // any equal request times? (rare)
+    OTF_NOUNROLL
+    for (int32_t i = tid + 1; i < n; i += nthreads) tie |= w.lw[i] == w.lw[i - 1];
+    const int any = __syncthreads_or(tie ? 1 : 0);
+    if (tid == 0) h->n_ties = any ? 1 : 0;
+    __syncthreads();
 }
 
 // Equal request times (rare): order each tie group by arm time (the tick order
@@ -1967,9 +2052,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
                     t1 = WCLOCK();
                     if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
                     t0 = t1;
-                    sort_list(w, lane);
-                    t1 = WCLOCK();
-                    if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
+                    if (WIN_WARPS == 1 || nlist <= RANK_SORT_MAX) {   // else both warps, below
+                        sort_list(w, lane);
+                        t1 = WCLOCK();
+                        if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
+                    }
                 }
             }
             if (lane == 0) h->ctl = ctl;
@@ -1978,6 +2065,13 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
         const int32_t ctl = h->ctl;
         if (ctl == CTL_STOP) break;
         if (ctl == CTL_REFILE) continue;
+        if constexpr (WIN_WARPS == 2) {
+            if (h->n_list > RANK_SORT_MAX) {           // a large window: both warps sort it
+                t0 = WCLOCK();
+                sort_list_cta(w, tid, WIN_THREADS);
+                if (tid == 0) h->stats[OTF_ST_CYC_SORT] += WCLOCK() - t0;
+            }
+        }
         const int32_t m = h->cur_m;
         w.k = m;
         w.E = (double)(m + 1) * w.W;
@@ -2132,6 +2226,8 @@ int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return 1;
     }
+    if (const char *e = getenv("OTF_WIN_CARVEOUT"))    // A/B: shared-memory carveout in percent (L1 size)
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     kern<<<b.n_scenarios, 32 * nw, smem, stream>>>(b);
     return 0;
 }

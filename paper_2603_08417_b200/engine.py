@@ -103,7 +103,10 @@ class DeviceBatch:
         order = np.lexsort((-cost, cls)).astype(np.int32)   # by class, then longest first
         self.order = torch.from_numpy(order).to(dev)
         self.groups = []
-        for c in np.unique(cls):
+        # the group holding the longest scenario launches first: its CTAs reach the SMs
+        # first, and the groups' kernels then run concurrently around it
+        classes = sorted(np.unique(cls), key=lambda c: -cost[cls == c].max())
+        for c in classes:
             idx = np.nonzero(cls[order] == c)[0]
             gb = _lib.Batch.from_buffer_copy(b)
             gb.n_scenarios = int(len(idx))
@@ -161,11 +164,14 @@ class DeviceBatch:
             rc = self.lib.otf_run_batch(ctypes.byref(self.batch), self.inp.engine, s.cuda_stream)
             _lib.check(rc, "otf_run_batch")
             return
-        # size classes run concurrently on side streams, joined back to `s`
+        # size classes run concurrently on side streams, joined back to `s`: the side
+        # streams wait for what precedes the launches (generation), not for group 0
+        ready = torch.cuda.Event()
+        ready.record(s)
         rc = self.lib.otf_run_batch(ctypes.byref(self.groups[0]), self.inp.engine, s.cuda_stream)
         _lib.check(rc, "otf_run_batch")
         for gb, st in zip(self.groups[1:], self.streams):
-            st.wait_stream(s)
+            st.wait_event(ready)
             rc = self.lib.otf_run_batch(ctypes.byref(gb), self.inp.engine, st.cuda_stream)
             _lib.check(rc, "otf_run_batch")
         for st in self.streams:

@@ -24,13 +24,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--nw", default="auto")
 ap.add_argument("--ns", default="1,2,4,8")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--seeds", type=int, default=0, help="time the first SEEDS seed groups instead of the N-GPU shards")
 args = ap.parse_args()
 if args.nw != "auto":
     os.environ["OTF_WIN_NW"] = args.nw
 full = workloads.c5_sweep(seeds=range(1, 65))
-for n in [int(x) for x in args.ns.split(",")]:
+for n in ([1] if args.seeds else [int(x) for x in args.ns.split(",")]):
     mine = dist.shard(full, 0, n)
-    cfgs = [full[i] for i in mine]
+    cfgs = [full[i] for i in mine] if not args.seeds else full[:16 * args.seeds]
     inp = inputs.build_inputs(cfgs, engine=_lib.ENGINE_WINDOWED, mode=_lib.MODE_HISTOGRAM, pin=True)
     db = engine.DeviceBatch(inp, pin=True)
     db.launch()
