@@ -1516,7 +1516,7 @@ __device__ void sort_list(Win &w, int lane) {
         return;
     }
 #endif
-#ifdef WIN_QSORT
+#ifndef WIN_NO_QSORT
     if (n <= RANK_SORT_MAX) {
         // fast path: rank by a 32-bit fixed-point key q = (t - window start) * 2^32 / W,
         // broadcast by shuffle.  q is monotone non-decreasing in t, so if the ranks come
