@@ -1013,6 +1013,32 @@ __device__ __forceinline__ bool parallel_ok(Win &w) {
            (lq_tail - lq_head + (uint32_t)n <= w.lq_mask);   // room for every touch
 }
 
+#ifndef WIN_NO_PREFIX
+// A window where a transcode completes (1-2% of config-5 windows) is otherwise
+// serial.  Its requests strictly before the earliest completion cannot see it, so
+// when every other condition of the parallel pass holds, that prefix of the
+// sorted list takes the parallel pass and the serial lane starts after it.
+// Returns the prefix length (0: no split).  Lane 0.
+__device__ __forceinline__ int32_t parallel_prefix(Win &w) {
+    const WinHeader *h = w.h;
+    const otf_scenario &sc = *w.S.sc;
+    const int32_t n = h->n_list;
+    if (n < 2 || h->n_ties != 0 || h->fq_n != 0 || sc.demand_priority != 0 || sc.queue_bound > 0 ||
+        (h->gq_n != 0 && h->hand_safe == 0))
+        return 0;
+    double t_w = INFINITY;                             // the earliest completion due in this window
+    for (int32_t q = 0; q < sc.n_workers; q++)
+        if (h->wk[q].win == w.k) t_w = fmin(t_w, h->wk[q].when);
+    int32_t lo = 0, hi = n < PAR_MAX ? n : PAR_MAX;   // requests with time < t_w: a prefix of the list
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (w.lw[mid] < t_w) lo = mid + 1; else hi = mid;
+    }
+    if (lo < 2 || h->lq_tail - h->lq_head + (uint32_t)lo > w.lq_mask) return 0;
+    return lo;
+}
+#endif
+
 // Arm time of window request `cid` (rare tie-breaks only): the window's bucket
 // entries carry it; a request pushed past a full bucket kept it in its WCold.
 __device__ __noinline__ double req_ctime_at(const SrvEnt *as, int32_t ns, const WCold *wc, int32_t cid) {
@@ -1025,7 +1051,7 @@ __device__ __forceinline__ double req_ctime(const Win &w, int32_t cid) {
 }
 
 // Phase A: replay the window's server events in (time, creation, tick) order.
-__device__ void phase_a(Win &w) {
+__device__ void phase_a(Win &w, int32_t i0) {
     WinHeader *h = w.h;
     const int32_t K = w.S.sc->n_workers;
     const int32_t n = h->n_list;
@@ -1038,12 +1064,12 @@ __device__ void phase_a(Win &w) {
     w.wdirty = due != 0;
     int32_t bw = -1;
     double bw_when = 0.0, bw_ctime = 0.0;
-    int32_t i = 0;
+    int32_t i = i0;                                    // requests before i0 took the parallel pass
     double cw = 0.0;                                   // next request, loaded one event ahead
     int32_t ncid = 0, nd = 0, npk = 0;
-    if (n > 0) { cw = w.lw[0]; ncid = w.li[0]; nd = w.ld[0]; npk = w.lp[0]; }
+    if (i < n) { cw = w.lw[i]; ncid = w.li[i]; nd = w.ld[i]; npk = w.lp[i]; }
     const int32_t *segcount = w.S.segcounts;
-    w.pops += n;                                       // every request is one timer pop
+    w.pops += n - i0;                                  // every request is one timer pop
     for (;;) {
         if (w.wdirty) {                                // earliest worker timer in this window
             bw = -1;
@@ -1453,6 +1479,70 @@ __device__ __forceinline__ bool key_gt(double wa, int32_t ia, double wb, int32_t
     return wa > wb || (wa == wb && ia > ib);
 }
 
+#ifndef WIN_NO_QSORT
+// Fast rank sort of a window's n <= 32 E server events (lane l holds positions
+// l, l + 32, ...): rank by a 32-bit fixed-point key q = (t - window start) *
+// 2^32 / W, broadcast by shuffle.  q is monotone non-decreasing in t, so if the
+// ranks form a permutation the order is the time order; equal keys collide,
+// which the check after the scatter sees (a position left unwritten, or not
+// strictly increasing: a tie).  Then the list is restored and false returned,
+// and the exact sorts run.
+template <int E>
+__device__ __forceinline__ bool qsort_fast(Win &w, int lane, int32_t n) {
+    double t[E];
+    int16_t c[E];
+    uint16_t d[E];
+    int32_t p[E], r[E];
+    uint32_t q[E];
+    const double base = (double)w.k * w.W, scale = w.invW * 4294967296.0;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int32_t i = lane + 32 * e;
+        const bool v = i < n;
+        t[e] = v ? w.lw[i] : INFINITY;
+        c[e] = v ? w.li[i] : 0;
+        d[e] = v ? w.ld[i] : 0;
+        p[e] = v ? w.lp[i] : 0;
+        const double x = (t[e] - base) * scale;
+        q[e] = x <= 0.0 ? 0u : x >= 4294967295.0 ? 0xffffffffu : (uint32_t)x;
+        r[e] = 0;
+    }
+#pragma unroll 2
+    for (int32_t j = 0; j < n; j++) {
+        uint32_t src = q[0];
+#pragma unroll
+        for (int e = 1; e < E; e++) src = (j >> 5) == e ? q[e] : src;
+        const uint32_t qj = __shfl_sync(0xffffffffu, src, j & 31);
+#pragma unroll
+        for (int e = 0; e < E; e++) r[e] += (int32_t)(qj < q[e]);
+    }
+    __syncwarp();                                      // every lane has read the list
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        if (lane + 32 * e < n) w.lw[lane + 32 * e] = NAN;   // unwritten positions stay NaN
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        if (lane + 32 * e < n) { w.lw[r[e]] = t[e]; w.li[r[e]] = c[e]; w.ld[r[e]] = d[e]; w.lp[r[e]] = p[e]; }
+    __syncwarp();
+    bool ok = true;                                    // strictly increasing, every position written
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int32_t i = lane + 32 * e;
+        if (i < n) ok &= w.lw[i] == w.lw[i] && (i == 0 || w.lw[i] > w.lw[i - 1]);
+    }
+    if (__all_sync(0xffffffffu, ok)) return true;
+    __syncwarp();                                      // collision or tie: restore the list
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int32_t i = lane + 32 * e;
+        if (i < n) { w.lw[i] = t[e]; w.li[i] = c[e]; w.ld[i] = d[e]; w.lp[i] = p[e]; }
+    }
+    __syncwarp();
+    return false;
+}
+#endif
+
 // Order the window's server events by time: rank sort for small windows, in-place
 // bitonic sort for large ones.  Equal times are flagged afterwards; order_ties
 // then orders each group by arm time, a result independent of the group's order.
@@ -1517,48 +1607,13 @@ __device__ void sort_list(Win &w, int lane) {
     }
 #endif
 #ifndef WIN_NO_QSORT
-    if (n <= RANK_SORT_MAX) {
-        // fast path: rank by a 32-bit fixed-point key q = (t - window start) * 2^32 / W,
-        // broadcast by shuffle.  q is monotone non-decreasing in t, so if the ranks come
-        // out a permutation the order is the time order; equal keys collide, which the
-        // check after the scatter sees (a position left unwritten) -- then the list is
-        // restored and ranked exactly below.
-        const int32_t i0 = lane, i1 = lane + 32;
-        const bool v0 = i0 < n, v1 = i1 < n;
-        const double w0 = v0 ? w.lw[i0] : INFINITY, w1 = v1 ? w.lw[i1] : INFINITY;
-        const int16_t c0 = v0 ? w.li[i0] : 0, c1 = v1 ? w.li[i1] : 0;
-        const uint16_t d0 = v0 ? w.ld[i0] : 0, d1 = v1 ? w.ld[i1] : 0;
-        const int32_t s0 = v0 ? w.lp[i0] : 0, s1 = v1 ? w.lp[i1] : 0;
-        const double base = (double)w.k * w.W, scale = w.invW * 4294967296.0;
-        const double x0 = (w0 - base) * scale, x1 = (w1 - base) * scale;
-        const uint32_t q0 = x0 <= 0.0 ? 0u : x0 >= 4294967295.0 ? 0xffffffffu : (uint32_t)x0;
-        const uint32_t q1 = x1 <= 0.0 ? 0u : x1 >= 4294967295.0 ? 0xffffffffu : (uint32_t)x1;
-        int32_t r0 = 0, r1 = 0;
-#pragma unroll 2
-        for (int32_t j = 0; j < n; j++) {
-            const uint32_t qj = __shfl_sync(0xffffffffu, j < 32 ? q0 : q1, j & 31);
-            r0 += (int32_t)(qj < q0);
-            r1 += (int32_t)(qj < q1);
-        }
-        __syncwarp();                                  // every lane has read the list
-        if (v0) w.lw[i0] = NAN;                        // unwritten positions stay NaN
-        if (v1) w.lw[i1] = NAN;
+#ifndef WIN_QSORT_MAX
+#define WIN_QSORT_MAX 128                              // fast rank sort up to this many events
+#endif
+    if (n <= 64 ? qsort_fast<2>(w, lane, n) : n <= WIN_QSORT_MAX && qsort_fast<4>(w, lane, n)) {
+        if (lane == 0) h->n_ties = 0;
         __syncwarp();
-        if (v0) { w.lw[r0] = w0; w.li[r0] = c0; w.ld[r0] = d0; w.lp[r0] = s0; }
-        if (v1) { w.lw[r1] = w1; w.li[r1] = c1; w.ld[r1] = d1; w.lp[r1] = s1; }
-        __syncwarp();
-        // strictly increasing and every position written: the exact order, no ties
-        const bool ok0 = !v0 || (w.lw[i0] == w.lw[i0] && (i0 == 0 || w.lw[i0] > w.lw[i0 - 1]));
-        const bool ok1 = !v1 || (w.lw[i1] == w.lw[i1] && w.lw[i1] > w.lw[i1 - 1]);
-        if (__all_sync(0xffffffffu, ok0 && ok1)) {
-            if (lane == 0) h->n_ties = 0;
-            __syncwarp();
-            return;
-        }
-        __syncwarp();                                  // collision or tie: restore, rank exactly
-        if (v0) { w.lw[i0] = w0; w.li[i0] = c0; w.ld[i0] = d0; w.lp[i0] = s0; }
-        if (v1) { w.lw[i1] = w1; w.li[i1] = c1; w.ld[i1] = d1; w.lp[i1] = s1; }
-        __syncwarp();
+        return;
     }
 #endif
     if (n <= RANK_SORT_MAX) {
@@ -2083,16 +2138,33 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(cons
 #ifdef WIN_DIAG
             long long dgp = clock64();
 #endif
-            if (tid == 0) par = parallel_ok(w) ? 1 : 0;
+            int32_t pre = 0;
+            if (tid == 0) {
+                par = parallel_ok(w) ? 1 : 0;
+#ifndef WIN_NO_PREFIX
+                if (!par) pre = parallel_prefix(w);
+#endif
+            }
 #ifdef WIN_DIAG
             if (tid == 0) h->stats[30] += clock64() - dgp;
 #endif
-            if (warp == 0) par = __shfl_sync(0xffffffffu, par, 0);
-            if (par && warp == 0) {
+            if (warp == 0) {
+                par = __shfl_sync(0xffffffffu, par, 0);
+                pre = __shfl_sync(0xffffffffu, pre, 0);
+            }
+            // one call site each (phase_a_parallel is inlined; a second copy of it, or a
+            // non-inlined phase_a taking `w` by reference, costs hot code / a stack frame)
+            if (warp == 0 && (par | pre)) {
+                const int32_t n_all = h->n_list;
+                __syncwarp();
+                if (pre && lane == 0) h->n_list = pre;     // the prefix before the completion
+                __syncwarp();
                 phase_a_parallel(w, lane);
-            } else if (tid == 0) {
-                if (h->n_ties) order_ties(w);
-                phase_a(w);
+                if (pre && lane == 0) h->n_list = n_all;
+            }
+            if (tid == 0 && !par) {                    // the serial lane (after a parallel prefix)
+                if (!pre && h->n_ties) order_ties(w);
+                phase_a(w, pre);
             }
             if (tid == 0) {
                 h->k_done = m;
