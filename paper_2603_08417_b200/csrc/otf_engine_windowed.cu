@@ -63,6 +63,10 @@ constexpr int PAR_MAX = 256;       // windows up to this many requests may take 
 #define WIN_SORT_UNROLL 2
 #endif
 constexpr int SORT_UNROLL = WIN_SORT_UNROLL;
+#ifndef WIN_QSORT_UNROLL
+#define WIN_QSORT_UNROLL 2                           // fast rank sort's loop unroll (A/B switch)
+#endif
+constexpr int QSORT_UNROLL = WIN_QSORT_UNROLL;
 #ifdef WIN_NO_PHASE_CYCLES                           // per-phase cycle counters (tools/probe.py)
 #define WCLOCK() 0LL
 #else
@@ -1326,8 +1330,9 @@ __device__ __forceinline__ bool wsegment_done(Win &w, WClient &c, int32_t cid, d
     atomicAdd(&S.qa->n_segments, 1u);
     wsync_session(w, c, now);
     c.index++;
+    // the final advance(now) (client.py:270) is a no-op here: on_segment just synced
+    // the buffer at this same instant (dt = 0 changes neither level nor stall time)
     if (c.index < S.segcount(c.seq)) return true;
-    wbuf_advance(c, now);
     return false;
 }
 
@@ -1507,7 +1512,7 @@ __device__ __forceinline__ bool qsort_fast(Win &w, int lane, int32_t n) {
         q[e] = x <= 0.0 ? 0u : x >= 4294967295.0 ? 0xffffffffu : (uint32_t)x;
         r[e] = 0;
     }
-#pragma unroll 2
+#pragma unroll QSORT_UNROLL
     for (int32_t j = 0; j < n; j++) {
         uint32_t src = q[0];
 #pragma unroll
