@@ -192,19 +192,26 @@ def _write(path, schema_key: str, config_hex: str, rows) -> None:
 
 
 def read_csv(path, schema_key: str):
-    """metrics.py:165-181"""
-    name, columns = SCHEMAS[schema_key]
+    """Load a bundle CSV written by `_write` (the reader of metrics.py:165-181):
+    (header tags, rows as dicts).  The `# schema=... config=...` tag line and the
+    column row must match the writer's current schema, else ValueError."""
+    want_name, want_cols = SCHEMAS[schema_key]
     with open(path, newline="", encoding="utf-8") as fh:
-        first = fh.readline().strip()
-        if not first.startswith("# schema="):
+        rows = csv.reader(fh)
+        tag = next(rows, [""])
+        tag_line = ",".join(tag).strip()
+        if not tag_line.startswith("# schema="):
             raise ValueError(f"{path}: missing schema header")
-        fields = dict(part.split("=", 1) for part in first[2:].split())
-        if fields.get("schema") != name:
-            raise ValueError(f"{path}: schema {fields.get('schema')!r} != expected {name!r}")
-        reader = csv.DictReader(fh)
-        if reader.fieldnames != columns:
-            raise ValueError(f"{path}: columns {reader.fieldnames} != expected {columns}")
-        return fields, list(reader)
+        tags = {}
+        for item in tag_line[1:].split():
+            key, _, val = item.partition("=")
+            tags[key] = val
+        if tags.get("schema") != want_name:
+            raise ValueError(f"{path}: schema {tags.get('schema')!r} != expected {want_name!r}")
+        cols = next(rows, None)
+        if cols != want_cols:
+            raise ValueError(f"{path}: columns {cols} != expected {want_cols}")
+        return tags, [dict(zip(cols, r)) for r in rows]
 
 
 def _opt(x: float):

@@ -49,9 +49,13 @@ def test_size_tables_match_oracle(golden):
         assert np.array_equal(br.sizes(i), want), cfg
 
 
-@pytest.mark.parametrize("eng", ["exact", "windowed"])
-def test_golden_parity_batched(golden, eng):
-    """All golden configs in ONE launch, each bit-exact vs the reference."""
+@pytest.mark.parametrize("eng,nw", [("exact", ""), ("windowed", ""), ("windowed", "1"), ("windowed", "2")])
+def test_golden_parity_batched(golden, eng, nw, monkeypatch):
+    """All golden configs in ONE launch, each bit-exact vs the reference; the windowed
+    engine also with one and with two warps per scenario forced (a small batch picks
+    two by default, full sweeps one)."""
+    if nw:
+        monkeypatch.setenv("OTF_WIN_NW", nw)
     names = sorted(golden)
     cfgs = [_cfg(golden[n][1]) for n in names]
     results = engine.run_batch(cfgs, mode="records", engine=eng)
