@@ -1691,77 +1691,9 @@ __device__ void sort_list(Win &w, int lane) {
 // compare-exchanges of every stage, a CTA barrier between stages.  Called by all
 // threads after the window selection; the result and the tie flag are the same
 // as sort_list's.
-#ifndef WIN_NO_QSORT
-// The fast rank sort of qsort_fast over a CTA of NT threads (NT = 64: two warps,
-// E keys per thread, n <= NT * E): the 32-bit keys go to the free upper half of
-// the list's pack array (2n <= list capacity) and every thread ranks its
-// elements against all n of them (broadcast loads).  Same collision check and
-// restore as qsort_fast; false -> the exact sort runs.
-template <int NT, int E>
-__device__ __forceinline__ bool qsort_fast_cta(Win &w, int tid, int32_t n) {
-    const int32_t cap = w.h->list_cap;
-    uint32_t *qs = reinterpret_cast<uint32_t *>(w.lp) + cap / 2;
-    double t[E];
-    int16_t c[E];
-    uint16_t d[E];
-    int32_t p[E], r[E];
-    uint32_t q[E];
-    const double base = (double)w.k * w.W, scale = w.invW * 4294967296.0;
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        const int32_t i = tid + NT * e;
-        const bool v = i < n;
-        t[e] = v ? w.lw[i] : INFINITY;
-        c[e] = v ? w.li[i] : 0;
-        d[e] = v ? w.ld[i] : 0;
-        p[e] = v ? w.lp[i] : 0;
-        const double x = (t[e] - base) * scale;
-        q[e] = x <= 0.0 ? 0u : x >= 4294967295.0 ? 0xffffffffu : (uint32_t)x;
-        r[e] = 0;
-        if (v) qs[i] = q[e];
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int32_t j = 0; j < n; j++) {
-        const uint32_t qj = qs[j];
-#pragma unroll
-        for (int e = 0; e < E; e++) r[e] += (int32_t)(qj < q[e]);
-    }
-#pragma unroll
-    for (int e = 0; e < E; e++)
-        if (tid + NT * e < n) w.lw[tid + NT * e] = NAN;   // every thread has its payloads in registers
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < E; e++)
-        if (tid + NT * e < n) { w.lw[r[e]] = t[e]; w.li[r[e]] = c[e]; w.ld[r[e]] = d[e]; w.lp[r[e]] = p[e]; }
-    __syncthreads();
-    bool ok = true;                                    // strictly increasing, every position written
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        const int32_t i = tid + NT * e;
-        if (i < n) ok &= w.lw[i] == w.lw[i] && (i == 0 || w.lw[i] > w.lw[i - 1]);
-    }
-    if (__syncthreads_and(ok ? 1 : 0)) return true;
-#pragma unroll
-    for (int e = 0; e < E; e++) {                      // collision or tie: restore the list
-        const int32_t i = tid + NT * e;
-        if (i < n) { w.lw[i] = t[e]; w.li[i] = c[e]; w.ld[i] = d[e]; w.lp[i] = p[e]; }
-    }
-    __syncthreads();
-    return false;
-}
-#endif
-
 __device__ void sort_list_cta(Win &w, int tid, int nthreads) {
     WinHeader *h = w.h;
     const int32_t n = h->n_list;
-#ifndef WIN_NO_QSORT
-    if (nthreads == 64 && n <= 256 && 2 * n <= h->list_cap && qsort_fast_cta<64, 4>(w, tid, n)) {
-        if (tid == 0) h->n_ties = 0;
-        __syncthreads();
-        return;
-    }
-#endif
     int32_t p = 1;
     while (p < n) p <<= 1;
     OTF_NOUNROLL
