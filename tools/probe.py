@@ -59,10 +59,14 @@ for w in which:
     if w == "c5sw": timeit("c5x8_h60", [workloads.c5(seed=s, horizon_s=60.0) for s in range(1, 9)], 1, reps=1)
     if w == "c5w": timeit("c5x64", workloads.c5_sweep(seeds=range(1, 5)), 1, reps=1)
     if w == "c5fw": timeit("c5x1024", workloads.c5_sweep(seeds=range(1, 65)), 1, reps=1)
+    if w == "c5tw": timeit("c5t_x1024", workloads.c5t_sweep(seeds=range(1, 65)), 1, reps=1)
 for w in which:
     if w == "c4w":
         cfgs = workloads.c4_sweep(seeds=range(1, 9))
         timeit("c4x8seeds", cfgs, 1, reps=1)
+    if w == "c4T10k":
+        timeit("c4_10k_T", [workloads.c4(seed=s, clients=10000, variant=v) for s in range(1, 9)
+                             for v in ("T", "TC")], 1, reps=1)
     if w == "c4big":
         cfgs = [workloads.c4(seed=s, clients=10000, variant=v) for s in (1, 2) for v in ("TC", "TCPF")]
         timeit("c4_10k", cfgs, 1, reps=1)
