@@ -143,7 +143,7 @@ def build(force: bool = False) -> str:
     srcs.append(os.path.join(os.path.dirname(HERE), "include", "otfgpu.h"))
     stale = not os.path.exists(LIB_PATH) or any(os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in srcs)
     if force or stale:
-        subprocess.run(["make", "-s", "-C", CSRC], check=True)
+        subprocess.run(["make", "-s"] + (["-B"] if force else []) + ["-C", CSRC], check=True)
     return LIB_PATH
 
 
