@@ -30,6 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "simulated segment requests/sec (device-timed) at 1/2/4/8 B200 vs CPU ref"
+PY_REF_ONE_CORE = 4734.0   # the Python reference (otfstream run_experiment), measured once; see cpu_baseline
 UNIT = "requests/s"
 
 
@@ -370,6 +371,12 @@ def main():
         if bad:
             raise RuntimeError(f"GPU results differ from the oracle on scenarios {bad[:10]}")
         cpu = {"value": v, "unit": UNIT, "cores": c, "kind": "port", "sample": sample,
+               # the unmodified Python reference cannot run on the GPU box (it is not shipped
+               # there); measured in the build container, one core, config 5's shape at 120 s
+               # (TCPF, uniform picks, seed 1): 254,821 requests in 53.8 s
+               "python_reference_one_core": {"value": PY_REF_ONE_CORE, "unit": UNIT,
+                                             "where": "build container (not the GPU box)",
+                                             "config": "config 5 shape, 120 s, TCPF, uniform popularity, seed 1"},
                "parity": {"scenarios_checked": len(digests), "mismatches": 0,
                           "fields": "requests, sessions, segments, jobs, backend/cache stats, response paths"}}
 
