@@ -1,12 +1,6 @@
 set -x
-R=${ROUND_TAG:-r02w}
-OTFGPU_LIB_OVERRIDE=$PWD/build/q4only/libotfgpu.so timeout 900 python -m pytest -x -q tests/test_gpu_parity.py tests/test_gpu_summary.py -k "golden or config5_full or config3" > gpurun_out/${R}_parity.log 2>&1; echo parity=$?
-tail -1 gpurun_out/${R}_parity.log
-for rep in 1 2 3; do
-for v in "" build/q4only/; do
-  if [ -z "$v" ]; then unset OTFGPU_LIB_OVERRIDE; name=intree; else export OTFGPU_LIB_OVERRIDE=$PWD/${v}libotfgpu.so; name=$(basename $v); fi
-  echo "== $name rep $rep $(timeout 300 python tools/probe.py c5fw 2>&1 | tail -1)"
-done
-done > gpurun_out/${R}_ab.txt 2>&1
-unset OTFGPU_LIB_OVERRIDE
-grep "^==" gpurun_out/${R}_ab.txt | cut -c1-150
+R=${ROUND_TAG:-r02v}
+timeout 900 python bench.py --workload c4 --steps 3 --no-cpu-baseline > gpurun_out/${R}_bench_c4.json 2> gpurun_out/${R}_bench_c4.err; echo c4=$?
+cut -c1-300 gpurun_out/${R}_bench_c4.json
+timeout 900 python -m pytest -x -q tests/test_gpu_summary.py tests/test_gpu_parity.py -k "config4 or golden" > gpurun_out/${R}_gputest.log 2>&1; echo gputest=$?
+tail -1 gpurun_out/${R}_gputest.log
