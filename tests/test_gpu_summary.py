@@ -183,3 +183,22 @@ def test_list_overflow_reruns_windowed_with_larger_list():
     errs = qoe_errors(res.qoe, want, "c5t seed 60")
     assert not errs, errs
     assert list(res.stats_raw[:18]) == want["stats"]
+
+
+def test_run_to_run_bit_identical():
+    """Two launches of the same batch produce identical QoE blocks, stats and counts,
+    bit for bit (the float sums are exact / registration-ordered, not atomic-order
+    dependent), in both warp layouts."""
+    import os
+    cfgs = [workloads.c5(seed=s, variant=v, clients=600, horizon_s=120.0) for s in (1, 2) for v in ("TC", "TCPF")]
+    for nw in ("1", "2"):
+        os.environ["OTF_WIN_NW"] = nw
+        try:
+            a = engine.run_batch(cfgs, mode="histogram")
+            b = engine.run_batch(cfgs, mode="histogram")
+        finally:
+            os.environ.pop("OTF_WIN_NW", None)
+        for x, y in zip(a, b):
+            # stats slots after OTF_ST_WINDOWS (22) are cycle counters: timing, not results
+            assert np.array_equal(x.qoe_row, y.qoe_row) and np.array_equal(x.stats_raw[:23], y.stats_raw[:23])
+            assert np.array_equal(x.counts, y.counts)
