@@ -1806,7 +1806,10 @@ enum { CTL_RUN = 0, CTL_REFILE = 1, CTL_STOP = 2 };
 // registers.  NW = 2 serves the shared-memory classes that fit at most 4 CTAs
 // per SM anyway (10,000-client scenarios): 8 warps per SM keep ~240 registers.
 template <bool RECORDS, int NW>
-__global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : 4) windowed_kernel(const otf_batch b) {
+#ifndef WIN_NW2_MINBLOCKS
+#define WIN_NW2_MINBLOCKS 4                            // two-warp CTAs per SM the register budget targets
+#endif
+__global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : WIN_NW2_MINBLOCKS) windowed_kernel(const otf_batch b) {
     constexpr int WIN_WARPS = NW, WIN_THREADS = 32 * NW;
     extern __shared__ __align__(16) uint8_t smem[];
     const int tid = threadIdx.x;
