@@ -120,8 +120,13 @@ struct WinHeader {
     uint8_t par_list[PAR_MAX];           //   the list partitioned by owner lane (time order kept)
     uint32_t par_cnt[32];                //   per owner lane: count, then next slot
     int32_t hand_safe;                   // no transcode can end within the window it starts in
+    uint32_t lc[16];                     // the server lane's event counters (LC_*): shared memory,
+                                         //   not registers (they are rarely on a critical path)
     double wmin[WIN_MAX_WARPS];          // per-warp partial minima (hand_safe)
 };
+
+// server-lane counters in WinHeader::lc (folded into the stats at server_end)
+enum { LC_HITS = 0, LC_MISS, LC_EVICT, LC_REJECT, LC_WASTED, LC_READY, LC_SPEC, LC_SKIP0, LC_POPS = LC_SKIP0 + 6 };
 
 // Server events one window can hold: the list lives in the dynamic shared region.
 __host__ __device__ inline int32_t win_list_cap(int32_t n_clients) {
@@ -279,10 +284,6 @@ struct Win {
     // server lane's register copies during phase A (loaded/stored around it)
     uint32_t stored_mask, lq_head, lq_tail, lq_stamp, lq_mask;
     bool cache_on, spec_on;
-    int64_t cur_bytes, entries, capacity;
-    uint32_t c_hits, c_miss, c_evict, c_reject, c_wasted, c_ready, c_spec, c_pops;
-    uint32_t c_skip[6];
-    int64_t pops;
     double svc_floor;                                  // min over ranks rho * min segment duration
 };
 
@@ -366,33 +367,33 @@ __device__ __forceinline__ void lru_touch(Win &w, int32_t d) {
     w.lq_tail++;
 }
 __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache.py:45-52
-    if (!(w.dflags[d] & DF_CACHED)) { w.c_miss++; return false; }
+    if (!(w.dflags[d] & DF_CACHED)) { w.h->lc[LC_MISS]++; return false; }
     lru_touch(w, d);
-    w.c_hits++;
+    w.h->lc[LC_HITS]++;
     return true;
 }
 __device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cache.py:58-81
-    const int64_t cap = w.capacity;
-    if (size > cap) { w.c_reject++; return; }
+    const int64_t cap = w.S.sc->cache_capacity;
+    if (size > cap) { w.h->lc[LC_REJECT]++; return; }
     if (w.dflags[d] & DF_CACHED) {                     // replace: its old queue entry goes stale
-        w.cur_bytes -= size;
+        w.h->st.cur_bytes -= size;
         w.dflags[d] &= (uint16_t)~DF_CACHED;
-        w.entries--;
+        w.h->st.entries--;
     }
-    while (w.cur_bytes + size > cap) {                 // popitem(last=False): oldest live entry
+    while (w.h->st.cur_bytes + size > cap) {                 // popitem(last=False): oldest live entry
         LqEnt e = w.lq[w.lq_head & w.lq_mask];
         w.lq_head++;
         int32_t v = e.desc;
         if (!(w.dflags[v] & DF_CACHED) || w.lstamp[v] != e.stamp) continue;
         w.dflags[v] &= (uint16_t)~DF_CACHED;
-        w.entries--;
-        w.cur_bytes -= w.S.size(v);
-        w.c_evict++;
+        w.h->st.entries--;
+        w.h->st.cur_bytes -= w.S.size(v);
+        w.h->lc[LC_EVICT]++;
     }
     lru_touch(w, d);
     w.dflags[d] |= DF_CACHED;
-    w.entries++;
-    w.cur_bytes += size;
+    w.h->st.entries++;
+    w.h->st.cur_bytes += size;
 }
 
 // Drop stale queue entries in place, keeping order (lane 0; only if a window
@@ -579,7 +580,7 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
     for (;;) {
         if (w.cache_on && (w.dflags[d] & DF_CACHED)) {  // dedup on dequeue (backend.py:193-198)
             w.S.job_outcome(j, OTF_OUTCOME_DROPPED);
-            w.c_wasted++;
+            w.h->lc[LC_WASTED]++;
             resolve(w, d);
         } else {                                             // run_transcode (transcode.py:123-128)
             WWorker &k = h->wk[wid];
@@ -609,7 +610,7 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
         h->fq_head = (h->fq_head + 1 == MAXK) ? 0 : h->fq_head + 1;
         h->fq_n--;
         w.fq_n--;
-        w.c_ready++;
+        w.h->lc[LC_READY]++;
         if (j < 0 && !take_job(w, wid, d, j)) continue;   // priority mode: a wakeup, not a job
         worker_run(w, wid, d, j);
     }
@@ -619,12 +620,12 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
 // not stored, with the next descriptor's word `fn` and the sequence's segment
 // count already loaded.
 __device__ __forceinline__ void speculate_next(Win &w, int32_t d, int32_t index, int32_t segc, uint16_t fn) {
-    if (!w.spec_on) { w.c_skip[0]++; return; }
-    if (index + 1 >= segc) { w.c_skip[1]++; return; }
-    if (w.cache_on && (fn & DF_CACHED)) { w.c_skip[3]++; return; }
-    if (df_inflight(fn)) { w.c_skip[4]++; return; }
-    if (enqueue_job(w, d + 1, OTF_ORIGIN_SPECULATIVE)) { w.c_skip[5]++; return; }
-    w.c_spec++;
+    if (!w.spec_on) { w.h->lc[LC_SKIP0 + 0]++; return; }
+    if (index + 1 >= segc) { w.h->lc[LC_SKIP0 + 1]++; return; }
+    if (w.cache_on && (fn & DF_CACHED)) { w.h->lc[LC_SKIP0 + 3]++; return; }
+    if (df_inflight(fn)) { w.h->lc[LC_SKIP0 + 4]++; return; }
+    if (enqueue_job(w, d + 1, OTF_ORIGIN_SPECULATIVE)) { w.h->lc[LC_SKIP0 + 5]++; return; }
+    w.h->lc[LC_SPEC]++;
 }
 
 // One client server event: MediaServer.segment + Backend.handle (server.py:61-78,
@@ -644,12 +645,12 @@ __device__ __forceinline__ void server_request_fast(Win &w, int32_t cid, int32_t
     if (w.cache_on) {                                  // SegmentCache.get (cache.py:45-52)
         if (f & DF_CACHED) {
             lru_touch(w, d);
-            w.c_hits++;
+            w.h->lc[LC_HITS]++;
             speculate_next(w, d, index, segc, fn);
             respond(w, cid, OTF_PATH_CACHE);
             return;
         }
-        w.c_miss++;
+        w.h->lc[LC_MISS]++;
     }
     if (df_inflight(f)) {
         speculate_next(w, d, index, segc, fn);
@@ -687,14 +688,11 @@ __device__ void server_begin(Win &w) {
     w.stored_mask = sc0.stored_mask;
     w.cache_on = sc0.cache_enabled != 0;
     w.spec_on = sc0.spec_enabled != 0;
-    w.capacity = sc0.cache_capacity;
-    w.cur_bytes = h->st.cur_bytes;
-    w.entries = h->st.entries;
     w.lq_stamp = h->lq_stamp;
     w.lq_mask = (uint32_t)h->lq_cap - 1u;
-    w.c_hits = w.c_miss = w.c_evict = w.c_reject = w.c_wasted = w.c_ready = w.c_spec = 0;
-    for (int q = 0; q < 6; q++) w.c_skip[q] = 0;
-    w.pops = 0;
+    w.h->lc[LC_HITS] = w.h->lc[LC_MISS] = w.h->lc[LC_EVICT] = w.h->lc[LC_REJECT] = w.h->lc[LC_WASTED] = w.h->lc[LC_READY] = w.h->lc[LC_SPEC] = 0;
+    for (int q = 0; q < 6; q++) w.h->lc[LC_SKIP0 + q] = 0;
+    w.h->lc[LC_POPS] = 0;
     double rho_min = INFINITY, dur_min = INFINITY;     // service-time floor (parallel pass guard)
     for (int32_t r = 0; r < sc0.n_ranks; r++) rho_min = fmin(rho_min, w.S.rho[r]);
     for (int32_t q = 0; q < sc0.n_seq; q++) {
@@ -706,18 +704,16 @@ __device__ void server_begin(Win &w) {
 
 __device__ void server_end(Win &w) {
     WinHeader *h = w.h;
-    h->stats[OTF_ST_TIMER_POPS] += w.pops;
-    h->st.cur_bytes = w.cur_bytes;
-    h->st.entries = w.entries;
+    h->stats[OTF_ST_TIMER_POPS] += w.h->lc[LC_POPS];
     h->lq_stamp = w.lq_stamp;
-    h->stats[OTF_ST_HITS] += w.c_hits;
-    h->stats[OTF_ST_MISSES] += w.c_miss;
-    h->stats[OTF_ST_EVICTIONS] += w.c_evict;
-    h->stats[OTF_ST_REJECTED] += w.c_reject;
-    h->stats[OTF_ST_WASTED] += w.c_wasted;
-    h->stats[OTF_ST_READY_CALLBACKS] += w.c_ready;
-    h->stats[OTF_ST_SPEC_ENQUEUED] += w.c_spec;
-    for (int q = 0; q < 6; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += w.c_skip[q];
+    h->stats[OTF_ST_HITS] += w.h->lc[LC_HITS];
+    h->stats[OTF_ST_MISSES] += w.h->lc[LC_MISS];
+    h->stats[OTF_ST_EVICTIONS] += w.h->lc[LC_EVICT];
+    h->stats[OTF_ST_REJECTED] += w.h->lc[LC_REJECT];
+    h->stats[OTF_ST_WASTED] += w.h->lc[LC_WASTED];
+    h->stats[OTF_ST_READY_CALLBACKS] += w.h->lc[LC_READY];
+    h->stats[OTF_ST_SPEC_ENQUEUED] += w.h->lc[LC_SPEC];
+    for (int q = 0; q < 6; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += w.h->lc[LC_SKIP0 + q];
     h->st.req_counter = w.req_counter;
     h->st.n_req = w.n_req;
 }
@@ -954,9 +950,9 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
         w.n_blist += (int32_t)n_imm;
         w.lq_tail += n_tch;
         w.lq_stamp += n_tch;
-        w.c_hits += hits; w.c_miss += miss; w.c_spec += spec;
-        w.c_skip[0] += sk0; w.c_skip[1] += sk1; w.c_skip[3] += sk3; w.c_skip[4] += sk4;
-        w.pops += n;
+        w.h->lc[LC_HITS] += hits; w.h->lc[LC_MISS] += miss; w.h->lc[LC_SPEC] += spec;
+        w.h->lc[LC_SKIP0 + 0] += sk0; w.h->lc[LC_SKIP0 + 1] += sk1; w.h->lc[LC_SKIP0 + 3] += sk3; w.h->lc[LC_SKIP0 + 4] += sk4;
+        w.h->lc[LC_POPS] += n;
         h->st.n_job += n_enq;
         h->jq_n += (int32_t)(n_enq - n_hand);
         // hand-offs, in time order: put_nowait -> the first getter's ready hop ->
@@ -969,7 +965,7 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
                 const int32_t wid = h->gq[h->gq_head];
                 h->gq_head = (h->gq_head + 1 == sc.n_workers) ? 0 : h->gq_head + 1;
                 h->gq_n--;
-                w.c_ready++;
+                w.h->lc[LC_READY]++;
                 w.now = w.lw[i];
                 worker_run(w, wid, w.ld[i] + k, (int32_t)(job_base + q));
                 q++;
@@ -1073,7 +1069,7 @@ __device__ void phase_a(Win &w, int32_t i0) {
     int32_t ncid = 0, nd = 0, npk = 0;
     if (i < n) { cw = w.lw[i]; ncid = w.li[i]; nd = w.ld[i]; npk = w.lp[i]; }
     const int32_t *segcount = w.S.segcounts;
-    w.pops += n - i0;                                  // every request is one timer pop
+    w.h->lc[LC_POPS] += n - i0;                                  // every request is one timer pop
     for (;;) {
         if (w.wdirty) {                                // earliest worker timer in this window
             bw = -1;
@@ -1107,7 +1103,7 @@ __device__ void phase_a(Win &w, int32_t i0) {
             else { w.S.flag(OTF_S_TIE); take_worker = true; }
         }
         if (take_worker) {
-            w.pops++;
+            w.h->lc[LC_POPS]++;
             w.now = bw_when;
             server_worker_done(w, bw);
         } else {
@@ -1301,11 +1297,12 @@ __device__ __forceinline__ bool wsegment_done(Win &w, WClient &c, int32_t cid, d
     Scn &S = w.S;
     double dt = now - xfer_start;                      // SegmentFetch.rate_bps
     double rate = dt > 0 ? ((double)size * 8.0) / dt : INFINITY;
-    c.est = c.est < 0 ? rate : S.alpha * rate + (1.0 - S.alpha) * c.est;
+    const double alpha = S.sc->alpha;                  // shared memory: not held in a register
+    c.est = c.est < 0 ? rate : alpha * rate + (1.0 - alpha) * c.est;
     const double duration = seg_duration(S.seqdur[c.seq], S.segdur[c.seq], c.index);
     Buffer b = wbuf_get(c);
     const int32_t ph0 = b.phase;
-    buf_on_segment(b, now, duration, S.startup, S.resume);
+    buf_on_segment(b, now, duration, S.sc->startup, S.sc->resume);
     wbuf_put(c, b);
     if (ph0 == PH_STARTUP && b.phase == PH_PLAYING) {  // playback started (client.py:117-119): the
         const double startup = b.started_at - b.session_start;   // startup delay is final now
@@ -1391,7 +1388,7 @@ __device__ __forceinline__ void client_local_body(Win &w, WClient &c, int32_t ci
             }
             if (c.index > 0)                           // client.py:255-256
                 c.rank = select_quality(c.level, c.rank, c.est >= 0, c.est, S.bitrates, sc.n_ranks,
-                                                 S.panic, S.safe, S.headroom);
+                                                 S.sc->panic, S.sc->safe, S.sc->headroom);
             c.attempt = 0;                             // _fetch_with_retry (client.py:291-305)
             if (S.records) w.wc[cid].requested = now;
             delay = w.L;                               // request latency, then MediaServer.segment
@@ -1805,11 +1802,12 @@ enum { CTL_RUN = 0, CTL_REFILE = 1, CTL_STOP = 2 };
 // (16 k each), so two-warp CTAs at that occupancy would cap the kernel at 128
 // registers.  NW = 2 serves the shared-memory classes that fit at most 4 CTAs
 // per SM anyway (10,000-client scenarios): 8 warps per SM keep ~240 registers.
-template <bool RECORDS, int NW>
-#ifndef WIN_NW2_MINBLOCKS
-#define WIN_NW2_MINBLOCKS 4                            // two-warp CTAs per SM the register budget targets
-#endif
-__global__ void __launch_bounds__(32 * NW, NW == 1 ? 8 : WIN_NW2_MINBLOCKS) windowed_kernel(const otf_batch b) {
+// MB: resident CTAs per SM the register budget is sized for.  Two-warp CTAs come
+// in two budgets: 4 per SM (up to 256 registers: the big shared-memory classes and
+// sparse launches) and 7 per SM (14 warps on 4 sub-partitions: 128 registers, so a
+// 1,024-scenario sweep stays one wave; measured 755 vs 785 ms for one warp).
+template <bool RECORDS, int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b) {
     constexpr int WIN_WARPS = NW, WIN_THREADS = 32 * NW;
     extern __shared__ __align__(16) uint8_t smem[];
     const int tid = threadIdx.x;
@@ -2278,30 +2276,38 @@ int64_t otf_windowed_shared_bytes(int32_t n_clients, int64_t n_desc, int32_t lis
 
 int32_t otf_windowed_list_cap(int32_t n_clients) { return otf::win_list_cap(n_clients); }
 
-// Warps per scenario: two once shared memory allows at most 4 CTAs per SM, or
-// once the launch has at most 4 scenarios per SM anyway (a strong-scaling shard
-// of a sweep: the second warp runs the window's local timers concurrently with
-// the server pass, and the responded clients in one round).  OTF_WIN_NW=1|2
-// overrides the choice (A/B measurements).
-static int windowed_warps(const otf_batch &b) {
+// Kernel shape per launch: 1 = one warp per scenario (8 per SM); 2 = two warps,
+// 256-register budget (4 per SM); 3 = two warps, 128-register budget (7 per SM).
+// Two warps once shared memory allows at most 4 CTAs per SM, or once at most 4
+// scenarios per SM are resident anyway (a strong-scaling shard: the second warp
+// runs the window's local timers during the server pass and the responded
+// clients take one round); the 7-per-SM two-warp budget while the launch (with
+// the launches running beside it) fits 7 per SM in one wave; else one warp.
+// OTF_WIN_NW=1|2|3 overrides the choice (A/B measurements).
+static int windowed_shape(const otf_batch &b) {
     const int smem = (int)b.shared_bytes;
-    int nw = (smem + 1024) * 5 > 228 * 1024 ? 2 : 1;
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int32_t resident = b.concurrent > b.n_scenarios ? b.concurrent : b.n_scenarios;
-    if (resident <= 4 * sms) nw = 2;
+    int shape = 1;
+    if ((smem + 1024) * 5 > 228 * 1024 || resident <= 4 * sms) shape = 2;
+    else if (resident <= 7 * sms && (smem + 1024) * 7 <= 228 * 1024) shape = 3;
     if (const char *e = getenv("OTF_WIN_NW")) {
         const int v = atoi(e);
-        if (v == 1 || v == 2) nw = v;
+        if (v >= 1 && v <= 3) shape = v;
     }
-    return nw;
+    return shape;
 }
 
 int otf_launch_windowed(const otf_batch &b, cudaStream_t stream) {
     int smem = (int)b.shared_bytes;
-    const int nw = windowed_warps(b);
-    auto kern = b.mode == OTF_MODE_RECORDS ? (nw == 2 ? otf::windowed_kernel<true, 2> : otf::windowed_kernel<true, 1>)
-                                           : (nw == 2 ? otf::windowed_kernel<false, 2> : otf::windowed_kernel<false, 1>);
+    const int shape = windowed_shape(b);
+    const int nw = shape == 1 ? 1 : 2;
+    auto kern = b.mode == OTF_MODE_RECORDS
+                    ? (shape == 1 ? otf::windowed_kernel<true, 1, 8>
+                                  : shape == 2 ? otf::windowed_kernel<true, 2, 4> : otf::windowed_kernel<true, 2, 7>)
+                    : (shape == 1 ? otf::windowed_kernel<false, 1, 8>
+                                  : shape == 2 ? otf::windowed_kernel<false, 2, 4> : otf::windowed_kernel<false, 2, 7>);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return 1;

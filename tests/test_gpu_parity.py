@@ -49,11 +49,12 @@ def test_size_tables_match_oracle(golden):
         assert np.array_equal(br.sizes(i), want), cfg
 
 
-@pytest.mark.parametrize("eng,nw", [("exact", ""), ("windowed", ""), ("windowed", "1"), ("windowed", "2")])
+@pytest.mark.parametrize("eng,nw", [("exact", ""), ("windowed", ""), ("windowed", "1"), ("windowed", "2"),
+                                    ("windowed", "3")])
 def test_golden_parity_batched(golden, eng, nw, monkeypatch):
     """All golden configs in ONE launch, each bit-exact vs the reference; the windowed
-    engine also with one and with two warps per scenario forced (a small batch picks
-    two by default, full sweeps one)."""
+    engine also with each kernel shape forced (1: one warp, 2: two warps with the
+    256-register budget, 3: two warps with the 128-register budget of 7 per SM)."""
     if nw:
         monkeypatch.setenv("OTF_WIN_NW", nw)
     names = sorted(golden)

@@ -188,10 +188,10 @@ def test_list_overflow_reruns_windowed_with_larger_list():
 def test_run_to_run_bit_identical():
     """Two launches of the same batch produce identical QoE blocks, stats and counts,
     bit for bit (the float sums are exact / registration-ordered, not atomic-order
-    dependent), in both warp layouts."""
+    dependent), in every kernel shape."""
     import os
     cfgs = [workloads.c5(seed=s, variant=v, clients=600, horizon_s=120.0) for s in (1, 2) for v in ("TC", "TCPF")]
-    for nw in ("1", "2"):
+    for nw in ("1", "2", "3"):
         os.environ["OTF_WIN_NW"] = nw
         try:
             a = engine.run_batch(cfgs, mode="histogram")

@@ -15,7 +15,7 @@ from tests import parity
 
 cfgs = [workloads.c1(seed=1), workloads.c2(seed=2, horizon_s=40.0), workloads.c3(seed=3, fraction=0.1, horizon_s=40.0),
         workloads.c5(seed=4, clients=120, horizon_s=30.0)]
-for nw in ("1", "2"):
+for nw in ("1", "2", "3"):
     os.environ["OTF_WIN_NW"] = nw
     for eng in ("windowed", "exact"):
         for mode in ("records", "histogram"):
