@@ -276,14 +276,12 @@ struct Win {
     double L, target;                                  // request latency, buffer target (registers)
     int32_t k;
     // lane 0's register copies of the hot server counters during phase A
-    int64_t req_counter, n_req;
     int32_t n_blist;
     int32_t fq_n;                                      // pending handed-off jobs (register mirror)
     bool wdirty;                                       // `due` changed: recompute the earliest due worker
     uint32_t due;                                      // workers whose service timer fires in this window
     // server lane's register copies during phase A (loaded/stored around it)
-    uint32_t stored_mask, lq_head, lq_tail, lq_stamp, lq_mask;
-    bool cache_on, spec_on;
+    uint32_t lq_head, lq_tail, lq_stamp, lq_mask;
     double svc_floor;                                  // min over ranks rho * min segment duration
 };
 
@@ -495,7 +493,7 @@ __device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
 // (a RespMsg: the client's own state is written by its lane only).  The
 // record itself and the request QoE are written by the client lane.
 __device__ __forceinline__ void respond(Win &w, int32_t cid, int32_t path) {
-    const int64_t slot = w.n_req++;
+    const int64_t slot = w.h->st.n_req++;
     if (w.S.records) w.wc[cid].req_slot = slot;
     RespMsg m;
     m.when = w.now;
@@ -578,7 +576,7 @@ __device__ void worker_run(Win &w, int32_t wid, int32_t d, int32_t j) {
     WinHeader *h = w.h;
     const otf_scenario &sc = *w.S.sc;
     for (;;) {
-        if (w.cache_on && (w.dflags[d] & DF_CACHED)) {  // dedup on dequeue (backend.py:193-198)
+        if (w.S.sc->cache_enabled && (w.dflags[d] & DF_CACHED)) {  // dedup on dequeue (backend.py:193-198)
             w.S.job_outcome(j, OTF_OUTCOME_DROPPED);
             w.h->lc[LC_WASTED]++;
             resolve(w, d);
@@ -620,9 +618,9 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
 // not stored, with the next descriptor's word `fn` and the sequence's segment
 // count already loaded.
 __device__ __forceinline__ void speculate_next(Win &w, int32_t d, int32_t index, int32_t segc, uint16_t fn) {
-    if (!w.spec_on) { w.h->lc[LC_SKIP0 + 0]++; return; }
+    if (!w.S.sc->spec_enabled) { w.h->lc[LC_SKIP0 + 0]++; return; }
     if (index + 1 >= segc) { w.h->lc[LC_SKIP0 + 1]++; return; }
-    if (w.cache_on && (fn & DF_CACHED)) { w.h->lc[LC_SKIP0 + 3]++; return; }
+    if (w.S.sc->cache_enabled && (fn & DF_CACHED)) { w.h->lc[LC_SKIP0 + 3]++; return; }
     if (df_inflight(fn)) { w.h->lc[LC_SKIP0 + 4]++; return; }
     if (enqueue_job(w, d + 1, OTF_ORIGIN_SPECULATIVE)) { w.h->lc[LC_SKIP0 + 5]++; return; }
     w.h->lc[LC_SPEC]++;
@@ -636,13 +634,13 @@ __device__ __forceinline__ void speculate_next(Win &w, int32_t d, int32_t index,
 __device__ __forceinline__ void server_request_fast(Win &w, int32_t cid, int32_t d, int32_t pk, uint16_t f,
                                                     uint16_t fn, int32_t segc) {
     const int32_t rank = pk & 0xff, index = (pk >> 8) & 0xff;
-    const int64_t rid = w.req_counter++;
+    const int64_t rid = w.h->st.req_counter++;
     if (w.S.records) w.wc[cid].req_id = rid;
-    if ((w.stored_mask >> rank) & 1u) {
+    if ((w.S.sc->stored_mask >> rank) & 1u) {
         respond(w, cid, OTF_PATH_STORAGE);
         return;
     }
-    if (w.cache_on) {                                  // SegmentCache.get (cache.py:45-52)
+    if (w.S.sc->cache_enabled) {                       // SegmentCache.get (cache.py:45-52)
         if (f & DF_CACHED) {
             lru_touch(w, d);
             w.h->lc[LC_HITS]++;
@@ -671,7 +669,7 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
     w.due &= ~(1u << wid);
     w.wdirty = true;
     w.S.job_finished(j, w.now);
-    if (w.cache_on) cache_put(w, d, k.size);
+    if (w.S.sc->cache_enabled) cache_put(w, d, k.size);
     resolve(w, d);
     int32_t nd, nj;                                    // next job
     if (take_job(w, wid, nd, nj)) worker_run(w, wid, nd, nj);
@@ -683,11 +681,6 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
 __device__ void server_begin(Win &w) {
     WinHeader *h = w.h;
     const otf_scenario &sc0 = *w.S.sc;
-    w.req_counter = h->st.req_counter;
-    w.n_req = h->st.n_req;
-    w.stored_mask = sc0.stored_mask;
-    w.cache_on = sc0.cache_enabled != 0;
-    w.spec_on = sc0.spec_enabled != 0;
     w.lq_stamp = h->lq_stamp;
     w.lq_mask = (uint32_t)h->lq_cap - 1u;
     w.h->lc[LC_HITS] = w.h->lc[LC_MISS] = w.h->lc[LC_EVICT] = w.h->lc[LC_REJECT] = w.h->lc[LC_WASTED] = w.h->lc[LC_READY] = w.h->lc[LC_SPEC] = 0;
@@ -714,8 +707,6 @@ __device__ void server_end(Win &w) {
     h->stats[OTF_ST_READY_CALLBACKS] += w.h->lc[LC_READY];
     h->stats[OTF_ST_SPEC_ENQUEUED] += w.h->lc[LC_SPEC];
     for (int q = 0; q < 6; q++) h->stats[OTF_ST_SKIP_DISABLED + q] += w.h->lc[LC_SKIP0 + q];
-    h->st.req_counter = w.req_counter;
-    h->st.n_req = w.n_req;
 }
 
 // One request of the window's sorted list (the list entry was loaded one event ahead).
@@ -867,8 +858,8 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
     const uint32_t n_imm = n_pk & 1023u, n_tch = (n_pk >> 10) & 1023u, n_enq = n_pk >> 20;
     const uint32_t n_enq_d = warp_sum(c_enq_d);
     // the server lane's scalars (lane 0's registers) as the bases
-    const int64_t req_base = __shfl_sync(0xffffffffu, (long long)w.req_counter, 0);
-    const int64_t slot_base = __shfl_sync(0xffffffffu, (long long)w.n_req, 0);
+    const int64_t req_base = h->st.req_counter;        // (shared: every lane reads the same word)
+    const int64_t slot_base = h->st.n_req;
     const int32_t blist_base = __shfl_sync(0xffffffffu, w.n_blist, 0);
     const uint32_t lq_tail = __shfl_sync(0xffffffffu, w.lq_tail, 0);
     const uint32_t stamp_base = __shfl_sync(0xffffffffu, w.lq_stamp, 0);
@@ -945,8 +936,8 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
     hits = warp_sum(hits); miss = warp_sum(miss); spec = warp_sum(spec);
     sk0 = warp_sum(sk0); sk1 = warp_sum(sk1); sk3 = warp_sum(sk3); sk4 = warp_sum(sk4);
     if (lane == 0) {
-        w.req_counter += n;
-        w.n_req += n_imm;
+        h->st.req_counter += n;
+        h->st.n_req += n_imm;
         w.n_blist += (int32_t)n_imm;
         w.lq_tail += n_tch;
         w.lq_stamp += n_tch;
