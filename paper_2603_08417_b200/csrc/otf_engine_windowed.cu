@@ -276,12 +276,9 @@ struct Win {
     double L, target;                                  // request latency, buffer target (registers)
     int32_t k;
     // lane 0's register copies of the hot server counters during phase A
-    int32_t n_blist;
-    int32_t fq_n;                                      // pending handed-off jobs (register mirror)
     bool wdirty;                                       // `due` changed: recompute the earliest due worker
     uint32_t due;                                      // workers whose service timer fires in this window
     // server lane's register copies during phase A (loaded/stored around it)
-    uint32_t lq_head, lq_tail, lq_stamp, lq_mask;
     double svc_floor;                                  // min over ranks rho * min segment duration
 };
 
@@ -356,13 +353,15 @@ __device__ __noinline__ uint32_t lq_compact_serial(LqEnt *lq, const uint16_t *df
                                                    uint32_t head, uint32_t tail, uint32_t mask);
 
 __device__ __forceinline__ void lru_touch(Win &w, int32_t d) {
-    uint32_t s = ++w.lq_stamp;
+    WinHeader *hh = w.h;
+    const uint32_t mask = (uint32_t)hh->lq_cap - 1u;
+    uint32_t s = ++hh->lq_stamp;
     w.lstamp[d] = s;
-    if (w.lq_tail - w.lq_head > w.lq_mask)
-        w.lq_tail = lq_compact_serial(w.lq, w.dflags, w.lstamp, w.lq_head, w.lq_tail, w.lq_mask);
+    if (hh->lq_tail - hh->lq_head > mask)
+        hh->lq_tail = lq_compact_serial(w.lq, w.dflags, w.lstamp, hh->lq_head, hh->lq_tail, mask);
     LqEnt e; e.desc = d; e.stamp = s;
-    w.lq[w.lq_tail & w.lq_mask] = e;
-    w.lq_tail++;
+    w.lq[hh->lq_tail & mask] = e;
+    hh->lq_tail++;
 }
 __device__ __forceinline__ bool cache_get(Win &w, int32_t d) {          // cache.py:45-52
     if (!(w.dflags[d] & DF_CACHED)) { w.h->lc[LC_MISS]++; return false; }
@@ -379,8 +378,8 @@ __device__ void cache_put(Win &w, int32_t d, int64_t size) {             // cach
         w.h->st.entries--;
     }
     while (w.h->st.cur_bytes + size > cap) {                 // popitem(last=False): oldest live entry
-        LqEnt e = w.lq[w.lq_head & w.lq_mask];
-        w.lq_head++;
+        LqEnt e = w.lq[w.h->lq_head & ((uint32_t)w.h->lq_cap - 1u)];
+        w.h->lq_head++;
         int32_t v = e.desc;
         if (!(w.dflags[v] & DF_CACHED) || w.lstamp[v] != e.stamp) continue;
         w.dflags[v] &= (uint16_t)~DF_CACHED;
@@ -462,7 +461,6 @@ __device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
             if (pos >= MAXK) pos -= MAXK;
             h->fq_w[pos] = wid; h->fq_d[pos] = -1; h->fq_j[pos] = -1;
             h->fq_n++;
-            w.fq_n++;
         } else {
             h->tokens++;
         }
@@ -476,7 +474,6 @@ __device__ bool enqueue_job(Win &w, int32_t d, int32_t origin) {
         if (pos >= MAXK) pos -= MAXK;
         h->fq_w[pos] = wid; h->fq_d[pos] = d; h->fq_j[pos] = j;
         h->fq_n++;
-        w.fq_n++;
     } else {
         if (h->jq_n >= h->jq_cap) { w.S.flag(OTF_S_INTERNAL); return false; }
         int32_t pos = h->jq_head + h->jq_n;
@@ -499,7 +496,7 @@ __device__ __forceinline__ void respond(Win &w, int32_t cid, int32_t path) {
     m.when = w.now;
     m.cid = cid;
     m.path = path;
-    w.blist[w.n_blist++] = m;
+    w.blist[w.h->n_blist++] = m;
 }
 
 // Waiter links reuse bnext (a waiting client has no pending timer): bits 0-14 are
@@ -607,7 +604,6 @@ __device__ void drain_handoffs(Win &w) {            // ready-queue hops of hande
         int32_t wid = h->fq_w[h->fq_head], d = h->fq_d[h->fq_head], j = h->fq_j[h->fq_head];
         h->fq_head = (h->fq_head + 1 == MAXK) ? 0 : h->fq_head + 1;
         h->fq_n--;
-        w.fq_n--;
         w.h->lc[LC_READY]++;
         if (j < 0 && !take_job(w, wid, d, j)) continue;   // priority mode: a wakeup, not a job
         worker_run(w, wid, d, j);
@@ -681,8 +677,6 @@ __device__ void server_worker_done(Win &w, int32_t wid) {
 __device__ void server_begin(Win &w) {
     WinHeader *h = w.h;
     const otf_scenario &sc0 = *w.S.sc;
-    w.lq_stamp = h->lq_stamp;
-    w.lq_mask = (uint32_t)h->lq_cap - 1u;
     w.h->lc[LC_HITS] = w.h->lc[LC_MISS] = w.h->lc[LC_EVICT] = w.h->lc[LC_REJECT] = w.h->lc[LC_WASTED] = w.h->lc[LC_READY] = w.h->lc[LC_SPEC] = 0;
     for (int q = 0; q < 6; q++) w.h->lc[LC_SKIP0 + q] = 0;
     w.h->lc[LC_POPS] = 0;
@@ -698,7 +692,6 @@ __device__ void server_begin(Win &w) {
 __device__ void server_end(Win &w) {
     WinHeader *h = w.h;
     h->stats[OTF_ST_TIMER_POPS] += w.h->lc[LC_POPS];
-    h->lq_stamp = w.lq_stamp;
     h->stats[OTF_ST_HITS] += w.h->lc[LC_HITS];
     h->stats[OTF_ST_MISSES] += w.h->lc[LC_MISS];
     h->stats[OTF_ST_EVICTIONS] += w.h->lc[LC_EVICT];
@@ -860,9 +853,9 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
     // the server lane's scalars (lane 0's registers) as the bases
     const int64_t req_base = h->st.req_counter;        // (shared: every lane reads the same word)
     const int64_t slot_base = h->st.n_req;
-    const int32_t blist_base = __shfl_sync(0xffffffffu, w.n_blist, 0);
-    const uint32_t lq_tail = __shfl_sync(0xffffffffu, w.lq_tail, 0);
-    const uint32_t stamp_base = __shfl_sync(0xffffffffu, w.lq_stamp, 0);
+    const int32_t blist_base = h->n_blist;             // the header copies (every lane reads them)
+    const uint32_t lq_tail = h->lq_tail;
+    const uint32_t stamp_base = h->lq_stamp;
     const uint32_t lq_mask = (uint32_t)h->lq_cap - 1u;
     const int32_t jq_base = h->jq_head + h->jq_n;
     const int64_t job_base = h->st.n_job;
@@ -938,9 +931,9 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
     if (lane == 0) {
         h->st.req_counter += n;
         h->st.n_req += n_imm;
-        w.n_blist += (int32_t)n_imm;
-        w.lq_tail += n_tch;
-        w.lq_stamp += n_tch;
+        h->n_blist += (int32_t)n_imm;
+        h->lq_tail += n_tch;
+        h->lq_stamp += n_tch;
         w.h->lc[LC_HITS] += hits; w.h->lc[LC_MISS] += miss; w.h->lc[LC_SPEC] += spec;
         w.h->lc[LC_SKIP0 + 0] += sk0; w.h->lc[LC_SKIP0 + 1] += sk1; w.h->lc[LC_SKIP0 + 3] += sk3; w.h->lc[LC_SKIP0 + 4] += sk4;
         w.h->lc[LC_POPS] += n;
@@ -965,8 +958,6 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
         h->stats[OTF_ST_JOBS_TOTAL] += n_enq;
         h->stats[OTF_ST_JOBS_DEMAND] += n_enq_d;
         h->stats[OTF_ST_JOBS_SPEC] += n_enq - n_enq_d;
-        h->lq_head = w.lq_head; h->lq_tail = w.lq_tail;
-        h->n_blist = w.n_blist;
 #ifdef WIN_DIAG
         h->stats[31] += clock64() - dga;
 #endif
@@ -996,12 +987,11 @@ __device__ __forceinline__ bool parallel_ok(Win &w) {
     bool due = false;                                  // a transcode completes in this window
 #pragma unroll 4
     for (int32_t q = 0; q < sc.n_workers; q++) due |= h->wk[q].win == w.k;
-    w.lq_head = lq_head; w.lq_tail = lq_tail; w.n_blist = n_blist;
     // an idle worker handed a job here must not finish inside the window (hand_safe:
     // svc >= svc_floor * (1 + min eps) >= 2 W for every job, checked at kernel start)
     return (n >= 2) & (n <= PAR_MAX) & (n_ties == 0) & (fq_n == 0) & (sc.demand_priority == 0) &
            (sc.queue_bound <= 0) & !due & ((gq_n == 0) | (hand_safe != 0)) &
-           (lq_tail - lq_head + (uint32_t)n <= w.lq_mask);   // room for every touch
+           (lq_tail - lq_head + (uint32_t)n <= (uint32_t)h->lq_cap - 1u);   // room for every touch
 }
 
 #ifndef WIN_NO_PREFIX
@@ -1025,7 +1015,7 @@ __device__ __forceinline__ int32_t parallel_prefix(Win &w) {
         const int32_t mid = (lo + hi) >> 1;
         if (w.lw[mid] < t_w) lo = mid + 1; else hi = mid;
     }
-    if (lo < 2 || h->lq_tail - h->lq_head + (uint32_t)lo > w.lq_mask) return 0;
+    if (lo < 2 || h->lq_tail - h->lq_head + (uint32_t)lo > (uint32_t)h->lq_cap - 1u) return 0;
     return lo;
 }
 #endif
@@ -1046,9 +1036,6 @@ __device__ void phase_a(Win &w, int32_t i0) {
     WinHeader *h = w.h;
     const int32_t K = w.S.sc->n_workers;
     const int32_t n = h->n_list;
-    w.lq_head = h->lq_head; w.lq_tail = h->lq_tail;    // the compaction step may have moved them
-    w.n_blist = h->n_blist;
-    w.fq_n = h->fq_n;
     uint32_t due = 0;
     for (int32_t q = 0; q < K; q++) due |= (h->wk[q].win == w.k ? 1u : 0u) << q;
     w.due = due;
@@ -1077,7 +1064,7 @@ __device__ void phase_a(Win &w, int32_t i0) {
         if (bw < 0) {                                  // no worker timer due: requests only (common)
             while (i < n) {
                 PHASE_A_REQUEST();
-                if (w.fq_n > 0) drain_handoffs(w);
+                if (w.h->fq_n > 0) drain_handoffs(w);
                 if (w.wdirty) break;                   // a started job ends inside this window (rare)
             }
             if (!w.wdirty) break;
@@ -1100,10 +1087,8 @@ __device__ void phase_a(Win &w, int32_t i0) {
         } else {
             PHASE_A_REQUEST();
         }
-        if (w.fq_n > 0) drain_handoffs(w);
+        if (w.h->fq_n > 0) drain_handoffs(w);
     }
-    h->lq_head = w.lq_head; h->lq_tail = w.lq_tail;
-    h->n_blist = w.n_blist;
 }
 
 // ---- client lanes ------------------------------------------------------------------
