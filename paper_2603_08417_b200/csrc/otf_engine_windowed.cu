@@ -2186,24 +2186,37 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
             __syncwarp();
             if (h->st.status & WIN_ABORT_BITS) break;
         } else {
-            if (warp > 0) {
-                // ---- phase B1: the window's client-local timers, concurrent with phase A ----
-                const int b1 = tid - 32;
-                const long long tb = clock64();
-                const int32_t nl = h->n_loc;
-                const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
-                for (int32_t i = b1; i < nl; i += WIN_THREADS - 32) client_event(w, al[i], 0.0, -1);
-                if (b1 == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
+            // ---- phase B1: warp 1 runs the window's client-local timers, concurrent with
+            // phase A; then (B2) both warps run the clients phase A responded to (and the
+            // overflowed local timers).  One loop, so ONE inlined copy of the client state
+            // machine (hot code); its trip counts are warp-uniform, so the CTA barrier
+            // between the stages is reached convergently ----
+            const int32_t *al = w.bloc + (int64_t)(m & (RING - 1)) * w.lcap;
+            const long long tb = clock64();
+            int32_t n_items = warp > 0 ? h->n_loc : 0, base = 0, step = 32;
+            bool b2 = false, abort = false;
+            for (;;) {
+                if (base >= n_items) {
+                    if (b2) break;
+                    if (warp > 0 && lane == 0) h->stats[OTF_ST_CYC_LOCAL] += clock64() - tb;
+                    __syncthreads();
+                    if (h->st.status & WIN_ABORT_BITS) { abort = true; break; }
+                    t0 = WCLOCK();
+                    b2 = true;
+                    n_items = h->n_blist;
+                    base = 32 * warp;
+                    step = WIN_THREADS;
+                    continue;
+                }
+                const int32_t i = base + lane;
+                base += step;
+                if (i < n_items) {
+                    RespMsg msg;
+                    if (b2) msg = w.blist[i]; else { msg.cid = al[i]; msg.when = 0.0; msg.path = -1; }
+                    client_event(w, msg.cid, msg.when, msg.path);
+                }
             }
-            __syncthreads();
-            if (h->st.status & WIN_ABORT_BITS) break;
-            // ---- phase B2: clients phase A responded to (and overflowed local timers) ----
-            t0 = WCLOCK();
-            const int32_t nb = h->n_blist;
-            for (int32_t i = tid; i < nb; i += WIN_THREADS) {
-                const RespMsg m = w.blist[i];
-                client_event(w, m.cid, m.when, m.path);
-            }
+            if (abort) break;
             __syncthreads();
         }
         if (tid == 0) h->stats[OTF_ST_CYC_CLIENTS] += WCLOCK() - t0;

@@ -295,17 +295,17 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
     require_cuda(device)                               # no CPU path: fail before any host work
     m = _lib.MODE_RECORDS if mode == "records" else _lib.MODE_HISTOGRAM
     eng = _lib.ENGINE_WINDOWED if engine == "windowed" else _lib.ENGINE_EXACT
-    configs = list(configs)
+    from .inputs import lower_any
+    configs = [lower_any(c) for c in configs]          # validated and lowered once per call
     if m == _lib.MODE_RECORDS and _caps is None and len(configs) > 1:
         # record buffers grow with the requests (~212 B per expected request): a big
         # sweep in records mode runs in chunks that fit half the free device memory
-        from .inputs import _default_caps, lower
-        from .config import ExperimentConfig
+        from .inputs import _default_caps
         dev = require_cuda(device)
         budget = torch.cuda.mem_get_info(dev)[0] // 2
         need = []
         for c in configs:
-            r, s_, g, j = _default_caps(lower(ExperimentConfig.from_reference(c)))
+            r, s_, g, j = _default_caps(c)
             need.append(48 * r + 48 * s_ + 28 * g + 44 * j)
         if sum(need) > budget:
             out, chunk, used = [], [], 0
@@ -397,10 +397,9 @@ def run_batch(configs, mode: str = "records", engine: str = "windowed", device=N
 def _grow_list_cap(cfg, lcaps: dict, i: int, device) -> bool:
     """Quadruple scenario i's server-event list (a power of two, at most 16,384
     entries and the device's shared memory); False when it cannot grow."""
-    from .config import ExperimentConfig
-    from .inputs import lower
+    from .inputs import lower_any
     L = _lib.lib()
-    low = lower(ExperimentConfig.from_reference(cfg))
+    low = lower_any(cfg)
     cur = lcaps.get(i) or int(L.otf_list_cap(low.cfg.clients))
     new = cur * 4
     limit = torch.cuda.get_device_properties(require_cuda(device)).shared_memory_per_block_optin

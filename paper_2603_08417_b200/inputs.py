@@ -127,7 +127,7 @@ def _lower_key(cfg: ExperimentConfig):
     """Every field validate() and the catalog read: configs of a sweep that differ
     only in client count, horizon, cache size within the policy's limits... share
     one validated lowering."""
-    seqs = tuple((e["id"], e.get("duration_s"), e.get("segment_duration_s")) for e in cfg.sequences) \
+    seqs = tuple([(e["id"], e.get("duration_s"), e.get("segment_duration_s")) for e in cfg.sequences]) \
         if cfg.sequences else None
     return (cfg.variant, cfg.cache_capacity_bytes > 0, cfg.workers, cfg.queue_bound, cfg.demand_priority,
             tuple(tuple(x) for x in cfg.ladder), seqs, cfg.seed, cfg.size_jitter, cfg.rho,
@@ -165,6 +165,50 @@ def lower(cfg: ExperimentConfig) -> Lowered:
         _LOWER_MEMO.clear()
     _LOWER_MEMO[key] = low
     return low
+
+
+def lower_any(c) -> Lowered:
+    """lower() of a config of either package, or a config already lowered (run_batch
+    lowers each config once per call)."""
+    return c if isinstance(c, Lowered) else lower(ExperimentConfig.from_reference(c))
+
+
+_GRID_MEMO: dict = {}
+
+
+def _trace_grid(duration: float, step: float):
+    """A synthetic trace's sample times, period and grid step (0 if the times are not
+    i * step exactly), shared by every (seed, client) with the same netem timing."""
+    key = (duration, step)
+    hit = _GRID_MEMO.get(key)
+    if hit is None:
+        ts = sample_times(duration, step)
+        if not ts:
+            raise ConfigError("trace has no samples")
+        gaps = [b - a for a, b in zip(ts, ts[1:])]
+        period = ts[-1] + (statistics.median(gaps) if gaps else 1.0)
+        grid = float(step) if all(x == float(i) * step for i, x in enumerate(ts)) else 0.0
+        if len(_GRID_MEMO) > 256:
+            _GRID_MEMO.clear()
+        hit = _GRID_MEMO[key] = (ts, period, grid)
+    return hit
+
+
+_SIZE_MEMO: dict = {}
+
+
+def _engine_bytes(engine: int, N: int, K: int, n_seq: int, n_ranks: int, max_nseg: int, lc: int):
+    """(global scratch, shared memory per CTA) of one scenario (memoized C-ABI queries)."""
+    key = (engine, N, K, n_seq, n_ranks, max_nseg, lc)
+    hit = _SIZE_MEMO.get(key)
+    if hit is None:
+        L = _lib.lib()
+        scratch = int(L.otf_scratch_bytes(engine, N, K, n_seq, n_ranks, max_nseg))
+        smem = int(L.otf_shared_bytes_cap(N, n_seq, n_ranks, max_nseg, lc)) if engine == _lib.ENGINE_WINDOWED else 0
+        if len(_SIZE_MEMO) > 65536:
+            _SIZE_MEMO.clear()
+        hit = _SIZE_MEMO[key] = (scratch, smem)
+    return hit
 
 
 class _Pools:
@@ -248,7 +292,7 @@ def windowed_fits(cfg, smem_limit: int | None = None) -> tuple[bool, str]:
     smem_limit is given, does its per-CTA shared memory fit the device?  Returns
     (fits, reason); scenarios that do not fit run on the exact engine."""
     L = _lib.lib()
-    low = lower(ExperimentConfig.from_reference(cfg))
+    low = lower_any(cfg)
     c = low.cfg
     sc = _lib.Scenario()
     sc.n_clients, sc.n_workers, sc.n_seq, sc.n_ranks = c.clients, c.workers, len(low.seq_ids), low.n_ranks
@@ -341,7 +385,7 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
     """Lower a list of ExperimentConfigs into one device batch (host arrays; page-locked if pin)."""
     L = _lib.lib()
     threads = threads or os.cpu_count() or 1
-    lows = [lower(ExperimentConfig.from_reference(c)) for c in configs]
+    lows = [lower_any(c) for c in configs]
     P = _Pools(threads)
     scen = (_lib.Scenario * max(1, len(lows)))()
     tables = []
@@ -375,14 +419,9 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         trace_groups[key] = (max(prev, low.cfg.clients), low.cfg.netem)
     trace_tab = {}
     for key, (nmax, ne) in trace_groups.items():
-        ts = sample_times(ne.trace_duration_s, ne.step_s)
-        if not ts:
-            raise ConfigError("trace has no samples")
-        gaps = [b - a for a, b in zip(ts, ts[1:])]
-        period = ts[-1] + (statistics.median(gaps) if gaps else 1.0)
+        ts, period, grid = _trace_grid(ne.trace_duration_s, ne.step_s)
         n = len(ts)
         decay = math.exp(-ne.theta_per_s * ne.step_s)
-        grid = float(ne.step_s) if all(x == float(i) * ne.step_s for i, x in enumerate(ts)) else 0.0
         trace_tab[key] = dict(n=n, period=period, grid=grid, ts=ts, values=P.device("f64", nmax * n),
                               pbits=P.device("f64", nmax), nmax=nmax,
                               job=dict(kind=_lib.GEN_TRACE, n=n, n_streams=nmax, seed=key[0], period=period,
@@ -423,42 +462,54 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         tt["starts"] = P.add("f64", np.asarray(tt["ts"], dtype=np.float64))
         add_job(off_out=tt["values"], off_pbits=tt["pbits"], off_starts=tt["starts"], **tt["job"])
 
+    cat_ids: dict = {}
+    cat_groups: dict = {}
     for si, low in enumerate(lows):
         cfg = low.cfg
         N, K = cfg.clients, cfg.workers
         n_seq, n_ranks = len(low.seq_ids), low.n_ranks
-        max_nseg = max(low.counts)
-        ladder = sorted(cfg.ladder)
-        cat_key = low.cat_key
-        o_bitrates = P.add("i64", [b for _, b in ladder], key=("bitrates", tuple(ladder)))
-        if ("i64", ("keys", tuple(low.seq_ids))) not in P.memo:
-            keys = [int.from_bytes(hashlib.sha256(s.encode("utf-8")).digest()[:8], "big") for s in low.seq_ids]
-            P.add("i64", np.array(keys, dtype=np.uint64).view(np.int64), key=("keys", tuple(low.seq_ids)))
-        o_keys = P.memo[("i64", ("keys", tuple(low.seq_ids)))]
-        o_seqdur = P.add("f64", low.seq_dur, key=("seqdur", cat_key))
-        o_segdur = P.add("f64", low.seq_segdur, key=("segdur", cat_key))
-        o_counts = P.add("i32", low.counts, key=("counts", cat_key))
-        if ("i64", ("sizes", cat_key)) not in P.memo:
-            o_sizes = P.reserve("i64", n_seq * n_ranks * max_nseg, key=("sizes", cat_key))
-            t = _lib.SizeTable()
-            t.n_seq, t.n_ranks, t.max_nseg = n_seq, n_ranks, max_nseg
-            t.seed, t.size_jitter = cfg.seed, cfg.size_jitter
-            t.off_out, t.off_keys, t.off_bitrates = o_sizes, o_keys, o_bitrates
-            t.off_seqdur, t.off_segdur, t.off_segcount = o_seqdur, o_segdur, o_counts
-            tables.append(t)
-            input_bytes += 8 * n_seq * n_ranks * max_nseg
-        o_sizes = P.memo[("i64", ("sizes", cat_key))]
-        mkey = ("manifest", cat_key[2:])                # manifests do not depend on the seed
-        if ("i64", mkey) not in P.memo:
-            P.add("i64", _manifest_bytes(low, ladder, cat_key[2:]), key=mkey)
-        o_man = P.memo[("i64", mkey)]
-        rho_map = cfg.per_rank_rho or {r: cfg.rho for r, _ in ladder}
-        o_rho = P.add("f64", [float(rho_map[r]) for r, _ in ladder], key=("rho", tuple(sorted(rho_map.items()))))
-        pop = 1 if cfg.popularity == "zipf" else 0
-        zkey = ("zipf", n_seq, pop, cfg.zipf_exponent)
-        o_zipf = P.memo.get(("f64", zkey))
-        if o_zipf is None:
-            o_zipf = P.add("f64", zipf_cdf(n_seq, cfg.zipf_exponent) if pop else np.zeros(n_seq), key=zkey)
+        # the catalog tables: once per lowering (configs lowered from one memo entry share
+        # seq_ids by identity; every Lowered of this call is alive, so ids are unique)
+        gkey = (id(low.seq_ids), cfg.popularity, cfg.zipf_exponent)
+        g = cat_groups.get(gkey)
+        if g is None:
+            max_nseg = max(low.counts)
+            ladder = sorted(cfg.ladder)
+            cat_key = cat_ids.setdefault(low.cat_key, len(cat_ids))   # small ids: the catalog tuples hash once
+            ids_key = cat_ids.setdefault(low.cat_key[2], len(cat_ids))
+            ladder_key = cat_ids.setdefault(low.cat_key[5], len(cat_ids))
+            o_bitrates = P.add("i64", [b for _, b in ladder], key=("bitrates", ladder_key))
+            if ("i64", ("keys", ids_key)) not in P.memo:
+                keys = [int.from_bytes(hashlib.sha256(s.encode("utf-8")).digest()[:8], "big") for s in low.seq_ids]
+                P.add("i64", np.array(keys, dtype=np.uint64).view(np.int64), key=("keys", ids_key))
+            o_keys = P.memo[("i64", ("keys", ids_key))]
+            o_seqdur = P.add("f64", low.seq_dur, key=("seqdur", cat_key))
+            o_segdur = P.add("f64", low.seq_segdur, key=("segdur", cat_key))
+            o_counts = P.add("i32", low.counts, key=("counts", cat_key))
+            if ("i64", ("sizes", cat_key)) not in P.memo:
+                o_sizes = P.reserve("i64", n_seq * n_ranks * max_nseg, key=("sizes", cat_key))
+                t = _lib.SizeTable()
+                t.n_seq, t.n_ranks, t.max_nseg = n_seq, n_ranks, max_nseg
+                t.seed, t.size_jitter = cfg.seed, cfg.size_jitter
+                t.off_out, t.off_keys, t.off_bitrates = o_sizes, o_keys, o_bitrates
+                t.off_seqdur, t.off_segdur, t.off_segcount = o_seqdur, o_segdur, o_counts
+                tables.append(t)
+                input_bytes += 8 * n_seq * n_ranks * max_nseg
+            o_sizes = P.memo[("i64", ("sizes", cat_key))]
+            mkey = ("manifest", cat_ids.setdefault(low.cat_key[2:], len(cat_ids)))   # not seed-dependent
+            if ("i64", mkey) not in P.memo:
+                P.add("i64", _manifest_bytes(low, ladder, low.cat_key[2:]), key=mkey)
+            o_man = P.memo[("i64", mkey)]
+            rho_map = cfg.per_rank_rho or {r: cfg.rho for r, _ in ladder}
+            o_rho = P.add("f64", [float(rho_map[r]) for r, _ in ladder], key=("rho", tuple(sorted(rho_map.items()))))
+            pop = 1 if cfg.popularity == "zipf" else 0
+            zkey = ("zipf", n_seq, pop, cfg.zipf_exponent)
+            o_zipf = P.memo.get(("f64", zkey))
+            if o_zipf is None:
+                o_zipf = P.add("f64", zipf_cdf(n_seq, cfg.zipf_exponent) if pop else np.zeros(n_seq), key=zkey)
+            g = cat_groups[gkey] = (o_bitrates, o_seqdur, o_segdur, o_counts, o_sizes, o_man, o_rho, o_zipf,
+                                    pop, max_nseg)
+        o_bitrates, o_seqdur, o_segdur, o_counts, o_sizes, o_man, o_rho, o_zipf, pop, max_nseg = g
         o_arr = arr_tab[(cfg.seed, N, cfg.arrival_rate_per_s)]
         if cfg.netem.trace_dir:                        # orchestrator.py:243-253
             tdir = cfg.netem.trace_dir
@@ -515,12 +566,12 @@ def build_inputs(configs, engine: int = _lib.ENGINE_WINDOWED, mode: int = _lib.M
         sc.off_arrivals = o_arr
         sc.off_eps, sc.eps_stride = o_eps, eps_stride
         sc.scratch_off = scratch_off
-        scratch_off += int(L.otf_scratch_bytes(engine, N, K, n_seq, n_ranks, max_nseg))
         lc = int(list_caps[si]) if list_caps is not None and list_caps[si] else 0
+        scratch, smem = _engine_bytes(engine, N, K, n_seq, n_ranks, max_nseg, lc)
+        scratch_off += scratch
         sc.list_cap = lc
-        smem_per.append(int(L.otf_shared_bytes_cap(N, n_seq, n_ranks, max_nseg, lc))
-                        if engine == _lib.ENGINE_WINDOWED else 0)
-        shared_bytes = max(shared_bytes, smem_per[-1])
+        smem_per.append(smem)
+        shared_bytes = max(shared_bytes, smem)
         scratch_off = (scratch_off + 255) & ~255
         tc = tail_caps[si] if tail_caps is not None and tail_caps[si] is not None else default_tail_caps(low)
         tcap_arr[si] = tc
