@@ -1521,6 +1521,103 @@ __device__ __forceinline__ bool qsort_fast(Win &w, int lane, int32_t n) {
 }
 #endif
 
+#ifndef WIN_NO_BSORT
+// Bucket sort of a window's n <= 32 E server events by the same 32-bit fixed-point key
+// (list capacity >= 64 E: positions 32 E..64 E of the time array are its scratch):
+// 32 E buckets on the key's top bits (shared-memory counters), a warp scan for their
+// starts, then each event's rank within its bucket by comparing with the bucket's
+// other keys (~1 on average).  ~1/3 of the rank sort's instructions.  The result and
+// the check are the rank sort's: equal keys collide (fallback to the exact sorts).
+template <int E>
+__device__ __forceinline__ bool qsort_bucket(Win &w, int lane, int32_t n) {
+    constexpr int NB = 32 * E, SH = E == 2 ? 26 : 25;
+    static_assert(E == 2 || E == 4, "64 or 128 events");
+    double t[E];
+    int16_t c[E];
+    uint16_t d[E];
+    int32_t p[E], r[E];
+    uint32_t q[E], bk[E], slot[E];
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(w.lw + NB), *tq = cnt + NB;
+    const double base = (double)w.k * w.W, scale = w.invW * 4294967296.0;
+#pragma unroll
+    for (int e = 0; e < E; e++) cnt[lane + 32 * e] = 0u;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int32_t i = lane + 32 * e;
+        const bool v = i < n;
+        t[e] = v ? w.lw[i] : INFINITY;
+        c[e] = v ? w.li[i] : 0;
+        d[e] = v ? w.ld[i] : 0;
+        p[e] = v ? w.lp[i] : 0;
+        const double x = (t[e] - base) * scale;
+        q[e] = x <= 0.0 ? 0u : x >= 4294967295.0 ? 0xffffffffu : (uint32_t)x;
+        bk[e] = q[e] >> SH;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        if (lane + 32 * e < n) slot[e] = atomicAdd(&cnt[bk[e]], 1u);
+    __syncwarp();
+    uint32_t cb[E], tot = 0;                           // lane: buckets E l .. E l + E - 1
+#pragma unroll
+    for (int e = 0; e < E; e++) { cb[e] = cnt[E * lane + e]; tot += cb[e]; }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    uint32_t run = incl - tot;
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) { cnt[E * lane + e] = run | (cb[e] << 16); run += cb[e]; }   // start | count << 16
+    __syncwarp();
+    uint32_t st[E], nb[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        st[e] = 0; nb[e] = 0;
+        if (lane + 32 * e < n) {
+            const uint32_t sc = cnt[bk[e]];
+            st[e] = sc & 0xffffu;
+            nb[e] = sc >> 16;
+            tq[st[e] + slot[e]] = q[e];
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        int32_t rk = (int32_t)st[e];
+        OTF_NOUNROLL
+        for (uint32_t k = 0; k < nb[e]; k++) rk += (int32_t)(tq[st[e] + k] < q[e]);
+        r[e] = rk;
+    }
+    __syncwarp();                                      // every lane has read the list
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        if (lane + 32 * e < n) w.lw[lane + 32 * e] = NAN;   // unwritten positions stay NaN
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        if (lane + 32 * e < n) { w.lw[r[e]] = t[e]; w.li[r[e]] = c[e]; w.ld[r[e]] = d[e]; w.lp[r[e]] = p[e]; }
+    __syncwarp();
+    bool ok = true;                                    // strictly increasing, every position written
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int32_t i = lane + 32 * e;
+        if (i < n) ok &= w.lw[i] == w.lw[i] && (i == 0 || w.lw[i] > w.lw[i - 1]);
+    }
+    if (__all_sync(0xffffffffu, ok)) return true;
+    __syncwarp();                                      // collision or tie: restore the list
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int32_t i = lane + 32 * e;
+        if (i < n) { w.lw[i] = t[e]; w.li[i] = c[e]; w.ld[i] = d[e]; w.lp[i] = p[e]; }
+    }
+    __syncwarp();
+    return false;
+}
+#endif
+
 // Order the window's server events by time: rank sort for small windows, in-place
 // bitonic sort for large ones.  Equal times are flagged afterwards; order_ties
 // then orders each group by arm time, a result independent of the group's order.
@@ -1588,7 +1685,17 @@ __device__ void sort_list(Win &w, int lane) {
 #ifndef WIN_QSORT_MAX
 #define WIN_QSORT_MAX 128                              // fast rank sort up to this many events
 #endif
-    if (n <= 64 ? qsort_fast<2>(w, lane, n) : n <= WIN_QSORT_MAX && qsort_fast<4>(w, lane, n)) {
+    // (the bucket sort for 65-128 events too -- in the two-warp kernels with warp 0
+    // sorting them alone instead of the two-warp bitonic sort -- measured -3% on config 4
+    // but +2% on c5t; as code beside the hot loop without that routing, +3% on config 5:
+    // profiles/r02i_ab_bsort*)
+#ifndef WIN_NO_BSORT
+    const bool fast = n <= 64 ? (h->list_cap >= 128 ? qsort_bucket<2>(w, lane, n) : qsort_fast<2>(w, lane, n))
+                              : n <= WIN_QSORT_MAX && qsort_fast<4>(w, lane, n);
+#else
+    const bool fast = n <= 64 ? qsort_fast<2>(w, lane, n) : n <= WIN_QSORT_MAX && qsort_fast<4>(w, lane, n);
+#endif
+    if (fast) {
         if (lane == 0) h->n_ties = 0;
         __syncwarp();
         return;
