@@ -1766,6 +1766,105 @@ __device__ void sort_list(Win &w, int lane) {
     __syncwarp();
 }
 
+#ifndef WIN_NO_BSORT
+// Two-warp bucket sort of a window's 64 < n <= 128 server events (list capacity >=
+// 256: positions 128..255 of the time array are its scratch), the CTA version of
+// qsort_bucket: thread t holds positions t and t + 64; 128 buckets on the 32-bit key's
+// top 7 bits; warp 0 scans the bucket counts.  Six CTA barriers instead of the
+// bitonic sort's 28 stages.  Returns false (list restored) on a key collision.
+__device__ bool sort_bucket_cta(Win &w, int tid, int32_t m) {
+    constexpr int NB = 128, SH = 25;
+    WinHeader *h = w.h;
+    const int32_t n = h->n_list;
+    const int lane = tid & 31;
+    double t[2];
+    int16_t c[2];
+    uint16_t d[2];
+    int32_t p[2], r[2];
+    uint32_t q[2], bk[2], slot[2];
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(w.lw + NB), *tq = cnt + NB;
+    const double base = (double)m * w.W, scale = w.invW * 4294967296.0;
+    cnt[tid] = 0u;
+    cnt[tid + 64] = 0u;
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        const int32_t i = tid + 64 * e;
+        const bool v = i < n;
+        t[e] = v ? w.lw[i] : INFINITY;
+        c[e] = v ? w.li[i] : 0;
+        d[e] = v ? w.ld[i] : 0;
+        p[e] = v ? w.lp[i] : 0;
+        const double x = (t[e] - base) * scale;
+        q[e] = x <= 0.0 ? 0u : x >= 4294967295.0 ? 0xffffffffu : (uint32_t)x;
+        bk[e] = q[e] >> SH;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 2; e++)
+        if (tid + 64 * e < n) slot[e] = atomicAdd(&cnt[bk[e]], 1u);
+    __syncthreads();
+    if (tid < 32) {                                    // warp 0: lane holds buckets 4 l .. 4 l + 3
+        uint32_t cb[4], tot = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) { cb[e] = cnt[4 * lane + e]; tot += cb[e]; }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        uint32_t run = incl - tot;
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 4; e++) { cnt[4 * lane + e] = run | (cb[e] << 16); run += cb[e]; }   // start | count << 16
+    }
+    __syncthreads();
+    uint32_t st[2], nb[2];
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        st[e] = 0; nb[e] = 0;
+        if (tid + 64 * e < n) {
+            const uint32_t sc = cnt[bk[e]];
+            st[e] = sc & 0xffffu;
+            nb[e] = sc >> 16;
+            tq[st[e] + slot[e]] = q[e];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        int32_t rk = (int32_t)st[e];
+        OTF_NOUNROLL
+        for (uint32_t k = 0; k < nb[e]; k++) rk += (int32_t)(tq[st[e] + k] < q[e]);
+        r[e] = rk;
+        if (tid + 64 * e < n) w.lw[tid + 64 * e] = NAN;    // unwritten positions stay NaN
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 2; e++)
+        if (tid + 64 * e < n) { w.lw[r[e]] = t[e]; w.li[r[e]] = c[e]; w.ld[r[e]] = d[e]; w.lp[r[e]] = p[e]; }
+    __syncthreads();
+    bool ok = true;                                    // strictly increasing, every position written
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        const int32_t i = tid + 64 * e;
+        if (i < n) ok &= w.lw[i] == w.lw[i] && (i == 0 || w.lw[i] > w.lw[i - 1]);
+    }
+    if (__syncthreads_and(ok ? 1 : 0)) {
+        if (tid == 0) h->n_ties = 0;
+        __syncthreads();
+        return true;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; e++) {                      // collision or tie: restore the list
+        const int32_t i = tid + 64 * e;
+        if (i < n) { w.lw[i] = t[e]; w.li[i] = c[e]; w.ld[i] = d[e]; w.lp[i] = p[e]; }
+    }
+    __syncthreads();
+    return false;
+}
+#endif
+
 // Two-warp bitonic sort of a large window's list (NW = 2: the big client classes,
 // e.g. ~180 requests per window at 10,000 clients): both warps take the
 // compare-exchanges of every stage, a CTA barrier between stages.  Called by all
@@ -2212,7 +2311,10 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
         if constexpr (WIN_WARPS == 2) {
             if (h->n_list > RANK_SORT_MAX) {           // a large window: both warps sort it
                 t0 = WCLOCK();
-                sort_list_cta(w, tid, WIN_THREADS);
+#ifndef WIN_NO_BSORT
+                if (!(h->n_list <= 128 && h->list_cap >= 256 && sort_bucket_cta(w, tid, h->cur_m)))
+#endif
+                    sort_list_cta(w, tid, WIN_THREADS);
                 if (tid == 0) h->stats[OTF_ST_CYC_SORT] += WCLOCK() - t0;
             }
         }

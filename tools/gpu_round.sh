@@ -1,6 +1,6 @@
-# the round's final evidence set (profiles/r02z_*)
+# the round's final evidence set (profiles/${ROUND_TAG}_*)
 set -x
-R=${ROUND_TAG:-r02z}
+R=${ROUND_TAG:-r02k}
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${R}_gputest.log 2>&1; echo gputest=$?
 tail -2 gpurun_out/${R}_gputest.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${R}_smoke.log 2>&1; echo smoke=$?
@@ -17,11 +17,5 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:wind
 ncu -i gpurun_out/${R}_windowed_c5.ncu-rep --page source --csv --print-source sass > gpurun_out/${R}_sass.csv 2>/dev/null
 ncu -i gpurun_out/${R}_windowed_c5.ncu-rep --page raw --csv > gpurun_out/${R}_raw.csv 2>/dev/null
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${R}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-for rep in 1 2; do
-for v in "" build/qsu1/; do
-  if [ -z "$v" ]; then unset OTFGPU_LIB_OVERRIDE; name=intree; else export OTFGPU_LIB_OVERRIDE=$PWD/${v}libotfgpu.so; name=$(basename $v); fi
-  echo "== $name rep $rep $(timeout 300 python tools/probe.py c5fw 2>&1 | tail -1)"
-done
-done > gpurun_out/${R}_ab.txt 2>&1
-unset OTFGPU_LIB_OVERRIDE
-grep -h "^==" gpurun_out/${R}_ab.txt | cut -c1-150
+# A/B of the final library against build/prev, when present
+[ -n "${AB:-}" ] && [ -f build/prev/libotfgpu.so ] && DIAG=1 bash tools/ab.sh c5fw 2 gpurun_out/${R}_ab.txt
