@@ -1621,6 +1621,10 @@ __device__ __forceinline__ bool qsort_bucket(Win &w, int lane, int32_t n) {
 // Order the window's server events by time: rank sort for small windows, in-place
 // bitonic sort for large ones.  Equal times are flagged afterwards; order_ties
 // then orders each group by arm time, a result independent of the group's order.
+// NW: warps per scenario of the calling kernel.  Two-warp kernels sort windows of more
+// than RANK_SORT_MAX events with both warps (sort_bucket_cta / sort_list_cta), so
+// their copy carries only the <= 64-event paths (hot code).
+template <int NW>
 __device__ void sort_list(Win &w, int lane) {
     WinHeader *h = w.h;
     const int32_t n = h->n_list;
@@ -1685,13 +1689,16 @@ __device__ void sort_list(Win &w, int lane) {
 #ifndef WIN_QSORT_MAX
 #define WIN_QSORT_MAX 128                              // fast rank sort up to this many events
 #endif
-    // (the bucket sort for 65-128 events too -- in the two-warp kernels with warp 0
-    // sorting them alone instead of the two-warp bitonic sort -- measured -3% on config 4
-    // but +2% on c5t; as code beside the hot loop without that routing, +3% on config 5:
-    // profiles/r02i_ab_bsort*)
+    // (in the two-warp kernels warp 0 alone bucket-sorting 65-128 events measured -3% on
+    // config 4 but +2% on c5t, profiles/r02i_ab_bsort*; they take sort_bucket_cta)
 #ifndef WIN_NO_BSORT
-    const bool fast = n <= 64 ? (h->list_cap >= 128 ? qsort_bucket<2>(w, lane, n) : qsort_fast<2>(w, lane, n))
-                              : n <= WIN_QSORT_MAX && qsort_fast<4>(w, lane, n);
+    bool fast;
+    if constexpr (NW == 1)
+        fast = n <= 64 ? (h->list_cap >= 128 ? qsort_bucket<2>(w, lane, n) : qsort_fast<2>(w, lane, n))
+                       : n <= WIN_QSORT_MAX &&
+                             (h->list_cap >= 256 ? qsort_bucket<4>(w, lane, n) : qsort_fast<4>(w, lane, n));
+    else
+        fast = h->list_cap >= 128 ? qsort_bucket<2>(w, lane, n) : qsort_fast<2>(w, lane, n);
 #else
     const bool fast = n <= 64 ? qsort_fast<2>(w, lane, n) : n <= WIN_QSORT_MAX && qsort_fast<4>(w, lane, n);
 #endif
@@ -1731,7 +1738,7 @@ __device__ void sort_list(Win &w, int lane) {
         if (lane == 0) h->n_ties = any ? 1 : 0;
         __syncwarp();
         return;
-    } else {
+    } else if constexpr (NW == 1) {
         int32_t p = 1;
         while (p < n) p <<= 1;
         OTF_NOUNROLL
@@ -1767,27 +1774,29 @@ __device__ void sort_list(Win &w, int lane) {
 }
 
 #ifndef WIN_NO_BSORT
-// Two-warp bucket sort of a window's 64 < n <= 128 server events (list capacity >=
-// 256: positions 128..255 of the time array are its scratch), the CTA version of
-// qsort_bucket: thread t holds positions t and t + 64; 128 buckets on the 32-bit key's
-// top 7 bits; warp 0 scans the bucket counts.  Six CTA barriers instead of the
-// bitonic sort's 28 stages.  Returns false (list restored) on a key collision.
+// Two-warp bucket sort of a window's 64 < n <= 64 E server events (list capacity >=
+// 128 E: positions 64 E..128 E of the time array are its scratch), the CTA version of
+// qsort_bucket: thread t holds positions t, t + 64, ...; 64 E buckets on the 32-bit
+// key's top bits; warp 0 scans the bucket counts.  Six CTA barriers instead of the
+// bitonic sort's 28 (36) stages.  Returns false (list restored) on a key collision.
+template <int E>
 __device__ bool sort_bucket_cta(Win &w, int tid, int32_t m) {
-    constexpr int NB = 128, SH = 25;
+    static_assert(E == 2 || E == 4, "128 or 256 events");
+    constexpr int NB = 64 * E, SH = E == 2 ? 25 : 24, PL = NB / 32;
     WinHeader *h = w.h;
     const int32_t n = h->n_list;
     const int lane = tid & 31;
-    double t[2];
-    int16_t c[2];
-    uint16_t d[2];
-    int32_t p[2], r[2];
-    uint32_t q[2], bk[2], slot[2];
+    double t[E];
+    int16_t c[E];
+    uint16_t d[E];
+    int32_t p[E], r[E];
+    uint32_t q[E], bk[E], slot[E];
     uint32_t *cnt = reinterpret_cast<uint32_t *>(w.lw + NB), *tq = cnt + NB;
     const double base = (double)m * w.W, scale = w.invW * 4294967296.0;
-    cnt[tid] = 0u;
-    cnt[tid + 64] = 0u;
 #pragma unroll
-    for (int e = 0; e < 2; e++) {
+    for (int e = 0; e < E; e++) cnt[tid + 64 * e] = 0u;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
         const int32_t i = tid + 64 * e;
         const bool v = i < n;
         t[e] = v ? w.lw[i] : INFINITY;
@@ -1800,13 +1809,13 @@ __device__ bool sort_bucket_cta(Win &w, int tid, int32_t m) {
     }
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 2; e++)
+    for (int e = 0; e < E; e++)
         if (tid + 64 * e < n) slot[e] = atomicAdd(&cnt[bk[e]], 1u);
     __syncthreads();
-    if (tid < 32) {                                    // warp 0: lane holds buckets 4 l .. 4 l + 3
-        uint32_t cb[4], tot = 0;
+    if (tid < 32) {                                    // warp 0: lane holds buckets PL l .. PL l + PL - 1
+        uint32_t cb[PL], tot = 0;
 #pragma unroll
-        for (int e = 0; e < 4; e++) { cb[e] = cnt[4 * lane + e]; tot += cb[e]; }
+        for (int e = 0; e < PL; e++) { cb[e] = cnt[PL * lane + e]; tot += cb[e]; }
         uint32_t incl = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1816,12 +1825,12 @@ __device__ bool sort_bucket_cta(Win &w, int tid, int32_t m) {
         uint32_t run = incl - tot;
         __syncwarp();
 #pragma unroll
-        for (int e = 0; e < 4; e++) { cnt[4 * lane + e] = run | (cb[e] << 16); run += cb[e]; }   // start | count << 16
+        for (int e = 0; e < PL; e++) { cnt[PL * lane + e] = run | (cb[e] << 16); run += cb[e]; }   // start | count << 16
     }
     __syncthreads();
-    uint32_t st[2], nb[2];
+    uint32_t st[E], nb[E];
 #pragma unroll
-    for (int e = 0; e < 2; e++) {
+    for (int e = 0; e < E; e++) {
         st[e] = 0; nb[e] = 0;
         if (tid + 64 * e < n) {
             const uint32_t sc = cnt[bk[e]];
@@ -1832,7 +1841,7 @@ __device__ bool sort_bucket_cta(Win &w, int tid, int32_t m) {
     }
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 2; e++) {
+    for (int e = 0; e < E; e++) {
         int32_t rk = (int32_t)st[e];
         OTF_NOUNROLL
         for (uint32_t k = 0; k < nb[e]; k++) rk += (int32_t)(tq[st[e] + k] < q[e]);
@@ -1841,12 +1850,12 @@ __device__ bool sort_bucket_cta(Win &w, int tid, int32_t m) {
     }
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 2; e++)
+    for (int e = 0; e < E; e++)
         if (tid + 64 * e < n) { w.lw[r[e]] = t[e]; w.li[r[e]] = c[e]; w.ld[r[e]] = d[e]; w.lp[r[e]] = p[e]; }
     __syncthreads();
     bool ok = true;                                    // strictly increasing, every position written
 #pragma unroll
-    for (int e = 0; e < 2; e++) {
+    for (int e = 0; e < E; e++) {
         const int32_t i = tid + 64 * e;
         if (i < n) ok &= w.lw[i] == w.lw[i] && (i == 0 || w.lw[i] > w.lw[i - 1]);
     }
@@ -1856,7 +1865,7 @@ __device__ bool sort_bucket_cta(Win &w, int tid, int32_t m) {
         return true;
     }
 #pragma unroll
-    for (int e = 0; e < 2; e++) {                      // collision or tie: restore the list
+    for (int e = 0; e < E; e++) {                      // collision or tie: restore the list
         const int32_t i = tid + 64 * e;
         if (i < n) { w.lw[i] = t[e]; w.li[i] = c[e]; w.ld[i] = d[e]; w.lp[i] = p[e]; }
     }
@@ -2296,7 +2305,7 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
                     if (lane == 0) h->stats[OTF_ST_CYC_SCAN] += t1 - t0;
                     t0 = t1;
                     if (WIN_WARPS == 1 || nlist <= RANK_SORT_MAX) {   // else both warps, below
-                        sort_list(w, lane);
+                        sort_list<WIN_WARPS>(w, lane);
                         t1 = WCLOCK();
                         if (lane == 0) h->stats[OTF_ST_CYC_SORT] += t1 - t0;
                     }
@@ -2312,7 +2321,14 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
             if (h->n_list > RANK_SORT_MAX) {           // a large window: both warps sort it
                 t0 = WCLOCK();
 #ifndef WIN_NO_BSORT
-                if (!(h->n_list <= 128 && h->list_cap >= 256 && sort_bucket_cta(w, tid, h->cur_m)))
+                const int32_t nl = h->n_list, lc = h->list_cap;
+                bool done;
+                if constexpr (MB <= 4)                 // the big classes' shape: up to 256 events
+                    done = nl <= 128 ? lc >= 256 && sort_bucket_cta<2>(w, tid, h->cur_m)
+                                     : nl <= 256 && lc >= 512 && sort_bucket_cta<4>(w, tid, h->cur_m);
+                else                                   // (the dense shape: 12 B of spills with both)
+                    done = nl <= 128 && lc >= 256 && sort_bucket_cta<2>(w, tid, h->cur_m);
+                if (!done)
 #endif
                     sort_list_cta(w, tid, WIN_THREADS);
                 if (tid == 0) h->stats[OTF_ST_CYC_SORT] += WCLOCK() - t0;
