@@ -919,12 +919,25 @@ __device__ __forceinline__ void phase_a_parallel(Win &w, int lane) {
         p_enq += ((f >> 5) & 1u) + ((f >> 6) & 1u);
     }
     __syncwarp();
-    // the latest touch stamp per descriptor: each lane over its own requests, in time order
+    // the latest touch stamp per descriptor: 32 requests at a time in time order; within
+    // a chunk only the last toucher of a descriptor (highest lane of its match group)
+    // stores, and a later chunk's stores follow the earlier one's
+#ifndef WIN_SERIAL_STAMPS
+    for (int32_t base = 0; base < n; base += 32) {
+        const int32_t i = base + lane;
+        const bool touch = i < n && (h->ev_flags[i] & EV_TOUCH);
+        const int32_t d = touch ? (int32_t)w.ld[i] : -1 - lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (touch && (peers >> lane) == 1u) w.lstamp[d] = stamp_base + h->ev_touch[i] + 1u;
+        __syncwarp();
+    }
+#else
     OTF_NOUNROLL
-    for (uint32_t k = my_off; k < my_off + my_cnt; k++) {
+    for (uint32_t k = my_off; k < my_off + my_cnt; k++) {   // each lane over its own requests
         const int32_t i = h->par_list[k];
         if (h->ev_flags[i] & EV_TOUCH) w.lstamp[w.ld[i]] = stamp_base + h->ev_touch[i] + 1u;
     }
+#endif
     // counters back into lane 0's registers / the header
     hits = warp_sum(hits); miss = warp_sum(miss); spec = warp_sum(spec);
     sk0 = warp_sum(sk0); sk1 = warp_sum(sk1); sk3 = warp_sum(sk3); sk4 = warp_sum(sk4);
