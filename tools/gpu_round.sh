@@ -10,7 +10,7 @@ timeout 900 python bench.py --workload c5t --steps 3 > gpurun_out/${R}_bench_c5t
 timeout 900 python bench.py --impl reference > gpurun_out/${R}_bench_reference.json 2> gpurun_out/${R}_bench_reference.err; echo ref=$?
 timeout 600 python tools/strong_probe.py > gpurun_out/${R}_strong.txt 2>&1; echo strong=$?
 timeout 300 python tools/e2e_breakdown.py > gpurun_out/${R}_e2e_breakdown.txt 2>&1
-for tool in memcheck racecheck synccheck; do
+for tool in ${SANITIZE_TOOLS:-}; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > gpurun_out/${R}_sanitize_$tool.txt 2>&1; echo $tool=$?
 done
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:windowed -c 1 -o gpurun_out/${R}_windowed_c5 python tools/prof_run.py c5 > gpurun_out/${R}_ncu.log 2>&1; echo ncu=$?
