@@ -96,6 +96,9 @@ struct WinHeader {
     int32_t jq_head, jq_n, jq_cap;
     int32_t sq_head, sq_n, tokens;       // demand-priority mode: speculative FIFO, wakeup tokens
     int32_t n_list, n_blist, n_ties;
+#ifdef WIN_BULK_GATHER
+    unsigned long long gbar;             // mbarrier of the window bucket's bulk copy (WIN_BULK_GATHER)
+#endif
     uint32_t wseq;
     int32_t far_head, far_n, far_min, k_done;
     int32_t arr_next;                    // next client (arrival order) not yet on the wheel
@@ -2017,6 +2020,9 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     long long t_start = 0, t0 = 0, t1 = 0;
+#ifdef WIN_BULK_GATHER
+    uint32_t gphase = 0;                               // the gather mbarrier's phase parity (warp 0)
+#endif
     const int32_t s = b.order ? b.order[blockIdx.x] : (int32_t)blockIdx.x;
     WinHeader *h = (WinHeader *)smem;
     if (tid == 0) { h->b = b; h->sc = b.scenarios[s]; }
@@ -2081,6 +2087,9 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
         h->ovf_head = -1; h->ovf_n = 0; h->ovf_min = WIN_NONE; h->n_loc = 0;
         h->lq_head = 0; h->lq_tail = 0; h->lq_stamp = 0; h->lq_cap = (int32_t)lq_capacity(D);
         h->list_cap = lcap;
+#ifdef WIN_BULK_GATHER
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&h->gbar)));
+#endif
         h->ctl = CTL_RUN; h->cur_m = 0;
         if (!fits) h->st.status |= OTF_S_UNFIT;        // not for this engine: host re-runs it exactly
     }
@@ -2268,7 +2277,29 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
                     if (lane == 0) atomicOr(&h->st.status, OTF_S_LIST_OVERFLOW);   // re-run with a larger one
                     ctl = CTL_STOP;
                 } else {
-                    const SrvEnt *as = w.bsrv + (int64_t)slot * w.scap;
+                    const SrvEnt *as_g = w.bsrv + (int64_t)slot * w.scap;
+                    const SrvEnt *as = as_g;
+#ifdef WIN_BULK_GATHER
+                    // the bucket (ns x 24 B, contiguous) into the list's free second half by
+                    // one bulk copy (TMA engine, mbarrier completion), then read from shared
+                    if (ns > 0 && ns <= 64 && h->list_cap >= 128) {
+                        SrvEnt *stage = reinterpret_cast<SrvEnt *>(w.lw + 64);
+                        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&h->gbar);
+                        if (lane == 0) {
+                            const uint32_t bytes = ((uint32_t)ns * (uint32_t)sizeof(SrvEnt) + 15u) & ~15u;
+                            asm volatile("fence.proxy.async;" ::: "memory");
+                            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+                            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                         :: "r"((uint32_t)__cvta_generic_to_shared(stage)), "l"(as), "r"(bytes), "r"(bar) : "memory");
+                        }
+                        uint32_t done = 0;
+                        while (!done)
+                            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                         : "=r"(done) : "r"(bar), "r"(gphase) : "memory");
+                        gphase ^= 1u;
+                        as = stage;
+                    }
+#endif
                     OTF_NOUNROLL
                     for (int32_t i = lane; i < ns; i += 64) {      // gather sort keys + request descriptors
                         const SrvEnt e = as[i];                    //   (both loads issue before the stores)
