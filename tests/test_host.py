@@ -290,3 +290,28 @@ def test_libm_restatement_matches_host_libm():
                 want[i] = np.inf
         bad = np.nonzero(out.view(np.int64) != want.view(np.int64))[0]
         assert bad.size == 0, (fn, xs[bad[:5]], out[bad[:5]], want[bad[:5]])
+
+
+def test_build_inputs_same_for_configs_and_lowered_memo_cold_and_warm():
+    """run_batch lowers each config once and hands the Lowered objects to
+    build_inputs, which memoizes the catalog tables per lowering group: the batch
+    must be byte-identical to one built from the configs with cold memos."""
+    import dataclasses
+    cfgs = workloads.c5_sweep(seeds=range(1, 4))
+    cfgs += [dataclasses.replace(c, clients=300, zipf_exponent=1.1) for c in cfgs[:5]]
+
+    def blob(inp):
+        return (bytes(inp.scenarios), bytes(inp.size_tables), bytes(inp.gen_jobs), inp.f64.tobytes(),
+                inp.i64.tobytes(), inp.i32.tobytes(), inp.scratch_bytes, inp.shared_bytes, tuple(inp.smem_per),
+                inp.tail_caps.tobytes(), inp.input_bytes)
+
+    for memo in (inputs._LOWER_MEMO, inputs._GRID_MEMO, inputs._SIZE_MEMO, inputs._EPS_MEMO, inputs._MAN_MEMO):
+        memo.clear()
+    cold = blob(inputs.build_inputs(cfgs, mode=_lib.MODE_HISTOGRAM))
+    lows = [inputs.lower_any(c) for c in cfgs]
+    assert all(inputs.lower_any(l) is l for l in lows)
+    warm = blob(inputs.build_inputs(lows, mode=_lib.MODE_HISTOGRAM))
+    assert cold == warm
+    again = blob(inputs.build_inputs(list(reversed(lows)), mode=_lib.MODE_HISTOGRAM))
+    assert again != warm                               # (order matters: the scenario table is reversed)
+    assert blob(inputs.build_inputs(cfgs, mode=_lib.MODE_HISTOGRAM)) == cold
