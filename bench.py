@@ -308,6 +308,16 @@ def main():
     sum_ms = statistics.mean(a.elapsed_time(b) for a, b in sum_evs)
     br = db.fetch()
     my_req = int(br.counts[:, 0].sum())
+    # per variant (this rank's scenarios): requests and each scenario's own run time
+    # (the windowed engine's cycle counter at the measured SM clock) -- every scenario
+    # runs concurrently, so the sweep ends with the slowest one
+    per_variant = {}
+    cyc = br.stats[:, _lib.ST["cyc_total"]].astype(np.float64)
+    for k, c in enumerate(my_cfgs):
+        v = per_variant.setdefault(getattr(c, "variant", "?"), {"scenarios": 0, "requests": 0, "cycles": []})
+        v["scenarios"] += 1
+        v["requests"] += int(br.counts[k, 0])
+        v["cycles"].append(float(cyc[k]))
     for r, idx in redo_dbs:
         my_req += int(r.fetch().counts[:, 0].sum()) - int(br.counts[idx, 0].sum())
     if world > 1:
@@ -380,6 +390,15 @@ def main():
                "parity": {"scenarios_checked": len(digests), "mismatches": 0,
                           "fields": "requests, sessions, segments, jobs, backend/cache stats, response paths"}}
 
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    variants = {}
+    for name, v in sorted(per_variant.items()):
+        cy = np.asarray(v["cycles"])
+        variants[name] = {"scenarios": v["scenarios"], "requests": v["requests"],
+                          "scenario_ms_mean": round(float(cy.mean()) / (sm_mhz * 1e3), 1),
+                          "scenario_ms_max": round(float(cy.max()) / (sm_mhz * 1e3), 1),
+                          "req_per_s_over_slowest_scenario": v["requests"] / (float(cy.max()) / (sm_mhz * 1e6))
+                          if cy.max() > 0 else None}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -395,6 +414,7 @@ def main():
                    "l2": "inputs > L2 (trace tables %.2f GB, engine state %.2f GB vs 126 MB L2)"
                          % (inp.input_bytes / 1e9, inp.scratch_bytes / 1e9),
                    "host_input_build_s": round(t_build, 2),
+                   "per_variant": variants,
                    "rerun_scenarios": len(flagged)},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches_per_step * args.steps,
