@@ -2316,7 +2316,7 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
                         w.lp[i] = e.pk;
                         if (two) { w.li[i + 32] = f.cid; w.lw[i + 32] = f.when; w.ld[i + 32] = f.desc; w.lp[i + 32] = f.pk; }
                     }
-#ifndef WIN_NO_NEXT_PF
+#ifdef WIN_NEXT_PF                                   // (measured -1.5% without it, profiles/r02q_abn_prefetch_flags.txt)
                     {                                      // warm L2 with the next window's request entries
                         const int32_t sn = (m + 1) & (RING - 1);
                         const int32_t nn = min((int32_t)((h->cnt_srv[sn >> 1] >> ((sn & 1) << 4)) & 0xffffu), w.scap);
