@@ -1150,8 +1150,11 @@ __device__ __forceinline__ bool arm(Win &w, WClient &c, int32_t cid, double &now
     // round of 32 lanes made the whole warp wait; they keep their own window's timer
     // (measured: 0.93 s -> 0.86 s on config 5).  The segment transfer is never
     // deferred: its start time and byte count live only in the chain's registers.
+    // (late round 2: deferring only the playout -- the manifest steps now run in their
+    // chain -- measured config 5 -1.6%, c5t -1.3%, config 4 -0.7%; deferring nothing
+    // +16%: profiles/r02r_abn_defer*)
 #ifndef WIN_DEFER_MASK
-#define WIN_DEFER_MASK ((1u << C_PLAYOUT) | (1u << C_MAN_LAT) | (1u << C_MAN_XFER))
+#define WIN_DEFER_MASK (1u << C_PLAYOUT)
 #endif
     static_assert(!((WIN_DEFER_MASK >> C_SEG_XFER) & 1u), "the segment transfer completes in its chain");
     if (!srv && when <= w.H && (!((WIN_DEFER_MASK >> next_pc) & 1u) || when < w.E)) {
