@@ -1000,9 +1000,15 @@ __device__ __forceinline__ bool parallel_ok(Win &w) {
     const int32_t n_ties = h->n_ties, fq_n = h->fq_n, gq_n = h->gq_n, hand_safe = h->hand_safe;
     const uint32_t lq_head = h->lq_head, lq_tail = h->lq_tail;
     const int32_t n_blist = h->n_blist;
+#ifndef WIN_SERIAL_PAR_OK
+    // the whole warp calls it: lane q checks worker q (K <= MAXK <= 32)
+    const int lane = threadIdx.x & 31;
+    const bool due = __any_sync(0xffffffffu, lane < sc.n_workers && h->wk[lane].win == w.k);
+#else
     bool due = false;                                  // a transcode completes in this window
 #pragma unroll 4
     for (int32_t q = 0; q < sc.n_workers; q++) due |= h->wk[q].win == w.k;
+#endif
     // an idle worker handed a job here must not finish inside the window (hand_safe:
     // svc >= svc_floor * (1 + min eps) >= 2 W for every job, checked at kernel start)
     return (n >= 2) & (n <= PAR_MAX) & (n_ties == 0) & (fq_n == 0) & (sc.demand_priority == 0) &
@@ -2393,17 +2399,28 @@ __global__ void __launch_bounds__(32 * NW, MB) windowed_kernel(const otf_batch b
             long long dgp = clock64();
 #endif
             int32_t pre = 0;
+#ifndef WIN_SERIAL_PAR_OK
+            if (warp == 0) {                           // warp-uniform answer
+                par = parallel_ok(w) ? 1 : 0;
+#ifndef WIN_NO_PREFIX
+                if (!par && lane == 0) pre = parallel_prefix(w);
+#endif
+            }
+#else
             if (tid == 0) {
                 par = parallel_ok(w) ? 1 : 0;
 #ifndef WIN_NO_PREFIX
                 if (!par) pre = parallel_prefix(w);
 #endif
             }
+#endif
 #ifdef WIN_DIAG
             if (tid == 0) h->stats[30] += clock64() - dgp;
 #endif
             if (warp == 0) {
+#ifdef WIN_SERIAL_PAR_OK
                 par = __shfl_sync(0xffffffffu, par, 0);
+#endif
                 pre = __shfl_sync(0xffffffffu, pre, 0);
             }
             // one call site each (phase_a_parallel is inlined; a second copy of it, or a
